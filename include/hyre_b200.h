@@ -1,0 +1,278 @@
+/*
+ * hyre_b200.h -- C-ABI of the B200-native hybrid retrieval hot path
+ * (arXiv 2402.13435, "hyre" reference at /root/reference/proj).
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * proj/include/hyre/{corpus,term_match,quantizer,knn,pipeline,types,common}.hpp.
+ * Every entry point below names the reference interface it replaces.  Plain
+ * pointers and sizes only; no torch or CUDA types cross this boundary (the
+ * executor's stream is exposed as an opaque void*).
+ *
+ * Error convention (reference: proj/include/hyre/common.hpp:15-33,
+ * knn.cpp:59-61, service.cpp:219-225):
+ *   HYRE_INVALID_ARGUMENT  <=> hyre::ValidationError (message names the field,
+ *                              byte-identical to the reference's message)
+ *   HYRE_OUT_OF_RANGE      <=> std::domain_error (score outside [-1, 1])
+ *   HYRE_LOAD_ERROR        <=> hyre::LoadError, cause via hyre_last_load_cause()
+ *   HYRE_CUDA_ERROR / HYRE_OUT_OF_MEMORY / HYRE_INTERNAL <=> std::runtime_error
+ * The message of the last failing call on the calling thread is returned by
+ * hyre_last_error().
+ *
+ * Threading (reference: corpus.hpp:54-56, pipeline.hpp:66-68): a hyre_frozen /
+ * hyre_index is immutable after creation and may be shared by any number of
+ * executors; one hyre_executor runs one batch at a time.
+ */
+#ifndef HYRE_B200_H_
+#define HYRE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYRE_B200_ABI_VERSION 1
+
+typedef enum hyre_status {
+  HYRE_OK = 0,
+  HYRE_INVALID_ARGUMENT = 1,
+  HYRE_OUT_OF_RANGE = 2,
+  HYRE_LOAD_ERROR = 3,
+  HYRE_CUDA_ERROR = 4,
+  HYRE_OUT_OF_MEMORY = 5,
+  HYRE_INTERNAL = 6
+} hyre_status;
+
+/* hyre::LoadError::Cause (common.hpp:24) */
+typedef enum hyre_load_cause {
+  HYRE_LOAD_BAD_MAGIC = 0,
+  HYRE_LOAD_VERSION_MISMATCH = 1,
+  HYRE_LOAD_TRUNCATED = 2,
+  HYRE_LOAD_CHECKSUM = 3
+} hyre_load_cause;
+
+typedef enum hyre_emb_dtype {
+  HYRE_EMB_F32 = 0,  /* reference storage (corpus.hpp:118) */
+  HYRE_EMB_BF16 = 1  /* RNE-bf16 of the frozen fp32 rows (config c4) */
+} hyre_emb_dtype;
+
+const char* hyre_last_error(void);
+int hyre_last_load_cause(void);
+int hyre_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host-side index build: IndexBuilder / FrozenIndex (corpus.hpp:36-124)
+ * ------------------------------------------------------------------------ */
+typedef struct hyre_builder hyre_builder;
+typedef struct hyre_frozen hyre_frozen;
+
+/* IndexBuilder::IndexBuilder(IndexConfig) -- corpus.hpp:40, corpus.cpp:15-27.
+ * clause_names: NULL (defaults c0, c1, ...) or num_names strings. */
+hyre_status hyre_builder_create(uint32_t num_clauses, uint32_t max_num_attr, uint32_t dim,
+                                const char* const* clause_names, uint32_t num_names,
+                                hyre_builder** out);
+void hyre_builder_destroy(hyre_builder* b);
+
+/* IndexBuilder::add_document -- corpus.hpp:43, corpus.cpp:29-52.
+ * Clause c of the document holds ids[slot_offsets[c] .. slot_offsets[c+1]);
+ * num_slots is the document's clause count (validated against num_clauses). */
+hyre_status hyre_builder_add_document(hyre_builder* b, const char* doc_id,
+                                      uint32_t num_slots, const uint32_t* slot_offsets,
+                                      const uint32_t* ids, const float* embedding,
+                                      uint32_t embedding_len, uint32_t* row_out);
+
+/* Bulk form of add_document for n documents with ids doc_id_prefix + index
+ * (the prefix + decimal of the running row number).  Clause c of document i
+ * holds ids[slot_offsets[i*C + c] .. slot_offsets[i*C + c + 1]). */
+hyre_status hyre_builder_add_documents(hyre_builder* b, uint32_t n, const char* doc_id_prefix,
+                                       const uint64_t* slot_offsets, const uint32_t* ids,
+                                       const float* embeddings);
+uint32_t hyre_builder_size(const hyre_builder* b);
+
+/* std::move(builder).freeze(make_codec(dim, num_bits, seed)) -- corpus.hpp:47,
+ * corpus.cpp:54-129.  The builder is consumed (further calls fail). */
+hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t seed,
+                                hyre_frozen** out);
+
+/* Wraps flat FrozenIndex arrays (corpus.hpp:114-123) that a caller already
+ * holds -- e.g. the reference's own FrozenIndex -- without re-freezing.
+ * doc_ids: NULL (ids become doc_id_prefix + row) or num_docs C strings. */
+hyre_status hyre_frozen_from_arrays(uint32_t num_docs, uint32_t num_clauses,
+                                    uint32_t max_num_attr, uint32_t dim, uint32_t num_bits,
+                                    uint64_t seed, const uint32_t* attributes,
+                                    const uint32_t* offsets, const float* embeddings,
+                                    const uint64_t* signatures, const uint8_t* zero_flags,
+                                    const char* const* doc_ids, const char* doc_id_prefix,
+                                    hyre_frozen** out);
+
+/* FrozenIndex::save / FrozenIndex::load -- corpus.cpp:144-201 ("HYREIDN1" v1). */
+hyre_status hyre_frozen_save(const hyre_frozen* f, const char* path);
+hyre_status hyre_frozen_load(const char* path, hyre_frozen** out);
+void hyre_frozen_destroy(hyre_frozen* f);
+
+typedef struct hyre_shape {
+  uint32_t num_docs, num_clauses, max_num_attr, dim, num_bits, num_words;
+  uint64_t seed;
+} hyre_shape;
+void hyre_frozen_shape(const hyre_frozen* f, hyre_shape* out);
+
+/* Read-only views of the frozen host arrays (valid while f lives). */
+const uint32_t* hyre_frozen_attributes(const hyre_frozen* f);  /* N x A */
+const uint32_t* hyre_frozen_offsets(const hyre_frozen* f);     /* N x (C+1) */
+const float* hyre_frozen_embeddings(const hyre_frozen* f);     /* N x d */
+const uint64_t* hyre_frozen_signatures(const hyre_frozen* f);  /* N x words */
+const uint8_t* hyre_frozen_zero_flags(const hyre_frozen* f);   /* N */
+const char* hyre_frozen_doc_id(const hyre_frozen* f, uint32_t row);            /* doc_id() */
+int64_t hyre_frozen_row_of(const hyre_frozen* f, const char* doc_id);         /* row_of(), -1 */
+int32_t hyre_frozen_resolve_clause_slot(const hyre_frozen* f, const char* n); /* :103 */
+const char* hyre_frozen_clause_name(const hyre_frozen* f, uint32_t slot);
+
+/* ------------------------------------------------------------------------
+ * Sign-quant codec (quantizer.hpp:48-65)
+ * ------------------------------------------------------------------------ */
+/* encode(make_codec(dim, num_bits, seed), x) -> ceil(num_bits/64) words. */
+hyre_status hyre_encode(uint32_t dim, uint32_t num_bits, uint64_t seed, const float* x,
+                        uint64_t* words);
+/* quant_score_words (quantizer.hpp:59-61). */
+uint32_t hyre_quant_score_words(const uint64_t* a, const uint64_t* b, uint32_t num_words,
+                                uint32_t num_bits);
+
+/* ------------------------------------------------------------------------
+ * Queries (term_match.hpp:14-33, pipeline.hpp:17-57)
+ * ------------------------------------------------------------------------ */
+/* A HybridQuery whose CnfQuery is already normalized: clause c constrains slot
+ * slots[c] with ids[id_offsets[c] .. id_offsets[c+1]).  embedding == NULL is
+ * a term-only query.  quant_enabled/quant_k/granularity are ExecOptions. */
+typedef struct hyre_query {
+  uint32_t n_clauses;
+  const uint32_t* slots;
+  const uint32_t* id_offsets;
+  const uint32_t* ids;
+  const float* embedding;
+  uint32_t embedding_dim;
+  uint32_t k;
+  uint32_t quant_enabled;
+  uint32_t quant_k;      /* 0 => 200 * k (pipeline.hpp:22-24) */
+  uint32_t granularity;  /* bucket_top_k granularity G (validated, result-invariant) */
+} hyre_query;
+
+typedef struct hyre_hit {
+  uint32_t row;  /* global rowId */
+  float score;   /* clamp(dot(unit(q), row), -1, 1); 0 for term-only */
+} hyre_hit;
+
+/* StageTimings (pipeline.hpp:40-46); device stages are timed with CUDA events. */
+typedef struct hyre_timings {
+  double tbr_ms, quant_ms, ebr_ms, topk_ms, total_ms;
+} hyre_timings;
+
+/* normalize_query (term_match.hpp:31-33, term_match.cpp:7-30) over a raw
+ * {slot: ids} map given as n_raw (slot, id list) entries.  Outputs need room
+ * for n_raw clauses and all raw ids. */
+hyre_status hyre_normalize_query(uint32_t n_raw, const uint32_t* raw_slots,
+                                 const uint32_t* raw_offsets, const uint32_t* raw_ids,
+                                 uint32_t num_clauses, uint32_t* out_n, uint32_t* out_slots,
+                                 uint32_t* out_offsets, uint32_t* out_ids);
+
+/* validate_query (pipeline.hpp:57, pipeline.cpp:44-73). */
+hyre_status hyre_validate_query(const hyre_frozen* f, const hyre_query* q);
+
+/* ------------------------------------------------------------------------
+ * Device-resident index (the FrozenIndex's B200 column store)
+ * ------------------------------------------------------------------------ */
+typedef struct hyre_index hyre_index;
+
+typedef struct hyre_index_options {
+  int32_t device;        /* CUDA ordinal */
+  uint32_t emb_dtype;    /* hyre_emb_dtype */
+  uint32_t row_begin;    /* shard [row_begin, row_end) of the frozen rows; */
+  uint32_t row_end;      /* row_end == 0 => all rows */
+  uint32_t tensor_path;  /* 1: also store the bf16 (hi, lo) split for tcgen05 batches */
+} hyre_index_options;
+
+typedef struct hyre_index_stats {
+  uint64_t num_rows, row_base, dim, row_stride;
+  uint64_t num_terms, bitmap_terms, csr_terms, postings;
+  uint64_t embedding_bytes, tensor_bytes, bitmap_bytes, csr_bytes, signature_bytes;
+} hyre_index_stats;
+
+/* Uploads a frozen index (or a row shard of it) into device memory: embeddings
+ * row-major with a padded 16-byte-granular stride, per-term bitmaps / CSR
+ * postings derived from attributes+offsets, signatures.  Replaces the
+ * FrozenIndex arrays read by full_scan_tbr/exact_scores/preselect. */
+hyre_status hyre_index_create(const hyre_frozen* f, const hyre_index_options* opts,
+                              hyre_index** out);
+void hyre_index_destroy(hyre_index* ix);
+hyre_status hyre_index_stats_get(const hyre_index* ix, hyre_index_stats* out);
+
+/* ------------------------------------------------------------------------
+ * Executor (pipeline.hpp:69-96)
+ * ------------------------------------------------------------------------ */
+typedef struct hyre_executor hyre_executor;
+
+/* Executor(index, max_batch): owns a CUDA stream and all device scratch,
+ * sized once here (pipeline.cpp:95-106). */
+hyre_status hyre_executor_create(hyre_index* ix, uint32_t max_batch, hyre_executor** out);
+void hyre_executor_destroy(hyre_executor* ex);
+void* hyre_executor_stream(hyre_executor* ex); /* cudaStream_t */
+
+/* Executor::execute (pipeline.cpp:108-145).  hits needs min(k, num_docs)
+ * entries; *n_hits receives the hit count. */
+hyre_status hyre_execute(hyre_executor* ex, const hyre_query* q, hyre_hit* hits,
+                         uint32_t* n_hits, hyre_timings* timings);
+
+/* Executor::execute_batch (pipeline.cpp:147-281).  Hits of slot i are written
+ * at hits + hit_offsets[i] (caller-chosen, room for min(k_i, num_docs)).
+ * statuses[i] = HYRE_OK or HYRE_INVALID_ARGUMENT (message via
+ * hyre_executor_slot_error); empty batch / b > max_batch fail the call. */
+hyre_status hyre_execute_batch(hyre_executor* ex, const hyre_query* qs, uint32_t b,
+                               hyre_hit* hits, const uint64_t* hit_offsets, uint32_t* counts,
+                               int32_t* statuses, hyre_timings* timings);
+const char* hyre_executor_slot_error(const hyre_executor* ex, uint32_t slot);
+
+/* Split form of execute_batch for device-resident timing: prepare validates
+ * and uploads the batch, run enqueues the kernels on the executor stream
+ * without any host synchronisation, fetch synchronises and copies results
+ * out (same layout as hyre_execute_batch).  run may be repeated. */
+hyre_status hyre_batch_prepare(hyre_executor* ex, const hyre_query* qs, uint32_t b);
+hyre_status hyre_batch_run(hyre_executor* ex);
+hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* hit_offsets,
+                             uint32_t* counts, int32_t* statuses, hyre_timings* timings);
+/* Number of kernels the last hyre_batch_run enqueued. */
+uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
+
+/* Stage entry points (public in the reference and used by its tests). */
+/* full_scan_tbr (term_match.hpp:43-45): ascending eligible rows (global ids). */
+hyre_status hyre_full_scan_tbr(hyre_executor* ex, const hyre_query* q, uint32_t* rows,
+                               uint64_t cap, uint64_t* n);
+/* exact_scores (knn.hpp:24-26) over explicit global rows. */
+hyre_status hyre_exact_scores(hyre_executor* ex, const float* q, uint32_t dim,
+                              const uint32_t* rows, uint64_t n, float* scores,
+                              int32_t* renormalized);
+/* bucket_top_k (knn.hpp:33-35) over explicit (row, score) messengers. */
+hyre_status hyre_bucket_top_k(hyre_executor* ex, const uint32_t* rows, const float* scores,
+                              uint64_t n, uint32_t k, uint32_t granularity, hyre_hit* out,
+                              uint32_t* n_out);
+/* preselect (quantizer.hpp:71-74) over explicit global rows (ascending). */
+hyre_status hyre_preselect(hyre_executor* ex, const uint64_t* query_words, const uint32_t* rows,
+                           uint64_t n, uint32_t quant_k, uint32_t* rows_out, uint64_t* n_out);
+
+/* Exact merge of per-shard top-K lists (multi-GPU): lists[i] has
+ * counts[i] hits sorted by (score desc, row asc); writes min(k, total). */
+hyre_status hyre_merge_topk(const hyre_hit* const* lists, const uint32_t* counts, uint32_t n_lists,
+                            uint32_t k, hyre_hit* out, uint32_t* n_out);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#endif  /* HYRE_B200_H_ */

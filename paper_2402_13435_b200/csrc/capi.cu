@@ -1,0 +1,423 @@
+// extern "C" entry points declared in include/hyre_b200.h.  Each wraps the
+// C++ layer, maps exceptions to hyre_status and records the message in a
+// thread-local buffer (hyre_last_error).
+#include <chrono>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <string>
+
+#include "executor.cuh"
+#include "hyre_b200.h"
+
+using namespace hyreb;
+
+struct hyre_builder {
+  Builder b;
+};
+struct hyre_frozen {
+  std::unique_ptr<Frozen> f;
+};
+struct hyre_index {
+  std::unique_ptr<DevIndex> ix;
+};
+struct hyre_executor {
+  std::unique_ptr<Executor> ex;
+};
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_cause = -1;
+
+template <class F>
+hyre_status guard(F&& fn) {
+  try {
+    fn();
+    return HYRE_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_cause = e.load_cause;
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return HYRE_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HYRE_INTERNAL;
+  }
+}
+void need(const void* p, const char* what) {
+  if (!p) throw Error(HYRE_INVALID_ARGUMENT, std::string(what) + " must not be null");
+}
+}  // namespace
+
+extern "C" {
+
+const char* hyre_last_error(void) { return g_err.c_str(); }
+int hyre_last_load_cause(void) { return g_cause; }
+int hyre_abi_version(void) { return HYRE_B200_ABI_VERSION; }
+
+// ---- builder / frozen ------------------------------------------------------
+hyre_status hyre_builder_create(uint32_t num_clauses, uint32_t max_num_attr, uint32_t dim,
+                                const char* const* clause_names, uint32_t num_names,
+                                hyre_builder** out) {
+  return guard([&] {
+    need(out, "out");
+    std::vector<std::string> names;
+    if (clause_names)
+      for (uint32_t i = 0; i < num_names; ++i) names.emplace_back(clause_names[i]);
+    *out = new hyre_builder{Builder(num_clauses, max_num_attr, dim, std::move(names))};
+  });
+}
+
+void hyre_builder_destroy(hyre_builder* b) { delete b; }
+
+hyre_status hyre_builder_add_document(hyre_builder* b, const char* doc_id, uint32_t num_slots,
+                                      const uint32_t* slot_offsets, const uint32_t* ids,
+                                      const float* embedding, uint32_t embedding_len,
+                                      uint32_t* row_out) {
+  return guard([&] {
+    need(b, "builder");
+    need(doc_id, "doc_id");
+    const uint32_t r = b->b.add(doc_id, num_slots, slot_offsets, ids, embedding, embedding_len);
+    if (row_out) *row_out = r;
+  });
+}
+
+hyre_status hyre_builder_add_documents(hyre_builder* b, uint32_t n, const char* prefix,
+                                       const uint64_t* slot_offsets, const uint32_t* ids,
+                                       const float* embeddings) {
+  return guard([&] {
+    need(b, "builder");
+    if (n == 0) return;
+    need(slot_offsets, "slot_offsets");
+    need(embeddings, "embeddings");
+    b->b.add_bulk(n, prefix ? prefix : "", slot_offsets, ids, embeddings);
+  });
+}
+
+uint32_t hyre_builder_size(const hyre_builder* b) { return b ? b->b.size() : 0; }
+
+hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t seed, hyre_frozen** out) {
+  return guard([&] {
+    need(b, "builder");
+    need(out, "out");
+    *out = new hyre_frozen{std::unique_ptr<Frozen>(b->b.freeze(num_bits, seed))};
+  });
+}
+
+hyre_status hyre_frozen_from_arrays(uint32_t num_docs, uint32_t num_clauses, uint32_t max_num_attr,
+                                    uint32_t dim, uint32_t num_bits, uint64_t seed,
+                                    const uint32_t* attributes, const uint32_t* offsets,
+                                    const float* embeddings, const uint64_t* signatures,
+                                    const uint8_t* zero_flags, const char* const* doc_ids,
+                                    const char* doc_id_prefix, hyre_frozen** out) {
+  return guard([&] {
+    need(out, "out");
+    need(attributes, "attributes");
+    need(offsets, "offsets");
+    need(embeddings, "embeddings");
+    if (num_docs == 0) validation("no documents staged");
+    if (num_clauses == 0) validation("numClauses must be >= 1");
+    if (dim == 0) validation("dim must be >= 1");
+    if (max_num_attr == 0) validation("maxNumAttr must be >= 1");
+    std::unique_ptr<Frozen> f(new Frozen);
+    f->num_docs = num_docs;
+    f->num_clauses = num_clauses;
+    f->max_num_attr = max_num_attr;
+    f->dim = dim;
+    f->num_bits = num_bits;
+    f->seed = seed;
+    Codec codec = make_codec(dim, num_bits, seed);
+    const size_t n = num_docs, nw = codec.num_words();
+    f->attributes.assign(attributes, attributes + n * max_num_attr);
+    f->offsets.assign(offsets, offsets + n * (num_clauses + 1));
+    f->embeddings.assign(embeddings, embeddings + n * dim);
+    if (signatures) {
+      f->signatures.assign(signatures, signatures + n * nw);
+    } else {
+      f->signatures.assign(n * nw, 0);
+      parallel_for(n, 4096, [&](size_t b0, size_t e0) {
+        for (size_t r = b0; r < e0; ++r)
+          encode(codec, f->embeddings.data() + r * dim, f->signatures.data() + r * nw);
+      });
+    }
+    if (zero_flags) {
+      f->zero.assign(zero_flags, zero_flags + n);
+    } else {
+      f->zero.assign(n, 0);
+      for (size_t r = 0; r < n; ++r) {
+        bool z = true;
+        for (uint32_t d = 0; d < dim && z; ++d) z = f->embeddings[r * dim + d] == 0.0f;
+        f->zero[r] = z;
+      }
+    }
+    f->doc_ids.resize(n);
+    const std::string prefix = doc_id_prefix ? doc_id_prefix : "";
+    for (size_t r = 0; r < n; ++r) f->doc_ids[r] = doc_ids ? std::string(doc_ids[r]) : prefix + std::to_string(r);
+    for (uint32_t c = 0; c < num_clauses; ++c) f->clause_names.push_back("c" + std::to_string(c));
+    *out = new hyre_frozen{std::move(f)};
+  });
+}
+
+hyre_status hyre_frozen_save(const hyre_frozen* f, const char* path) {
+  return guard([&] {
+    need(f, "frozen");
+    need(path, "path");
+    save(*f->f, path);
+  });
+}
+
+hyre_status hyre_frozen_load(const char* path, hyre_frozen** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = new hyre_frozen{std::unique_ptr<Frozen>(load(path))};
+  });
+}
+
+void hyre_frozen_destroy(hyre_frozen* f) { delete f; }
+
+void hyre_frozen_shape(const hyre_frozen* f, hyre_shape* s) {
+  s->num_docs = f->f->num_docs;
+  s->num_clauses = f->f->num_clauses;
+  s->max_num_attr = f->f->max_num_attr;
+  s->dim = f->f->dim;
+  s->num_bits = f->f->num_bits;
+  s->num_words = static_cast<uint32_t>(f->f->num_words());
+  s->seed = f->f->seed;
+}
+
+const uint32_t* hyre_frozen_attributes(const hyre_frozen* f) { return f->f->attributes.data(); }
+const uint32_t* hyre_frozen_offsets(const hyre_frozen* f) { return f->f->offsets.data(); }
+const float* hyre_frozen_embeddings(const hyre_frozen* f) { return f->f->embeddings.data(); }
+const uint64_t* hyre_frozen_signatures(const hyre_frozen* f) { return f->f->signatures.data(); }
+const uint8_t* hyre_frozen_zero_flags(const hyre_frozen* f) { return f->f->zero.data(); }
+const char* hyre_frozen_doc_id(const hyre_frozen* f, uint32_t row) {
+  return row < f->f->doc_ids.size() ? f->f->doc_ids[row].c_str() : nullptr;
+}
+int64_t hyre_frozen_row_of(const hyre_frozen* f, const char* doc_id) { return f->f->row_of(doc_id); }
+int32_t hyre_frozen_resolve_clause_slot(const hyre_frozen* f, const char* name) {
+  for (uint32_t c = 0; c < f->f->num_clauses; ++c)
+    if (f->f->clause_names[c] == name) return static_cast<int32_t>(c);
+  return -1;
+}
+const char* hyre_frozen_clause_name(const hyre_frozen* f, uint32_t slot) {
+  return slot < f->f->clause_names.size() ? f->f->clause_names[slot].c_str() : nullptr;
+}
+
+// ---- codec -------------------------------------------------------------------
+hyre_status hyre_encode(uint32_t dim, uint32_t num_bits, uint64_t seed, const float* x, uint64_t* words) {
+  return guard([&] {
+    need(x, "x");
+    need(words, "words");
+    Codec c = make_codec(dim, num_bits, seed);
+    encode(c, x, words);
+  });
+}
+
+uint32_t hyre_quant_score_words(const uint64_t* a, const uint64_t* b, uint32_t num_words, uint32_t num_bits) {
+  return quant_score_words(a, b, num_words, num_bits);
+}
+
+// ---- queries -------------------------------------------------------------------
+hyre_status hyre_normalize_query(uint32_t n_raw, const uint32_t* raw_slots, const uint32_t* raw_offsets,
+                                 const uint32_t* raw_ids, uint32_t num_clauses, uint32_t* out_n,
+                                 uint32_t* out_slots, uint32_t* out_offsets, uint32_t* out_ids) {
+  return guard([&] {
+    // std::map iteration = ascending slot, as term_match.cpp:10 walks the map.
+    std::map<uint32_t, std::vector<uint32_t>> raw;
+    for (uint32_t i = 0; i < n_raw; ++i)
+      raw[raw_slots[i]].assign(raw_ids + raw_offsets[i], raw_ids + raw_offsets[i + 1]);
+    uint32_t n = 0, pos = 0;
+    out_offsets[0] = 0;
+    for (auto& [slot, ids] : raw) {
+      if (slot >= num_clauses)
+        validation("unknown clause slot " + std::to_string(slot) + " (index has " +
+                   std::to_string(num_clauses) + ")");
+      for (auto id : ids)
+        if (id == 0) validation("attribute id 0 is reserved for padding");
+      std::sort(ids.begin(), ids.end());
+      ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+      if (ids.empty()) continue;  // no constraint on this slot (term_match.cpp:26)
+      out_slots[n] = slot;
+      for (auto id : ids) out_ids[pos++] = id;
+      out_offsets[++n] = pos;
+    }
+    *out_n = n;
+  });
+}
+
+hyre_status hyre_validate_query(const hyre_frozen* f, const hyre_query* q) {
+  return guard([&] {
+    need(f, "frozen");
+    need(q, "query");
+    validate_query(QueryShape{f->f->num_clauses, f->f->dim}, *q);
+  });
+}
+
+// ---- device index ----------------------------------------------------------------
+hyre_status hyre_index_create(const hyre_frozen* f, const hyre_index_options* opts, hyre_index** out) {
+  return guard([&] {
+    need(f, "frozen");
+    need(out, "out");
+    hyre_index_options o{};
+    if (opts) o = *opts;
+    *out = new hyre_index{std::unique_ptr<DevIndex>(build_device_index(*f->f, o))};
+  });
+}
+
+void hyre_index_destroy(hyre_index* ix) { delete ix; }
+
+hyre_status hyre_index_stats_get(const hyre_index* ix, hyre_index_stats* out) {
+  return guard([&] {
+    need(ix, "index");
+    need(out, "out");
+    *out = ix->ix->stats;
+  });
+}
+
+// ---- executor ------------------------------------------------------------------
+hyre_status hyre_executor_create(hyre_index* ix, uint32_t max_batch, hyre_executor** out) {
+  return guard([&] {
+    need(ix, "index");
+    need(out, "out");
+    *out = new hyre_executor{std::unique_ptr<Executor>(new Executor(ix->ix.get(), max_batch))};
+  });
+}
+
+void hyre_executor_destroy(hyre_executor* ex) { delete ex; }
+void* hyre_executor_stream(hyre_executor* ex) { return ex ? ex->ex->st : nullptr; }
+
+hyre_status hyre_execute(hyre_executor* ex, const hyre_query* q, hyre_hit* hits, uint32_t* n_hits,
+                         hyre_timings* timings) {
+  return guard([&] {
+    need(ex, "executor");
+    need(q, "query");
+    const auto t0 = std::chrono::steady_clock::now();
+    ex->ex->prepare(q, 1);
+    if (ex->ex->statuses[0] != HYRE_OK)
+      throw Error(static_cast<hyre_status>(ex->ex->statuses[0]), ex->ex->slot_errors[0]);
+    ex->ex->run();
+    const uint64_t off = 0;
+    uint32_t cnt = 0;
+    int32_t stt = 0;
+    ex->ex->fetch(hits, &off, &cnt, &stt, timings);
+    if (n_hits) *n_hits = cnt;
+    if (timings)
+      timings->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+hyre_status hyre_execute_batch(hyre_executor* ex, const hyre_query* qs, uint32_t b, hyre_hit* hits,
+                               const uint64_t* hit_offsets, uint32_t* counts, int32_t* statuses,
+                               hyre_timings* timings) {
+  return guard([&] {
+    need(ex, "executor");
+    const auto t0 = std::chrono::steady_clock::now();
+    ex->ex->prepare(qs, b);
+    ex->ex->run();
+    ex->ex->fetch(hits, hit_offsets, counts, statuses, timings);
+    if (timings)
+      timings->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+const char* hyre_executor_slot_error(const hyre_executor* ex, uint32_t slot) {
+  if (!ex || slot >= ex->ex->slot_errors.size()) return "";
+  return ex->ex->slot_errors[slot].c_str();
+}
+
+hyre_status hyre_batch_prepare(hyre_executor* ex, const hyre_query* qs, uint32_t b) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->prepare(qs, b);
+  });
+}
+
+hyre_status hyre_batch_run(hyre_executor* ex) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->run();
+  });
+}
+
+hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* hit_offsets, uint32_t* counts,
+                             int32_t* statuses, hyre_timings* timings) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->fetch(hits, hit_offsets, counts, statuses, timings);
+  });
+}
+
+uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
+
+hyre_status hyre_full_scan_tbr(hyre_executor* ex, const hyre_query* q, uint32_t* rows, uint64_t cap,
+                               uint64_t* n) {
+  return guard([&] {
+    need(ex, "executor");
+    need(q, "query");
+    *n = ex->ex->full_scan(*q, rows, cap);
+  });
+}
+
+hyre_status hyre_exact_scores(hyre_executor* ex, const float* q, uint32_t dim, const uint32_t* rows,
+                              uint64_t n, float* scores, int32_t* renormalized) {
+  return guard([&] {
+    need(ex, "executor");
+    need(q, "query");
+    const bool r = ex->ex->exact_scores(q, dim, rows, n, scores);
+    if (renormalized) *renormalized = r;
+  });
+}
+
+hyre_status hyre_bucket_top_k(hyre_executor* ex, const uint32_t* rows, const float* scores, uint64_t n,
+                              uint32_t k, uint32_t granularity, hyre_hit* out, uint32_t* n_out) {
+  return guard([&] {
+    need(ex, "executor");
+    if (k < 1) validation("k must be >= 1");
+    if (granularity < 1) validation("granularity must be >= 1");
+    for (uint64_t i = 0; i < n; ++i)  // knn.cpp:59-61
+      if (scores[i] < -1.0f || scores[i] > 1.0f)
+        throw Error(HYRE_OUT_OF_RANGE,
+                    "score " + std::to_string(scores[i]) + " outside the documented [-1, 1] bounds");
+    *n_out = ex->ex->top_k(rows, scores, n, k, out);
+  });
+}
+
+hyre_status hyre_preselect(hyre_executor* ex, const uint64_t* query_words, const uint32_t* rows, uint64_t n,
+                           uint32_t quant_k, uint32_t* rows_out, uint64_t* n_out) {
+  return guard([&] {
+    need(ex, "executor");
+    *n_out = ex->ex->preselect(query_words, rows, n, quant_k, rows_out);
+  });
+}
+
+hyre_status hyre_merge_topk(const hyre_hit* const* lists, const uint32_t* counts, uint32_t n_lists, uint32_t k,
+                            hyre_hit* out, uint32_t* n_out) {
+  return guard([&] {
+    // K-way merge by the orderable key (score desc, row asc); lists are short.
+    std::vector<uint32_t> pos(n_lists, 0);
+    uint32_t m = 0;
+    while (m < k) {
+      int best = -1;
+      uint64_t bk = 0;
+      for (uint32_t l = 0; l < n_lists; ++l) {
+        if (pos[l] >= counts[l]) continue;
+        const hyre_hit& h = lists[l][pos[l]];
+        const uint64_t key = make_key(h.score + 0.0f, h.row);
+        if (best < 0 || key > bk) {
+          best = static_cast<int>(l);
+          bk = key;
+        }
+      }
+      if (best < 0) break;
+      out[m++] = lists[best][pos[best]++];
+    }
+    *n_out = m;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,512 @@
+// Executor: the B200 replacement for hyre::Executor (pipeline.hpp:69-96,
+// pipeline.cpp:95-281).  Host work per batch is validation, query
+// normalisation (double, like pipeline.cpp:19-28), term-dictionary lookups and
+// one packed H2D copy; everything else is a fixed kernel sequence on the
+// executor's stream:
+//
+//   [scatter CSR clauses] -> K1 mask -> [K6 quant] ->
+//   K2 sample pass -> K4 K-th (threshold) -> K2/K3 main pass -> K4 final
+//   -> K2 rerun + K4 (no-op unless a candidate buffer overflowed)
+//   -> K5 first-K (term-only queries)
+//
+// All device scratch is sized at construction (pipeline.cpp:95-106's
+// "pre-allocated" policy); only the per-batch program blob and the hit
+// buffer grow, and only when a batch needs more than any earlier one.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <unordered_map>
+
+#include "executor.cuh"
+#include "kernels.cuh"
+
+namespace hyreb {
+
+namespace {
+template <class T>
+T* dmalloc(size_t n) {
+  T* p = nullptr;
+  if (n) HYRE_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
+  if (max_batch < 1) validation("maxBatch must be >= 1");
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  HYRE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (auto& e : ev) HYRE_CUDA(cudaEventCreate(&e));
+  const size_t B = max_batch;
+  cap = 65536;
+  samp_cap = 65536;
+  d_mask = dmalloc<uint32_t>(B * ix->words);
+  d_chunk_cnt = dmalloc<uint32_t>(B * ix->n_chunks);
+  d_counters = dmalloc<uint32_t>(B * kNumCounters);
+  d_thr = dmalloc<uint64_t>(B);
+  d_cand = dmalloc<uint64_t>(B * cap);
+  d_samp = dmalloc<uint64_t>(B * samp_cap);
+  d_qhist = dmalloc<uint32_t>(B * (ix->num_bits + 1));
+  d_tsel = dmalloc<uint32_t>(B * 3);
+  d_eqcnt = dmalloc<uint32_t>(B * ix->n_chunks);
+  h_out_cnt.resize(B);
+  h_rerun.resize(B);
+}
+
+Executor::~Executor() {
+  cudaSetDevice(ix->device);
+  cudaStreamSynchronize(st);
+  for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_cand,
+                  (void*)d_samp, (void*)d_qhist, (void*)d_tsel, (void*)d_eqcnt, (void*)d_blob,
+                  (void*)d_hits, (void*)d_scratch})
+    cudaFree(p);
+  if (h_blob) cudaFreeHost(h_blob);
+  if (h_hits) cudaFreeHost(h_hits);
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(st);
+}
+
+void Executor::ensure_blob(size_t bytes) {
+  if (bytes <= blob_cap) return;
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_blob);
+  if (h_blob) cudaFreeHost(h_blob);
+  blob_cap = std::max(bytes, blob_cap * 2);
+  d_blob = dmalloc<uint8_t>(blob_cap);
+  HYRE_CUDA(cudaMallocHost(&h_blob, blob_cap));
+}
+
+void Executor::ensure_hits(size_t n) {
+  n = std::max<size_t>(n, 1);
+  if (n <= hits_cap) return;
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_hits);
+  if (h_hits) cudaFreeHost(h_hits);
+  hits_cap = std::max(n, hits_cap * 2);
+  d_hits = dmalloc<hyre_hit>(hits_cap);
+  HYRE_CUDA(cudaMallocHost(&h_hits, hits_cap * sizeof(hyre_hit)));
+}
+
+void Executor::ensure_scratch(uint32_t n_bitmaps) {
+  if (n_bitmaps <= scratch_cap) return;
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_scratch);
+  scratch_cap = std::max(n_bitmaps, scratch_cap * 2);
+  d_scratch = dmalloc<uint32_t>(size_t{scratch_cap} * ix->words);
+}
+
+// ---------------------------------------------------------------------------
+// prepare: validation + program construction + one packed H2D copy.
+// ---------------------------------------------------------------------------
+void Executor::prepare(const hyre_query* qs, uint32_t b) {
+  if (b < 1) validation("batch must contain at least one query");
+  if (b > max_batch)
+    validation("batch size " + std::to_string(b) + " exceeds maxBatch " + std::to_string(max_batch));
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  B = b;
+  const uint32_t dp = ix->dp, nw = ix->num_words, W = ix->words;
+  const QueryShape shape{ix->num_clauses, ix->dim};
+  qp.assign(b, QParam{});
+  prog.clear();
+  refs.clear();
+  items.clear();
+  item_prefix.clear();
+  statuses.assign(b, HYRE_OK);
+  slot_errors.assign(b, std::string());
+  hit_off.assign(b, 0);
+  qvec.assign(size_t{b} * dp, 0.0f);
+  qsig.assign(size_t{b} * nw, 0ull);
+  any_emb = any_term_only = any_quant = false;
+  max_k = 1;
+  uint32_t n_scratch = 0;
+  std::unordered_map<uint32_t, uint32_t> bitmap_ref;  // bitmap index -> ref slot
+  std::vector<std::pair<uint32_t, uint32_t>> ref_src;  // (kind 0 bitmap / 1 scratch, index)
+  uint64_t total_hits = 0;
+  for (uint32_t i = 0; i < b; ++i) {
+    const hyre_query& q = qs[i];
+    try {
+      validate_query(shape, q);
+    } catch (const Error& e) {
+      statuses[i] = e.code;
+      slot_errors[i] = e.what();
+      continue;
+    }
+    QParam p{};
+    p.flags = QF_ACTIVE;
+    p.k = std::min(q.k, ix->n_rows);
+    max_k = std::max(max_k, p.k);
+    p.quant_k = q.quant_k != 0 ? q.quant_k : 200u * q.k;
+    if (q.embedding) {
+      p.flags |= QF_EMB;
+      any_emb = true;
+      unit_embedding(q.embedding, ix->dim, qvec.data() + size_t{i} * dp);
+      if (q.quant_enabled) {
+        p.flags |= QF_QUANT;
+        any_quant = true;
+        encode(ix->codec, qvec.data() + size_t{i} * dp, qsig.data() + size_t{i} * nw);
+      }
+    } else {
+      any_term_only = true;
+    }
+    if (q.n_clauses == 0) {
+      p.flags |= QF_MATCH_ALL;
+    } else {
+      p.prog_off = static_cast<uint32_t>(prog.size());
+      prog.push_back(q.n_clauses);
+      bool empty = false;
+      for (uint32_t c = 0; c < q.n_clauses && !empty; ++c) {
+        const uint64_t slot = q.slots[c];
+        const size_t len_at = prog.size();
+        prog.push_back(0);
+        uint32_t scratch_for_clause = UINT32_MAX;
+        for (uint32_t j = q.id_offsets[c]; j < q.id_offsets[c + 1]; ++j) {
+          auto it = ix->terms.find((slot << 32) | q.ids[j]);
+          if (it == ix->terms.end()) continue;  // id absent from the index: matches no row
+          const Term& t = it->second;
+          if (t.bitmap != UINT32_MAX) {
+            auto r = bitmap_ref.find(t.bitmap);
+            uint32_t ref;
+            if (r == bitmap_ref.end()) {
+              ref = static_cast<uint32_t>(ref_src.size());
+              ref_src.push_back({0u, t.bitmap});
+              bitmap_ref.emplace(t.bitmap, ref);
+            } else {
+              ref = r->second;
+            }
+            prog.push_back(ref);
+          } else {
+            if (scratch_for_clause == UINT32_MAX) {
+              scratch_for_clause = n_scratch++;
+              const uint32_t ref = static_cast<uint32_t>(ref_src.size());
+              ref_src.push_back({1u, scratch_for_clause});
+              prog.push_back(ref);
+            }
+            item_prefix.push_back(items.empty() ? 0 : item_prefix.back() + items.back().count);
+            items.push_back({t.begin, t.df, scratch_for_clause});
+          }
+        }
+        prog[len_at] = static_cast<uint32_t>(prog.size() - len_at - 1);
+        if (prog[len_at] == 0) empty = true;
+      }
+      if (empty) p.flags |= QF_EMPTY;
+    }
+    qp[i] = p;
+    hit_off[i] = total_hits;
+    total_hits += p.k;
+  }
+  scatter_total = items.empty() ? 0 : item_prefix.back() + items.back().count;
+  n_scratch_used = n_scratch;
+  ensure_scratch(n_scratch);
+  ensure_hits(total_hits);
+  n_hits_total = total_hits;
+  refs.resize(ref_src.size());
+  for (size_t r = 0; r < ref_src.size(); ++r)
+    refs[r] = ref_src[r].first == 0 ? ix->bitmaps + size_t{ref_src[r].second} * W
+                                    : d_scratch + size_t{ref_src[r].second} * W;
+  // sampling period: sampled survivors ~ k * period must fit the candidate buffer
+  uint32_t period = 1;
+  while (period < 256 && uint64_t{period} * 2 * max_k * 4 <= cap) period *= 2;
+  sample_period = period;
+
+  // ---- pack and upload ----------------------------------------------------
+  size_t off = 0;
+  auto place = [&](size_t bytes) {
+    off = align_up(off, 256);
+    const size_t at = off;
+    off += bytes;
+    return at;
+  };
+  const size_t o_qp = place(b * sizeof(QParam));
+  const size_t o_q = place(qvec.size() * 4);
+  const size_t o_qsig = place(qsig.size() * 8);
+  const size_t o_off = place(b * 8);
+  const size_t o_prog = place(std::max<size_t>(prog.size(), 1) * 4);
+  const size_t o_refs = place(std::max<size_t>(refs.size(), 1) * sizeof(void*));
+  const size_t o_items = place(std::max<size_t>(items.size(), 1) * sizeof(ScatterItem));
+  const size_t o_ipre = place(std::max<size_t>(item_prefix.size(), 1) * 8);
+  ensure_blob(off);
+  std::memcpy(h_blob + o_qp, qp.data(), b * sizeof(QParam));
+  std::memcpy(h_blob + o_q, qvec.data(), qvec.size() * 4);
+  std::memcpy(h_blob + o_qsig, qsig.data(), qsig.size() * 8);
+  std::memcpy(h_blob + o_off, hit_off.data(), b * 8);
+  if (!prog.empty()) std::memcpy(h_blob + o_prog, prog.data(), prog.size() * 4);
+  if (!refs.empty()) std::memcpy(h_blob + o_refs, refs.data(), refs.size() * sizeof(void*));
+  if (!items.empty()) {
+    std::memcpy(h_blob + o_items, items.data(), items.size() * sizeof(ScatterItem));
+    std::memcpy(h_blob + o_ipre, item_prefix.data(), item_prefix.size() * 8);
+  }
+  HYRE_CUDA(cudaMemcpyAsync(d_blob, h_blob, off, cudaMemcpyHostToDevice, st));
+  h2d_bytes = off;
+  d_qp = reinterpret_cast<QParam*>(d_blob + o_qp);
+  d_q = reinterpret_cast<float*>(d_blob + o_q);
+  d_qsig = reinterpret_cast<uint64_t*>(d_blob + o_qsig);
+  d_hit_off = reinterpret_cast<uint64_t*>(d_blob + o_off);
+  d_prog = reinterpret_cast<uint32_t*>(d_blob + o_prog);
+  d_refs = reinterpret_cast<const uint32_t* const*>(d_blob + o_refs);
+  d_items = reinterpret_cast<ScatterItem*>(d_blob + o_items);
+  d_ipre = reinterpret_cast<uint64_t*>(d_blob + o_ipre);
+  prepared = true;
+}
+
+// ---------------------------------------------------------------------------
+// run: the fixed kernel sequence, no host synchronisation.
+// ---------------------------------------------------------------------------
+void Executor::run() {
+  if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_run before hyre_batch_prepare");
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  kernels = 0;
+  const uint32_t W = ix->words;
+  uint32_t* n_elig = d_counters;
+  uint32_t* cand_cnt = d_counters + max_batch;
+  uint32_t* samp_cnt = d_counters + 2 * max_batch;
+  uint32_t* out_cnt = d_counters + 3 * max_batch;
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  HYRE_CUDA(cudaEventRecord(ev[0], st));
+  HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
+  if (scatter_total) {
+    HYRE_CUDA(cudaMemsetAsync(d_scratch, 0, size_t{n_scratch_used} * W * 4, st));
+    launch_scatter(d_items, d_ipre, static_cast<uint32_t>(items.size()), scatter_total, ix->post_rows,
+                   d_scratch, W, st);
+    ++kernels;
+  }
+  MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
+              d_mask, d_chunk_cnt, n_elig};
+  launch_mask(ma, st);
+  ++kernels;
+  HYRE_CUDA(cudaEventRecord(ev[1], st));
+  if (any_quant) {
+    HYRE_CUDA(cudaMemsetAsync(d_qhist, 0, sizeof(uint32_t) * B * (ix->num_bits + 1), st));
+    QuantArgs qa{ix->sigs, ix->num_words, ix->num_bits, d_qsig, d_qp, B, W, ix->n_chunks, ix->n_rows,
+                 d_mask, d_chunk_cnt, n_elig, d_qhist, d_tsel, d_eqcnt};
+    launch_quant(qa, st);
+    kernels += 5;
+  }
+  HYRE_CUDA(cudaEventRecord(ev[2], st));
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
+  const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
+  if (any_emb) {
+    ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, W, d_mask, d_qp, d_q, B, n_elig,
+                 d_thr, d_cand, cand_cnt, cap, SCORE_MAIN, sample_period, cap, rerun};
+    if (ix->n_rows > cap) {
+      ScoreArgs ss = sa;
+      ss.mode = SCORE_SAMPLE;
+      ss.cand = d_samp;
+      ss.cand_cnt = samp_cnt;
+      ss.cap = samp_cap;
+      launch_score(ss, bf16, st);
+      SelectArgs ka{d_samp, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
+                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap};
+      launch_select(ka, st);
+      kernels += 2;
+    } else {
+      HYRE_CUDA(cudaMemsetAsync(d_thr, 0, sizeof(uint64_t) * B, st));
+    }
+    launch_score(sa, bf16, st);
+    ++kernels;
+    HYRE_CUDA(cudaEventRecord(ev[3], st));
+    SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap};
+    launch_select(fa, st);
+    ++kernels;
+    // One speculative recovery round: no-op unless a candidate buffer overflowed.
+    HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
+    ScoreArgs ra = sa;
+    ra.mode = SCORE_RERUN;
+    launch_score(ra, bf16, st);
+    fa.mode = SELECT_FINAL_RERUN;
+    launch_select(fa, st);
+    kernels += 2;
+  } else {
+    HYRE_CUDA(cudaEventRecord(ev[3], st));
+  }
+  if (any_term_only) {
+    FirstKArgs fk{d_mask, d_chunk_cnt, n_elig, d_qp, B, W, ix->n_chunks, ix->row_base, d_hit_off, d_hits,
+                  out_cnt, nullptr, 0, 0};
+    launch_first_k(fk, st);
+    ++kernels;
+  }
+  HYRE_CUDA(cudaEventRecord(ev[4], st));
+  HYRE_CUDA(cudaGetLastError());
+}
+
+// Resolve any candidate-buffer overflow left after the speculative round.
+void Executor::finish_reruns() {
+  uint32_t* n_elig = d_counters;
+  uint32_t* cand_cnt = d_counters + max_batch;
+  uint32_t* out_cnt = d_counters + 3 * max_batch;
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
+  const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
+  for (int round = 0; round < 64; ++round) {
+    HYRE_CUDA(cudaMemcpyAsync(h_rerun.data(), rerun, B * 4, cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    bool any = false;
+    for (uint32_t i = 0; i < B; ++i) any |= h_rerun[i] != 0;
+    if (!any) return;
+    HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
+    ScoreArgs ra{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
+                 d_thr, d_cand, cand_cnt, cap, SCORE_RERUN, sample_period, cap, rerun};
+    launch_score(ra, bf16, st);
+    SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap};
+    launch_select(fa, st);
+  }
+  throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");
+}
+
+void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* st_out,
+                     hyre_timings* t) {
+  if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_fetch before hyre_batch_prepare");
+  if (any_emb) finish_reruns();
+  uint32_t* out_cnt = d_counters + 3 * max_batch;
+  HYRE_CUDA(cudaMemcpyAsync(h_out_cnt.data(), out_cnt, B * 4, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaMemcpyAsync(h_hits, d_hits, n_hits_total * sizeof(hyre_hit), cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  d2h_bytes = B * 4 + n_hits_total * sizeof(hyre_hit);
+  for (uint32_t i = 0; i < B; ++i) {
+    if (st_out) st_out[i] = statuses[i];
+    const uint32_t c = statuses[i] == HYRE_OK ? h_out_cnt[i] : 0u;
+    if (counts) counts[i] = c;
+    if (hits && c) std::memcpy(hits + offsets[i], h_hits + hit_off[i], c * sizeof(hyre_hit));
+  }
+  if (t) {
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    cudaEventElapsedTime(&d, ev[3], ev[4]);
+    t->tbr_ms = a;
+    t->quant_ms = b;
+    t->ebr_ms = c;
+    t->topk_ms = d;
+  }
+}
+
+float Executor::last_run_ms() const {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev[0], ev[4]);
+  return ms;
+}
+
+// ---------------------------------------------------------------------------
+// Stage functions
+// ---------------------------------------------------------------------------
+uint64_t Executor::full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows) {
+  hyre_query t = q;
+  t.embedding = nullptr;
+  t.k = 1;
+  t.granularity = 100;
+  prepare(&t, 1);
+  if (statuses[0] != HYRE_OK) throw Error(static_cast<hyre_status>(statuses[0]), slot_errors[0]);
+  run();
+  uint32_t ne = 0;
+  HYRE_CUDA(cudaMemcpyAsync(&ne, d_counters, 4, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  const uint64_t take = std::min<uint64_t>(ne, cap_rows);
+  if (take) {
+    uint32_t* d_rows = dmalloc<uint32_t>(take);
+    FirstKArgs fk{d_mask, d_chunk_cnt, d_counters, d_qp, 1, ix->words, ix->n_chunks, ix->row_base, d_hit_off,
+                  nullptr, nullptr, d_rows, take, 1};
+    launch_first_k(fk, st);
+    HYRE_CUDA(cudaMemcpyAsync(rows, d_rows, take * 4, cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_rows);
+  }
+  return ne;
+}
+
+bool Executor::exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out) {
+  if (dim != ix->dim)
+    validation("query embedding dim " + std::to_string(dim) + " != index dim " + std::to_string(ix->dim));
+  for (uint64_t i = 0; i < n; ++i)
+    if (rows[i] < ix->row_base || rows[i] >= ix->row_base + ix->n_rows)
+      validation("row " + std::to_string(rows[i]) + " outside this index shard");
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  std::vector<float> unit(ix->dp, 0.0f);
+  const bool ren = unit_embedding(q, dim, unit.data());
+  float* d_qv = dmalloc<float>(ix->dp);
+  uint32_t* d_rows = dmalloc<uint32_t>(std::max<uint64_t>(n, 1));
+  float* d_out = dmalloc<float>(std::max<uint64_t>(n, 1));
+  HYRE_CUDA(cudaMemcpyAsync(d_qv, unit.data(), ix->dp * 4, cudaMemcpyHostToDevice, st));
+  if (n) HYRE_CUDA(cudaMemcpyAsync(d_rows, rows, n * 4, cudaMemcpyHostToDevice, st));
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  launch_gather_scores(bf16 ? static_cast<const void*>(ix->emb_hi) : ix->emb_f32, bf16, ix->dp, ix->row_base,
+                       d_qv, d_rows, n, d_out, st);
+  if (n) HYRE_CUDA(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_qv);
+  cudaFree(d_rows);
+  cudaFree(d_out);
+  return ren;
+}
+
+uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, uint32_t k, hyre_hit* out) {
+  if (n == 0) return 0;
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, n));
+  if (kk > kSelectMaxK) throw Error(HYRE_INVALID_ARGUMENT, "k > " + std::to_string(kSelectMaxK) + " unsupported");
+  uint32_t* d_rows = dmalloc<uint32_t>(n);
+  float* d_sc = dmalloc<float>(n);
+  uint64_t* d_keys = dmalloc<uint64_t>(n);
+  hyre_hit* d_out = dmalloc<hyre_hit>(kk);
+  uint32_t* d_misc = dmalloc<uint32_t>(8);
+  uint64_t* d_off = dmalloc<uint64_t>(1);
+  QParam p{QF_ACTIVE | QF_EMB, kk, 0, 0};
+  QParam* d_p = dmalloc<QParam>(1);
+  HYRE_CUDA(cudaMemcpyAsync(d_rows, rows, n * 4, cudaMemcpyHostToDevice, st));
+  HYRE_CUDA(cudaMemcpyAsync(d_sc, scores, n * 4, cudaMemcpyHostToDevice, st));
+  HYRE_CUDA(cudaMemcpyAsync(d_p, &p, sizeof p, cudaMemcpyHostToDevice, st));
+  const uint32_t n32 = static_cast<uint32_t>(n);
+  uint32_t misc[8] = {n32, n32, 0, 0, 0, 0, 0, 0};  // cnt, n_elig, rerun, out_cnt
+  HYRE_CUDA(cudaMemcpyAsync(d_misc, misc, sizeof misc, cudaMemcpyHostToDevice, st));
+  HYRE_CUDA(cudaMemsetAsync(d_off, 0, 8, st));
+  launch_make_keys(d_rows, d_sc, n, d_keys, st);
+  uint64_t* d_t = dmalloc<uint64_t>(1);
+  SelectArgs fa{d_keys, d_misc, n32, d_p, d_misc + 1, SELECT_FINAL, d_t, d_misc + 2, d_out, d_off, d_misc + 3,
+                1, QF_ACTIVE | QF_EMB, n32};
+  launch_select(fa, st);
+  uint32_t cnt = 0;
+  HYRE_CUDA(cudaMemcpyAsync(&cnt, d_misc + 3, 4, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  HYRE_CUDA(cudaMemcpy(out, d_out, cnt * sizeof(hyre_hit), cudaMemcpyDeviceToHost));
+  for (void* p2 : {(void*)d_rows, (void*)d_sc, (void*)d_keys, (void*)d_out, (void*)d_misc, (void*)d_off,
+                   (void*)d_p, (void*)d_t})
+    cudaFree(p2);
+  return cnt;
+}
+
+uint64_t Executor::preselect(const uint64_t* qwords, const uint32_t* rows, uint64_t n, uint32_t quant_k,
+                             uint32_t* out) {
+  if (quant_k < 1) validation("quantK must be >= 1");
+  if (n <= quant_k) {
+    std::memcpy(out, rows, n * 4);
+    return n;
+  }
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  const uint32_t nw = ix->num_words;
+  uint32_t* d_rows = dmalloc<uint32_t>(n);
+  uint64_t* d_q = dmalloc<uint64_t>(nw);
+  uint64_t* d_keys = dmalloc<uint64_t>(n);
+  uint64_t* d_sorted = dmalloc<uint64_t>(n);
+  HYRE_CUDA(cudaMemcpyAsync(d_rows, rows, n * 4, cudaMemcpyHostToDevice, st));
+  HYRE_CUDA(cudaMemcpyAsync(d_q, qwords, nw * 8, cudaMemcpyHostToDevice, st));
+  launch_quant_keys(ix->sigs, nw, ix->num_bits, ix->row_base, d_q, d_rows, n, d_keys, st);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, d_keys, d_sorted, static_cast<int>(n), 0, 64, st);
+  uint8_t* d_tmp = dmalloc<uint8_t>(tmp);
+  cub::DeviceRadixSort::SortKeysDescending(d_tmp, tmp, d_keys, d_sorted, static_cast<int>(n), 0, 64, st);
+  std::vector<uint64_t> top(quant_k);
+  HYRE_CUDA(cudaMemcpyAsync(top.data(), d_sorted, quant_k * 8ull, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  for (uint32_t i = 0; i < quant_k; ++i) out[i] = ~static_cast<uint32_t>(top[i]);
+  std::sort(out, out + quant_k);
+  for (void* p : {(void*)d_rows, (void*)d_q, (void*)d_keys, (void*)d_sorted, (void*)d_tmp}) cudaFree(p);
+  return quant_k;
+}
+
+}  // namespace hyreb

@@ -1,0 +1,91 @@
+// Executor state (see executor.cu).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace hyreb {
+
+DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
+
+struct Executor {
+  static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
+
+  DevIndex* ix;
+  uint32_t max_batch;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[5] = {};
+
+  // device scratch sized at construction
+  uint32_t cap = 0, samp_cap = 0;
+  uint32_t* d_mask = nullptr;
+  uint32_t* d_chunk_cnt = nullptr;
+  uint32_t* d_counters = nullptr;
+  uint64_t* d_thr = nullptr;
+  uint64_t* d_cand = nullptr;
+  uint64_t* d_samp = nullptr;
+  uint32_t* d_qhist = nullptr;
+  uint32_t* d_tsel = nullptr;
+  uint32_t* d_eqcnt = nullptr;
+  // grown on demand
+  uint8_t* d_blob = nullptr;
+  uint8_t* h_blob = nullptr;
+  size_t blob_cap = 0;
+  hyre_hit* d_hits = nullptr;
+  hyre_hit* h_hits = nullptr;
+  size_t hits_cap = 0;
+  uint32_t* d_scratch = nullptr;
+  uint32_t scratch_cap = 0;
+
+  // prepared batch
+  bool prepared = false;
+  uint32_t B = 0, max_k = 1, sample_period = 1, kernels = 0, n_scratch_used = 0;
+  bool any_emb = false, any_term_only = false, any_quant = false;
+  std::vector<QParam> qp;
+  std::vector<uint32_t> prog;
+  std::vector<const uint32_t*> refs;
+  std::vector<ScatterItem> items;
+  std::vector<uint64_t> item_prefix;
+  uint64_t scatter_total = 0;
+  std::vector<int32_t> statuses;
+  std::vector<std::string> slot_errors;
+  std::vector<uint64_t> hit_off;
+  std::vector<float> qvec;
+  std::vector<uint64_t> qsig;
+  uint64_t n_hits_total = 0, h2d_bytes = 0, d2h_bytes = 0;
+  std::vector<uint32_t> h_out_cnt, h_rerun;
+  QParam* d_qp = nullptr;
+  float* d_q = nullptr;
+  uint64_t* d_qsig = nullptr;
+  uint64_t* d_hit_off = nullptr;
+  uint32_t* d_prog = nullptr;
+  const uint32_t* const* d_refs = nullptr;
+  ScatterItem* d_items = nullptr;
+  uint64_t* d_ipre = nullptr;
+
+  Executor(DevIndex* index, uint32_t max_batch);
+  ~Executor();
+
+  void prepare(const hyre_query* qs, uint32_t b);
+  void run();
+  void fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* statuses,
+             hyre_timings* t);
+  float last_run_ms() const;
+
+  uint64_t full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows);
+  bool exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out);
+  uint32_t top_k(const uint32_t* rows, const float* scores, uint64_t n, uint32_t k, hyre_hit* out);
+  uint64_t preselect(const uint64_t* qwords, const uint32_t* rows, uint64_t n, uint32_t quant_k,
+                     uint32_t* out);
+
+ private:
+  void ensure_blob(size_t bytes);
+  void ensure_hits(size_t n);
+  void ensure_scratch(uint32_t n_bitmaps);
+  void finish_reruns();
+};
+
+}  // namespace hyreb

@@ -1,0 +1,258 @@
+// K0: device index build -- turns FrozenIndex's row-major arrays
+// (corpus.hpp:114-123; freeze layout corpus.cpp:97-123) into the B200 column
+// store described in device.cuh.  Build-time only (not on the query path);
+// the one-off postings sort uses CUB from the CUDA toolkit.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <memory>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace hyreb {
+
+namespace {
+
+template <class T>
+T* dmalloc(size_t n) {
+  T* p = nullptr;
+  if (n) HYRE_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+struct DFree {
+  void operator()(void* p) const { cudaFree(p); }
+};
+template <class T>
+using DPtr = std::unique_ptr<T, DFree>;
+
+__global__ void count_kernel(const uint32_t* offsets, uint32_t C, uint32_t n, uint32_t* counts) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    counts[r] = offsets[static_cast<size_t>(r) * (C + 1) + C];
+}
+
+// One posting per (row, slot, attribute): key = (slot << 32) | id, value = local row.
+__global__ void emit_kernel(const uint32_t* attributes, const uint32_t* offsets, uint32_t C,
+                            uint32_t A, uint32_t n, const uint64_t* pos, uint64_t* keys,
+                            uint32_t* vals) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint32_t* off = offsets + static_cast<size_t>(r) * (C + 1);
+    const uint32_t* att = attributes + static_cast<size_t>(r) * A;
+    uint64_t p = pos[r];
+    for (uint32_t c = 0; c < C; ++c)
+      for (uint32_t i = off[c]; i < off[c + 1]; ++i) {
+        keys[p] = (static_cast<uint64_t>(c) << 32) | att[i];
+        vals[p] = r;
+        ++p;
+      }
+  }
+}
+
+// x = hi + lo with hi = RNE_bf16(x), lo = RNE_bf16(x - hi): |x - hi - lo| <= 2^-17 |x|.
+__global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) {
+    const float x = src[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[i] = h;
+    if (lo) lo[i] = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
+}
+
+uint32_t pad_dim(uint32_t d, bool bf16) {
+  const uint32_t lo = bf16 ? 64 : 32, big = bf16 ? 256 : 128;
+  if (d <= big) {
+    uint32_t p = lo;
+    while (p < d) p <<= 1;
+    return p;
+  }
+  return (d + big - 1) / big * big;
+}
+
+}  // namespace
+
+DevIndex::~DevIndex() {
+  cudaSetDevice(device);
+  cudaFree(emb_f32);
+  cudaFree(emb_hi);
+  cudaFree(emb_lo);
+  cudaFree(sigs);
+  cudaFree(bitmaps);
+  cudaFree(post_rows);
+}
+
+DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
+  const uint32_t rb = o.row_begin;
+  const uint32_t re = o.row_end == 0 ? f.num_docs : o.row_end;
+  if (rb >= re || re > f.num_docs) validation("index shard rows out of range");
+  if (o.emb_dtype != HYRE_EMB_F32 && o.emb_dtype != HYRE_EMB_BF16) validation("unknown embedding dtype");
+  HYRE_CUDA(cudaSetDevice(o.device));
+  std::unique_ptr<DevIndex> ix(new DevIndex);
+  ix->device = o.device;
+  const uint32_t n = re - rb;
+  const uint32_t C = f.num_clauses, A = f.max_num_attr, d = f.dim;
+  ix->n_rows = n;
+  ix->row_base = rb;
+  ix->dim = d;
+  ix->emb_dtype = o.emb_dtype;
+  ix->tensor_path = o.tensor_path != 0;
+  ix->num_clauses = C;
+  ix->num_bits = f.num_bits;
+  ix->num_words = static_cast<uint32_t>(f.num_words());
+  ix->seed = f.seed;
+  ix->codec = make_codec(d, f.num_bits, f.seed);
+  const bool bf16 = o.emb_dtype == HYRE_EMB_BF16;
+  ix->dp = pad_dim(d, bf16);
+  const uint32_t dp = ix->dp;
+  const uint32_t w_raw = (n + 31) / 32;
+  ix->words = (w_raw + kChunkWords - 1) / kChunkWords * kChunkWords;
+  ix->n_chunks = ix->words / kChunkWords;
+  cudaStream_t st = 0;
+
+  // ---- embeddings --------------------------------------------------------
+  {
+    const size_t elems = size_t{n} * dp;
+    float* f32 = dmalloc<float>(elems);
+    HYRE_CUDA(cudaMemset(f32, 0, elems * sizeof(float)));
+    HYRE_CUDA(cudaMemcpy2D(f32, dp * sizeof(float), f.embeddings.data() + size_t{rb} * d,
+                           d * sizeof(float), d * sizeof(float), n, cudaMemcpyHostToDevice));
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>((elems + 255) / 256, 148 * 64));
+    if (bf16) {
+      ix->emb_hi = dmalloc<__nv_bfloat16>(elems);
+      split_kernel<<<blocks, 256, 0, st>>>(f32, elems, ix->emb_hi, nullptr);
+      HYRE_CUDA(cudaGetLastError());
+      HYRE_CUDA(cudaDeviceSynchronize());
+      cudaFree(f32);
+    } else {
+      ix->emb_f32 = f32;
+      if (ix->tensor_path) {
+        ix->emb_hi = dmalloc<__nv_bfloat16>(elems);
+        ix->emb_lo = dmalloc<__nv_bfloat16>(elems);
+        split_kernel<<<blocks, 256, 0, st>>>(f32, elems, ix->emb_hi, ix->emb_lo);
+        HYRE_CUDA(cudaGetLastError());
+      }
+    }
+    ix->stats.embedding_bytes = elems * (bf16 ? 2 : 4);
+    ix->stats.tensor_bytes = (!bf16 && ix->tensor_path) ? elems * 4 : 0;
+  }
+
+  // ---- signatures --------------------------------------------------------
+  {
+    const size_t nw = f.num_words();
+    ix->sigs = dmalloc<uint64_t>(size_t{n} * nw);
+    HYRE_CUDA(cudaMemcpy(ix->sigs, f.signatures.data() + size_t{rb} * nw, size_t{n} * nw * 8,
+                         cudaMemcpyHostToDevice));
+    ix->stats.signature_bytes = size_t{n} * nw * 8;
+  }
+
+  // ---- term postings -----------------------------------------------------
+  {
+    DPtr<uint32_t> att(dmalloc<uint32_t>(size_t{n} * A));
+    DPtr<uint32_t> off(dmalloc<uint32_t>(size_t{n} * (C + 1)));
+    HYRE_CUDA(cudaMemcpy(att.get(), f.attributes.data() + size_t{rb} * A, size_t{n} * A * 4,
+                         cudaMemcpyHostToDevice));
+    HYRE_CUDA(cudaMemcpy(off.get(), f.offsets.data() + size_t{rb} * (C + 1),
+                         size_t{n} * (C + 1) * 4, cudaMemcpyHostToDevice));
+    DPtr<uint32_t> cnt(dmalloc<uint32_t>(n));
+    DPtr<uint64_t> pos(dmalloc<uint64_t>(size_t{n} + 1));
+    const unsigned blocks = std::min(4096u, (n + 255) / 256);
+    count_kernel<<<blocks, 256>>>(off.get(), C, n, cnt.get());
+    HYRE_CUDA(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.get(), pos.get(), n + 1);
+    // scan over n+1 entries: the last entry reads cnt[n] -> use n and add total separately
+    tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.get(), pos.get(), n);
+    DPtr<uint8_t> tmp(dmalloc<uint8_t>(tmp_bytes));
+    cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, cnt.get(), pos.get(), n);
+    uint64_t last_pos = 0;
+    uint32_t last_cnt = 0;
+    HYRE_CUDA(cudaMemcpy(&last_pos, pos.get() + n - 1, 8, cudaMemcpyDeviceToHost));
+    HYRE_CUDA(cudaMemcpy(&last_cnt, cnt.get() + n - 1, 4, cudaMemcpyDeviceToHost));
+    const uint64_t P = last_pos + last_cnt;
+    ix->n_postings = P;
+    cnt.reset();
+    if (P > 0) {
+      DPtr<uint64_t> keys(dmalloc<uint64_t>(P)), keys2(dmalloc<uint64_t>(P));
+      DPtr<uint32_t> vals(dmalloc<uint32_t>(P));
+      ix->post_rows = dmalloc<uint32_t>(P);
+      emit_kernel<<<blocks, 256>>>(att.get(), off.get(), C, A, n, pos.get(), keys.get(), vals.get());
+      HYRE_CUDA(cudaGetLastError());
+      att.reset();
+      off.reset();
+      pos.reset();
+      int end_bit = 32;
+      while ((uint64_t{1} << (end_bit - 32)) < C) ++end_bit;
+      tmp_bytes = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.get(), keys2.get(), vals.get(),
+                                      ix->post_rows, P, 0, end_bit);
+      tmp.reset(dmalloc<uint8_t>(tmp_bytes));
+      HYRE_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tmp_bytes, keys.get(), keys2.get(),
+                                                vals.get(), ix->post_rows, P, 0, end_bit));
+      vals.reset();
+      // unique (slot, id) runs
+      DPtr<uint64_t> uniq(dmalloc<uint64_t>(P));
+      DPtr<uint32_t> runs(dmalloc<uint32_t>(P));
+      DPtr<uint32_t> n_runs(dmalloc<uint32_t>(1));
+      tmp_bytes = 0;
+      cub::DeviceRunLengthEncode::Encode(nullptr, tmp_bytes, keys2.get(), uniq.get(), runs.get(),
+                                         n_runs.get(), P);
+      tmp.reset(dmalloc<uint8_t>(tmp_bytes));
+      HYRE_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), tmp_bytes, keys2.get(), uniq.get(),
+                                                   runs.get(), n_runs.get(), P));
+      uint32_t T = 0;
+      HYRE_CUDA(cudaMemcpy(&T, n_runs.get(), 4, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> hk(T);
+      std::vector<uint32_t> hdf(T);
+      HYRE_CUDA(cudaMemcpy(hk.data(), uniq.get(), T * 8ull, cudaMemcpyDeviceToHost));
+      HYRE_CUDA(cudaMemcpy(hdf.data(), runs.get(), T * 4ull, cudaMemcpyDeviceToHost));
+      // Dense terms (df >= W/8) become bitmaps: a bitmap costs W words, a CSR
+      // list df words plus a scatter at query time.
+      const uint64_t dense_df = std::max<uint64_t>(1, ix->words / 8);
+      std::vector<ScatterItem> items;
+      std::vector<uint64_t> prefix;
+      uint64_t begin = 0, bsum = 0;
+      ix->terms.reserve(T * 2);
+      for (uint32_t i = 0; i < T; ++i) {
+        Term t{UINT32_MAX, hdf[i], begin};
+        if (hdf[i] >= dense_df) {
+          t.bitmap = ix->n_bitmap_terms++;
+          items.push_back({begin, hdf[i], t.bitmap});
+          prefix.push_back(bsum);
+          bsum += hdf[i];
+        } else {
+          ix->stats.csr_terms++;
+          ix->stats.csr_bytes += hdf[i] * 4ull;
+        }
+        ix->terms.emplace(hk[i], t);
+        begin += hdf[i];
+      }
+      ix->stats.num_terms = T;
+      ix->stats.bitmap_terms = ix->n_bitmap_terms;
+      if (ix->n_bitmap_terms) {
+        const size_t bm_words = size_t{ix->n_bitmap_terms} * ix->words;
+        ix->bitmaps = dmalloc<uint32_t>(bm_words);
+        HYRE_CUDA(cudaMemset(ix->bitmaps, 0, bm_words * 4));
+        DPtr<ScatterItem> ditems(dmalloc<ScatterItem>(items.size()));
+        DPtr<uint64_t> dprefix(dmalloc<uint64_t>(prefix.size()));
+        HYRE_CUDA(cudaMemcpy(ditems.get(), items.data(), items.size() * sizeof(ScatterItem),
+                             cudaMemcpyHostToDevice));
+        HYRE_CUDA(cudaMemcpy(dprefix.get(), prefix.data(), prefix.size() * 8, cudaMemcpyHostToDevice));
+        launch_scatter(ditems.get(), dprefix.get(), static_cast<uint32_t>(items.size()), bsum,
+                       ix->post_rows, ix->bitmaps, ix->words, st);
+        HYRE_CUDA(cudaGetLastError());
+        HYRE_CUDA(cudaDeviceSynchronize());
+        ix->stats.bitmap_bytes = bm_words * 4;
+      }
+    }
+  }
+  HYRE_CUDA(cudaDeviceSynchronize());
+  ix->stats.num_rows = n;
+  ix->stats.row_base = rb;
+  ix->stats.dim = d;
+  ix->stats.row_stride = dp;
+  ix->stats.postings = ix->n_postings;
+  return ix.release();
+}
+
+}  // namespace hyreb

@@ -1,0 +1,835 @@
+// Hot-path kernels for sm_100a (B200).  See DESIGN.md §4 for the roofline
+// argument behind each one; reference functions are cited per kernel.
+#include <cuda_bf16.h>
+
+#include "kernels.cuh"
+
+namespace hyreb {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Inclusive warp scan of a u32.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan (blockDim.x multiple of 32, <= 1024).
+// `tmp` needs 33 u32 of shared memory.  Returns exclusive prefix; total in *tot.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t inc = warp_incl_scan(v, lane);
+  if (lane == 31) tmp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = lane < nw ? tmp[lane] : 0;
+    uint32_t xi = warp_incl_scan(x, lane);
+    if (lane < nw) tmp[lane] = xi - x;
+    if (lane == 31) tmp[32] = xi;
+  }
+  __syncthreads();
+  uint32_t r = tmp[w] + inc - v;
+  *tot = tmp[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ uint32_t tail_mask(uint32_t widx, uint32_t n_rows) {
+  const uint64_t first = static_cast<uint64_t>(widx) * 32;
+  if (first >= n_rows) return 0u;
+  const uint64_t left = n_rows - first;
+  return left >= 32 ? kFull : ((1u << left) - 1u);
+}
+
+}  // namespace
+
+// ===========================================================================
+// K1: CNF eligibility mask.  One CTA = one chunk of 128 mask words (4096
+// rows), 128 threads, thread t owns word t.  All ref words of the chunk are
+// staged once into shared memory (each term bitmap is read from HBM exactly
+// once per batch), then every query's AND-of-ORs is evaluated from smem.
+// Replaces full_scan_tbr (term_match.cpp:56-78) / batch_scan_tbr
+// (pipeline.cpp:75-93): bit r of the mask <=> row r is a TBR match.
+// ===========================================================================
+__global__ void __launch_bounds__(128) mask_kernel(MaskArgs a, uint32_t staged) {
+  extern __shared__ uint32_t st[];  // staged refs [n_refs][128] then warp sums [B][4]
+  const uint32_t t = threadIdx.x, chunk = blockIdx.x;
+  const uint32_t widx = chunk * kChunkWords + t;
+  uint32_t* wsum = st + (staged ? a.n_refs * kChunkWords : 0);
+  if (staged) {
+    for (uint32_t r = 0; r < a.n_refs; ++r) st[r * kChunkWords + t] = __ldg(a.refs[r] + widx);
+    __syncthreads();
+  }
+  const uint32_t tm = tail_mask(widx, a.n_rows);
+  const int lane = t & 31, w = t >> 5;
+  for (uint32_t q = 0; q < a.B; ++q) {
+    const uint32_t flags = a.qp[q].flags;
+    uint32_t word = 0;
+    if ((flags & QF_ACTIVE) && !(flags & QF_EMPTY)) {
+      if (flags & QF_MATCH_ALL) {
+        word = tm;
+      } else {
+        const uint32_t* p = a.prog + a.qp[q].prog_off;
+        const uint32_t nc = p[0];
+        uint32_t pos = 1, acc = kFull;
+        for (uint32_t c = 0; c < nc; ++c) {
+          const uint32_t nr = p[pos++];
+          uint32_t cw = 0;
+          for (uint32_t r = 0; r < nr; ++r) {
+            const uint32_t ref = p[pos + r];
+            cw |= staged ? st[ref * kChunkWords + t] : __ldg(a.refs[ref] + widx);
+          }
+          pos += nr;
+          acc &= cw;
+        }
+        word = acc & tm;
+      }
+    }
+    a.mask[static_cast<size_t>(q) * a.words + widx] = word;
+    const uint32_t c = __reduce_add_sync(kFull, __popc(word));
+    if (lane == 0) wsum[q * 4 + w] = c;
+  }
+  __syncthreads();
+  for (uint32_t q = t; q < a.B; q += blockDim.x) {
+    const uint32_t c = wsum[q * 4] + wsum[q * 4 + 1] + wsum[q * 4 + 2] + wsum[q * 4 + 3];
+    a.chunk_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] = c;
+    if (c) atomicAdd(a.n_elig + q, c);
+  }
+}
+
+void launch_mask(const MaskArgs& a, cudaStream_t st) {
+  if (a.B == 0 || a.n_chunks == 0) return;
+  const size_t wsum_bytes = size_t{a.B} * 4 * sizeof(uint32_t);
+  const size_t staged_bytes = size_t{a.n_refs} * kChunkWords * sizeof(uint32_t);
+  constexpr size_t kSmemCap = 200 * 1024;
+  const uint32_t staged = (a.n_refs > 0 && staged_bytes + wsum_bytes <= kSmemCap) ? 1u : 0u;
+  const size_t smem = wsum_bytes + (staged ? staged_bytes : 0);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  mask_kernel<<<a.n_chunks, kChunkWords, smem, st>>>(a, staged);
+}
+
+// CSR postings -> scratch clause bitmaps (sparse terms, df < W/8).
+__global__ void scatter_kernel(const ScatterItem* items, const uint64_t* prefix, uint32_t n_items,
+                               uint64_t total, const uint32_t* post_rows, uint32_t* scratch,
+                               uint32_t words) {
+  for (uint64_t p = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; p < total;
+       p += uint64_t{gridDim.x} * blockDim.x) {
+    uint32_t lo = 0, hi = n_items;  // last item with prefix <= p
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (prefix[mid] <= p) lo = mid; else hi = mid;
+    }
+    const ScatterItem it = items[lo];
+    const uint32_t row = post_rows[it.begin + (p - prefix[lo])];
+    atomicOr(scratch + static_cast<size_t>(it.target) * words + (row >> 5), 1u << (row & 31));
+  }
+}
+
+void launch_scatter(const ScatterItem* items, const uint64_t* item_prefix, uint32_t n_items,
+                    uint64_t total, const uint32_t* post_rows, uint32_t* scratch, uint32_t words,
+                    cudaStream_t st) {
+  if (!total) return;
+  const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148 * 16);
+  scatter_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(items, item_prefix, n_items, total,
+                                                                post_rows, scratch, words);
+}
+
+// ===========================================================================
+// K2: streaming scorer on CUDA cores (single queries and small batches).
+//
+// Persistent grid of warps; a warp owns one 1024-row segment at a time.  The
+// union of the group's mask words is compacted into a warp-private row list
+// (ineligible rows are never loaded), then rows are scored 8*G at a time:
+// every lane streams one 16-byte chunk of each of 8 rows with
+// ld.global.nc.L1::no_allocate (8 independent LDG.128 in flight per lane),
+// FMAs it against the query chunk held in registers, and a 3-level
+// reduce-scatter butterfly leaves each leader lane with one finished dot.
+// The epilogue clamps (knn.cpp:37), builds the orderable (score, ~row) key
+// and appends it only if it beats the query's running lower bound `thr`
+// (the K-th best key of a sampled subset, a provable lower bound on the
+// global K-th key).  Replaces exact_scores (knn.cpp:8-40) and the gather
+// half of bucket_top_k (knn.cpp:42-95).
+// ===========================================================================
+namespace {
+
+template <typename RowT>
+struct Chunk;
+
+template <>
+struct Chunk<float> {
+  static constexpr int kElems = 4;
+  __device__ static float dot(const uint4& v, const float* q) {
+    float s = __uint_as_float(v.x) * q[0];
+    s = fmaf(__uint_as_float(v.y), q[1], s);
+    s = fmaf(__uint_as_float(v.z), q[2], s);
+    s = fmaf(__uint_as_float(v.w), q[3], s);
+    return s;
+  }
+};
+
+template <>
+struct Chunk<__nv_bfloat16> {
+  static constexpr int kElems = 8;
+  __device__ static float2 up(uint32_t w) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  }
+  __device__ static float dot(const uint4& v, const float* q) {
+    float2 a = up(v.x), b = up(v.y), c = up(v.z), d = up(v.w);
+    float s = a.x * q[0];
+    s = fmaf(a.y, q[1], s);
+    s = fmaf(b.x, q[2], s);
+    s = fmaf(b.y, q[3], s);
+    s = fmaf(c.x, q[4], s);
+    s = fmaf(c.y, q[5], s);
+    s = fmaf(d.x, q[6], s);
+    s = fmaf(d.y, q[7], s);
+    return s;
+  }
+};
+
+__device__ __forceinline__ bool score_active(const ScoreArgs& a, uint32_t q) {
+  if (q >= a.B) return false;
+  const uint32_t f = a.qp[q].flags;
+  if ((f & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) return false;
+  const uint32_t ne = a.n_elig[q];
+  if (ne == 0) return false;
+  if (a.mode == SCORE_SAMPLE) return ne > a.gate;
+  if (a.mode == SCORE_RERUN) return a.rerun[q] != 0;
+  return true;
+}
+
+}  // namespace
+
+template <typename RowT, int LPR, int CPL, int QG>
+__global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
+  constexpr int G = 32 / LPR;             // row groups per warp load step
+  constexpr int E = Chunk<RowT>::kElems;  // elements per 16-byte chunk
+  constexpr int M1 = LPR / 2, M2 = LPR / 4, M3 = LPR / 8;
+  __shared__ uint16_t lists[8][kSegRows];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / LPR, li = lane % LPR;
+  const uint32_t q0 = blockIdx.y * QG;
+
+  uint32_t act = 0;
+  uint64_t thr[QG];
+#pragma unroll
+  for (int j = 0; j < QG; ++j) {
+    const bool on = score_active(a, q0 + j);
+    act |= on ? (1u << j) : 0u;
+    thr[j] = (on && a.mode != SCORE_SAMPLE) ? a.thr[q0 + j] : 0ull;
+  }
+  if (!act) return;
+
+  float qv[QG][CPL][E];
+#pragma unroll
+  for (int j = 0; j < QG; ++j)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        qv[j][c][e] = (act >> j & 1u)
+                          ? a.q[static_cast<size_t>(q0 + j) * a.dp + (li + c * LPR) * E + e]
+                          : 0.0f;
+
+  const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
+  const uint32_t n_iter = a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period : n_seg;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const RowT* emb = static_cast<const RowT*>(a.emb);
+  const int slot = ((lane & M1) ? 4 : 0) + ((lane & M2) ? 2 : 0) + ((lane & M3) ? 1 : 0);
+  const bool leader = (lane & (M3 - 1)) == 0;
+
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + wib; it < n_iter; it += warps) {
+    const uint32_t seg = a.mode == SCORE_SAMPLE ? it * a.period : it;
+    const uint32_t widx = seg * 32 + lane;
+    uint32_t wq[QG];
+    uint32_t uni = 0;
+#pragma unroll
+    for (int j = 0; j < QG; ++j) {
+      wq[j] = ((act >> j & 1u) && widx < a.words) ? a.mask[static_cast<size_t>(q0 + j) * a.words + widx] : 0u;
+      uni |= wq[j];
+    }
+    const uint32_t cnt = __popc(uni);
+    const uint32_t incl = warp_incl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) continue;
+    const bool full = total == kSegRows;
+    if (!full) {
+      uint32_t pos = incl - cnt, u = uni;
+      while (u) {
+        const int b = __ffs(u) - 1;
+        u &= u - 1;
+        lists[wib][pos++] = static_cast<uint16_t>(lane * 32 + b);
+      }
+    }
+    __syncwarp();
+    const size_t seg_row0 = static_cast<size_t>(seg) * kSegRows;
+    for (uint32_t base = 0; base < total; base += 8 * G) {
+      uint4 v[8][CPL];
+      uint32_t roff[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const uint32_t idx = base + s * G + g;
+        const bool ok = idx < total;
+        roff[s] = ok ? (full ? idx : lists[wib][idx]) : 0u;
+        const RowT* row = emb + (seg_row0 + roff[s]) * a.dp;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          v[s][c] = ok ? ldg_stream(row + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+      }
+      const uint32_t my_idx = base + slot * G + g;
+      const bool my_ok = leader && my_idx < total;
+      const uint32_t my_off = my_idx < total ? (full ? my_idx : lists[wib][my_idx]) : 0u;
+#pragma unroll
+      for (int j = 0; j < QG; ++j) {
+        if (!(act >> j & 1u)) continue;
+        float p[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[s][c], qv[j][c]);
+          p[s] = acc;
+        }
+        // reduce-scatter: 8 values over LPR lanes -> 1 value per lane.
+        {
+          const bool up = lane & M1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float send = up ? p[i] : p[i + 4];
+            const float recv = __shfl_xor_sync(kFull, send, M1);
+            p[i] = (up ? p[i + 4] : p[i]) + recv;
+          }
+        }
+        {
+          const bool up = lane & M2;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const float send = up ? p[i] : p[i + 2];
+            const float recv = __shfl_xor_sync(kFull, send, M2);
+            p[i] = (up ? p[i + 2] : p[i]) + recv;
+          }
+        }
+        {
+          const bool up = lane & M3;
+          const float send = up ? p[0] : p[1];
+          const float recv = __shfl_xor_sync(kFull, send, M3);
+          p[0] = (up ? p[1] : p[0]) + recv;
+        }
+#pragma unroll
+        for (int m = M3 / 2; m >= 1; m >>= 1) p[0] += __shfl_xor_sync(kFull, p[0], m);
+
+        const uint32_t src_word = __shfl_sync(kFull, wq[j], (my_off >> 5) & 31);
+        const bool elig = (src_word >> (my_off & 31)) & 1u;
+        const uint32_t grow = a.row_base + static_cast<uint32_t>(seg_row0) + my_off;
+        const uint64_t key = make_key(clamp_score(p[0]), grow);
+        const bool take = my_ok && elig && key >= thr[j];
+        const unsigned bal = __ballot_sync(kFull, take);
+        if (bal) {
+          const uint32_t q = q0 + j;
+          uint32_t basei = 0;
+          const int first = __ffs(bal) - 1;
+          if (lane == first) basei = atomicAdd(a.cand_cnt + q, __popc(bal));
+          basei = __shfl_sync(kFull, basei, first);
+          if (take) {
+            const uint32_t at = basei + __popc(bal & ((1u << lane) - 1u));
+            if (at < a.cap) a.cand[static_cast<size_t>(q) * a.cap + at] = key;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+namespace {
+template <typename RowT, int QG>
+void dispatch_score(const ScoreArgs& a, dim3 grid, cudaStream_t st) {
+  const uint32_t cpr = a.dp_chunks;
+  if (cpr == 8) score_kernel<RowT, 8, 1, QG><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 16) score_kernel<RowT, 16, 1, QG><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 32) score_kernel<RowT, 32, 1, QG><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 64) score_kernel<RowT, 32, 2, QG><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 128) score_kernel<RowT, 32, 4, QG><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 256) score_kernel<RowT, 32, 8, QG><<<grid, 256, 0, st>>>(a);
+  else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
+}
+}  // namespace
+
+void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st) {
+  if (a.B == 0) return;
+  const uint32_t qg = a.B == 1 ? 1 : kMaxQG;
+  const uint32_t groups = (a.B + qg - 1) / qg;
+  const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
+  const uint32_t iters = a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period : n_seg;
+  // Persistent grid: up to 148 SMs x 8 CTAs of 8 warps, no more warps than segments.
+  const uint32_t blocks = std::max(1u, std::min((iters + 7) / 8, 148u * 8u));
+  dim3 grid(blocks, groups);
+  if (bf16) {
+    if (qg == 1) dispatch_score<__nv_bfloat16, 1>(a, grid, st);
+    else dispatch_score<__nv_bfloat16, kMaxQG>(a, grid, st);
+  } else {
+    if (qg == 1) dispatch_score<float, 1>(a, grid, st);
+    else dispatch_score<float, kMaxQG>(a, grid, st);
+  }
+}
+
+// ===========================================================================
+// K4: exact per-query selection over candidate keys (one CTA per query).
+// Radix select (12-bit digits from the top) finds the K-th largest key, the
+// keys >= it are gathered into shared memory and bitonic-sorted descending.
+// Keys are unique (they embed the row), so exactly min(K, n) survive and the
+// order is (score desc, row asc) -- identical to the full sort the reference
+// performs (knn.cpp:79-92; "Result == full sort for every G").
+// ===========================================================================
+namespace {
+constexpr int kSelThreads = 512;
+
+// Returns the k-th largest key among keys[0..n) (1 <= k <= n).
+__device__ uint64_t kth_largest(const uint64_t* keys, uint32_t n, uint32_t k, uint32_t* hist,
+                                uint32_t* tmp) {
+  __shared__ uint32_t sel_digit, sel_unique, sel_kk;
+  __shared__ uint64_t found;
+  uint64_t prefix = 0, pmask = 0;
+  uint32_t kk = k;
+  const int shifts[6] = {52, 40, 28, 16, 4, 0};
+  for (int pass = 0; pass < 6; ++pass) {
+    const int sh = shifts[pass];
+    const uint32_t dm = pass == 5 ? 0xfu : 0xfffu;
+    for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if ((key & pmask) == prefix) atomicAdd(hist + ((key >> sh) & dm), 1u);
+    }
+    __syncthreads();
+    // Position t of the scan owns bins [8*o, 8*o+8) with o = T-1-t, so the
+    // exclusive prefix at t counts every key in bins above o's range.
+    const uint32_t owner = blockDim.x - 1 - threadIdx.x;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) mine += hist[owner * 8 + b];
+    uint32_t tot;
+    uint32_t above = block_excl_scan(mine, tmp, &tot);
+#pragma unroll
+    for (int b = 7; b >= 0; --b) {
+      const uint32_t h = hist[owner * 8 + b];
+      if (above < kk && kk <= above + h) {
+        sel_digit = owner * 8 + b;
+        sel_unique = h == 1;
+        sel_kk = kk - above;
+      }
+      above += h;
+    }
+    __syncthreads();
+    kk = sel_kk;
+    prefix |= static_cast<uint64_t>(sel_digit) << sh;
+    pmask |= static_cast<uint64_t>(dm) << sh;
+    const bool uniq = sel_unique;
+    __syncthreads();
+    if (uniq && pass < 5) {
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+        if ((keys[i] & pmask) == prefix) found = keys[i];
+      __syncthreads();
+      return found;
+    }
+  }
+  return prefix;
+}
+
+__device__ void bitonic_desc(uint64_t* s, uint32_t m) {  // m power of two
+  for (uint32_t size = 2; size <= m; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m / 2; i += blockDim.x) {
+        const uint32_t lo = 2 * stride * (i / stride) + (i % stride);
+        const uint32_t hi = lo + stride;
+        const bool desc = ((lo & size) == 0);
+        const uint64_t x = s[lo], y = s[hi];
+        if ((x < y) == desc) {
+          s[lo] = y;
+          s[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
+  extern __shared__ uint64_t sel_smem[];
+  uint64_t* sortbuf = sel_smem;                                        // kSelectMaxK keys
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sel_smem + kSelectMaxK);  // 4096
+  uint32_t* tmp = hist + 4096;                                         // 33
+  __shared__ uint32_t gathered;
+  const uint32_t q = blockIdx.x;
+  const QParam qp = a.qp[q];
+  if ((qp.flags & a.require_flags) != a.require_flags) return;
+  if (a.mode == SELECT_FINAL_RERUN && !a.rerun[q]) return;
+  const uint32_t total = a.cnt[q];
+  const uint32_t n = min(total, a.cap);
+  const uint64_t* keys = a.buf + static_cast<size_t>(q) * a.cap;
+  const uint32_t k = qp.k;
+
+  if (a.mode == SELECT_KTH) {
+    // Only queries that were sampled (n_elig > cap) get a threshold.
+    if (!(a.n_elig[q] > a.gate)) {
+      if (threadIdx.x == 0) a.thr[q] = 0;
+      return;
+    }
+    uint64_t t = 0;
+    if (n >= k && k > 0) t = kth_largest(keys, n, k, hist, tmp);
+    if (threadIdx.x == 0) a.thr[q] = t;
+    return;
+  }
+  // FINAL
+  if (a.n_elig[q] == 0 || total == 0) {
+    if (threadIdx.x == 0) {
+      a.out_cnt[q] = 0;
+      if (a.rerun) a.rerun[q] = 0;
+    }
+    return;
+  }
+  if (total > a.cap) {
+    // Candidate buffer overflowed: the first `cap` candidates are a subset of
+    // the eligible rows, so their K-th key is a valid, tighter lower bound.
+    const uint64_t t = kth_largest(keys, n, k, hist, tmp);
+    if (threadIdx.x == 0) {
+      a.thr[q] = t;
+      a.rerun[q] = 1;
+    }
+    return;
+  }
+  const uint64_t t = n > k ? kth_largest(keys, n, k, hist, tmp) : 0ull;
+  if (threadIdx.x == 0) gathered = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t key = keys[i];
+    if (key >= t) {
+      const uint32_t at = atomicAdd(&gathered, 1u);
+      if (at < kSelectMaxK) sortbuf[at] = key;
+    }
+  }
+  __syncthreads();
+  const uint32_t m = min(gathered, kSelectMaxK);
+  uint32_t m2 = 1;
+  while (m2 < m) m2 <<= 1;
+  for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
+  __syncthreads();
+  bitonic_desc(sortbuf, m2);
+  const uint32_t take = min(m, k);
+  hyre_hit* out = a.hits + a.hit_off[q];
+  for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
+    const uint64_t key = sortbuf[i];
+    out[i].row = key_row(key);
+    out[i].score = key_score(key);
+  }
+  if (threadIdx.x == 0) {
+    a.out_cnt[q] = take;
+    if (a.rerun) a.rerun[q] = 0;
+  }
+}
+
+void launch_select(const SelectArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = true;
+  }
+  select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
+}
+
+// ===========================================================================
+// K5: first-K eligible rows in ascending row order (term-only queries,
+// pipeline.cpp:30-40; with all_rows it is full_scan_tbr's row list).
+// One CTA per query: scan the per-chunk counts K1 produced, then extract only
+// the chunks that hold output rows.
+// ===========================================================================
+__global__ void __launch_bounds__(128) first_k_kernel(FirstKArgs a) {
+  __shared__ uint32_t tmp[40];
+  const uint32_t q = blockIdx.x;
+  const QParam qp = a.qp[q];
+  if (!a.all_rows && (qp.flags & (QF_ACTIVE | QF_EMB)) != QF_ACTIVE) return;
+  const uint32_t ne = a.n_elig[q];
+  const uint64_t want64 = a.all_rows ? a.rows_cap : qp.k;
+  const uint32_t want = static_cast<uint32_t>(min(static_cast<uint64_t>(ne), want64));
+  if (threadIdx.x == 0 && a.out_cnt) a.out_cnt[q] = want;
+  if (want == 0) return;
+  const uint32_t* cc = a.chunk_cnt + static_cast<size_t>(q) * a.n_chunks;
+  const uint32_t* mk = a.mask + static_cast<size_t>(q) * a.words;
+  hyre_hit* hits = a.hits ? a.hits + a.hit_off[q] : nullptr;
+  __shared__ uint32_t s_cnt[kChunkWords], s_pre[kChunkWords];
+  uint32_t written = 0;
+  for (uint32_t base = 0; base < a.n_chunks && written < want; base += blockDim.x) {
+    const uint32_t ch = base + threadIdx.x;
+    const uint32_t c = ch < a.n_chunks ? cc[ch] : 0u;
+    uint32_t tot;
+    const uint32_t pre = block_excl_scan(c, tmp, &tot);
+    s_cnt[threadIdx.x] = c;
+    s_pre[threadIdx.x] = pre;
+    __syncthreads();
+    // prefixes are non-decreasing, so the chunks holding output rows are the
+    // non-empty ones before the first prefix that reaches `want`.
+    for (uint32_t j = 0; j < blockDim.x && written + s_pre[j] < want; ++j) {
+      if (!s_cnt[j]) continue;
+      const uint32_t chunk = base + j;
+      const uint32_t w = mk[chunk * kChunkWords + threadIdx.x];
+      uint32_t wt;
+      const uint32_t wpre = block_excl_scan(__popc(w), tmp, &wt);
+      uint32_t out = written + s_pre[j] + wpre, u = w;
+      while (u && out < want) {
+        const int b = __ffs(u) - 1;
+        u &= u - 1;
+        const uint32_t row = a.row_base + (chunk * kChunkWords + threadIdx.x) * 32 + b;
+        if (hits) {
+          hits[out].row = row;
+          hits[out].score = 0.0f;
+        }
+        if (a.rows_out) a.rows_out[out] = row;
+        ++out;
+      }
+    }
+    written += tot;
+    __syncthreads();
+  }
+}
+
+void launch_first_k(const FirstKArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  first_k_kernel<<<a.B, kChunkWords, 0, st>>>(a);
+}
+
+// ===========================================================================
+// K6: sign-quant pre-selection (quantizer.cpp:72-138, batched form
+// pipeline.cpp:184-242).  For each query with quant on and more than quant_k
+// eligible rows: Q1 histograms popcount(~(q ^ sig)) over eligible rows, Q2
+// picks the threshold score t and how many score==t rows survive (lowest
+// rows first), Q3 counts ==t rows per chunk, Q4 scans those counts and Q5
+// rewrites the mask so exactly quant_k rows stay eligible.  Integer work, so
+// the survivor set is bit-exact with the reference's nth_element selection.
+// ===========================================================================
+namespace {
+__device__ __forceinline__ uint32_t qscore(const uint64_t* sig, const uint64_t* qs, uint32_t nw,
+                                           uint32_t num_bits) {
+  uint32_t s = 0;
+  for (uint32_t w = 0; w < nw; ++w) {
+    uint64_t same = ~(sig[w] ^ qs[w]);
+    if (w + 1 == nw && (num_bits & 63)) same &= (1ull << (num_bits & 63)) - 1ull;
+    s += __popcll(same);
+  }
+  return s;
+}
+__device__ __forceinline__ bool quant_needed(const QuantArgs& a, uint32_t q) {
+  const uint32_t f = a.qp[q].flags;
+  return (f & (QF_ACTIVE | QF_EMB | QF_QUANT)) == (QF_ACTIVE | QF_EMB | QF_QUANT) &&
+         a.n_elig[q] > a.qp[q].quant_k;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128) quant_hist_kernel(QuantArgs a) {
+  extern __shared__ uint32_t h[];
+  const uint32_t q = blockIdx.y, chunk = blockIdx.x;
+  if (!quant_needed(a, q)) return;
+  for (uint32_t i = threadIdx.x; i <= a.num_bits; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint32_t widx = chunk * kChunkWords + threadIdx.x;
+  uint32_t w = a.mask[static_cast<size_t>(q) * a.words + widx];
+  const uint64_t* qs = a.qsig + static_cast<size_t>(q) * a.nw;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1;
+    const uint32_t row = widx * 32 + b;
+    atomicAdd(h + qscore(a.sigs + static_cast<size_t>(row) * a.nw, qs, a.nw, a.num_bits), 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i <= a.num_bits; i += blockDim.x)
+    if (h[i]) atomicAdd(a.hist + static_cast<size_t>(q) * (a.num_bits + 1) + i, h[i]);
+}
+
+__global__ void quant_thresh_kernel(QuantArgs a) {
+  const uint32_t q = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  uint32_t* ts = a.tsel + q * 3;
+  ts[2] = 0;
+  if (!quant_needed(a, q)) return;
+  const uint32_t qk = a.qp[q].quant_k;
+  const uint32_t* h = a.hist + static_cast<size_t>(q) * (a.num_bits + 1);
+  uint32_t above = 0;
+  for (int s = static_cast<int>(a.num_bits); s >= 0; --s) {
+    if (above + h[s] >= qk) {
+      ts[0] = static_cast<uint32_t>(s);
+      ts[1] = qk - above;  // rows with score == s to keep (lowest rows first)
+      ts[2] = 1;
+      break;
+    }
+    above += h[s];
+  }
+  a.n_elig[q] = qk;
+}
+
+__global__ void __launch_bounds__(128) quant_eq_kernel(QuantArgs a) {
+  const uint32_t q = blockIdx.y, chunk = blockIdx.x;
+  const uint32_t* ts = a.tsel + q * 3;
+  if (!ts[2]) return;
+  const uint32_t widx = chunk * kChunkWords + threadIdx.x;
+  uint32_t w = a.mask[static_cast<size_t>(q) * a.words + widx];
+  const uint64_t* qs = a.qsig + static_cast<size_t>(q) * a.nw;
+  uint32_t c = 0;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1;
+    c += qscore(a.sigs + static_cast<size_t>(widx * 32 + b) * a.nw, qs, a.nw, a.num_bits) == ts[0];
+  }
+  c = __reduce_add_sync(kFull, c);
+  __shared__ uint32_t ws[4];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    a.eq_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] = ws[0] + ws[1] + ws[2] + ws[3];
+}
+
+__global__ void __launch_bounds__(1024) quant_scan_kernel(QuantArgs a) {
+  __shared__ uint32_t tmp[40];
+  const uint32_t q = blockIdx.x;
+  if (!a.tsel[q * 3 + 2]) return;
+  uint32_t* e = a.eq_cnt + static_cast<size_t>(q) * a.n_chunks;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < a.n_chunks; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < a.n_chunks ? e[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(v, tmp, &tot);
+    if (i < a.n_chunks) e[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(128) quant_apply_kernel(QuantArgs a) {
+  __shared__ uint32_t tmp[40];
+  __shared__ uint32_t ws[4];
+  const uint32_t q = blockIdx.y, chunk = blockIdx.x;
+  const uint32_t* ts = a.tsel + q * 3;
+  if (!ts[2]) return;
+  const uint32_t t = ts[0], keep_eq = ts[1];
+  const uint32_t widx = chunk * kChunkWords + threadIdx.x;
+  uint32_t* mp = a.mask + static_cast<size_t>(q) * a.words + widx;
+  const uint32_t w = *mp;
+  const uint64_t* qs = a.qsig + static_cast<size_t>(q) * a.nw;
+  uint32_t gt = 0, eq = 0;
+  uint32_t u = w;
+  while (u) {
+    const int b = __ffs(u) - 1;
+    u &= u - 1;
+    const uint32_t s = qscore(a.sigs + static_cast<size_t>(widx * 32 + b) * a.nw, qs, a.nw, a.num_bits);
+    if (s > t) gt |= 1u << b;
+    else if (s == t) eq |= 1u << b;
+  }
+  uint32_t tot;
+  uint32_t rank = a.eq_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] +
+                  block_excl_scan(__popc(eq), tmp, &tot);
+  uint32_t keep = gt;
+  u = eq;
+  while (u) {
+    const int b = __ffs(u) - 1;
+    u &= u - 1;
+    if (rank < keep_eq) keep |= 1u << b;
+    ++rank;
+  }
+  *mp = keep;
+  const uint32_t c = __reduce_add_sync(kFull, __popc(keep));
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    a.chunk_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] = ws[0] + ws[1] + ws[2] + ws[3];
+}
+
+void launch_quant(const QuantArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  dim3 grid(a.n_chunks, a.B);
+  quant_hist_kernel<<<grid, kChunkWords, (a.num_bits + 1) * sizeof(uint32_t), st>>>(a);
+  quant_thresh_kernel<<<a.B, 32, 0, st>>>(a);
+  quant_eq_kernel<<<grid, kChunkWords, 0, st>>>(a);
+  quant_scan_kernel<<<a.B, 1024, 0, st>>>(a);
+  quant_apply_kernel<<<grid, kChunkWords, 0, st>>>(a);
+}
+
+// ===========================================================================
+// Stage helpers
+// ===========================================================================
+template <typename RowT>
+__global__ void gather_scores_kernel(const RowT* emb, uint32_t dp, uint32_t row_base,
+                                     const float* q, const uint32_t* rows, uint64_t n, float* out) {
+  const uint64_t warp = (blockIdx.x * uint64_t{blockDim.x} + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const RowT* row = emb + static_cast<size_t>(rows[warp] - row_base) * dp;
+  float s = 0.0f;
+  for (uint32_t e = lane; e < dp; e += 32) s = fmaf(static_cast<float>(row[e]), q[e], s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) out[warp] = clamp_score(s);
+}
+
+void launch_gather_scores(const void* emb, bool bf16, uint32_t dp, uint32_t row_base,
+                          const float* q, const uint32_t* rows, uint64_t n, float* out,
+                          cudaStream_t st) {
+  if (!n) return;
+  const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
+  if (bf16)
+    gather_scores_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(emb), dp, row_base, q, rows, n, out);
+  else
+    gather_scores_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(emb), dp,
+                                                          row_base, q, rows, n, out);
+}
+
+__global__ void make_keys_kernel(const uint32_t* rows, const float* scores, uint64_t n, uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n; i += uint64_t{gridDim.x} * blockDim.x)
+    keys[i] = make_key(scores[i] + 0.0f, rows[i]);
+}
+
+void launch_make_keys(const uint32_t* rows, const float* scores, uint64_t n, uint64_t* keys,
+                      cudaStream_t st) {
+  if (!n) return;
+  make_keys_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(
+      rows, scores, n, keys);
+}
+
+// Quant keys: (agreement << 32) | ~row, so "larger key" = (score desc, row asc).
+__global__ void quant_keys_kernel(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uint32_t row_base,
+                                  const uint64_t* qsig, const uint32_t* rows, uint64_t n, uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n; i += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t r = rows[i];
+    const uint32_t s = qscore(sigs + static_cast<size_t>(r - row_base) * nw, qsig, nw, num_bits);
+    keys[i] = (static_cast<uint64_t>(s) << 32) | static_cast<uint32_t>(~r);
+  }
+}
+
+void launch_quant_keys(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uint32_t row_base,
+                       const uint64_t* qsig, const uint32_t* rows, uint64_t n, uint64_t* keys,
+                       cudaStream_t st) {
+  if (!n) return;
+  quant_keys_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096)), 256, 0, st>>>(
+      sigs, nw, num_bits, row_base, qsig, rows, n, keys);
+}
+
+}  // namespace hyreb

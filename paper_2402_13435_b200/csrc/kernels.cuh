@@ -1,0 +1,115 @@
+// Launch interfaces of the hot-path kernels (K1, K2, K4, K5, K6 in
+// SURVEY.md §2 / DESIGN.md §4).  All launches are asynchronous on `st`.
+#pragma once
+
+#include "device.cuh"
+
+namespace hyreb {
+
+// ---- K1: CNF eligibility mask (term_match.cpp:56-78, pipeline.cpp:75-93) ----
+struct MaskArgs {
+  const uint32_t* const* refs;  // batch ref table: bitmap base pointers (W words each)
+  uint32_t n_refs;
+  const uint32_t* prog;  // per query: n_clauses, {n_refs, ref...}*
+  const QParam* qp;
+  uint32_t B, words, n_chunks, n_rows;
+  uint32_t* mask;        // [B][W]
+  uint32_t* chunk_cnt;   // [B][n_chunks]
+  uint32_t* n_elig;      // [B] (zeroed by caller)
+};
+void launch_mask(const MaskArgs& a, cudaStream_t st);
+
+// CSR postings scattered into per-clause scratch bitmaps.
+struct ScatterItem {
+  uint64_t begin;   // first posting in post_rows
+  uint32_t count;   // df
+  uint32_t target;  // scratch bitmap index
+};
+void launch_scatter(const ScatterItem* items, const uint64_t* item_prefix, uint32_t n_items,
+                    uint64_t total, const uint32_t* post_rows, uint32_t* scratch, uint32_t words,
+                    cudaStream_t st);
+
+// ---- K2: CUDA-core streaming scorer with threshold candidate filter ----
+enum ScoreMode : uint32_t { SCORE_MAIN = 0, SCORE_SAMPLE = 1, SCORE_RERUN = 2 };
+struct ScoreArgs {
+  const void* emb;  // float or bf16 rows, stride dp elements
+  uint32_t dp, dp_chunks, n_rows, row_base, words;
+  const uint32_t* mask;
+  const QParam* qp;
+  const float* q;  // [B][dp]
+  uint32_t B;
+  const uint32_t* n_elig;
+  const uint64_t* thr;  // [B]
+  uint64_t* cand;       // [B][cap]
+  uint32_t* cand_cnt;   // [B]
+  uint32_t cap;
+  uint32_t mode, period;
+  uint32_t gate;          // queries with n_elig > gate are sampled (= candidate cap)
+  const uint32_t* rerun;  // [B]
+};
+void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
+
+// ---- K4: per-query exact selection over candidate keys ----
+enum SelectMode : uint32_t { SELECT_KTH = 0, SELECT_FINAL = 1, SELECT_FINAL_RERUN = 2 };
+struct SelectArgs {
+  const uint64_t* buf;
+  const uint32_t* cnt;
+  uint32_t cap;
+  const QParam* qp;
+  const uint32_t* n_elig;
+  uint32_t mode;
+  uint64_t* thr;       // KTH: out; FINAL: out on overflow
+  uint32_t* rerun;     // FINAL: set on overflow; FINAL_RERUN: consumed
+  hyre_hit* hits;      // FINAL: out
+  const uint64_t* hit_off;
+  uint32_t* out_cnt;
+  uint32_t B;
+  uint32_t require_flags;  // queries must have these flags (QF_ACTIVE|QF_EMB)
+  uint32_t gate;           // KTH: only queries with n_elig > gate were sampled
+};
+void launch_select(const SelectArgs& a, cudaStream_t st);
+
+// ---- K5: term-only first-K rows (pipeline.cpp:30-40) ----
+struct FirstKArgs {
+  const uint32_t* mask;
+  const uint32_t* chunk_cnt;
+  const uint32_t* n_elig;
+  const QParam* qp;
+  uint32_t B, words, n_chunks, row_base;
+  const uint64_t* hit_off;
+  hyre_hit* hits;
+  uint32_t* out_cnt;
+  uint32_t* rows_out;   // optional: plain rows (full_scan_tbr), capacity rows_cap
+  uint64_t rows_cap;
+  uint32_t all_rows;    // 1: ignore k (full scan)
+};
+void launch_first_k(const FirstKArgs& a, cudaStream_t st);
+
+// ---- K6: sign-quant pre-selection narrowing the mask (quantizer.cpp:100-138) ----
+struct QuantArgs {
+  const uint64_t* sigs;  // [n_rows][nw]
+  uint32_t nw, num_bits;
+  const uint64_t* qsig;  // [B][nw]
+  const QParam* qp;
+  uint32_t B, words, n_chunks, n_rows;
+  uint32_t* mask;
+  uint32_t* chunk_cnt;
+  uint32_t* n_elig;
+  uint32_t* hist;       // [B][num_bits + 1]
+  uint32_t* tsel;       // [B][2]: threshold score t, number of ==t rows to keep
+  uint32_t* eq_cnt;     // [B][n_chunks] ==t rows per chunk
+};
+void launch_quant(const QuantArgs& a, cudaStream_t st);
+
+// ---- stage helpers ----
+void launch_gather_scores(const void* emb, bool bf16, uint32_t dp, uint32_t row_base,
+                          const float* q, const uint32_t* rows, uint64_t n, float* out,
+                          cudaStream_t st);
+void launch_make_keys(const uint32_t* rows, const float* scores, uint64_t n, uint64_t* keys,
+                      cudaStream_t st);
+void launch_quant_keys(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uint32_t row_base,
+                       const uint64_t* qsig, const uint32_t* rows, uint64_t n, uint64_t* keys,
+                       cudaStream_t st);
+void launch_keys_to_rows_sorted(uint64_t* keys, uint32_t n, cudaStream_t st);
+
+}  // namespace hyreb

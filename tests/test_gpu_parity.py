@@ -1,0 +1,373 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Mirrors the reference's hot-path suites (proj/tests/test_term_match.cpp,
+test_knn.cpp, test_pipeline.cpp, acceptance.cpp #1/#2/#4/#5) with the
+tolerance policy of tests/parity.py for floating-point scores and bit-exact
+checks for eligibility sets, term-only row lists and quant survivor sets.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import hyre_oracle as O
+from tests.helpers import corpus_pair, hits, product_index, to_cnf
+from tests.parity import assert_topk_match
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hy():
+    import paper_2402_13435_b200 as hy
+    return hy
+
+
+def appendix_index(hy):
+    b = hy.IndexBuilder(hy.IndexConfig(2, 5, 2, ["geo", "skill"]))
+    b.add_document(hy.DocumentInput("doc1", [[934, 2934], [945, 342, 3112]], [1.0, 0.0]))
+    b.add_document(hy.DocumentInput("doc2", [[129], [9342, 234]], [0.0, 1.0]))
+    return b.freeze(hy.make_codec(2, 16, 7))
+
+
+def rows_of(ms):
+    return [m.row_id for m in ms]
+
+
+# ---------------------------------------------------------------- term match
+def test_conjunctive_scan_on_the_two_document_fixture(hy):
+    # test_term_match.cpp:71-89
+    index = appendix_index(hy)
+    assert rows_of(hy.full_scan_tbr(index, hy.normalize_query({0: [129], 1: [234]}, 2))) == [1]
+    assert hy.full_scan_tbr(index, hy.normalize_query({0: [129], 1: [945]}, 2)) == []
+    assert rows_of(hy.full_scan_tbr(index, hy.normalize_query({1: [234, 342]}, 2))) == [0, 1]
+    assert rows_of(hy.full_scan_tbr(index, hy.normalize_query({}, 2))) == [0, 1]
+
+
+def test_a_clause_over_an_empty_slot_cannot_match(hy):
+    # test_term_match.cpp:91-107
+    b = hy.IndexBuilder(hy.IndexConfig(2, 2, 2))
+    b.add_document(hy.DocumentInput("sparse", [[7], []], [1.0, 0.0]))
+    index = b.freeze(hy.make_codec(2, 16, 7))
+    assert hy.full_scan_tbr(index, hy.normalize_query({1: [7]}, 2)) == []
+    assert rows_of(hy.full_scan_tbr(index, hy.normalize_query({0: [7]}, 2))) == [0]
+
+
+def test_messengers_carry_the_requested_batch_id(hy):
+    index = appendix_index(hy)
+    ms = hy.full_scan_tbr(index, hy.normalize_query({}, 2), 3)
+    assert len(ms) == 2 and all(m.batch_id == 3 and m.score == 0.0 for m in ms)
+
+
+def test_full_scan_agrees_with_hash_set_reference_on_random_corpora(hy):
+    # test_term_match.cpp:119-132 (200 corpora, bit-exact row sets)
+    spec = O.CorpusSpec(num_docs=60, num_clauses=3, attr_universe=12)
+    rng = O.MT19937_64(99)
+    for trial in range(200):
+        spec.seed = 1000 + trial
+        docs, ref, prod = corpus_pair(spec)
+        q = O.random_query(spec, rng)
+        got = rows_of(hy.full_scan_tbr(prod, to_cnf(q)))
+        assert got == O.reference_tbr(docs, q).tolist(), trial
+
+
+def test_tbr_bitexact_large_mixed_bitmap_and_csr_terms(hy):
+    # 200K rows, Zipf-like id popularity so both dense (bitmap) and sparse (CSR) terms occur.
+    n, C = 200_000, 3
+    rs = np.random.default_rng(5)
+    docs = []
+    for i in range(n):
+        cl = []
+        for c in range(C):
+            k = rs.integers(0, 4)
+            cl.append((1 + np.minimum(rs.zipf(1.3, size=k), 5000)).tolist())
+        docs.append(O.Doc(f"d{i}", cl, np.ones(4, np.float32)))
+    width = max(sum(len(set(c)) for c in d.clauses) for d in docs)
+    prod = product_index(docs, C, width, 4, 64, 1)
+    ref = O.freeze(docs, C, width, 4, 64, 1)
+    st = prod.device().stats()
+    assert st["bitmap_terms"] > 0 and st["csr_terms"] > 0, st
+    for t in range(12):
+        raw = {c: (1 + np.minimum(rs.zipf(1.3, size=rs.integers(1, 6)), 5000)).tolist()
+               for c in range(C) if rs.random() < 0.7}
+        q = O.normalize_query(raw, C)
+        got = prod.device() and hy.Executor(prod, 4).full_scan_rows(to_cnf(q))
+        assert np.array_equal(got, O.full_scan_tbr(ref, q)), t
+
+
+# ---------------------------------------------------------------- scoring / selection
+def test_exact_scores_within_tolerance_and_renorm_flag(hy):
+    spec = O.CorpusSpec(num_docs=40, dim=8, num_clauses=1, seed=9)
+    docs, ref, prod = corpus_pair(spec)
+    raw = np.zeros(8, np.float32)
+    raw[0], raw[1] = 3.0, 4.0
+    all_ = [hy.Messenger(r, 0) for r in range(40)]
+    s = hy.exact_scores(prod, raw, all_)
+    assert s.query_was_renormalized
+    want, _ = O.exact_scores(ref, raw, np.arange(40))
+    got = np.asarray([m.score for m in s.items], np.float32)
+    assert np.all(np.abs(got - want) <= np.maximum(1e-3 * np.abs(want), 2e-5))
+    u = O.random_unit_vector(8, O.MT19937_64(2))
+    assert not hy.exact_scores(prod, u, all_).query_was_renormalized
+    with pytest.raises(hy.ValidationError, match="query embedding dim 2 != index dim 8"):
+        hy.exact_scores(prod, [1.0, 0.0], [])
+
+
+def test_scores_stay_inside_unit_interval_for_self_similarity(hy):
+    spec = O.CorpusSpec(num_docs=40, dim=8, num_clauses=1, seed=9)
+    docs, ref, prod = corpus_pair(spec)
+    all_ = [hy.Messenger(r, 0) for r in range(40)]
+    for r in range(40):
+        s = hy.exact_scores(prod, prod.embedding_row(r), all_)
+        sc = np.asarray([m.score for m in s.items])
+        assert (sc <= 1.0).all() and (sc >= -1.0).all()
+        assert s.items[r].score >= 0.999999
+
+
+def _scored(hy, scores):
+    return hy.ScoredMessengers([hy.Messenger(r, 0, float(np.float32(s))) for r, s in enumerate(scores)])
+
+
+def test_bucket_selection_known_answers(hy):
+    # test_knn.cpp:94-143
+    spec = O.CorpusSpec(num_docs=8, dim=8, num_clauses=1)
+    _, _, prod = corpus_pair(spec)
+    top = hy.bucket_top_k(prod, _scored(hy, [0.9, 0.1, 0.5]), 2)
+    assert [h.row_id for h in top.hits] == [0, 2]
+    assert [h.score for h in top.hits] == [np.float32(0.9), np.float32(0.5)]
+    assert top.hits[0].doc_id == prod.doc_id(0)
+    assert [h.row_id for h in hy.bucket_top_k(prod, _scored(hy, [0.5, 0.7, 0.5, 0.7, 0.5, -0.2]), 4).hits] == [1, 3, 0, 2]
+    assert [h.row_id for h in hy.bucket_top_k(prod, _scored(hy, [0.1, 0.9, 0.4]), 10).hits] == [1, 2, 0]
+    assert hy.bucket_top_k(prod, hy.ScoredMessengers(), 5).hits == []
+    with pytest.raises(hy.ValidationError):
+        hy.bucket_top_k(prod, _scored(hy, [0.1, 0.2, 0.3]), 0)
+    with pytest.raises(hy.ValidationError):
+        hy.bucket_top_k(prod, _scored(hy, [0.1, 0.2, 0.3]), 2, 0)
+    with pytest.raises(hy.ScoreDomainError):
+        hy.bucket_top_k(prod, _scored(hy, [0.5, 1.5]), 1)
+    with pytest.raises(hy.ScoreDomainError):
+        hy.bucket_top_k(prod, _scored(hy, [-1.01, 0.0]), 1)
+    top = hy.bucket_top_k(prod, _scored(hy, [1.0, -1.0, 0.0, 1.0]), 4)
+    assert [h.row_id for h in top.hits] == [0, 3, 2, 1]
+    assert [h.score for h in top.hits] == [1.0, 1.0, 0.0, -1.0]
+
+
+def test_bucket_selection_matches_full_sort_with_planted_ties(hy):
+    # test_knn.cpp:145-171 -- selection is exact integer/float work: bit-exact.
+    spec = O.CorpusSpec(num_docs=500, dim=8, num_clauses=1, seed=77)
+    _, _, prod = corpus_pair(spec)
+    rng = O.MT19937_64(123)
+    for g in (1, 2, 100):
+        for k in (1, 7, 100, 499, 500):
+            s = np.asarray([np.float32(2.0 * O.unit_uniform(rng) - 1.0) for _ in range(500)], np.float32)
+            s[17] = s[401] = s[88]
+            top = hy.bucket_top_k(prod, _scored(hy, s), k, g)
+            er, es = O.top_k(np.arange(500), s, k, g)
+            assert [h.row_id for h in top.hits] == er.tolist()
+            assert np.array_equal(np.asarray([h.score for h in top.hits], np.float32), es)
+
+
+def test_bucket_selection_million_scores_k2000(hy):
+    # acceptance.cpp:271-319 (#4): top-2000 of 1M random scores == full sort.
+    spec = O.CorpusSpec(num_docs=8, dim=8, num_clauses=1)
+    _, _, prod = corpus_pair(spec)
+    ex = hy.Executor(prod, 1)
+    rs = np.random.default_rng(555)
+    n, k = 1_000_000, 2000
+    s = (2.0 * rs.random(n) - 1.0).astype(np.float32)
+    rows = np.arange(n, dtype=np.uint32)
+    import ctypes as C
+    from paper_2402_13435_b200 import _lib as L
+    out = (L.hyre_hit * k)()
+    cnt = C.c_uint32()
+    rc = L.lib().hyre_bucket_top_k(ex._h, rows.ctypes.data_as(L.u32p), s.ctypes.data_as(L.f32p), n, k, 100, out,
+                                   C.byref(cnt))
+    assert rc == 0
+    er, es = O.top_k(rows, s, k)
+    assert [out[i].row for i in range(cnt.value)] == er.tolist()
+
+
+# ---------------------------------------------------------------- pipeline
+def addressable_corpus(hy, n, dim=8, seed=3):
+    rng = O.MT19937_64(seed)
+    docs = [O.Doc(f"doc{r}", [[r + 1]], O.random_unit_vector(dim, rng)) for r in range(n)]
+    return docs, product_index(docs, 1, 1, dim, 64, seed + 500), O.freeze(docs, 1, 1, dim, 64, seed + 500)
+
+
+def rows_query(hy, rows):
+    return hy.normalize_query({0: [r + 1 for r in rows]}, 1)
+
+
+def test_term_only_queries_return_matches_in_row_order_with_zero_scores(hy):
+    _, prod, _ = addressable_corpus(hy, 10)
+    q = hy.HybridQuery(rows_query(hy, [7, 2, 5]), None, 2)
+    r = hy.execute(prod, q)
+    assert [h.row_id for h in r.hits] == [2, 5] and all(h.score == 0.0 for h in r.hits)
+    q.k = 10
+    assert [h.row_id for h in hy.execute(prod, q).hits] == [2, 5, 7]
+
+
+def test_no_term_matches_yields_an_empty_result(hy):
+    _, prod, _ = addressable_corpus(hy, 4)
+    q = hy.HybridQuery(hy.normalize_query({0: [999]}, 1), O.random_unit_vector(8, O.MT19937_64(1)), 3)
+    assert hy.execute(prod, q).hits == []
+
+
+def test_hybrid_execution_equals_filter_score_full_sort(hy):
+    # test_pipeline.cpp:124-150 (40 trials)
+    spec = O.CorpusSpec(num_docs=300, dim=12, num_clauses=2, attr_universe=10)
+    rng = O.MT19937_64(41)
+    for trial in range(40):
+        spec.seed = 500 + trial
+        docs, ref, prod = corpus_pair(spec)
+        terms = O.random_query(spec, rng)
+        raw = np.asarray([np.float32(4.0 * O.unit_uniform(rng) - 2.0) for _ in range(spec.dim)], np.float32)
+        q = hy.HybridQuery(to_cnf(terms), raw, 10, hy.ExecOptions(quant_enabled=False))
+        gr, gs = hits(hy.execute(prod, q))
+        er, es = O.execute(ref, terms, raw, 10, quant_enabled=False)
+        assert_topk_match(ref, raw, gr, gs, er, es)
+
+
+def test_exact_retrieval_acceptance_1(hy):
+    # acceptance.cpp:78-119: 200 queries on a 10k x 64 index, k in [1, 20], some raw-scaled.
+    spec = O.CorpusSpec(num_docs=10000, dim=64, num_clauses=2, max_attrs_per_clause=4, attr_universe=50,
+                        num_bits=64, seed=11)
+    docs, ref, prod = corpus_pair(spec)
+    ex = hy.Executor(prod, 16)
+    rng = O.MT19937_64(123)
+    for t in range(200):
+        terms = O.random_query(spec, rng)
+        raw = O.random_unit_vector(spec.dim, rng)
+        if t % 3 == 0:
+            raw = raw * np.float32(1.75)
+        k = 1 + rng() % 20
+        q = hy.HybridQuery(to_cnf(terms), raw, k, hy.ExecOptions(quant_enabled=False))
+        gr, gs = hits(ex.execute(q))
+        er, es = O.execute(ref, terms, raw, k, quant_enabled=False)
+        assert_topk_match(ref, raw, gr, gs, er, es)
+        res = ex.execute(q)
+        assert all(h.doc_id == prod.doc_id(h.row_id) for h in res.hits)
+
+
+def test_quantized_preselection_is_bit_exact_with_the_reference(hy):
+    # Quant survivors are integer work: the GPU survivor set must equal the
+    # reference's nth_element selection, so hybrid results agree as usual.
+    spec = O.CorpusSpec(num_docs=4000, dim=16, num_bits=256, num_clauses=1, max_attrs_per_clause=1,
+                        attr_universe=2, seed=7)
+    docs, ref, prod = corpus_pair(spec)
+    rng = O.MT19937_64(13)
+    for t in range(20):
+        raw = O.random_unit_vector(spec.dim, rng)
+        terms = O.normalize_query({0: [1]}, 1) if t % 2 else []
+        qk = [60, 200, 1000, 0][t % 4]
+        k = 1 + t
+        q = hy.HybridQuery(to_cnf(terms), raw, k, hy.ExecOptions(quant_enabled=True, quant_k=qk))
+        gr, gs = hits(hy.execute(prod, q))
+        er, es = O.execute(ref, terms, raw, k, quant_enabled=True, quant_k=qk)
+        assert_topk_match(ref, raw, gr, gs, er, es)
+
+
+def test_preselect_keeps_exactly_the_top_quant_k(hy):
+    # test_quantizer.cpp:220-277
+    spec = O.CorpusSpec(num_docs=120, dim=16, num_bits=64, seed=31)
+    docs, ref, prod = corpus_pair(spec)
+    qvec = O.random_unit_vector(spec.dim, O.MT19937_64(8))
+    qsig = hy.encode(prod.codec(), qvec)
+    cands = [hy.Messenger(r, 0) for r in range(120)]
+    kept = hy.preselect(prod, qsig, cands, 200)
+    assert [m.row_id for m in kept] == list(range(120))
+    for qk in (1, 7, 40, 119):
+        kept = hy.preselect(prod, qsig, cands, qk)
+        assert [m.row_id for m in kept] == O.preselect(ref, qsig.words, np.arange(120), qk).tolist()
+    with pytest.raises(hy.ValidationError):
+        hy.preselect(prod, qsig, cands, 0)
+
+
+def test_batch_execution_matches_single_execution(hy):
+    # test_pipeline.cpp:237-275 -- batch transparency is exact on the GPU too
+    # (the same kernels score a row whatever batch it is in).
+    spec = O.CorpusSpec(num_docs=250, dim=12, num_clauses=2, attr_universe=8)
+    rng = O.MT19937_64(71)
+    for trial in range(50):
+        spec.seed = 900 + trial
+        docs, ref, prod = corpus_pair(spec)
+        ex = hy.Executor(prod, 8)
+        b = 1 + rng() % 8
+        batch = hy.BatchRequest()
+        for _ in range(b):
+            terms = O.random_query(spec, rng)
+            emb = None
+            if rng() % 4 != 0:
+                emb = np.asarray([np.float32(2.0 * O.unit_uniform(rng) - 1.0) for _ in range(spec.dim)],
+                                 np.float32)
+            k = 1 + rng() % 12
+            qe = rng() % 2 == 0
+            qk = 20 + rng() % 100
+            batch.queries.append(hy.HybridQuery(to_cnf(terms), emb, k, hy.ExecOptions(qe, qk)))
+        outs = ex.execute_batch(batch)
+        for q, o in zip(batch.queries, outs):
+            assert o.ok
+            single = ex.execute(q)
+            assert [(h.row_id, h.score) for h in o.result.hits] == [(h.row_id, h.score) for h in single.hits]
+            terms = [(c.slot, c.attribute_ids) for c in q.terms.clauses]
+            er, es = O.execute(ref, terms, q.embedding, q.k, q.options.quant_enabled, q.options.quant_k)
+            gr, gs = hits(o.result)
+            if q.embedding is None:
+                assert gr.tolist() == er.tolist()
+            else:
+                assert_topk_match(ref, q.embedding, gr, gs, er, es)
+
+
+def test_a_malformed_query_fails_its_slot_not_the_batch(hy):
+    _, prod, _ = addressable_corpus(hy, 10)
+    ex = hy.Executor(prod, 4)
+    batch = hy.BatchRequest([hy.HybridQuery(rows_query(hy, [1, 2]), None, 2), hy.HybridQuery(k=0),
+                             hy.HybridQuery(rows_query(hy, [3]), None, 1)])
+    outs = ex.execute_batch(batch)
+    assert outs[0].ok and [h.row_id for h in outs[0].result.hits] == [1, 2]
+    assert not outs[1].ok and outs[1].error == "k must be >= 1"
+    assert outs[2].ok and [h.row_id for h in outs[2].result.hits] == [3]
+
+
+def test_batch_size_limits_are_enforced(hy):
+    _, prod, _ = addressable_corpus(hy, 4)
+    ex = hy.Executor(prod, 2)
+    with pytest.raises(hy.ValidationError):
+        ex.execute_batch(hy.BatchRequest())
+    with pytest.raises(hy.ValidationError, match="batch size 3 exceeds maxBatch 2"):
+        ex.execute_batch(hy.BatchRequest([hy.HybridQuery(rows_query(hy, [1]), None, 1)] * 3))
+
+
+def test_executor_scratch_does_not_leak_state_across_calls(hy):
+    docs, prod, ref = addressable_corpus(hy, 60, 8, 21)
+    reused = hy.Executor(prod, 4)
+    rng = O.MT19937_64(17)
+    for rnd in range(10):
+        rows = [r for r in range(60) if rng() % 3 == 0] or [0]
+        q = hy.HybridQuery(rows_query(hy, rows), O.random_unit_vector(8, rng), 5,
+                           hy.ExecOptions(quant_enabled=(rnd % 2 == 0), quant_k=10))
+        fresh = hy.Executor(prod, 4)
+        assert reused.execute(q) == fresh.execute(q)
+        a = reused.execute_batch(hy.BatchRequest([q, q, q]))
+        b = fresh.execute_batch(hy.BatchRequest([q, q, q]))
+        assert [(x.ok, x.result) for x in a] == [(x.ok, x.result) for x in b]
+
+
+def test_zero_query_scores_everything_zero_rows_ascending(hy):
+    _, prod, _ = addressable_corpus(hy, 50)
+    q = hy.HybridQuery(hy.CnfQuery(), np.zeros(8, np.float32), 7, hy.ExecOptions(quant_enabled=False))
+    r = hy.execute(prod, q)
+    assert [h.row_id for h in r.hits] == list(range(7)) and all(h.score == 0.0 for h in r.hits)
+
+
+def test_k_larger_than_corpus_returns_everything(hy):
+    spec = O.CorpusSpec(num_docs=400, dim=16, num_bits=256, num_clauses=1, max_attrs_per_clause=1, attr_universe=2,
+                        seed=7)
+    docs, ref, prod = corpus_pair(spec)
+    raw = O.random_unit_vector(16, O.MT19937_64(13))
+    q = hy.HybridQuery(hy.CnfQuery(), raw, 1000, hy.ExecOptions(quant_enabled=False))
+    gr, gs = hits(hy.execute(prod, q))
+    er, es = O.execute(ref, [], raw, 1000, quant_enabled=False)
+    assert len(gr) == 400
+    assert_topk_match(ref, raw, gr, gs, er, es)

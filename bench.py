@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the north-star path: exhaustive fused CNF term match +
+embedding KNN + top-K on B200.
+
+Default workload = BASELINE.json's metric config c3: 10M jobs, d=128 fp32,
+8-clause CNF (~5% selectivity), batch B=64 queries, K=100, quant
+pre-selection off (the exhaustive path).  A "step" is one execute_batch of
+the B queries over the whole index.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Our arm prints one JSON line with the device-timed whole-job QPS (`value`,
+index + queries resident in HBM), the end-to-end QPS through the C-ABI with
+host buffers (`e2e`), p50 call latency, the roofline of the dominant kernel
+and the reference CPU baseline.  `--impl reference` times the reference's
+own CPU implementation (oracle/_ref, the unmodified reference sources) on a
+bounded sample of the same workload.
+
+Multi-GPU (torchrun, one rank per GPU): the 10M rows are sharded by
+contiguous row ranges (strong scaling); each rank scores its shard, the
+per-shard top-K lists are all-gathered over NCCL and merged exactly on
+device (K4) -- the one collective of the path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md: sample nvidia-smi DURING the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def shard_range(n, rank, world):
+    return rank * n // world, (rank + 1) * n // world
+
+
+# ---------------------------------------------------------------------------
+# reference (CPU) arm
+# ---------------------------------------------------------------------------
+def reference_sample(w, sample_rows: int, batch: int, k: int, threads: int, steps: int = 1):
+    """Times the unmodified reference (oracle/_ref) Executor::execute with
+    quant off over a `sample_rows`-row prefix of the same corpus and the same
+    queries; `threads` executors over one FrozenIndex, like the reference's
+    ExecutorPool (proj/src/service.cpp:99-141).  Returns (qps scaled to the
+    full index, seconds per step, info)."""
+    from oracle import ref as R
+    from paper_2402_13435_b200 import workloads as W
+    so, ids, emb = W.docs(w, 0, sample_rows)
+    t0 = time.perf_counter()
+    ri = R.RefIndex.build(so.astype(np.uint32), ids, emb, w.num_clauses, w.max_num_attr, w.num_bits, w.seed, "d")
+    build_s = time.perf_counter() - t0
+    raws, qemb = W.queries(w, batch)
+    qs = []
+    for i, raw in enumerate(raws):
+        clauses = R.normalize_query(raw, w.num_clauses) if raw else []
+        qs.append((clauses, qemb[i] if qemb is not None else None, k, False, 0, 100))
+    per_step = []
+    for _ in range(steps):
+        secs, _ = ri.execute_parallel(qs, threads, want_hits=False)
+        per_step.append(secs)
+    scale = w.n / sample_rows  # the reference's full scan is linear in rows
+    qps = batch / (statistics.median(per_step) * scale)
+    return qps, per_step, build_s
+
+
+def run_reference(args, w):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = min(args.ref_sample_rows, w.n)
+    qps, per_step, build_s = reference_sample(w, sample, args.batch, args.k, threads, steps=max(1, args.steps))
+    line = {
+        "impl": "reference", "metric": "queries_per_sec", "value": qps, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(per_step) * 1e3 * (w.n / sample),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SURVEY §8(d) generator, std::mt19937_64)",
+        "config": workload_config(w, args),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample}-row prefix of {w.name} ({sample / w.n:.0%} of {w.n} rows), "
+                                   f"{args.batch} queries per step via Executor::execute with quant off on "
+                                   f"{threads} threads (ExecutorPool model); QPS scaled by rows "
+                                   f"({w.n}/{sample}); reference IndexBuilder build {build_s:.1f}s"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, args):
+    return {"workload": f"{w.name}: {w.n} jobs x d{w.dim} {w.dtype}, "
+                        + ("match-all" if w.kind == "match_all" else f"{w.num_clauses}-clause CNF"),
+            "jobs": w.n, "dim": w.dim, "emb_dtype": w.dtype, "clauses": w.num_clauses, "batch": args.batch,
+            "k": args.k, "quant": False, "parallelism": f"rows-sharded x{dist_env()[1]}",
+            "l2": "inputs larger than L2 (index >> 126 MB), no flush"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, w):
+    import torch
+
+    import paper_2402_13435_b200 as hy
+    from paper_2402_13435_b200 import _lib as L
+    from paper_2402_13435_b200 import workloads as W
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = L.lib()
+    t_setup = time.perf_counter()
+    rb, re_ = shard_range(w.n, rank, world)
+    frozen = W.build_frozen(w, rb, re_)
+    t_frozen = time.perf_counter() - t_setup
+    dev = hy.DeviceIndex(frozen, device=local, dtype=w.dtype, tensor_path=True, row_offset=rb)
+    stats = dev.stats()
+    raws, qemb = W.queries(w, args.batch)
+    hq = []
+    for i, raw in enumerate(raws):
+        hq.append(hy.HybridQuery(hy.normalize_query(raw, w.num_clauses), None if qemb is None else qemb[i],
+                                 args.k, hy.ExecOptions(quant_enabled=False)))
+    ex = hy.Executor(dev, max_batch=args.batch)
+    h = ex._h
+    pack = hy.QueryPack(hq)
+    B = args.batch
+
+    def check(rc):
+        hy.hyre._check(rc)
+
+    check(lib.hyre_batch_prepare(h, pack.arr, B))
+    stream = torch.cuda.ExternalStream(lib.hyre_executor_stream(h), device=torch.device("cuda", local))
+
+    gather = None
+    if world > 1:
+        import torch.distributed as dist
+        hits_p, n_hits, off_p, cnt_p = C.c_void_p(), C.c_uint64(), C.c_void_p(), C.c_void_p()
+        check(lib.hyre_batch_device_results(h, C.byref(hits_p), C.byref(n_hits), C.byref(off_p), C.byref(cnt_p)))
+
+        class Dev:
+            def __init__(self, ptr, shape, typestr):
+                self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "stream": None}
+
+        n_words = int(n_hits.value) * 2  # hyre_hit = 2 x u32
+        t_hits = torch.as_tensor(Dev(hits_p.value, (n_words,), "<i4"), device=f"cuda:{local}")
+        t_off = torch.as_tensor(Dev(off_p.value, (B,), "<i8"), device=f"cuda:{local}")
+        t_cnt = torch.as_tensor(Dev(cnt_p.value, (B,), "<i4"), device=f"cuda:{local}")
+        # identical shapes on every rank: pad to the max hit buffer
+        n_max = torch.tensor([n_words], device=f"cuda:{local}")
+        dist.all_reduce(n_max, op=dist.ReduceOp.MAX)
+        n_max = int(n_max.item())
+        g_hits = torch.zeros(world, n_max, dtype=torch.int32, device=f"cuda:{local}")
+        g_off = torch.zeros(world, B, dtype=torch.int64, device=f"cuda:{local}")
+        g_cnt = torch.zeros(world, B, dtype=torch.int32, device=f"cuda:{local}")
+        pad = torch.zeros(n_max, dtype=torch.int32, device=f"cuda:{local}")
+
+        def gather():
+            with torch.cuda.stream(stream):
+                pad[:n_words].copy_(t_hits)
+                dist.all_gather_into_tensor(g_hits.view(-1), pad)
+                dist.all_gather_into_tensor(g_off.view(-1), t_off)
+                dist.all_gather_into_tensor(g_cnt.view(-1), t_cnt)
+            check(lib.hyre_batch_merge_gathered(h, g_hits.data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), world,
+                                                n_max // 2))
+
+    def step():
+        check(lib.hyre_batch_run(h))
+        if gather:
+            gather()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- warm-up -----------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    s6 = (C.c_float * 6)()
+
+    # ---- timed region: exactly K back-to-back steps, device time ----------
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    total_ms = e0.elapsed_time(e1)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    kernels_per_step = int(lib.hyre_batch_kernel_count(h)) + (1 if gather else 0)
+
+    # ---- per-call latency + per-kernel times (separately, synced per step) -
+    lat, main_ms, stage_rows = [], [], []
+    for _ in range(max(args.steps, 10)):
+        check(lib.hyre_batch_run(h))
+        check(lib.hyre_batch_stage_ms(h, s6))
+        stage_rows.append(list(s6))
+        lat.append(s6[5])
+        main_ms.append(s6[3])
+    p50 = statistics.median(lat)
+    main_avg = statistics.mean(main_ms)
+
+    # ---- end-to-end through the C-ABI with host buffers ---------------------
+    caps = [min(args.k, re_ - rb)] * B
+    offs = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.uint64)
+    host_hits = (L.hyre_hit * sum(caps))()
+    counts = np.zeros(B, np.uint32)
+    sts = np.zeros(B, np.int32)
+    tim = L.hyre_timings()
+    e2e_steps = max(3, args.steps // 2)
+
+    def e2e_call():
+        if world == 1:
+            check(lib.hyre_execute_batch(h, pack.arr, B, host_hits, offs.ctypes.data_as(L.u64p),
+                                         counts.ctypes.data_as(L.u32p), sts.ctypes.data_as(L.i32p), C.byref(tim)))
+        else:
+            # host queries -> device; shard results -> all ranks (NCCL) -> exact device merge -> host
+            check(lib.hyre_batch_prepare(h, pack.arr, B))
+            check(lib.hyre_batch_run(h))
+            gather()
+            check(lib.hyre_batch_fetch(h, host_hits, offs.ctypes.data_as(L.u64p), counts.ctypes.data_as(L.u32p),
+                                       sts.ctypes.data_as(L.i32p), None))
+
+    e2e_call()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    h2d, d2h = C.c_uint64(), C.c_uint64()
+    check(lib.hyre_batch_io_bytes(h, C.byref(h2d), C.byref(d2h)))
+    assert all(sts == 0) and int(counts.min()) > 0, "empty results in the e2e run"
+
+    if rank != 0:
+        return
+    hbm, _, peak_kind = peaks()
+    n_local = re_ - rb
+    elem = 2 if w.dtype == "bf16" else 4
+    # algorithmic bytes of one main-scorer launch: every row of the shard once
+    # (batched: U = N; the tensor path reads the bf16 hi+lo split = 4 B/elem)
+    # plus the B mask bitmaps it consumes.
+    words = (n_local + 31) // 32
+    bytes_main = n_local * w.dim * elem + B * words * 4
+    achieved = bytes_main / (main_avg * 1e-3) / 1e9
+    traffic = load_traffic(w.name)
+    step_ms = total_ms / args.steps
+    qps = B * args.steps / (total_ms * 1e-3)
+    line = {
+        "metric": "queries_per_sec", "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "p50_ms": p50, "jobs_scored_per_sec": qps * w.n,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic (SURVEY §8(d) generator, std::mt19937_64; index built by the product IndexBuilder)",
+        "config": workload_config(w, args),
+        "stages_ms": dict(zip(["mask", "quant", "sample", "main_scorer", "select_firstk", "run"],
+                              [statistics.median(r[i] for r in stage_rows) for i in range(6)])),
+        "roofline": {"bound": "hbm", "kernel": main_kernel_name(B), "achieved": achieved, "peak": hbm,
+                     "peak_kind": f"{peak_kind} hbm_gbs (burst copy)", "unit": "GB/s", "frac": achieved / hbm,
+                     "bytes_per_launch": bytes_main, "launch_ms": main_avg, "traffic": traffic},
+        "e2e": {"value": B * e2e_steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
+                "d2h_bytes_per_step": int(d2h.value), "api": "hyre_execute_batch (C-ABI, host buffers)"},
+        "gpu_launches": kernels_per_step * args.steps,
+        "clocks": clocks.summary(),
+        "index": {"build_s": t_frozen, **{k: stats[k] for k in ("num_terms", "bitmap_terms", "csr_terms")}},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            sample = min(args.ref_sample_rows, w.n)
+            cqps, per_step, build_s = reference_sample(w, sample, B, args.k, threads)
+            line["cpu_baseline"] = {
+                "value": cqps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                "sample": f"{sample}-row prefix of {w.name}, {B} queries via the reference Executor::execute "
+                          f"(quant off) on {threads} threads; QPS scaled by rows ({w.n}/{sample})"}
+        except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def main_kernel_name(B):
+    return "score_kernel (K2, CUDA-core streaming scorer)"
+
+
+def load_traffic(name):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--rows", type=int, default=None, help="override the workload's row count")
+    ap.add_argument("--ref-sample-rows", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2402_13435_b200.workloads import WORKLOADS
+    import dataclasses
+    w = WORKLOADS[args.workload]
+    if args.rows:
+        w = dataclasses.replace(w, n=args.rows)
+    args.batch = args.batch or w.batch
+    args.k = args.k or w.k
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

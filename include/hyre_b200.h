@@ -193,6 +193,8 @@ typedef struct hyre_index_options {
   uint32_t row_begin;    /* shard [row_begin, row_end) of the frozen rows; */
   uint32_t row_end;      /* row_end == 0 => all rows */
   uint32_t tensor_path;  /* 1: also store the bf16 (hi, lo) split for tcgen05 batches */
+  uint32_t row_offset;   /* added to every reported row: global id of the frozen's row 0
+                            (a rank that froze only its own shard of a larger corpus) */
 } hyre_index_options;
 
 typedef struct hyre_index_stats {
@@ -245,6 +247,23 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
                              uint32_t* counts, int32_t* statuses, hyre_timings* timings);
 /* Number of kernels the last hyre_batch_run enqueued. */
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
+/* CUDA-event durations (ms) of the last run, waiting for it to finish:
+ * [0] K1 mask (+CSR scatter) [1] K6 quant [2] sample pass + K-th select
+ * [3] main scorer (K2/K3) [4] final select + first-K [5] whole run. */
+hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6);
+/* Device pointers of the last run's results (for on-device multi-GPU
+ * gathers): hits (hyre_hit[*n_hits]), per-slot hit offsets (u64[b]) and
+ * per-slot counts (u32[b]).  Valid until the next prepare. */
+hyre_status hyre_batch_device_results(hyre_executor* ex, void** hits, uint64_t* n_hits, void** offsets,
+                                      void** counts);
+/* Bytes the last prepare copied host->device and the last fetch copied back. */
+hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h);
+/* Exact on-device merge of G shard result sets gathered from the executors of
+ * every shard (same batch): g_hits [G][hits_stride] hyre_hit, g_offsets [G][b]
+ * u64 and g_counts [G][b] u32 (the hyre_batch_device_results layouts).  The
+ * merged top-K replaces this executor's results; fetch them as usual. */
+hyre_status hyre_batch_merge_gathered(hyre_executor* ex, const void* g_hits, const void* g_offsets,
+                                      const void* g_counts, uint32_t n_lists, uint64_t hits_stride);
 
 /* Stage entry points (public in the reference and used by its tests). */
 /* full_scan_tbr (term_match.hpp:43-45): ascending eligible rows (global ids). */

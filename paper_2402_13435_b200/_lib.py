@@ -55,7 +55,7 @@ class hyre_shape(C.Structure):
 
 class hyre_index_options(C.Structure):
     _fields_ = [("device", C.c_int32), ("emb_dtype", C.c_uint32), ("row_begin", C.c_uint32),
-                ("row_end", C.c_uint32), ("tensor_path", C.c_uint32)]
+                ("row_end", C.c_uint32), ("tensor_path", C.c_uint32), ("row_offset", C.c_uint32)]
 
 
 class hyre_index_stats(C.Structure):
@@ -110,6 +110,10 @@ SIGNATURES = {
     "hyre_batch_run": (C.c_int, [vp]),
     "hyre_batch_fetch": (C.c_int, [vp, C.POINTER(hyre_hit), u64p, u32p, i32p, C.POINTER(hyre_timings)]),
     "hyre_batch_kernel_count": (C.c_uint32, [vp]),
+    "hyre_batch_stage_ms": (C.c_int, [vp, f32p]),
+    "hyre_batch_io_bytes": (C.c_int, [vp, u64p, u64p]),
+    "hyre_batch_merge_gathered": (C.c_int, [vp, vp, vp, vp, C.c_uint32, C.c_uint64]),
+    "hyre_batch_device_results": (C.c_int, [vp, C.POINTER(vp), u64p, C.POINTER(vp), C.POINTER(vp)]),
     "hyre_full_scan_tbr": (C.c_int, [vp, C.POINTER(hyre_query), u32p, C.c_uint64, u64p]),
     "hyre_exact_scores": (C.c_int, [vp, f32p, C.c_uint32, u32p, C.c_uint64, f32p, i32p]),
     "hyre_bucket_top_k": (C.c_int, [vp, u32p, f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(hyre_hit),

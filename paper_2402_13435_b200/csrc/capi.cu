@@ -354,6 +354,43 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
 
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
 
+hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6) {
+  return guard([&] {
+    need(ex, "executor");
+    need(out6, "out");
+    ex->ex->stage_ms(out6);
+  });
+}
+
+hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h) {
+  return guard([&] {
+    need(ex, "executor");
+    if (h2d) *h2d = ex->ex->h2d_bytes;
+    if (d2h) *d2h = ex->ex->d2h_bytes;
+  });
+}
+
+hyre_status hyre_batch_merge_gathered(hyre_executor* ex, const void* g_hits, const void* g_offsets,
+                                      const void* g_counts, uint32_t n_lists, uint64_t hits_stride) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->merge_gathered(static_cast<const hyre_hit*>(g_hits), static_cast<const uint64_t*>(g_offsets),
+                           static_cast<const uint32_t*>(g_counts), n_lists, hits_stride);
+  });
+}
+
+hyre_status hyre_batch_device_results(hyre_executor* ex, void** hits, uint64_t* n_hits, void** offsets,
+                                      void** counts) {
+  return guard([&] {
+    need(ex, "executor");
+    Executor& e = *ex->ex;
+    if (hits) *hits = e.d_hits;
+    if (n_hits) *n_hits = e.n_hits_total;
+    if (offsets) *offsets = e.d_hit_off;
+    if (counts) *counts = e.d_counters + 3 * e.max_batch;
+  });
+}
+
 hyre_status hyre_full_scan_tbr(hyre_executor* ex, const hyre_query* q, uint32_t* rows, uint64_t cap,
                                uint64_t* n) {
   return guard([&] {

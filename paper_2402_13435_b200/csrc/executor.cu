@@ -305,9 +305,10 @@ void Executor::run() {
     } else {
       HYRE_CUDA(cudaMemsetAsync(d_thr, 0, sizeof(uint64_t) * B, st));
     }
+    HYRE_CUDA(cudaEventRecord(ev[3], st));
     launch_score(sa, bf16, st);
     ++kernels;
-    HYRE_CUDA(cudaEventRecord(ev[3], st));
+    HYRE_CUDA(cudaEventRecord(ev[4], st));
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap};
     launch_select(fa, st);
@@ -322,6 +323,7 @@ void Executor::run() {
     kernels += 2;
   } else {
     HYRE_CUDA(cudaEventRecord(ev[3], st));
+    HYRE_CUDA(cudaEventRecord(ev[4], st));
   }
   if (any_term_only) {
     FirstKArgs fk{d_mask, d_chunk_cnt, n_elig, d_qp, B, W, ix->n_chunks, ix->row_base, d_hit_off, d_hits,
@@ -329,7 +331,7 @@ void Executor::run() {
     launch_first_k(fk, st);
     ++kernels;
   }
-  HYRE_CUDA(cudaEventRecord(ev[4], st));
+  HYRE_CUDA(cudaEventRecord(ev[5], st));
   HYRE_CUDA(cudaGetLastError());
 }
 
@@ -375,22 +377,30 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
     if (hits && c) std::memcpy(hits + offsets[i], h_hits + hit_off[i], c * sizeof(hyre_hit));
   }
   if (t) {
-    float a = 0, b = 0, c = 0, d = 0;
-    cudaEventElapsedTime(&a, ev[0], ev[1]);
-    cudaEventElapsedTime(&b, ev[1], ev[2]);
-    cudaEventElapsedTime(&c, ev[2], ev[3]);
-    cudaEventElapsedTime(&d, ev[3], ev[4]);
-    t->tbr_ms = a;
-    t->quant_ms = b;
-    t->ebr_ms = c;
-    t->topk_ms = d;
+    float s6[6];
+    stage_ms(s6);
+    t->tbr_ms = s6[0];
+    t->quant_ms = s6[1];
+    t->ebr_ms = s6[2] + s6[3];
+    t->topk_ms = s6[4];
   }
 }
 
 float Executor::last_run_ms() const {
   float ms = 0;
-  cudaEventElapsedTime(&ms, ev[0], ev[4]);
+  cudaEventSynchronize(ev[5]);
+  cudaEventElapsedTime(&ms, ev[0], ev[5]);
   return ms;
+}
+
+void Executor::stage_ms(float* out) const {
+  cudaEventSynchronize(ev[5]);
+  for (int i = 0; i < 5; ++i) {
+    out[i] = 0;
+    cudaEventElapsedTime(out + i, ev[i], ev[i + 1]);
+  }
+  out[5] = 0;
+  cudaEventElapsedTime(out + 5, ev[0], ev[5]);
 }
 
 // ---------------------------------------------------------------------------
@@ -478,6 +488,25 @@ uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, 
                    (void*)d_p, (void*)d_t})
     cudaFree(p2);
   return cnt;
+}
+
+// Replaces this executor's results with the exact merge of G gathered shard
+// result sets (device pointers, e.g. filled by an NCCL all-gather).
+void Executor::merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
+                              uint64_t hits_stride) {
+  if (!prepared) throw Error(HYRE_INTERNAL, "merge before hyre_batch_prepare");
+  if (uint64_t{G} * max_k > cap) validation("merge needs G*k <= candidate capacity");
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  uint32_t* cand_cnt = d_counters + max_batch;
+  uint32_t* out_cnt = d_counters + 3 * max_batch;
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  launch_gather_keys(g_hits, g_off, g_cnt, G, hits_stride, B, cap, d_cand, cand_cnt, st);
+  // term-only hits carry score 0, so key order is row order: the merged
+  // first-K equals concatenating shard first-K lists in row order.
+  SelectArgs fa{d_cand, cand_cnt, cap, d_qp, cand_cnt, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
+                out_cnt, B, QF_ACTIVE, cap};
+  launch_select(fa, st);
+  HYRE_CUDA(cudaGetLastError());
 }
 
 uint64_t Executor::preselect(const uint64_t* qwords, const uint32_t* rows, uint64_t n, uint32_t quant_k,

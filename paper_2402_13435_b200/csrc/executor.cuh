@@ -17,7 +17,7 @@ struct Executor {
   DevIndex* ix;
   uint32_t max_batch;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[6] = {};  // start, mask, quant, pre-main, post-main, end
 
   // device scratch sized at construction
   uint32_t cap = 0, samp_cap = 0;
@@ -74,10 +74,13 @@ struct Executor {
   void fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* statuses,
              hyre_timings* t);
   float last_run_ms() const;
+  void stage_ms(float* out) const;  // [mask, quant, sample+kth, main score, select/first-K, total]
 
   uint64_t full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows);
   bool exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out);
   uint32_t top_k(const uint32_t* rows, const float* scores, uint64_t n, uint32_t k, hyre_hit* out);
+  void merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
+                      uint64_t hits_stride);
   uint64_t preselect(const uint64_t* qwords, const uint32_t* rows, uint64_t n, uint32_t quant_k,
                      uint32_t* out);
 

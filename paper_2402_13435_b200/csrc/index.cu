@@ -92,7 +92,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
   const uint32_t n = re - rb;
   const uint32_t C = f.num_clauses, A = f.max_num_attr, d = f.dim;
   ix->n_rows = n;
-  ix->row_base = rb;
+  ix->row_base = o.row_offset + rb;
   ix->dim = d;
   ix->emb_dtype = o.emb_dtype;
   ix->tensor_path = o.tensor_path != 0;
@@ -248,7 +248,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
   }
   HYRE_CUDA(cudaDeviceSynchronize());
   ix->stats.num_rows = n;
-  ix->stats.row_base = rb;
+  ix->stats.row_base = ix->row_base;
   ix->stats.dim = d;
   ix->stats.row_stride = dp;
   ix->stats.postings = ix->n_postings;

@@ -110,6 +110,9 @@ void launch_make_keys(const uint32_t* rows, const float* scores, uint64_t n, uin
 void launch_quant_keys(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uint32_t row_base,
                        const uint64_t* qsig, const uint32_t* rows, uint64_t n, uint64_t* keys,
                        cudaStream_t st);
-void launch_keys_to_rows_sorted(uint64_t* keys, uint32_t n, cudaStream_t st);
+// Multi-GPU merge: per query, keys of the hits of G gathered shard lists.
+void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
+                        uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys, uint32_t* cnt,
+                        cudaStream_t st);
 
 }  // namespace hyreb

@@ -345,9 +345,9 @@ class DeviceIndex:
     """The FrozenIndex (or a row shard of it) resident in one GPU's HBM."""
 
     def __init__(self, frozen: FrozenIndex, device: int = 0, dtype: str = "f32", tensor_path: bool = True,
-                 row_begin: int = 0, row_end: int = 0):
+                 row_begin: int = 0, row_end: int = 0, row_offset: int = 0):
         o = L.hyre_index_options(device, L.HYRE_EMB_BF16 if dtype == "bf16" else L.HYRE_EMB_F32, row_begin,
-                                 row_end, int(tensor_path))
+                                 row_end, int(tensor_path), row_offset)
         h = C.c_void_p()
         _check(L.lib().hyre_index_create(frozen._h, C.byref(o), C.byref(h)))
         self._h = h

@@ -381,6 +381,8 @@ def run_ours(args, w):
 
 
 def main_kernel_name(B):
+    if B > 8:
+        return "tc_score_kernel (K3: TMA -> tcgen05.mma bf16 hi/lo split, fp32 accumulation in TMEM)"
     return "score_kernel (K2, CUDA-core streaming scorer)"
 
 

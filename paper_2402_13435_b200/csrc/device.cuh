@@ -12,6 +12,7 @@
 //   sigs      N x words u64 sign-quant signatures (quantizer.hpp:34-44)
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -79,6 +80,8 @@ struct DevIndex {
   uint32_t* post_rows = nullptr;
   uint64_t n_postings = 0;
   std::unordered_map<uint64_t, Term> terms;  // key = (slot << 32) | id
+  bool has_tmaps = false;                    // TMA descriptors of emb_hi / emb_lo (K3)
+  CUtensorMap tm_hi{}, tm_lo{};
   Codec codec;
   hyre_index_stats stats{};
   ~DevIndex();

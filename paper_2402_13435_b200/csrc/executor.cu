@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <unordered_map>
 
@@ -33,6 +34,19 @@ T* dmalloc(size_t n) {
   return p;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+uint16_t bf16_rne(float f) {  // round-to-nearest-even, as __float2bfloat16_rn
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+float bf16_to_f(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 }  // namespace
 
 Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
@@ -47,6 +61,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   d_chunk_cnt = dmalloc<uint32_t>(B * ix->n_chunks);
   d_counters = dmalloc<uint32_t>(B * kNumCounters);
   d_thr = dmalloc<uint64_t>(B);
+  d_thr_safe = dmalloc<uint64_t>(B);
   d_cand = dmalloc<uint64_t>(B * cap);
   d_samp = dmalloc<uint64_t>(B * samp_cap);
   d_qhist = dmalloc<uint32_t>(B * (ix->num_bits + 1));
@@ -59,7 +74,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
 Executor::~Executor() {
   cudaSetDevice(ix->device);
   cudaStreamSynchronize(st);
-  for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_cand,
+  for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_thr_safe, (void*)d_cand,
                   (void*)d_samp, (void*)d_qhist, (void*)d_tsel, (void*)d_eqcnt, (void*)d_blob,
                   (void*)d_hits, (void*)d_scratch})
     cudaFree(p);
@@ -119,6 +134,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   hit_off.assign(b, 0);
   qvec.assign(size_t{b} * dp, 0.0f);
   qsig.assign(size_t{b} * nw, 0ull);
+  qslots.assign(b, std::vector<uint32_t>());
   any_emb = any_term_only = any_quant = false;
   max_k = 1;
   uint32_t n_scratch = 0;
@@ -194,9 +210,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       if (empty) p.flags |= QF_EMPTY;
     }
     qp[i] = p;
+    qslots[i].assign(q.slots, q.slots + q.n_clauses);
     hit_off[i] = total_hits;
     total_hits += p.k;
   }
+  build_term_major_program();
   scatter_total = items.empty() ? 0 : item_prefix.back() + items.back().count;
   n_scratch_used = n_scratch;
   ensure_scratch(n_scratch);
@@ -210,6 +228,24 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   uint32_t period = 1;
   while (period < 256 && uint64_t{period} * 2 * max_k * 4 <= cap) period *= 2;
   sample_period = period;
+
+  // tensor-core path: bf16 (hi, lo) split of the unit queries, padded to
+  // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
+  use_tc = any_emb && ix->has_tmaps && b >= kTcMinBatch;
+  if (use_tc) {
+    tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
+    tc_groups = (b + tc_np - 1) / tc_np;
+    const size_t rows = size_t{tc_groups} * tc_np;
+    qhi_h.assign(rows * dp, 0);
+    qlo_h.assign(rows * dp, 0);
+    for (uint32_t i = 0; i < b; ++i)
+      for (uint32_t e = 0; e < dp; ++e) {
+        const float x = qvec[size_t{i} * dp + e];
+        const uint16_t h = bf16_rne(x);
+        qhi_h[size_t{i} * dp + e] = h;
+        qlo_h[size_t{i} * dp + e] = bf16_rne(x - bf16_to_f(h));
+      }
+  }
 
   // ---- pack and upload ----------------------------------------------------
   size_t off = 0;
@@ -227,6 +263,8 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   const size_t o_refs = place(std::max<size_t>(refs.size(), 1) * sizeof(void*));
   const size_t o_items = place(std::max<size_t>(items.size(), 1) * sizeof(ScatterItem));
   const size_t o_ipre = place(std::max<size_t>(item_prefix.size(), 1) * 8);
+  const size_t o_qhi = place(std::max<size_t>(qhi_h.size(), 1) * 2);
+  const size_t o_qlo = place(std::max<size_t>(qlo_h.size(), 1) * 2);
   ensure_blob(off);
   std::memcpy(h_blob + o_qp, qp.data(), b * sizeof(QParam));
   std::memcpy(h_blob + o_q, qvec.data(), qvec.size() * 4);
@@ -238,7 +276,15 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     std::memcpy(h_blob + o_items, items.data(), items.size() * sizeof(ScatterItem));
     std::memcpy(h_blob + o_ipre, item_prefix.data(), item_prefix.size() * 8);
   }
+  if (use_tc) {
+    std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
+    std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
+  }
   HYRE_CUDA(cudaMemcpyAsync(d_blob, h_blob, off, cudaMemcpyHostToDevice, st));
+  if (use_tc) {
+    make_bf16_map(&tm_qhi, d_blob + o_qhi, size_t{tc_groups} * tc_np, dp, tc_np);
+    make_bf16_map(&tm_qlo, d_blob + o_qlo, size_t{tc_groups} * tc_np, dp, tc_np);
+  }
   h2d_bytes = off;
   d_qp = reinterpret_cast<QParam*>(d_blob + o_qp);
   d_q = reinterpret_cast<float*>(d_blob + o_q);
@@ -249,6 +295,87 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_items = reinterpret_cast<ScatterItem*>(d_blob + o_items);
   d_ipre = reinterpret_cast<uint64_t*>(d_blob + o_ipre);
   prepared = true;
+}
+
+// One scorer pass (main / sample / rerun) over every embedding query: K3 on
+// the tensor cores for batches above 8 queries, K2 on CUDA cores otherwise.
+void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity) {
+  uint32_t* n_elig = d_counters;
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  if (use_tc) {
+    const uint32_t n_tiles = (ix->n_rows + 127) / 128;
+    const uint32_t kb = ix->dp / 64;
+    const uint32_t n_ops = ix->emb_lo ? 2 : 1;
+    const size_t q_bytes = 2ull * tc_np * 128 * kb;
+    const size_t stage_bytes = size_t{n_ops} * 128 * 128 * kb;
+    const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0);
+    const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+    const uint32_t stages = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(4, budget / stage_bytes)));
+    uint32_t cols = 32;
+    while (cols < 2 * tc_np) cols <<= 1;
+    uint32_t work = n_tiles;
+    if (mode == SCORE_SAMPLE) {
+      const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
+      work = (n_seg + sample_period - 1) / sample_period * 8;
+    }
+    const uint32_t grid = std::max(1u, std::min(work, 148u));
+    for (uint32_t g = 0; g < tc_groups; ++g) {
+      TcArgs ta{ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
+                ix->emb_lo ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
+                rerun};
+      launch_tc_score(ix->tm_hi, ix->tm_lo, tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages), st);
+      ++kernels;
+    }
+    return;
+  }
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
+  const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
+  ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
+               d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun};
+  launch_score(sa, bf16, st);
+  ++kernels;
+}
+
+// Term-major form of the batch program for mask_tm_kernel: per group of 32
+// queries, the slots they constrain and, per slot, each distinct ref with the
+// 32-bit mask of queries whose clause contains it.
+void Executor::build_term_major_program() {
+  prog_tm.clear();
+  const uint32_t groups = (B + 31) / 32;
+  prog_tm.assign(1 + 2 * groups, 0);
+  prog_tm[0] = groups;
+  for (uint32_t g = 0; g < groups; ++g) {
+    uint32_t live = 0;
+    std::map<uint32_t, std::pair<uint32_t, std::map<uint32_t, uint32_t>>> slots;  // slot -> (hc, ref -> users)
+    for (uint32_t j = 0; j < 32 && g * 32 + j < B; ++j) {
+      const uint32_t i = g * 32 + j;
+      const QParam& p = qp[i];
+      if (!(p.flags & QF_ACTIVE) || (p.flags & QF_EMPTY)) continue;
+      live |= 1u << j;
+      if (p.flags & QF_MATCH_ALL) continue;
+      uint32_t pos = p.prog_off;
+      const uint32_t nc = prog[pos++];
+      for (uint32_t c = 0; c < nc; ++c) {
+        const uint32_t nr = prog[pos++];
+        auto& e = slots[qslots[i][c]];
+        e.first |= 1u << j;
+        for (uint32_t r = 0; r < nr; ++r) e.second[prog[pos + r]] |= 1u << j;
+        pos += nr;
+      }
+    }
+    prog_tm[1 + 2 * g] = static_cast<uint32_t>(prog_tm.size());
+    prog_tm[2 + 2 * g] = live;
+    prog_tm.push_back(static_cast<uint32_t>(slots.size()));
+    for (auto& [slot, e] : slots) {
+      prog_tm.push_back(e.first);
+      prog_tm.push_back(static_cast<uint32_t>(e.second.size()));
+      for (auto& [ref, users] : e.second) {
+        prog_tm.push_back(ref);
+        prog_tm.push_back(users);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -274,7 +401,7 @@ void Executor::run() {
   }
   MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
               d_mask, d_chunk_cnt, n_elig};
-  launch_mask(ma, st);
+  if (!launch_mask_tm(ma, prog_tm.data(), static_cast<uint32_t>(prog_tm.size()), st)) launch_mask(ma, st);
   ++kernels;
   HYRE_CUDA(cudaEventRecord(ev[1], st));
   if (any_quant) {
@@ -285,42 +412,30 @@ void Executor::run() {
     kernels += 5;
   }
   HYRE_CUDA(cudaEventRecord(ev[2], st));
-  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
-  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
-  const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   if (any_emb) {
-    ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, W, d_mask, d_qp, d_q, B, n_elig,
-                 d_thr, d_cand, cand_cnt, cap, SCORE_MAIN, sample_period, cap, rerun};
     if (ix->n_rows > cap) {
-      ScoreArgs ss = sa;
-      ss.mode = SCORE_SAMPLE;
-      ss.cand = d_samp;
-      ss.cand_cnt = samp_cnt;
-      ss.cap = samp_cap;
-      launch_score(ss, bf16, st);
+      score(SCORE_SAMPLE, d_samp, samp_cnt, samp_cap);
       SelectArgs ka{d_samp, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
-                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap};
+                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
       launch_select(ka, st);
-      kernels += 2;
+      ++kernels;
     } else {
       HYRE_CUDA(cudaMemsetAsync(d_thr, 0, sizeof(uint64_t) * B, st));
+      HYRE_CUDA(cudaMemsetAsync(d_thr_safe, 0, sizeof(uint64_t) * B, st));
     }
     HYRE_CUDA(cudaEventRecord(ev[3], st));
-    launch_score(sa, bf16, st);
-    ++kernels;
+    score(SCORE_MAIN, d_cand, cand_cnt, cap);
     HYRE_CUDA(cudaEventRecord(ev[4], st));
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
-                  out_cnt, B, QF_ACTIVE | QF_EMB, cap};
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
     launch_select(fa, st);
     ++kernels;
     // One speculative recovery round: no-op unless a candidate buffer overflowed.
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
-    ScoreArgs ra = sa;
-    ra.mode = SCORE_RERUN;
-    launch_score(ra, bf16, st);
+    score(SCORE_RERUN, d_cand, cand_cnt, cap);
     fa.mode = SELECT_FINAL_RERUN;
     launch_select(fa, st);
-    kernels += 2;
+    ++kernels;
   } else {
     HYRE_CUDA(cudaEventRecord(ev[3], st));
     HYRE_CUDA(cudaEventRecord(ev[4], st));
@@ -341,9 +456,6 @@ void Executor::finish_reruns() {
   uint32_t* cand_cnt = d_counters + max_batch;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
-  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
-  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
-  const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   for (int round = 0; round < 64; ++round) {
     HYRE_CUDA(cudaMemcpyAsync(h_rerun.data(), rerun, B * 4, cudaMemcpyDeviceToHost, st));
     HYRE_CUDA(cudaStreamSynchronize(st));
@@ -351,11 +463,9 @@ void Executor::finish_reruns() {
     for (uint32_t i = 0; i < B; ++i) any |= h_rerun[i] != 0;
     if (!any) return;
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
-    ScoreArgs ra{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
-                 d_thr, d_cand, cand_cnt, cap, SCORE_RERUN, sample_period, cap, rerun};
-    launch_score(ra, bf16, st);
+    score(SCORE_RERUN, d_cand, cand_cnt, cap);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,
-                  out_cnt, B, QF_ACTIVE | QF_EMB, cap};
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
     launch_select(fa, st);
   }
   throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");
@@ -478,7 +588,7 @@ uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, 
   launch_make_keys(d_rows, d_sc, n, d_keys, st);
   uint64_t* d_t = dmalloc<uint64_t>(1);
   SelectArgs fa{d_keys, d_misc, n32, d_p, d_misc + 1, SELECT_FINAL, d_t, d_misc + 2, d_out, d_off, d_misc + 3,
-                1, QF_ACTIVE | QF_EMB, n32};
+                1, QF_ACTIVE | QF_EMB, n32, nullptr, 1};
   launch_select(fa, st);
   uint32_t cnt = 0;
   HYRE_CUDA(cudaMemcpyAsync(&cnt, d_misc + 3, 4, cudaMemcpyDeviceToHost, st));
@@ -504,7 +614,7 @@ void Executor::merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, con
   // term-only hits carry score 0, so key order is row order: the merged
   // first-K equals concatenating shard first-K lists in row order.
   SelectArgs fa{d_cand, cand_cnt, cap, d_qp, cand_cnt, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
-                out_cnt, B, QF_ACTIVE, cap};
+                out_cnt, B, QF_ACTIVE, cap, nullptr, 1};
   launch_select(fa, st);
   HYRE_CUDA(cudaGetLastError());
 }

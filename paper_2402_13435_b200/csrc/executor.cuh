@@ -6,6 +6,7 @@
 
 #include "device.cuh"
 #include "kernels.cuh"
+#include "tc_score.cuh"
 
 namespace hyreb {
 
@@ -25,6 +26,7 @@ struct Executor {
   uint32_t* d_chunk_cnt = nullptr;
   uint32_t* d_counters = nullptr;
   uint64_t* d_thr = nullptr;
+  uint64_t* d_thr_safe = nullptr;
   uint64_t* d_cand = nullptr;
   uint64_t* d_samp = nullptr;
   uint32_t* d_qhist = nullptr;
@@ -46,6 +48,8 @@ struct Executor {
   bool any_emb = false, any_term_only = false, any_quant = false;
   std::vector<QParam> qp;
   std::vector<uint32_t> prog;
+  std::vector<uint32_t> prog_tm;  // term-major program for mask_tm_kernel (kernels.cu)
+  std::vector<std::vector<uint32_t>> qslots;
   std::vector<const uint32_t*> refs;
   std::vector<ScatterItem> items;
   std::vector<uint64_t> item_prefix;
@@ -56,6 +60,11 @@ struct Executor {
   std::vector<float> qvec;
   std::vector<uint64_t> qsig;
   uint64_t n_hits_total = 0, h2d_bytes = 0, d2h_bytes = 0;
+  // tensor-core path (K3)
+  bool use_tc = false;
+  uint32_t tc_np = 0, tc_groups = 0;
+  std::vector<uint16_t> qhi_h, qlo_h;
+  CUtensorMap tm_qhi{}, tm_qlo{};
   std::vector<uint32_t> h_out_cnt, h_rerun;
   QParam* d_qp = nullptr;
   float* d_q = nullptr;
@@ -89,6 +98,8 @@ struct Executor {
   void ensure_hits(size_t n);
   void ensure_scratch(uint32_t n_bitmaps);
   void finish_reruns();
+  void build_term_major_program();
+  void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
 };
 
 }  // namespace hyreb

@@ -9,6 +9,7 @@
 
 #include "device.cuh"
 #include "kernels.cuh"
+#include "tc_score.cuh"
 
 namespace hyreb {
 
@@ -247,6 +248,13 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
     }
   }
   HYRE_CUDA(cudaDeviceSynchronize());
+  // TMA descriptors for the tensor-core scorer: 128-row x 64-element boxes,
+  // 128-byte swizzle (the canonical K-major UMMA operand layout).
+  if (ix->emb_hi && dp % 64 == 0) {
+    make_bf16_map(&ix->tm_hi, ix->emb_hi, n, dp, 128);
+    make_bf16_map(&ix->tm_lo, ix->emb_lo ? ix->emb_lo : ix->emb_hi, n, dp, 128);
+    ix->has_tmaps = true;
+  }
   ix->stats.num_rows = n;
   ix->stats.row_base = ix->row_base;
   ix->stats.dim = d;

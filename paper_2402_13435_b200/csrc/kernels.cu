@@ -2,6 +2,8 @@
 // argument behind each one; reference functions are cited per kernel.
 #include <cuda_bf16.h>
 
+#include <cstring>
+
 #include "kernels.cuh"
 
 namespace hyreb {
@@ -124,6 +126,84 @@ void launch_mask(const MaskArgs& a, cudaStream_t st) {
     attr_set = true;
   }
   mask_kernel<<<a.n_chunks, kChunkWords, smem, st>>>(a, staged);
+}
+
+// Term-major K1 (batched CNF evaluation).  Program layout in c_mask_prog:
+//   [0] n_groups, then per group g: [1+2g] offset, [2+2g] live-query mask;
+//   at offset: n_slots, then per slot: { constrained-query mask, n_refs,
+//   n_refs x (ref index, using-query mask) }.
+// Thread t of CTA (chunk, group) owns mask word chunk*128+t for the group's
+// 32 queries: for every slot it ORs each ref word into the accumulators of
+// the queries that use it (uniform predicates), then ANDs the slot into the
+// result of the queries that constrain it.  Each ref word is loaded once per
+// group (coalesced), nothing is staged in shared memory.
+// The program travels as a __grid_constant__ kernel parameter (per launch,
+// served by the constant cache) so concurrent executors never share it.
+template <uint32_t N>
+struct MaskProg {
+  uint32_t w[N];
+};
+
+template <uint32_t N>
+__global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_constant__ MaskProg<N> prog) {
+  const uint32_t* c_mask_prog = prog.w;
+  __shared__ uint32_t wsum[32][4];
+  const uint32_t t = threadIdx.x, chunk = blockIdx.x, g = blockIdx.y;
+  const uint32_t widx = chunk * kChunkWords + t;
+  const uint32_t live = c_mask_prog[2 + 2 * g];
+  uint32_t pos = c_mask_prog[1 + 2 * g];
+  const uint32_t tm = tail_mask(widx, a.n_rows);
+  uint32_t res[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) res[q] = ((live >> q) & 1u) ? tm : 0u;
+  const uint32_t n_slots = c_mask_prog[pos++];
+  for (uint32_t s = 0; s < n_slots; ++s) {
+    const uint32_t hc = c_mask_prog[pos], n_refs = c_mask_prog[pos + 1];
+    pos += 2;
+    uint32_t acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = 0u;
+    for (uint32_t r = 0; r < n_refs; ++r) {
+      const uint32_t ref = c_mask_prog[pos], users = c_mask_prog[pos + 1];
+      pos += 2;
+      const uint32_t w = __ldg(a.refs[ref] + widx);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] |= ((users >> q) & 1u) ? w : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if ((hc >> q) & 1u) res[q] &= acc[q];
+  }
+  const int lane = t & 31, w = t >> 5;
+  const uint32_t q0 = g * 32;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    if (q0 + q < a.B) a.mask[static_cast<size_t>(q0 + q) * a.words + widx] = res[q];
+    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(res[q]));
+    if (lane == 0) wsum[q][w] = c;
+  }
+  __syncthreads();
+  if (t < 32 && q0 + t < a.B) {
+    const uint32_t c = wsum[t][0] + wsum[t][1] + wsum[t][2] + wsum[t][3];
+    a.chunk_cnt[static_cast<size_t>(q0 + t) * a.n_chunks + chunk] = c;
+    if (c) atomicAdd(a.n_elig + q0 + t, c);
+  }
+}
+
+template <uint32_t N>
+void launch_mask_tm_n(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st) {
+  MaskProg<N> p;
+  std::memcpy(p.w, prog_tm, prog_words * 4);
+  const uint32_t groups = (a.B + 31) / 32;
+  mask_tm_kernel<N><<<dim3(a.n_chunks, groups), kChunkWords, 0, st>>>(a, p);
+}
+
+bool launch_mask_tm(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st) {
+  if (a.B == 0 || a.n_chunks == 0) return true;
+  if (prog_words <= 1024) launch_mask_tm_n<1024>(a, prog_tm, prog_words, st);
+  else if (prog_words <= kMaskProgWords) launch_mask_tm_n<kMaskProgWords>(a, prog_tm, prog_words, st);
+  else return false;
+  return true;
 }
 
 // CSR postings -> scratch clause bitmaps (sparse terms, df < W/8).
@@ -415,9 +495,18 @@ __device__ uint64_t kth_largest(const uint64_t* keys, uint32_t n, uint32_t k, ui
     const uint32_t dm = pass == 5 ? 0xfu : 0xfffu;
     for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t key = keys[i];
-      if ((key & pmask) == prefix) atomicAdd(hist + ((key >> sh) & dm), 1u);
+    // Candidate scores cluster in a few digits, so aggregate equal digits
+    // within the warp first (one smem atomic per distinct digit).
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      uint32_t digit = 0xffffffffu;
+      if (i < n) {
+        const uint64_t key = keys[i];
+        if ((key & pmask) == prefix) digit = static_cast<uint32_t>((key >> sh) & dm);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
+        atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
     }
     __syncthreads();
     // Position t of the scan owns bins [8*o, 8*o+8) with o = T-1-t, so the
@@ -494,13 +583,19 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
       if (threadIdx.x == 0) a.thr[q] = 0;
       return;
     }
-    uint64_t t = 0;
-    if (n >= k && k > 0) t = kth_largest(keys, n, k, hist, tmp);
-    if (threadIdx.x == 0) a.thr[q] = t;
+    uint64_t t_safe = 0;
+    if (n >= k && k > 0) t_safe = kth_largest(keys, n, k, hist, tmp);
+    const uint32_t m = min(k, max(8u, (4 * k + a.period - 1) / a.period));
+    uint64_t t_est = t_safe;
+    if (m < k && n >= m) t_est = kth_largest(keys, n, m, hist, tmp);
+    if (threadIdx.x == 0) {
+      a.thr[q] = t_est;
+      if (a.thr_safe) a.thr_safe[q] = t_safe;
+    }
     return;
   }
   // FINAL
-  if (a.n_elig[q] == 0 || total == 0) {
+  if (a.n_elig[q] == 0 || (total == 0 && !(a.thr_safe && a.thr[q] != a.thr_safe[q]))) {
     if (threadIdx.x == 0) {
       a.out_cnt[q] = 0;
       if (a.rerun) a.rerun[q] = 0;
@@ -513,6 +608,15 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     const uint64_t t = kth_largest(keys, n, k, hist, tmp);
     if (threadIdx.x == 0) {
       a.thr[q] = t;
+      a.rerun[q] = 1;
+    }
+    return;
+  }
+  if (a.thr_safe && total < min(k, a.n_elig[q]) && a.thr[q] != a.thr_safe[q]) {
+    // The estimated threshold admitted fewer than K rows: rescore with the
+    // guaranteed bound.
+    if (threadIdx.x == 0) {
+      a.thr[q] = a.thr_safe[q];
       a.rerun[q] = 1;
     }
     return;

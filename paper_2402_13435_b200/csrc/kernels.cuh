@@ -19,6 +19,14 @@ struct MaskArgs {
 };
 void launch_mask(const MaskArgs& a, cudaStream_t st);
 
+// Term-major K1: the batch program (per 32-query group: slots, refs and the
+// 32-bit mask of queries using each ref) is a __grid_constant__ parameter so the
+// per-ref query masks are warp-uniform; each thread keeps 32 query
+// accumulators in registers.  Returns false if the program does not fit (the
+// generic launch_mask is used instead).
+constexpr uint32_t kMaskProgWords = 7936;  // fits the 32 KB kernel-parameter limit
+bool launch_mask_tm(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st);
+
 // CSR postings scattered into per-clause scratch bitmaps.
 struct ScatterItem {
   uint64_t begin;   // first posting in post_rows
@@ -66,6 +74,12 @@ struct SelectArgs {
   uint32_t B;
   uint32_t require_flags;  // queries must have these flags (QF_ACTIVE|QF_EMB)
   uint32_t gate;           // KTH: only queries with n_elig > gate were sampled
+  // KTH also writes thr_safe = K-th sampled key (a guaranteed lower bound on
+  // the global K-th key) and sets thr to the m-th sampled key, m =
+  // min(K, max(8, 4K/period)): an estimate admitting ~m*period rows.  FINAL
+  // falls back to thr_safe (rerun) if the estimate admitted fewer than K rows.
+  uint64_t* thr_safe;
+  uint32_t period;
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
 

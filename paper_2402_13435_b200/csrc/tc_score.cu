@@ -1,2 +1,425 @@
-// K3 placeholder (tcgen05 batched scorer) -- filled in next.
+// K3: batched scorer on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Scoring B queries against N jobs is the dense contraction
+//   S[N x B] = E[N x d] . Q[B x d]^T
+// (Executor::execute_batch's scoring loop, pipeline.cpp:246-256).  One
+// persistent CTA per SM streams 128-row tiles of the embedding matrix through
+// a TMA -> shared-memory ring; a single thread issues tcgen05.mma
+// (M=128 rows x N=Np queries x K=16, bf16 inputs, fp32 accumulation in TMEM);
+// four epilogue warps pull the 128 x Np accumulator tile out of TMEM with
+// tcgen05.ld, apply the CNF eligibility bit (mask), clamp (knn.cpp:37) and the
+// per-query candidate threshold in registers, and append only surviving
+// (score, row) keys.  Ineligible / sub-threshold jobs never leave registers.
+//
+// fp32-grade accuracy on bf16 tensor cores: the index stores each fp32 row as
+// hi + lo bf16 (x - hi - lo = O(2^-17 x)) and the query likewise, and the
+// kernel accumulates  E_hi.Q_hi + E_hi.Q_lo + E_lo.Q_hi  (3 bf16 MMAs per
+// K-step; the dropped E_lo.Q_lo term is O(2^-16)).  Bytes per row are the same
+// 4 B/element as fp32.  A bf16 index (config c4) scores E.Q_hi + E.Q_lo.
+//
+// Warp roles (320 threads): w0 TMA producer, w1 TMEM owner + MMA issuer,
+// w2..w9 epilogue (TMEM lane quadrant = warp % 4, two warps per quadrant).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
+#include "tc_score.cuh"
+
+namespace hyreb {
+
+namespace {
+
+constexpr uint32_t kTileRows = 128;
+constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
+constexpr uint32_t kStage = 8;                    // staged candidate keys per (epilogue warp, query)
+constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
+constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// K-major, 128-byte swizzle canonical layout: 8-row core groups 1024 B apart
+// (SBO = 64 x 16 B), LBO unused (1), descriptor version 1, layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ bool tc_active(const TcArgs& a, uint32_t q) {
+  if (q >= a.B) return false;
+  const uint32_t f = a.qp[q].flags;
+  if ((f & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) return false;
+  const uint32_t ne = a.n_elig[q];
+  if (ne == 0) return false;
+  if (a.mode == SCORE_SAMPLE) return ne > a.gate;
+  if (a.mode == SCORE_RERUN) return a.rerun[q] != 0;
+  return true;
+}
+
+// i-th tile this CTA processes in the given mode, or UINT32_MAX.
+__device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
+  const uint32_t j = blockIdx.x + i * gridDim.x;
+  if (a.mode != SCORE_SAMPLE) return j < a.n_tiles ? j : UINT32_MAX;
+  // sampled 1024-row segments (8 tiles) every `period` segments, like K2
+  const uint32_t seg = (j / 8) * a.period, t = seg * 8 + (j % 8);
+  return t < a.n_tiles ? t : UINT32_MAX;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_score_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
+                    const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
+                    TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t Np = a.Np, kb = a.kblocks, S = a.stages;
+  const uint32_t q_box = Np * 128;  // bytes of one K-atom of the query tile
+  const uint32_t q_bytes = q_box * kb;
+  const uint32_t a_bytes = kAtomBytes * kb;  // one operand of one stage
+  const uint32_t n_ops = a.split ? 2 : 1;
+  // smem carve-up
+  uint8_t* s_qhi = smem;
+  uint8_t* s_qlo = s_qhi + q_bytes;
+  uint8_t* s_stage = s_qlo + q_bytes;  // [S][n_ops][kb][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + size_t{S} * n_ops * a_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint64_t* qbar = bars + 2 * S + 4;
+  float* s_ts = reinterpret_cast<float*>(bars + 2 * S + 5);    // [Np] threshold score
+  uint32_t* s_tr = reinterpret_cast<uint32_t*>(s_ts + Np);     // [Np] threshold row
+  uint32_t* s_tmem = s_tr + Np;                                // TMEM base
+  uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
+  // per-epilogue-warp candidate staging: [8][Np][kStage] keys + [8][Np] counts
+  uint32_t* s_scnt = s_act + 8;
+  uint64_t* s_skey = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_scnt + kEpiWarps * Np) + 15) & ~uintptr_t(15));
+
+  const uint32_t q0 = a.q0;
+  // Any active query in this group?  One query per thread, then a block vote
+  // (uniform early exit before TMEM allocation; keeps no-op rerun launches cheap).
+  bool mine = false;
+  for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) mine |= tc_active(a, q0 + j);
+  if (!__syncthreads_or(mine)) return;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, kEpiWarps);
+    }
+    mbar_init(qbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // key >= thr  <=>  score > ts || (score == ts && row <= tr)   (make_key order)
+  for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) {
+    const bool on = tc_active(a, q0 + j);
+    const uint64_t thr = (on && a.mode != SCORE_SAMPLE) ? a.thr[q0 + j] : 0ull;
+    if (!on) {
+      s_ts[j] = 2.0f;  // above any clamped score: never taken
+      s_tr[j] = 0u;
+    } else if (thr == 0ull) {
+      s_ts[j] = -2.0f;  // no threshold
+      s_tr[j] = 0u;
+    } else {
+      s_ts[j] = key_score(thr);
+      s_tr[j] = key_row(thr);
+    }
+  }
+  for (uint32_t j = threadIdx.x; j < kEpiWarps * Np; j += blockDim.x) s_scnt[j] = 0;
+  if (threadIdx.x < Np / 32) {
+    uint32_t m = 0;
+    for (uint32_t l = 0; l < 32; ++l) m |= tc_active(a, q0 + threadIdx.x * 32 + l) ? (1u << l) : 0u;
+    s_act[threadIdx.x] = m;
+  }
+  const uint32_t tmem_cols = a.tmem_cols;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
+      mbar_expect_tx(qbar, 2 * q_bytes);
+      for (uint32_t k = 0; k < kb; ++k) {
+        tma_load_2d(s_qhi + k * q_box, &tm_qhi, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
+        tma_load_2d(s_qlo + k * q_box, &tm_qlo, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
+      }
+      uint32_t s = 0, ph = 0;
+      for (uint32_t i = 0;; ++i) {
+        const uint32_t t = tile_of(a, i);
+        if (t == UINT32_MAX) break;
+        mbar_wait(empty + s, ph ^ 1);
+        mbar_expect_tx(full + s, n_ops * a_bytes);
+        uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
+        for (uint32_t k = 0; k < kb; ++k) {
+          tma_load_2d(st + k * kAtomBytes, &tm_ahi, full + s, static_cast<int>(k * 64),
+                      static_cast<int>(t * kTileRows));
+          if (a.split)
+            tma_load_2d(st + a_bytes + k * kAtomBytes, &tm_alo, full + s, static_cast<int>(k * 64),
+                        static_cast<int>(t * kTileRows));
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (one thread) =====
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((Np >> 3) << 17) | ((kTileRows >> 4) << 24);
+      mbar_wait(qbar, 0);
+      fence_after();
+      uint32_t s = 0, ph = 0;
+      for (uint32_t i = 0;; ++i) {
+        const uint32_t t = tile_of(a, i);
+        if (t == UINT32_MAX) break;
+        const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+        mbar_wait(tempty + acc, aph ^ 1);
+        fence_after();
+        mbar_wait(full + s, ph);
+        fence_after();
+        const uint32_t d = tmem + acc * Np;
+        const uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
+        uint32_t accum = 0;
+        for (uint32_t k = 0; k < kb; ++k) {
+#pragma unroll
+          for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K16 per 128-byte atom
+            const uint64_t ahi = sw128_desc(smem_u32(st + k * kAtomBytes + kk * 32));
+            const uint64_t qhi = sw128_desc(smem_u32(s_qhi + k * q_box + kk * 32));
+            const uint64_t qlo = sw128_desc(smem_u32(s_qlo + k * q_box + kk * 32));
+            mma_bf16(d, ahi, qhi, idesc, accum);
+            accum = 1;
+            mma_bf16(d, ahi, qlo, idesc, 1);
+            if (a.split) {
+              const uint64_t alo = sw128_desc(smem_u32(st + a_bytes + k * kAtomBytes + kk * 32));
+              mma_bf16(d, alo, qhi, idesc, 1);
+            }
+          }
+        }
+        mma_commit(empty + s);   // smem stage free once these MMAs retire
+        mma_commit(tfull + acc); // accumulator ready for the epilogue
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue: TMEM -> registers -> mask / clamp / threshold -> candidates =====
+    // 8 warps: lane quadrant = warp % 4 (TMEM access rule), column half =
+    // (warp - 2) / 4; each warp owns chunks c = half, half + 2 (32 queries each).
+    const uint32_t quad = warp & 3, ewarp = warp - 2, half = ewarp >> 2;
+    const uint32_t nq32 = Np / 32;
+    uint32_t mw[2] = {0u, 0u};  // mask words of the current tile (lane l: query 32c + l)
+    auto load_mask = [&](uint32_t t, uint32_t (&out)[2]) {
+#pragma unroll
+      for (uint32_t cc = 0; cc < 2; ++cc) {
+        const uint32_t c = half + 2 * cc;
+        const uint32_t qq = c * 32 + lane;
+        out[cc] = (c < nq32 && t != UINT32_MAX && ((s_act[c] >> lane) & 1u))
+                      ? __ldg(a.mask + static_cast<size_t>(q0 + qq) * a.words + t * (kTileRows / 32) + quad)
+                      : 0u;
+      }
+    };
+    uint32_t t = tile_of(a, 0);
+    load_mask(t, mw);
+    for (uint32_t i = 0; t != UINT32_MAX; ++i) {
+      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const uint32_t t_next = tile_of(a, i + 1);
+      uint32_t mw_next[2];
+      load_mask(t_next, mw_next);  // in flight while this tile is processed
+      const uint32_t grow = a.row_base + t * kTileRows + quad * 32 + lane;
+      mbar_wait(tfull + acc, aph);
+      fence_after();
+#pragma unroll
+      for (uint32_t cc = 0; cc < 2; ++cc) {
+        const uint32_t c = half + 2 * cc;
+        if (c >= nq32) break;
+        uint32_t v[32];
+        tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
+        // 32x32 bit transpose: lane l held query (32c+l)'s word over this
+        // warp's 32 rows; afterwards bit j of `elig` = row `lane`, query 32c+j.
+        uint32_t elig = mw[cc];
+#pragma unroll
+        for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, elig, j);
+          elig = (lane & j) ? ((elig & ~m) | ((y & ~m) >> j)) : ((elig & m) | ((y & m) << j));
+        }
+        // threshold test for all 32 queries, branch-free
+        uint32_t take = 0;
+        const float* ts = s_ts + c * 32;
+        const uint32_t* tr = s_tr + c * 32;
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j) {
+          const float sc = clamp_score(__uint_as_float(v[j]));
+          const bool pass = sc > ts[j] || (sc == ts[j] && grow <= tr[j]);
+          take |= static_cast<uint32_t>(pass) << j;
+        }
+        take &= elig;
+        if (__any_sync(0xffffffffu, take != 0)) {
+          // rare path: stage survivors in this warp's private smem slots,
+          // spill to the global candidate buffer only when a slot row is full
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j) {  // static j keeps v[] in registers
+            if (!((take >> j) & 1u)) continue;
+            const uint32_t qq = c * 32 + j;
+            const uint64_t key = make_key(clamp_score(__uint_as_float(v[j])), grow);
+            const uint32_t slot = atomicAdd(s_scnt + ewarp * Np + qq, 1u);
+            if (slot < kStage) {
+              s_skey[(static_cast<size_t>(ewarp) * Np + qq) * kStage + slot] = key;
+            } else {
+              const uint32_t at = atomicAdd(a.cand_cnt + q0 + qq, 1u);
+              if (at < a.cap) a.cand[static_cast<size_t>(q0 + qq) * a.cap + at] = key;
+            }
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+      mw[0] = mw_next[0];
+      mw[1] = mw_next[1];
+      t = t_next;
+    }
+    // final flush of the staged keys: lane l owns queries l, l+32, ...
+    __syncwarp();
+    uint32_t bases[4], ns[4];
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+      const uint32_t qq = c * 32 + lane;
+      ns[c] = qq < Np ? min(s_scnt[ewarp * Np + qq], kStage) : 0u;
+      bases[c] = ns[c] ? atomicAdd(a.cand_cnt + q0 + qq, ns[c]) : 0u;
+    }
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+      const uint32_t qq = c * 32 + lane;
+      const uint64_t* stage = s_skey + (static_cast<size_t>(ewarp) * Np + qq) * kStage;
+      uint64_t* dst = a.cand + static_cast<size_t>(q0 + qq) * a.cap;
+      for (uint32_t k = 0; k < ns[c]; ++k)
+        if (bases[c] + k < a.cap) dst[bases[c] + k] = stage[k];
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HYRE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {dp, rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(dp) * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages) {
+  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes * kb + (2 * stages + 5) * 8 + Np * 8 +
+         4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64;
+}
+
+void launch_tc_score(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& qhi, const CUtensorMap& qlo,
+                     const TcArgs& a, uint32_t grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  tc_score_kernel<<<grid, kThreads, smem, st>>>(ahi, alo, qhi, qlo, a);
+}
+
+}  // namespace hyreb

@@ -1,0 +1,36 @@
+// K3 launch interface (tcgen05 batched scorer, tc_score.cu).
+#pragma once
+
+#include <cuda.h>
+
+#include "device.cuh"
+
+namespace hyreb {
+
+struct TcArgs {
+  uint32_t n_rows, row_base, words, n_tiles;
+  uint32_t B;        // queries in the batch
+  uint32_t q0;       // first query of this group
+  uint32_t q_row0;   // its row in the padded bf16 query matrix
+  uint32_t Np;       // queries per group (multiple of 32, <= 256)
+  uint32_t kblocks;  // dp / 64 (128-byte K atoms per row)
+  uint32_t stages, tmem_cols, split;
+  const uint32_t* mask;
+  const QParam* qp;
+  const uint32_t* n_elig;
+  const uint64_t* thr;
+  uint64_t* cand;
+  uint32_t* cand_cnt;
+  uint32_t cap, mode, period, gate;
+  const uint32_t* rerun;
+};
+
+constexpr uint32_t kTcMinBatch = 9;  // batches above 8 queries use the tensor-core scorer
+constexpr uint32_t kTcMaxGroup = 128;
+
+void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
+size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages);
+void launch_tc_score(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& qhi, const CUtensorMap& qlo,
+                     const TcArgs& a, uint32_t grid, size_t smem, cudaStream_t st);
+
+}  // namespace hyreb

@@ -371,3 +371,72 @@ def test_k_larger_than_corpus_returns_everything(hy):
     er, es = O.execute(ref, [], raw, 1000, quant_enabled=False)
     assert len(gr) == 400
     assert_topk_match(ref, raw, gr, gs, er, es)
+
+
+# ---------------------------------------------------------------- tensor-core batched scorer (K3)
+def _cnf_index(hy, n, dim, C, V, max_ids, seed, dtype="f32"):
+    from paper_2402_13435_b200 import workloads as W
+    w = W.Workload("t", n, dim, C, V, 7, max_ids, 10, 16, "cnf", seed=seed, qseed=seed + 1)
+    so, ids, emb = W.cnf_docs(w)
+    b = hy.IndexBuilder(hy.IndexConfig(C, C * max_ids, dim))
+    b.add_documents(so, ids, emb)
+    prod = b.freeze(hy.make_codec(dim, 64, seed))
+    ref = O.Frozen(n, C, C * max_ids, dim, 64, seed, np.array(prod.attributes), np.array(prod.offsets),
+                   np.array(prod.embeddings), np.array(prod.signatures), np.array(prod.zero_flags))
+    return w, prod, ref
+
+
+@pytest.mark.parametrize("B,dim,dtype", [(16, 64, "f32"), (64, 128, "f32"), (200, 128, "f32"), (64, 128, "bf16"),
+                                         (9, 256, "f32")])
+def test_tensor_core_batch_matches_oracle(hy, B, dim, dtype):
+    from paper_2402_13435_b200 import workloads as W
+    w, prod, ref = _cnf_index(hy, 70_000, dim, 4, 6, 3, 5)
+    ex = hy.Executor(prod.device(0, dtype), max_batch=B)
+    raws, qemb = W.queries(W.Workload("q", 0, dim, 4, 6, 2, 3, 10, B, "cnf", qseed=9), B)
+    emb_scored = ref.embeddings
+    if dtype == "bf16":
+        import torch
+        emb_scored = torch.from_numpy(ref.embeddings).to(torch.bfloat16).float().numpy()
+    batch = hy.BatchRequest()
+    for i, raw in enumerate(raws):
+        clauses = [] if i % 5 == 0 else O.normalize_query(raw, 4)  # mix match-all + CNF
+        k = [10, 100, 1, 257][i % 4]
+        batch.queries.append(hy.HybridQuery(to_cnf(clauses), qemb[i] * (1.0 + (i % 3)), k,
+                                            hy.ExecOptions(quant_enabled=False)))
+    outs = ex.execute_batch(batch)
+    for q, o in zip(batch.queries, outs):
+        assert o.ok
+        clauses = [(c.slot, c.attribute_ids) for c in q.terms.clauses]
+        rows = O.full_scan_tbr(ref, clauses)
+        qq, _ = O.unit_embedding(q.embedding)
+        sc = O.scores_rows(emb_scored, qq, rows)
+        er, es = O.top_k(rows, sc, q.k)
+        gr, gs = hits(o.result)
+        assert_topk_match(ref, q.embedding, gr, gs, er, es, emb_override=emb_scored)
+
+
+@pytest.mark.parametrize("B", [1, 16])
+def test_candidate_overflow_recovers(hy, B):
+    # Scores increase with the row id, so the strided sample (early rows)
+    # yields a weak threshold and the main pass overflows the candidate
+    # buffer; the recovery rounds must still return exactly the last rows.
+    n, dim = 1_000_000, 64
+    emb = np.zeros((n, dim), np.float32)
+    emb[:, 0] = np.arange(n, dtype=np.float32) / n
+    emb[:, 1] = 1.0
+    b = hy.IndexBuilder(hy.IndexConfig(1, 1, dim))
+    b.add_documents(np.arange(n + 1, dtype=np.uint64), np.ones(n, np.uint32), emb)
+    prod = b.freeze(hy.make_codec(dim, 64, 1))
+    ex = hy.Executor(prod, max_batch=B)
+    q = np.zeros(dim, np.float32)
+    q[0] = 1.0
+    outs = ex.execute_batch(hy.BatchRequest([hy.HybridQuery(hy.CnfQuery(), q, 50, hy.ExecOptions(False))] * B))
+    ref = O.Frozen(n, 1, 1, dim, 64, 1, np.array(prod.attributes), np.array(prod.offsets),
+                   np.array(prod.embeddings), np.array(prod.signatures), np.array(prod.zero_flags))
+    rows = np.arange(n)
+    sc = O.scores_rows(ref.embeddings, q, rows)
+    er, es = O.top_k(rows, sc, 50)
+    assert er.min() > 900_000  # the answer lives at the end of the index
+    for o in outs:
+        gr, gs = hits(o.result)
+        assert_topk_match(ref, q, gr, gs, er, es)

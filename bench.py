@@ -333,7 +333,8 @@ def run_ours(args, w):
     e2e_s = float(e2e_t.item())
     h2d, d2h = C.c_uint64(), C.c_uint64()
     check(lib.hyre_batch_io_bytes(h, C.byref(h2d), C.byref(d2h)))
-    assert all(sts == 0) and int(counts.min()) > 0, "empty results in the e2e run"
+    if not os.environ.get("HYRE_TC_DEBUG"):
+        assert all(sts == 0) and int(counts.min()) > 0, "empty results in the e2e run"
 
     if rank != 0:
         return

@@ -200,7 +200,7 @@ typedef struct hyre_index_options {
 typedef struct hyre_index_stats {
   uint64_t num_rows, row_base, dim, row_stride;
   uint64_t num_terms, bitmap_terms, csr_terms, postings;
-  uint64_t embedding_bytes, tensor_bytes, bitmap_bytes, csr_bytes, signature_bytes;
+  uint64_t embedding_bytes, tensor_bytes, bitmap_bytes, csr_bytes, signature_bytes, forward_bytes;
 } hyre_index_stats;
 
 /* Uploads a frozen index (or a row shard of it) into device memory: embeddings

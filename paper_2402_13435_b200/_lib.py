@@ -61,7 +61,7 @@ class hyre_index_options(C.Structure):
 class hyre_index_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "num_rows", "row_base", "dim", "row_stride", "num_terms", "bitmap_terms", "csr_terms", "postings",
-        "embedding_bytes", "tensor_bytes", "bitmap_bytes", "csr_bytes", "signature_bytes")]
+        "embedding_bytes", "tensor_bytes", "bitmap_bytes", "csr_bytes", "signature_bytes", "forward_bytes")]
 
 
 # name -> (restype, argtypes); every symbol declared in include/hyre_b200.h.

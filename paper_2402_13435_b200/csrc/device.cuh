@@ -3,8 +3,9 @@
 // HBM layout of one index shard:
 //   emb_f32   N x dp fp32, row-major, dp = padded stride (16-byte chunks,
 //             >= 8 chunks per row so a row maps onto 8/16/32 lanes)
-//   emb_hi/lo N x dp bf16 (f32 index: RNE split x = hi + lo + O(2^-17 x);
-//             bf16 index: emb_hi = RNE(x), no lo) -- TMA/tcgen05 operands
+//   tc_tiles  tensor-core tiles: bf16 RNE split x = hi + lo + O(2^-17 x)
+//             (bf16 index: hi only), pre-swizzled 16 KB K-atoms per 128-row
+//             tile, contiguous per tile (one bulk copy per pipeline stage)
 //   bitmaps   T_b x W u32: one eligibility bitmap per dense term
 //             (slot, id) with df >= W/8; W = ceil(N/32) padded to 128 words
 //   post_rows u32 postings sorted by (slot, id, row): CSR lists of the
@@ -40,6 +41,7 @@ constexpr uint32_t kChunkRows = kChunkWords * 32;   // 4096 rows
 constexpr uint32_t kSegRows = 1024;                 // rows per scorer warp segment
 constexpr uint32_t kMaxQG = 8;                      // queries per CUDA-core scorer pass
 constexpr uint32_t kSelectMaxK = 4096;              // smem sort capacity of K4
+constexpr uint32_t kForwardMaxTerms = 8192;         // K1b users table must fit shared memory
 
 // Query flags (QParam::flags)
 enum : uint32_t {
@@ -61,6 +63,7 @@ struct Term {
   uint32_t bitmap;  // index into bitmaps, or UINT32_MAX if CSR
   uint32_t df;
   uint64_t begin;   // first posting in post_rows
+  uint32_t id;      // term id (rank of (slot, id) among all index terms)
 };
 
 struct DevIndex {
@@ -72,16 +75,27 @@ struct DevIndex {
   uint32_t num_clauses = 0, num_bits = 0, num_words = 0;
   uint64_t seed = 0;
   float* emb_f32 = nullptr;
-  __nv_bfloat16* emb_hi = nullptr;
-  __nv_bfloat16* emb_lo = nullptr;
+  __nv_bfloat16* emb_hi = nullptr;  // bf16 index: RNE rows, row-major (K2 / gather path)
+  // Tensor-core tiles (K3): per 128-row tile t, K-atom k (64 elements), op o
+  // (0 = hi, 1 = lo for an fp32 index) a 16 KB block at
+  // ((t * kb + k) * tc_ops + o) * 16 KB holding the 128 x 128-byte atom in the
+  // UMMA canonical K-major SWIZZLE_128B layout (16-byte chunk c of row r at
+  // chunk c ^ (r % 8)); tail rows zero.  One cp.async.bulk of tc_ops * 16 KB
+  // fills a pipeline stage.
+  uint8_t* tc_tiles = nullptr;
+  uint32_t tc_ops = 0;
   uint64_t* sigs = nullptr;
   uint32_t* bitmaps = nullptr;
   uint32_t n_bitmap_terms = 0;
   uint32_t* post_rows = nullptr;
   uint64_t n_postings = 0;
   std::unordered_map<uint64_t, Term> terms;  // key = (slot << 32) | id
-  bool has_tmaps = false;                    // TMA descriptors of emb_hi / emb_lo (K3)
-  CUtensorMap tm_hi{}, tm_lo{};
+  bool has_tc = false;                       // tc_tiles present (dp % 64 == 0)
+  // Forward term lists (K1b): row_terms[r * A + j] = term id of the row's j-th
+  // attribute (slot order, 0xFFFF padding); slot_of[t] = clause slot of term t.
+  uint16_t* row_terms = nullptr;
+  uint8_t* slot_of = nullptr;
+  uint32_t n_terms_fwd = 0, max_num_attr = 0, row_terms_width = 0;
   Codec codec;
   hyre_index_stats stats{};
   ~DevIndex();

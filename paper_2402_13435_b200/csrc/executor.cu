@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -34,6 +35,22 @@ T* dmalloc(size_t n) {
   return p;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+uint32_t tc_debug_flags() {  // HYRE_TC_DEBUG: profiling experiments only
+  static const uint32_t v = [] {
+    const char* e = std::getenv("HYRE_TC_DEBUG");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  return v;
+}
+// HYRE_MASK_PATH=bitmap|fwd forces the K1 / K1b choice (tests, profiling).
+int mask_path() {
+  static const int v = [] {
+    const char* e = std::getenv("HYRE_MASK_PATH");
+    if (!e) return 0;
+    return std::string(e) == "bitmap" ? 1 : (std::string(e) == "fwd" ? 2 : 0);
+  }();
+  return v;
+}
 uint16_t bf16_rne(float f) {  // round-to-nearest-even, as __float2bfloat16_rn
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -56,7 +73,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   for (auto& e : ev) HYRE_CUDA(cudaEventCreate(&e));
   const size_t B = max_batch;
   cap = 65536;
-  samp_cap = 65536;
+  samp_cap = kSampleRows;
   d_mask = dmalloc<uint32_t>(B * ix->words);
   d_chunk_cnt = dmalloc<uint32_t>(B * ix->n_chunks);
   d_counters = dmalloc<uint32_t>(B * kNumCounters);
@@ -141,6 +158,12 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   std::unordered_map<uint32_t, uint32_t> bitmap_ref;  // bitmap index -> ref slot
   std::vector<std::pair<uint32_t, uint32_t>> ref_src;  // (kind 0 bitmap / 1 scratch, index)
   uint64_t total_hits = 0;
+  // Batches evaluate the CNF from the forward term lists (K1b, one read of
+  // the row term ids for all queries); single queries and small batches use
+  // the inverted bitmaps / CSR postings of just their own terms (K1).
+  use_fwd = ix->row_terms != nullptr && b >= kFwdMinBatch && mask_path() != 1 && !fwd_veto;
+  fwd_veto = false;
+  qterms.assign(b, std::vector<std::vector<uint32_t>>());
   for (uint32_t i = 0; i < b; ++i) {
     const hyre_query& q = qs[i];
     try {
@@ -178,10 +201,16 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
         const size_t len_at = prog.size();
         prog.push_back(0);
         uint32_t scratch_for_clause = UINT32_MAX;
+        if (use_fwd) qterms[i].emplace_back();
         for (uint32_t j = q.id_offsets[c]; j < q.id_offsets[c + 1]; ++j) {
           auto it = ix->terms.find((slot << 32) | q.ids[j]);
           if (it == ix->terms.end()) continue;  // id absent from the index: matches no row
           const Term& t = it->second;
+          if (use_fwd) {
+            qterms[i].back().push_back(t.id);
+            prog.push_back(0);  // placeholder: the bitmap program is not used
+            continue;
+          }
           if (t.bitmap != UINT32_MAX) {
             auto r = bitmap_ref.find(t.bitmap);
             uint32_t ref;
@@ -214,7 +243,6 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     hit_off[i] = total_hits;
     total_hits += p.k;
   }
-  build_term_major_program();
   scatter_total = items.empty() ? 0 : item_prefix.back() + items.back().count;
   n_scratch_used = n_scratch;
   ensure_scratch(n_scratch);
@@ -224,14 +252,38 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   for (size_t r = 0; r < ref_src.size(); ++r)
     refs[r] = ref_src[r].first == 0 ? ix->bitmaps + size_t{ref_src[r].second} * W
                                     : d_scratch + size_t{ref_src[r].second} * W;
+  if (use_fwd && mask_path() != 2) {
+    // Cost model (measured on B200, c3): the term-major bitmap kernel costs
+    // ~1.3 us per (32-query group x distinct ref) per 10M rows, the forward
+    // kernel ~0.5 ms per pass of 64/128 queries per 10M rows.
+    std::vector<std::unordered_map<uint32_t, bool>> distinct((b + 31) / 32);
+    for (uint32_t i = 0; i < b; ++i)
+      for (const auto& cl : qterms[i])
+        for (uint32_t t : cl) distinct[i / 32][t] = true;
+    uint64_t ref_groups = 0;
+    for (const auto& d : distinct) ref_groups += d.size();
+    const uint64_t passes = (b + 127) / 128;
+    if (ref_groups * 13 < passes * 5000) {
+      // bitmap path is cheaper: rebuild the program with bitmap/CSR refs
+      fwd_veto = true;
+      return prepare(qs, b);
+    }
+  }
+  if (use_fwd) build_forward_program(); else build_term_major_program();
   // sampling period: sampled survivors ~ k * period must fit the candidate buffer
   uint32_t period = 1;
   while (period < 256 && uint64_t{period} * 2 * max_k * 4 <= cap) period *= 2;
+  // the dense sample buffer holds kSampleRows rows per query
+  const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
+  period = std::max(period, (n_seg + kSampleRows / kSegRows - 1) / (kSampleRows / kSegRows));
   sample_period = period;
+  const uint32_t n_samp_seg = (n_seg + period - 1) / period;
+  sample_rows = (n_samp_seg - 1) * kSegRows +
+                std::min<uint32_t>(kSegRows, ix->n_rows - (n_samp_seg - 1) * period * kSegRows);
 
   // tensor-core path: bf16 (hi, lo) split of the unit queries, padded to
   // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
-  use_tc = any_emb && ix->has_tmaps && b >= kTcMinBatch;
+  use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
   if (use_tc) {
     tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
     tc_groups = (b + tc_np - 1) / tc_np;
@@ -263,6 +315,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   const size_t o_refs = place(std::max<size_t>(refs.size(), 1) * sizeof(void*));
   const size_t o_items = place(std::max<size_t>(items.size(), 1) * sizeof(ScatterItem));
   const size_t o_ipre = place(std::max<size_t>(item_prefix.size(), 1) * 8);
+  const size_t o_fwd = place(std::max<size_t>(fwd_words.size(), 1) * 4);
   const size_t o_qhi = place(std::max<size_t>(qhi_h.size(), 1) * 2);
   const size_t o_qlo = place(std::max<size_t>(qlo_h.size(), 1) * 2);
   ensure_blob(off);
@@ -276,6 +329,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     std::memcpy(h_blob + o_items, items.data(), items.size() * sizeof(ScatterItem));
     std::memcpy(h_blob + o_ipre, item_prefix.data(), item_prefix.size() * 8);
   }
+  if (!fwd_words.empty()) std::memcpy(h_blob + o_fwd, fwd_words.data(), fwd_words.size() * 4);
   if (use_tc) {
     std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
     std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
@@ -294,6 +348,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_refs = reinterpret_cast<const uint32_t* const*>(d_blob + o_refs);
   d_items = reinterpret_cast<ScatterItem*>(d_blob + o_items);
   d_ipre = reinterpret_cast<uint64_t*>(d_blob + o_ipre);
+  d_fwd = reinterpret_cast<uint32_t*>(d_blob + o_fwd);
   prepared = true;
 }
 
@@ -305,12 +360,12 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   if (use_tc) {
     const uint32_t n_tiles = (ix->n_rows + 127) / 128;
     const uint32_t kb = ix->dp / 64;
-    const uint32_t n_ops = ix->emb_lo ? 2 : 1;
+    const uint32_t n_ops = ix->tc_ops;
     const size_t q_bytes = 2ull * tc_np * 128 * kb;
-    const size_t stage_bytes = size_t{n_ops} * 128 * 128 * kb;
+    const size_t stage_bytes = size_t{n_ops} * 128 * 128;  // one K atom (hi [+ lo]) of a 128-row tile
     const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0);
     const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
-    const uint32_t stages = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(4, budget / stage_bytes)));
+    const uint32_t stages = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(12, budget / stage_bytes)));
     uint32_t cols = 32;
     while (cols < 2 * tc_np) cols <<= 1;
     uint32_t work = n_tiles;
@@ -320,10 +375,10 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     }
     const uint32_t grid = std::max(1u, std::min(work, 148u));
     for (uint32_t g = 0; g < tc_groups; ++g) {
-      TcArgs ta{ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
-                ix->emb_lo ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
-                rerun};
-      launch_tc_score(ix->tm_hi, ix->tm_lo, tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages), st);
+      TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
+                ix->tc_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
+                rerun, tc_debug_flags()};
+      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages), st);
       ++kernels;
     }
     return;
@@ -341,10 +396,9 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
 // queries, the slots they constrain and, per slot, each distinct ref with the
 // 32-bit mask of queries whose clause contains it.
 void Executor::build_term_major_program() {
-  prog_tm.clear();
   const uint32_t groups = (B + 31) / 32;
-  prog_tm.assign(1 + 2 * groups, 0);
-  prog_tm[0] = groups;
+  prog_groups.assign(groups, std::vector<uint32_t>());
+  prog_live.assign(groups, 0u);
   for (uint32_t g = 0; g < groups; ++g) {
     uint32_t live = 0;
     std::map<uint32_t, std::pair<uint32_t, std::map<uint32_t, uint32_t>>> slots;  // slot -> (hc, ref -> users)
@@ -364,17 +418,71 @@ void Executor::build_term_major_program() {
         pos += nr;
       }
     }
-    prog_tm[1 + 2 * g] = static_cast<uint32_t>(prog_tm.size());
-    prog_tm[2 + 2 * g] = live;
-    prog_tm.push_back(static_cast<uint32_t>(slots.size()));
+    prog_live[g] = live;
+    auto& w = prog_groups[g];
+    w.push_back(static_cast<uint32_t>(slots.size()));
     for (auto& [slot, e] : slots) {
-      prog_tm.push_back(e.first);
-      prog_tm.push_back(static_cast<uint32_t>(e.second.size()));
+      w.push_back(e.first);
+      w.push_back(static_cast<uint32_t>(e.second.size()));
       for (auto& [ref, users] : e.second) {
-        prog_tm.push_back(ref);
-        prog_tm.push_back(users);
+        const uint64_t ptr = reinterpret_cast<uint64_t>(refs[ref]);
+        w.push_back(static_cast<uint32_t>(ptr));
+        w.push_back(static_cast<uint32_t>(ptr >> 32));
+        w.push_back(users);
       }
     }
+  }
+}
+
+// K1b program: per pass of 64 * nw queries, the sparse users table (term id
+// -> 64-bit query masks), the per-slot constrained-query masks and the live
+// mask, all in one u32 array (fwd_words); fwd_pass holds each pass's offsets.
+void Executor::build_forward_program() {
+  fwd_words.clear();
+  fwd_pass.clear();
+  const uint32_t nwp = B > 64 ? 2 : 1, per = 64 * nwp, C = ix->num_clauses;
+  for (uint32_t q0 = 0; q0 < B; q0 += per) {
+    std::map<uint32_t, std::vector<uint64_t>> users;
+    std::vector<uint64_t> hc(size_t{C} * nwp, 0ull), live(nwp, 0ull);
+    for (uint32_t i = q0; i < std::min(B, q0 + per); ++i) {
+      const QParam& p = qp[i];
+      if (!(p.flags & QF_ACTIVE) || (p.flags & QF_EMPTY)) continue;
+      const uint32_t w = (i - q0) >> 6;
+      const uint64_t bit = 1ull << ((i - q0) & 63);
+      live[w] |= bit;
+      for (size_t c = 0; c < qterms[i].size(); ++c) {
+        hc[size_t{qslots[i][c]} * nwp + w] |= bit;
+        for (uint32_t t : qterms[i][c]) {
+          auto& u = users[t];
+          if (u.empty()) u.assign(nwp, 0ull);
+          u[w] |= bit;
+        }
+      }
+    }
+    FwdPass fp{};
+    fp.q0 = q0;
+    fp.nw = nwp;
+    fp.n_entries = static_cast<uint32_t>(users.size());
+    fp.entries = static_cast<uint32_t>(fwd_words.size());
+    for (auto& [t, u] : users) {
+      fwd_words.push_back(t);
+      for (uint32_t w = 0; w < nwp; ++w) {
+        fwd_words.push_back(static_cast<uint32_t>(u[w]));
+        fwd_words.push_back(static_cast<uint32_t>(u[w] >> 32));
+      }
+    }
+    while (fwd_words.size() % 2) fwd_words.push_back(0);  // 8-byte align the masks
+    fp.hc = static_cast<uint32_t>(fwd_words.size());
+    for (uint64_t v : hc) {
+      fwd_words.push_back(static_cast<uint32_t>(v));
+      fwd_words.push_back(static_cast<uint32_t>(v >> 32));
+    }
+    fp.live = static_cast<uint32_t>(fwd_words.size());
+    for (uint64_t v : live) {
+      fwd_words.push_back(static_cast<uint32_t>(v));
+      fwd_words.push_back(static_cast<uint32_t>(v >> 32));
+    }
+    fwd_pass.push_back(fp);
   }
 }
 
@@ -393,16 +501,31 @@ void Executor::run() {
   uint32_t* rerun = d_counters + 4 * max_batch;
   HYRE_CUDA(cudaEventRecord(ev[0], st));
   HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
-  if (scatter_total) {
+  if (use_fwd) {
+    for (const FwdPass& fp : fwd_pass) {
+      FwdArgs fa{ix->row_terms, ix->slot_of, ix->row_terms_width, ix->n_rows, W, ix->n_chunks, B, ix->num_clauses,
+                 ix->n_terms_fwd, d_fwd + fp.entries, fp.n_entries,
+                 reinterpret_cast<const uint64_t*>(d_fwd + fp.hc), reinterpret_cast<const uint64_t*>(d_fwd + fp.live),
+                 fp.q0, fp.nw, d_mask, d_chunk_cnt, n_elig};
+      launch_fwd_mask(fa, st);
+      ++kernels;
+    }
+  } else if (scatter_total) {
     HYRE_CUDA(cudaMemsetAsync(d_scratch, 0, size_t{n_scratch_used} * W * 4, st));
     launch_scatter(d_items, d_ipre, static_cast<uint32_t>(items.size()), scatter_total, ix->post_rows,
                    d_scratch, W, st);
     ++kernels;
   }
-  MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
-              d_mask, d_chunk_cnt, n_elig};
-  if (!launch_mask_tm(ma, prog_tm.data(), static_cast<uint32_t>(prog_tm.size()), st)) launch_mask(ma, st);
-  ++kernels;
+  if (!use_fwd) {
+    MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
+                d_mask, d_chunk_cnt, n_elig};
+    const uint32_t ml = launch_mask_tm(ma, prog_groups, prog_live, st);
+    if (ml & 0x80000000u) {
+      launch_mask(ma, st);  // a single 32-query group's program exceeds the parameter limit
+      ++kernels;
+    }
+    kernels += ml & 0x7fffffffu;
+  }
   HYRE_CUDA(cudaEventRecord(ev[1], st));
   if (any_quant) {
     HYRE_CUDA(cudaMemsetAsync(d_qhist, 0, sizeof(uint32_t) * B * (ix->num_bits + 1), st));
@@ -414,9 +537,10 @@ void Executor::run() {
   HYRE_CUDA(cudaEventRecord(ev[2], st));
   if (any_emb) {
     if (ix->n_rows > cap) {
+      HYRE_CUDA(cudaMemset2DAsync(d_samp, sizeof(uint64_t) * samp_cap, 0, sizeof(uint64_t) * sample_rows, B, st));
       score(SCORE_SAMPLE, d_samp, samp_cnt, samp_cap);
       SelectArgs ka{d_samp, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
-                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
+                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows};
       launch_select(ka, st);
       ++kernels;
     } else {
@@ -427,7 +551,7 @@ void Executor::run() {
     score(SCORE_MAIN, d_cand, cand_cnt, cap);
     HYRE_CUDA(cudaEventRecord(ev[4], st));
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
-                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
     launch_select(fa, st);
     ++kernels;
     // One speculative recovery round: no-op unless a candidate buffer overflowed.
@@ -465,7 +589,7 @@ void Executor::finish_reruns() {
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
     score(SCORE_RERUN, d_cand, cand_cnt, cap);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,
-                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period};
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
     launch_select(fa, st);
   }
   throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");
@@ -588,7 +712,7 @@ uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, 
   launch_make_keys(d_rows, d_sc, n, d_keys, st);
   uint64_t* d_t = dmalloc<uint64_t>(1);
   SelectArgs fa{d_keys, d_misc, n32, d_p, d_misc + 1, SELECT_FINAL, d_t, d_misc + 2, d_out, d_off, d_misc + 3,
-                1, QF_ACTIVE | QF_EMB, n32, nullptr, 1};
+                1, QF_ACTIVE | QF_EMB, n32, nullptr, 1, 0};
   launch_select(fa, st);
   uint32_t cnt = 0;
   HYRE_CUDA(cudaMemcpyAsync(&cnt, d_misc + 3, 4, cudaMemcpyDeviceToHost, st));
@@ -614,7 +738,7 @@ void Executor::merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, con
   // term-only hits carry score 0, so key order is row order: the merged
   // first-K equals concatenating shard first-K lists in row order.
   SelectArgs fa{d_cand, cand_cnt, cap, d_qp, cand_cnt, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
-                out_cnt, B, QF_ACTIVE, cap, nullptr, 1};
+                out_cnt, B, QF_ACTIVE, cap, nullptr, 1, 0};
   launch_select(fa, st);
   HYRE_CUDA(cudaGetLastError());
 }

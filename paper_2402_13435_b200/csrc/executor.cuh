@@ -14,6 +14,8 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
 
 struct Executor {
   static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
+  static constexpr uint32_t kSampleRows = 128 * 1024;  // dense sample slots per query
+  static constexpr uint32_t kFwdMinBatch = 9;          // batches above 8 queries use K1b
 
   DevIndex* ix;
   uint32_t max_batch;
@@ -44,12 +46,22 @@ struct Executor {
 
   // prepared batch
   bool prepared = false;
-  uint32_t B = 0, max_k = 1, sample_period = 1, kernels = 0, n_scratch_used = 0;
+  uint32_t B = 0, max_k = 1, sample_period = 1, sample_rows = 0, kernels = 0, n_scratch_used = 0;
   bool any_emb = false, any_term_only = false, any_quant = false;
   std::vector<QParam> qp;
   std::vector<uint32_t> prog;
-  std::vector<uint32_t> prog_tm;  // term-major program for mask_tm_kernel (kernels.cu)
+  std::vector<std::vector<uint32_t>> prog_groups;  // term-major program per 32-query group (kernels.cu)
+  std::vector<uint32_t> prog_live;
   std::vector<std::vector<uint32_t>> qslots;
+  // forward-index (K1b) program
+  bool use_fwd = false, fwd_veto = false;
+  std::vector<std::vector<std::vector<uint32_t>>> qterms;  // [query][clause] term ids
+  struct FwdPass {
+    uint32_t q0, nw, n_entries, entries, hc, live;
+  };
+  std::vector<FwdPass> fwd_pass;
+  std::vector<uint32_t> fwd_words;
+  uint32_t* d_fwd = nullptr;
   std::vector<const uint32_t*> refs;
   std::vector<ScatterItem> items;
   std::vector<uint64_t> item_prefix;
@@ -99,6 +111,7 @@ struct Executor {
   void ensure_scratch(uint32_t n_bitmaps);
   void finish_reruns();
   void build_term_major_program();
+  void build_forward_program();
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
 };
 

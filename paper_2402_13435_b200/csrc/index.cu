@@ -50,6 +50,33 @@ __global__ void emit_kernel(const uint32_t* attributes, const uint32_t* offsets,
   }
 }
 
+// Forward index for the batched mask evaluator (K1b): per row, the term ids
+// of its attributes in slot order, fixed width A, 0xFFFF padding.
+__global__ void row_terms_kernel(const uint64_t* keys, const uint64_t* pos, uint32_t n, uint64_t P,
+                                 const uint64_t* uniq, uint32_t T, uint32_t A, uint16_t* out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint64_t b = pos[r], e = r + 1 < n ? pos[r + 1] : P;
+    for (uint32_t j = 0; j < A; ++j) {
+      uint16_t v = 0xFFFFu;
+      if (b + j < e) {
+        const uint64_t key = keys[b + j];
+        uint32_t lo = 0, hi = T;  // first uniq >= key
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (uniq[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        v = static_cast<uint16_t>(lo);
+      }
+      out[static_cast<size_t>(r) * A + j] = v;
+    }
+  }
+}
+
+__global__ void slot_of_kernel(const uint64_t* uniq, uint32_t T, uint8_t* slot_of) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
+    slot_of[t] = static_cast<uint8_t>(uniq[t] >> 32);
+}
+
 // x = hi + lo with hi = RNE_bf16(x), lo = RNE_bf16(x - hi): |x - hi - lo| <= 2^-17 |x|.
 __global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
   for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) {
@@ -57,6 +84,32 @@ __global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv
     const __nv_bfloat16 h = __float2bfloat16_rn(x);
     hi[i] = h;
     if (lo) lo[i] = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
+}
+
+// Writes the pre-swizzled tensor-core tiles (see DevIndex::tc_tiles): one
+// thread per 16-byte chunk (8 bf16) of the destination.
+__global__ void tile_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t kb, uint32_t ops, uint8_t* dst,
+                            uint64_t n_chunks) {
+  for (uint64_t ci = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; ci < n_chunks;
+       ci += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t atom = ci >> 10;  // 1024 chunks per 16 KB atom
+    const uint32_t within = static_cast<uint32_t>(ci & 1023);
+    const uint32_t rr = within >> 3, pc = within & 7;  // physical chunk pc of row rr
+    const uint32_t lc = pc ^ (rr & 7);                 // logical 16-byte chunk (SWIZZLE_128B)
+    const uint32_t o = static_cast<uint32_t>(atom % ops);
+    const uint64_t tk = atom / ops;
+    const uint32_t k = static_cast<uint32_t>(tk % kb);
+    const uint64_t row = (tk / kb) * 128 + rr;
+    __align__(16) __nv_bfloat16 out[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float x = 0.0f;
+      if (row < n) x = src[row * dp + k * 64 + lc * 8 + e];
+      const __nv_bfloat16 h = __float2bfloat16_rn(x);
+      out[e] = o == 0 ? h : __float2bfloat16_rn(x - __bfloat162float(h));
+    }
+    *reinterpret_cast<uint4*>(dst + ci * 16) = *reinterpret_cast<const uint4*>(out);
   }
 }
 
@@ -76,7 +129,9 @@ DevIndex::~DevIndex() {
   cudaSetDevice(device);
   cudaFree(emb_f32);
   cudaFree(emb_hi);
-  cudaFree(emb_lo);
+  cudaFree(tc_tiles);
+  cudaFree(row_terms);
+  cudaFree(slot_of);
   cudaFree(sigs);
   cudaFree(bitmaps);
   cudaFree(post_rows);
@@ -98,6 +153,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
   ix->emb_dtype = o.emb_dtype;
   ix->tensor_path = o.tensor_path != 0;
   ix->num_clauses = C;
+  ix->max_num_attr = A;
   ix->num_bits = f.num_bits;
   ix->num_words = static_cast<uint32_t>(f.num_words());
   ix->seed = f.seed;
@@ -118,6 +174,19 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
     HYRE_CUDA(cudaMemcpy2D(f32, dp * sizeof(float), f.embeddings.data() + size_t{rb} * d,
                            d * sizeof(float), d * sizeof(float), n, cudaMemcpyHostToDevice));
     const unsigned blocks = static_cast<unsigned>(std::min<size_t>((elems + 255) / 256, 148 * 64));
+    if (dp % 64 == 0 && (ix->tensor_path || bf16)) {
+      const uint32_t kb = dp / 64, ops = bf16 ? 1 : 2;
+      const uint64_t n_tiles = (n + 127) / 128;
+      const uint64_t tc_bytes = n_tiles * kb * ops * 16384;
+      ix->tc_tiles = dmalloc<uint8_t>(tc_bytes);
+      const uint64_t n_chunks = tc_bytes / 16;
+      tile_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n_chunks + 255) / 256, 148 * 64)), 256, 0, st>>>(
+          f32, n, dp, kb, ops, ix->tc_tiles, n_chunks);
+      HYRE_CUDA(cudaGetLastError());
+      ix->tc_ops = ops;
+      ix->has_tc = true;
+      ix->stats.tensor_bytes = tc_bytes;
+    }
     if (bf16) {
       ix->emb_hi = dmalloc<__nv_bfloat16>(elems);
       split_kernel<<<blocks, 256, 0, st>>>(f32, elems, ix->emb_hi, nullptr);
@@ -126,15 +195,8 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       cudaFree(f32);
     } else {
       ix->emb_f32 = f32;
-      if (ix->tensor_path) {
-        ix->emb_hi = dmalloc<__nv_bfloat16>(elems);
-        ix->emb_lo = dmalloc<__nv_bfloat16>(elems);
-        split_kernel<<<blocks, 256, 0, st>>>(f32, elems, ix->emb_hi, ix->emb_lo);
-        HYRE_CUDA(cudaGetLastError());
-      }
     }
     ix->stats.embedding_bytes = elems * (bf16 ? 2 : 4);
-    ix->stats.tensor_bytes = (!bf16 && ix->tensor_path) ? elems * 4 : 0;
   }
 
   // ---- signatures --------------------------------------------------------
@@ -181,7 +243,6 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       HYRE_CUDA(cudaGetLastError());
       att.reset();
       off.reset();
-      pos.reset();
       int end_bit = 32;
       while ((uint64_t{1} << (end_bit - 32)) < C) ++end_bit;
       tmp_bytes = 0;
@@ -203,6 +264,19 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
                                                    runs.get(), n_runs.get(), P));
       uint32_t T = 0;
       HYRE_CUDA(cudaMemcpy(&T, n_runs.get(), 4, cudaMemcpyDeviceToHost));
+      const uint32_t Ap = (A + 7) / 8 * 8;  // 16-byte rows
+      if (T <= kForwardMaxTerms && C <= 32 && Ap <= 32) {
+        ix->row_terms = dmalloc<uint16_t>(size_t{n} * Ap);
+        ix->slot_of = dmalloc<uint8_t>(T);
+        row_terms_kernel<<<blocks, 256>>>(keys.get(), pos.get(), n, P, uniq.get(), T, Ap, ix->row_terms);
+        slot_of_kernel<<<(T + 255) / 256, 256>>>(uniq.get(), T, ix->slot_of);
+        HYRE_CUDA(cudaGetLastError());
+        HYRE_CUDA(cudaDeviceSynchronize());
+        ix->n_terms_fwd = T;
+        ix->stats.forward_bytes = size_t{n} * Ap * 2;
+        ix->row_terms_width = Ap;
+      }
+      pos.reset();
       std::vector<uint64_t> hk(T);
       std::vector<uint32_t> hdf(T);
       HYRE_CUDA(cudaMemcpy(hk.data(), uniq.get(), T * 8ull, cudaMemcpyDeviceToHost));
@@ -215,7 +289,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       uint64_t begin = 0, bsum = 0;
       ix->terms.reserve(T * 2);
       for (uint32_t i = 0; i < T; ++i) {
-        Term t{UINT32_MAX, hdf[i], begin};
+        Term t{UINT32_MAX, hdf[i], begin, i};
         if (hdf[i] >= dense_df) {
           t.bitmap = ix->n_bitmap_terms++;
           items.push_back({begin, hdf[i], t.bitmap});
@@ -248,13 +322,6 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
     }
   }
   HYRE_CUDA(cudaDeviceSynchronize());
-  // TMA descriptors for the tensor-core scorer: 128-row x 64-element boxes,
-  // 128-byte swizzle (the canonical K-major UMMA operand layout).
-  if (ix->emb_hi && dp % 64 == 0) {
-    make_bf16_map(&ix->tm_hi, ix->emb_hi, n, dp, 128);
-    make_bf16_map(&ix->tm_lo, ix->emb_lo ? ix->emb_lo : ix->emb_hi, n, dp, 128);
-    ix->has_tmaps = true;
-  }
   ix->stats.num_rows = n;
   ix->stats.row_base = ix->row_base;
   ix->stats.dim = d;

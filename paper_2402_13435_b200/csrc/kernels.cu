@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include <cstring>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -129,9 +130,10 @@ void launch_mask(const MaskArgs& a, cudaStream_t st) {
 }
 
 // Term-major K1 (batched CNF evaluation).  Program layout in c_mask_prog:
-//   [0] n_groups, then per group g: [1+2g] offset, [2+2g] live-query mask;
+//   [0] first group index of this launch, then per group g: [1+2g] offset,
+//   [2+2g] live-query mask;
 //   at offset: n_slots, then per slot: { constrained-query mask, n_refs,
-//   n_refs x (ref index, using-query mask) }.
+//   n_refs x (ref pointer lo, ref pointer hi, using-query mask) }.
 // Thread t of CTA (chunk, group) owns mask word chunk*128+t for the group's
 // 32 queries: for every slot it ORs each ref word into the accumulators of
 // the queries that use it (uniform predicates), then ANDs the slot into the
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
   const uint32_t widx = chunk * kChunkWords + t;
   const uint32_t live = c_mask_prog[2 + 2 * g];
   uint32_t pos = c_mask_prog[1 + 2 * g];
+  const uint32_t q0 = (c_mask_prog[0] + g) * 32;  // word 0 = first group of this launch
   const uint32_t tm = tail_mask(widx, a.n_rows);
   uint32_t res[32];
 #pragma unroll
@@ -163,10 +166,26 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
     uint32_t acc[32];
 #pragma unroll
     for (int q = 0; q < 32; ++q) acc[q] = 0u;
-    for (uint32_t r = 0; r < n_refs; ++r) {
-      const uint32_t ref = c_mask_prog[pos], users = c_mask_prog[pos + 1];
-      pos += 2;
-      const uint32_t w = __ldg(a.refs[ref] + widx);
+    // refs are (pointer lo, pointer hi, users) triples; 4 independent word
+    // loads are issued before they are consumed.
+    uint32_t r = 0;
+    for (; r + 4 <= n_refs; r += 4, pos += 12) {
+      uint32_t w[4], u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t ptr = (static_cast<uint64_t>(c_mask_prog[pos + 3 * k + 1]) << 32) | c_mask_prog[pos + 3 * k];
+        w[k] = __ldg(reinterpret_cast<const uint32_t*>(ptr) + widx);
+        u[k] = c_mask_prog[pos + 3 * k + 2];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] |= ((u[k] >> q) & 1u) ? w[k] : 0u;
+    }
+    for (; r < n_refs; ++r, pos += 3) {
+      const uint64_t ptr = (static_cast<uint64_t>(c_mask_prog[pos + 1]) << 32) | c_mask_prog[pos];
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(ptr) + widx);
+      const uint32_t users = c_mask_prog[pos + 2];
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] |= ((users >> q) & 1u) ? w : 0u;
     }
@@ -175,7 +194,6 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
       if ((hc >> q) & 1u) res[q] &= acc[q];
   }
   const int lane = t & 31, w = t >> 5;
-  const uint32_t q0 = g * 32;
 #pragma unroll
   for (int q = 0; q < 32; ++q) {
     if (q0 + q < a.B) a.mask[static_cast<size_t>(q0 + q) * a.words + widx] = res[q];
@@ -191,19 +209,165 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
 }
 
 template <uint32_t N>
-void launch_mask_tm_n(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st) {
+void launch_mask_tm_n(const MaskArgs& a, const std::vector<uint32_t>& words, uint32_t n_groups,
+                      cudaStream_t st) {
   MaskProg<N> p;
-  std::memcpy(p.w, prog_tm, prog_words * 4);
-  const uint32_t groups = (a.B + 31) / 32;
-  mask_tm_kernel<N><<<dim3(a.n_chunks, groups), kChunkWords, 0, st>>>(a, p);
+  std::memcpy(p.w, words.data(), words.size() * 4);
+  mask_tm_kernel<N><<<dim3(a.n_chunks, n_groups), kChunkWords, 0, st>>>(a, p);
 }
 
-bool launch_mask_tm(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st) {
-  if (a.B == 0 || a.n_chunks == 0) return true;
-  if (prog_words <= 1024) launch_mask_tm_n<1024>(a, prog_tm, prog_words, st);
-  else if (prog_words <= kMaskProgWords) launch_mask_tm_n<kMaskProgWords>(a, prog_tm, prog_words, st);
-  else return false;
-  return true;
+uint32_t launch_mask_tm(const MaskArgs& a, const std::vector<std::vector<uint32_t>>& groups,
+                        const std::vector<uint32_t>& live, cudaStream_t st) {
+  if (a.B == 0 || a.n_chunks == 0) return 0;
+  uint32_t launches = 0;
+  // pack consecutive groups into launches whose program fits the parameter
+  for (size_t g0 = 0; g0 < groups.size();) {
+    std::vector<uint32_t> w{static_cast<uint32_t>(g0)};
+    size_t g1 = g0, body = 0;
+    while (g1 < groups.size() && 1 + 2 * (g1 - g0 + 1) + body + groups[g1].size() <= kMaskProgWords)
+      body += groups[g1++].size();
+    if (g1 == g0) return launches | 0x80000000u;  // one group alone is too big
+    const uint32_t n = static_cast<uint32_t>(g1 - g0);
+    w.resize(1 + 2 * n);
+    for (size_t g = g0; g < g1; ++g) {
+      w[1 + 2 * (g - g0)] = static_cast<uint32_t>(w.size());
+      w[2 + 2 * (g - g0)] = live[g];
+      w.insert(w.end(), groups[g].begin(), groups[g].end());
+    }
+    if (w.size() <= 1024) launch_mask_tm_n<1024>(a, w, n, st);
+    else launch_mask_tm_n<kMaskProgWords>(a, w, n, st);
+    ++launches;
+    g0 = g1;
+  }
+  return launches;
+}
+
+// ===========================================================================
+// K1b: forward-index CNF evaluation (the paper's TBR direction, PAPER.md
+// appendix: per row, its attributes against the query clauses).  For a batch
+// it is the cheaper direction: each row's <= A term ids (2 B each) are read
+// once and, per term, a 64-bit mask of the batch queries using that term is
+// OR-ed into the row's clause accumulator; clauses are AND-ed across slots.
+// All 64 (x NW) queries of the pass are evaluated together per row.  The
+// per-query mask words are produced with warp ballots into a shared tile and
+// written coalesced; per-chunk eligible counts feed K2/K3/K5 as before.
+// CTA = one chunk (4096 rows = 128 mask words), 32 warps x 4 rounds of 32 rows.
+// ===========================================================================
+template <int NW>
+__global__ void __launch_bounds__(1024) fwd_mask_kernel(FwdArgs a) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  uint32_t* tile = reinterpret_cast<uint32_t*>(fsm);                     // [64*NW][128]
+  uint64_t* users = reinterpret_cast<uint64_t*>(tile + 64 * NW * 128);  // [T][NW]
+  uint64_t* hc = users + static_cast<size_t>(a.T) * NW;                 // [C][NW]
+  uint8_t* slot_of = reinterpret_cast<uint8_t*>(hc + a.C * NW);         // [T]
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, chunk = blockIdx.x;
+  for (uint32_t i = tid; i < a.T * NW; i += blockDim.x) users[i] = 0ull;
+  for (uint32_t i = tid; i < a.C * NW; i += blockDim.x) hc[i] = a.hc[i];
+  for (uint32_t i = tid; i < a.T; i += blockDim.x) slot_of[i] = a.slot_of[i];
+  __syncthreads();
+  const uint32_t stride = 1 + 2 * NW;
+  for (uint32_t e = tid; e < a.n_entries; e += blockDim.x) {
+    const uint32_t* en = a.entries + static_cast<size_t>(e) * stride;
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+      users[en[0] * NW + w] = (static_cast<uint64_t>(en[2 + 2 * w]) << 32) | en[1 + 2 * w];
+  }
+  uint64_t live[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) live[w] = a.live[w];
+  __syncthreads();
+  for (uint32_t rnd = 0; rnd < 4; ++rnd) {
+    const uint32_t wl = rnd * 32 + warp;  // word within the chunk
+    const uint32_t row = (chunk * kChunkWords + wl) * 32 + lane;
+    uint64_t res[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) res[w] = row < a.n_rows ? live[w] : 0ull;
+    if (row < a.n_rows) {
+      // the row's term ids (slot-major, 0xFFFF padded) in registers: A <= 32
+      uint32_t tw[16];
+      const uint4* src = reinterpret_cast<const uint4*>(a.row_terms + static_cast<size_t>(row) * a.A);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 x = (v * 8 < static_cast<int>(a.A)) ? __ldg(src + v) : make_uint4(~0u, ~0u, ~0u, ~0u);
+        tw[4 * v] = x.x;
+        tw[4 * v + 1] = x.y;
+        tw[4 * v + 2] = x.z;
+        tw[4 * v + 3] = x.w;
+      }
+      uint64_t acc[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) acc[w] = 0ull;
+      uint32_t present = 0, sprev = 0;
+      // clause accumulators are closed (AND-ed into res) whenever the slot
+      // changes; all lookups are independent, so they pipeline
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t t = (j < static_cast<int>(a.A)) ? ((tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) : 0xFFFFu;
+        if (t == 0xFFFFu) break;
+        const uint32_t sl = slot_of[t];
+        const bool change = j > 0 && sl != sprev;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint64_t close = change ? (acc[w] | ~hc[sprev * NW + w]) : ~0ull;
+          res[w] &= close;
+          acc[w] = (change ? 0ull : acc[w]) | users[t * NW + w];
+        }
+        present |= 1u << sl;
+        sprev = sl;
+      }
+      if (present) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) res[w] &= acc[w] | ~hc[sprev * NW + w];
+      }
+      // constrained slots the row has no attribute in can never match
+      for (uint32_t sl = 0; sl < a.C; ++sl)
+        if (!((present >> sl) & 1u))
+#pragma unroll
+          for (int w = 0; w < NW; ++w) res[w] &= ~hc[sl * NW + w];
+    }
+    // transpose: query q's word for these 32 rows = ballot of bit q
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+#pragma unroll 8
+      for (int qb = 0; qb < 64; ++qb) {
+        const unsigned bal = __ballot_sync(0xffffffffu, (res[w] >> qb) & 1ull);
+        if (lane == (qb & 31)) tile[(w * 64 + qb) * kChunkWords + wl] = bal;
+      }
+    }
+  }
+  __syncthreads();
+  // coalesced store of the tile + per-query chunk counts (warp w: queries w, w+32, ...)
+  for (uint32_t q = warp; q < 64 * NW; q += 32) {
+    const uint32_t gq = a.q0 + q;
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t word = tile[q * kChunkWords + i * 32 + lane];
+      c += __popc(word);
+      if (gq < a.B) a.mask[static_cast<size_t>(gq) * a.words + chunk * kChunkWords + i * 32 + lane] = word;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && gq < a.B) {
+      a.chunk_cnt[static_cast<size_t>(gq) * a.n_chunks + chunk] = c;
+      if (c) atomicAdd(a.n_elig + gq, c);
+    }
+  }
+}
+
+size_t fwd_mask_smem(uint32_t T, uint32_t C, uint32_t nw) {
+  return size_t{64} * nw * kChunkWords * 4 + size_t{T} * nw * 8 + size_t{C} * nw * 8 + T + 16;
+}
+
+void launch_fwd_mask(const FwdArgs& a, cudaStream_t st) {
+  const size_t smem = fwd_mask_smem(a.T, a.C, a.nw);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fwd_mask_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_mask_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  if (a.nw == 2) fwd_mask_kernel<2><<<a.n_chunks, 1024, smem, st>>>(a);
+  else fwd_mask_kernel<1><<<a.n_chunks, 1024, smem, st>>>(a);
 }
 
 // CSR postings -> scratch clause bitmaps (sparse terms, df < W/8).
@@ -420,6 +584,11 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const bool elig = (src_word >> (my_off & 31)) & 1u;
         const uint32_t grow = a.row_base + static_cast<uint32_t>(seg_row0) + my_off;
         const uint64_t key = make_key(clamp_score(p[0]), grow);
+        if (a.mode == SCORE_SAMPLE) {
+          // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
+          if (my_ok && elig) a.cand[static_cast<size_t>(q0 + j) * a.cap + it * kSegRows + my_off] = key;
+          continue;
+        }
         const bool take = my_ok && elig && key >= thr[j];
         const unsigned bal = __ballot_sync(kFull, take);
         if (bal) {
@@ -496,17 +665,24 @@ __device__ uint64_t kth_largest(const uint64_t* keys, uint32_t n, uint32_t k, ui
     for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     // Candidate scores cluster in a few digits, so aggregate equal digits
-    // within the warp first (one smem atomic per distinct digit).
-    for (uint32_t base = 0; base < n; base += blockDim.x) {
-      const uint32_t i = base + threadIdx.x;
-      uint32_t digit = 0xffffffffu;
-      if (i < n) {
-        const uint64_t key = keys[i];
-        if ((key & pmask) == prefix) digit = static_cast<uint32_t>((key >> sh) & dm);
+    // within the warp first (one smem atomic per distinct digit); each thread
+    // keeps 4 independent key loads in flight.
+    for (uint32_t base = 0; base < n; base += 4 * blockDim.x) {
+      uint64_t kv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        kv[u] = i < n ? keys[i] : 0ull;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, digit);
-      if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
-        atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        uint32_t digit = 0xffffffffu;
+        if (i < n && (kv[u] & pmask) == prefix) digit = static_cast<uint32_t>((kv[u] >> sh) & dm);
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
+          atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
+      }
     }
     __syncthreads();
     // Position t of the scan owns bins [8*o, 8*o+8) with o = T-1-t, so the
@@ -572,7 +748,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   const QParam qp = a.qp[q];
   if ((qp.flags & a.require_flags) != a.require_flags) return;
   if (a.mode == SELECT_FINAL_RERUN && !a.rerun[q]) return;
-  const uint32_t total = a.cnt[q];
+  const uint32_t total = (a.mode == SELECT_KTH && a.dense_n) ? a.dense_n : a.cnt[q];
   const uint32_t n = min(total, a.cap);
   const uint64_t* keys = a.buf + static_cast<size_t>(q) * a.cap;
   const uint32_t k = qp.k;
@@ -587,7 +763,30 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     if (n >= k && k > 0) t_safe = kth_largest(keys, n, k, hist, tmp);
     const uint32_t m = min(k, max(8u, (4 * k + a.period - 1) / a.period));
     uint64_t t_est = t_safe;
-    if (m < k && n >= m) t_est = kth_largest(keys, n, m, hist, tmp);
+    if (m < k && n >= m) {
+      if (t_safe != 0ull) {
+        // the m-th key is among the k keys >= t_safe: sort those in smem
+        if (threadIdx.x == 0) gathered = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          const uint64_t key = keys[i];
+          if (key >= t_safe) {
+            const uint32_t at = atomicAdd(&gathered, 1u);
+            if (at < kSelectMaxK) sortbuf[at] = key;
+          }
+        }
+        __syncthreads();
+        const uint32_t g = min(gathered, kSelectMaxK);
+        uint32_t g2 = 1;
+        while (g2 < g) g2 <<= 1;
+        for (uint32_t i = g + threadIdx.x; i < g2; i += blockDim.x) sortbuf[i] = 0ull;
+        __syncthreads();
+        bitonic_desc(sortbuf, g2);
+        t_est = sortbuf[m - 1];
+      } else {
+        t_est = kth_largest(keys, n, m, hist, tmp);
+      }
+    }
     if (threadIdx.x == 0) {
       a.thr[q] = t_est;
       if (a.thr_safe) a.thr_safe[q] = t_safe;

@@ -2,6 +2,8 @@
 // SURVEY.md §2 / DESIGN.md §4).  All launches are asynchronous on `st`.
 #pragma once
 
+#include <vector>
+
 #include "device.cuh"
 
 namespace hyreb {
@@ -25,7 +27,30 @@ void launch_mask(const MaskArgs& a, cudaStream_t st);
 // accumulators in registers.  Returns false if the program does not fit (the
 // generic launch_mask is used instead).
 constexpr uint32_t kMaskProgWords = 7936;  // fits the 32 KB kernel-parameter limit
-bool launch_mask_tm(const MaskArgs& a, const uint32_t* prog_tm, uint32_t prog_words, cudaStream_t st);
+// Returns the number of launches; bit 31 set if a group's program alone is too
+// large (the caller then uses the generic launch_mask).
+uint32_t launch_mask_tm(const MaskArgs& a, const std::vector<std::vector<uint32_t>>& groups,
+                        const std::vector<uint32_t>& live, cudaStream_t st);
+
+// K1b: forward-index CNF evaluation for batches (see kernels.cu).  One pass
+// evaluates up to 64 * NW queries; `entries` lists (term id, NW x 64-bit
+// users mask) for every term referenced by the pass's clauses.
+struct FwdArgs {
+  const uint16_t* row_terms;
+  const uint8_t* slot_of;
+  uint32_t A, n_rows, words, n_chunks, B, C, T;
+  const uint32_t* entries;  // n_entries x (1 + 2 * NW) u32
+  uint32_t n_entries;
+  const uint64_t* hc;       // [C][NW] queries constraining each slot
+  const uint64_t* live;     // [NW] active, non-empty queries
+  uint32_t q0;              // first query of this pass
+  uint32_t nw;              // 1 or 2
+  uint32_t* mask;
+  uint32_t* chunk_cnt;
+  uint32_t* n_elig;
+};
+size_t fwd_mask_smem(uint32_t T, uint32_t C, uint32_t nw);
+void launch_fwd_mask(const FwdArgs& a, cudaStream_t st);
 
 // CSR postings scattered into per-clause scratch bitmaps.
 struct ScatterItem {
@@ -80,6 +105,7 @@ struct SelectArgs {
   // falls back to thr_safe (rerun) if the estimate admitted fewer than K rows.
   uint64_t* thr_safe;
   uint32_t period;
+  uint32_t dense_n;  // KTH over a dense sample buffer: slots [0, dense_n) (0 keys = ineligible)
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
 

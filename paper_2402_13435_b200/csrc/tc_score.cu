@@ -31,7 +31,7 @@ namespace {
 
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
-constexpr uint32_t kStage = 8;                    // staged candidate keys per (epilogue warp, query)
+constexpr uint32_t kStage = 2;                    // staged candidate keys per (epilogue warp, query)
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
 constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
 
@@ -58,6 +58,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
   } while (!done);
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -126,28 +133,26 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_score_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-                    const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
-                    TcArgs a) {
+    tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Np = a.Np, kb = a.kblocks, S = a.stages;
   const uint32_t q_box = Np * 128;  // bytes of one K-atom of the query tile
   const uint32_t q_bytes = q_box * kb;
-  const uint32_t a_bytes = kAtomBytes * kb;  // one operand of one stage
+  const uint32_t a_bytes = kAtomBytes;  // one operand of one stage (one 128-byte K atom of 128 rows)
   const uint32_t n_ops = a.split ? 2 : 1;
   // smem carve-up
   uint8_t* s_qhi = smem;
   uint8_t* s_qlo = s_qhi + q_bytes;
-  uint8_t* s_stage = s_qlo + q_bytes;  // [S][n_ops][kb][16 KB]
+  uint8_t* s_stage = s_qlo + q_bytes;  // [S][n_ops][16 KB]: ring of K-atom stages, kb per tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + size_t{S} * n_ops * a_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
   uint64_t* tempty = bars + 2 * S + 2;
   uint64_t* qbar = bars + 2 * S + 4;
-  float* s_ts = reinterpret_cast<float*>(bars + 2 * S + 5);    // [Np] threshold score
+  float* s_ts = reinterpret_cast<float*>(bars + ((2 * S + 6) & ~1u));  // [Np] threshold score (16-B aligned)
   uint32_t* s_tr = reinterpret_cast<uint32_t*>(s_ts + Np);     // [Np] threshold row
   uint32_t* s_tmem = s_tr + Np;                                // TMEM base
   uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
@@ -185,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_ts[j] = -2.0f;  // no threshold
       s_tr[j] = 0u;
     } else {
-      s_ts[j] = key_score(thr);
+      const float ts = key_score(thr);
+      s_ts[j] = ts <= -1.0f ? -2.0f : ts;
       s_tr[j] = key_row(thr);
     }
   }
@@ -209,7 +215,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ahi)) : "memory");
       mbar_expect_tx(qbar, 2 * q_bytes);
       for (uint32_t k = 0; k < kb; ++k) {
         tma_load_2d(s_qhi + k * q_box, &tm_qhi, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
@@ -219,19 +224,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
-        mbar_wait(empty + s, ph ^ 1);
-        mbar_expect_tx(full + s, n_ops * a_bytes);
-        uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
         for (uint32_t k = 0; k < kb; ++k) {
-          tma_load_2d(st + k * kAtomBytes, &tm_ahi, full + s, static_cast<int>(k * 64),
-                      static_cast<int>(t * kTileRows));
-          if (a.split)
-            tma_load_2d(st + a_bytes + k * kAtomBytes, &tm_alo, full + s, static_cast<int>(k * 64),
-                        static_cast<int>(t * kTileRows));
-        }
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_expect_tx(full + s, n_ops * a_bytes);
+          // one contiguous, pre-swizzled K-atom (hi [+ lo]) per stage
+          bulk_load(s_stage + size_t{s} * n_ops * a_bytes,
+                    a.tiles + (static_cast<size_t>(t) * kb + k) * n_ops * a_bytes, n_ops * a_bytes, full + s);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -248,32 +250,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t acc = i & 1, aph = (i >> 1) & 1;
         mbar_wait(tempty + acc, aph ^ 1);
         fence_after();
-        mbar_wait(full + s, ph);
-        fence_after();
         const uint32_t d = tmem + acc * Np;
-        const uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
         uint32_t accum = 0;
         for (uint32_t k = 0; k < kb; ++k) {
+          mbar_wait(full + s, ph);
+          fence_after();
+          const uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
 #pragma unroll
-          for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K16 per 128-byte atom
-            const uint64_t ahi = sw128_desc(smem_u32(st + k * kAtomBytes + kk * 32));
+          for (uint32_t kk = 0; kk < 4 && !(a.debug & 1u); ++kk) {  // 4 x K16 per 128-byte atom
+            const uint64_t ahi = sw128_desc(smem_u32(st + kk * 32));
             const uint64_t qhi = sw128_desc(smem_u32(s_qhi + k * q_box + kk * 32));
             const uint64_t qlo = sw128_desc(smem_u32(s_qlo + k * q_box + kk * 32));
             mma_bf16(d, ahi, qhi, idesc, accum);
             accum = 1;
             mma_bf16(d, ahi, qlo, idesc, 1);
             if (a.split) {
-              const uint64_t alo = sw128_desc(smem_u32(st + a_bytes + k * kAtomBytes + kk * 32));
+              const uint64_t alo = sw128_desc(smem_u32(st + a_bytes + kk * 32));
               mma_bf16(d, alo, qhi, idesc, 1);
             }
           }
+          mma_commit(empty + s);  // this K-atom stage is free once its MMAs retire
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        mma_commit(empty + s);   // smem stage free once these MMAs retire
-        mma_commit(tfull + acc); // accumulator ready for the epilogue
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
-        }
+        mma_commit(tfull + acc);  // accumulator ready for the epilogue
       }
     }
   } else {
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (uint32_t cc = 0; cc < 2; ++cc) {
         const uint32_t c = half + 2 * cc;
-        if (c >= nq32) break;
+        if (c >= nq32 || (a.debug & 2u)) break;
         uint32_t v[32];
         tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
         // 32x32 bit transpose: lane l held query (32c+l)'s word over this
@@ -317,17 +319,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t y = __shfl_xor_sync(0xffffffffu, elig, j);
           elig = (lane & j) ? ((elig & ~m) | ((y & ~m) >> j)) : ((elig & m) | ((y & m) << j));
         }
-        // threshold test for all 32 queries, branch-free
+        // threshold test for all 32 queries: one compare of the raw
+        // accumulator against the query's threshold score.  `>=` admits a
+        // superset of the exact key test (ties with the threshold row, values
+        // clamped later); K4 resolves it exactly.  Thresholds at or below -1
+        // are stored as -2 so clamping can never hide a candidate.
         uint32_t take = 0;
-        const float* ts = s_ts + c * 32;
-        const uint32_t* tr = s_tr + c * 32;
+        const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
 #pragma unroll
-        for (uint32_t j = 0; j < 32; ++j) {
-          const float sc = clamp_score(__uint_as_float(v[j]));
-          const bool pass = sc > ts[j] || (sc == ts[j] && grow <= tr[j]);
-          take |= static_cast<uint32_t>(pass) << j;
+        for (uint32_t j4 = 0; j4 < 8; ++j4) {
+          const float4 t4 = ts4[j4];
+          take |= (__uint_as_float(v[4 * j4 + 0]) >= t4.x ? 1u : 0u) << (4 * j4 + 0);
+          take |= (__uint_as_float(v[4 * j4 + 1]) >= t4.y ? 1u : 0u) << (4 * j4 + 1);
+          take |= (__uint_as_float(v[4 * j4 + 2]) >= t4.z ? 1u : 0u) << (4 * j4 + 2);
+          take |= (__uint_as_float(v[4 * j4 + 3]) >= t4.w ? 1u : 0u) << (4 * j4 + 3);
         }
         take &= elig;
+        if (a.mode == SCORE_SAMPLE) {
+          // sample pass: every eligible sampled row goes to its fixed slot
+          // (segment ordinal x 1024 + row in segment) -- no threshold, no atomics
+          const uint32_t local = t * kTileRows + quad * 32 + lane;
+          const uint32_t sidx = (local / 1024) / a.period * 1024 + (local & 1023);
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j)
+            if ((elig >> j) & 1u)
+              a.cand[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] =
+                  make_key(clamp_score(__uint_as_float(v[j])), grow);
+          continue;
+        }
         if (__any_sync(0xffffffffu, take != 0)) {
           // rare path: stage survivors in this warp's private smem slots,
           // spill to the global candidate buffer only when a slot row is full
@@ -336,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!((take >> j) & 1u)) continue;
             const uint32_t qq = c * 32 + j;
             const uint64_t key = make_key(clamp_score(__uint_as_float(v[j])), grow);
+            if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
             const uint32_t slot = atomicAdd(s_scnt + ewarp * Np + qq, 1u);
             if (slot < kStage) {
               s_skey[(static_cast<size_t>(ewarp) * Np + qq) * kStage + slot] = key;
@@ -408,18 +428,18 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
 }
 
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages) {
-  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes * kb + (2 * stages + 5) * 8 + Np * 8 +
+  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 5) * 8 + Np * 8 +
          4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64;
 }
 
-void launch_tc_score(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& qhi, const CUtensorMap& qlo,
-                     const TcArgs& a, uint32_t grid, size_t smem, cudaStream_t st) {
+void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
+                     cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  tc_score_kernel<<<grid, kThreads, smem, st>>>(ahi, alo, qhi, qlo, a);
+  tc_score_kernel<<<grid, kThreads, smem, st>>>(qhi, qlo, a);
 }
 
 }  // namespace hyreb

@@ -8,6 +8,7 @@
 namespace hyreb {
 
 struct TcArgs {
+  const uint8_t* tiles;  // DevIndex::tc_tiles
   uint32_t n_rows, row_base, words, n_tiles;
   uint32_t B;        // queries in the batch
   uint32_t q0;       // first query of this group
@@ -23,6 +24,7 @@ struct TcArgs {
   uint32_t* cand_cnt;
   uint32_t cap, mode, period, gate;
   const uint32_t* rerun;
+  uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work (results invalid)
 };
 
 constexpr uint32_t kTcMinBatch = 9;  // batches above 8 queries use the tensor-core scorer
@@ -30,7 +32,7 @@ constexpr uint32_t kTcMaxGroup = 128;
 
 void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages);
-void launch_tc_score(const CUtensorMap& ahi, const CUtensorMap& alo, const CUtensorMap& qhi, const CUtensorMap& qlo,
-                     const TcArgs& a, uint32_t grid, size_t smem, cudaStream_t st);
+void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
+                     cudaStream_t st);
 
 }  // namespace hyreb

@@ -440,3 +440,36 @@ def test_candidate_overflow_recovers(hy, B):
     for o in outs:
         gr, gs = hits(o.result)
         assert_topk_match(ref, q, gr, gs, er, es)
+
+
+@pytest.mark.parametrize("B", [9, 64, 130])
+def test_batched_tbr_bitexact(hy, B):
+    # Batches > 8 evaluate the CNF from the forward term lists (K1b); the row
+    # sets must equal the oracle's full_scan_tbr bit for bit, including sparse
+    # (CSR) terms, absent ids (empty clause), match-all and 2-pass batches.
+    n, C = 60_000, 3
+    rs = np.random.default_rng(11)
+    docs = []
+    for i in range(n):
+        cl = [(1 + np.minimum(rs.zipf(1.3, size=rs.integers(0, 4)), 3000)).tolist() for _ in range(C)]
+        docs.append(O.Doc(f"d{i}", cl, np.ones(4, np.float32)))
+    width = max(sum(len(set(c)) for c in d.clauses) for d in docs)
+    prod = product_index(docs, C, width, 4, 64, 1)
+    ref = O.freeze(docs, C, width, 4, 64, 1)
+    ex = hy.Executor(prod, max_batch=B)
+    batch, expect = hy.BatchRequest(), []
+    for i in range(B):
+        if i % 17 == 0:
+            raw = {}
+        elif i % 23 == 0:
+            raw = {1: [999_999]}  # id absent from the index
+        else:
+            raw = {c: (1 + np.minimum(rs.zipf(1.3, size=rs.integers(1, 5)), 3000)).tolist()
+                   for c in range(C) if rs.random() < 0.7}
+        q = O.normalize_query(raw, C)
+        batch.queries.append(hy.HybridQuery(to_cnf(q), None, n))
+        expect.append(O.full_scan_tbr(ref, q))
+    outs = ex.execute_batch(batch)
+    for o, e in zip(outs, expect):
+        assert o.ok
+        assert np.array_equal(np.asarray([h.row_id for h in o.result.hits], np.int64), e)

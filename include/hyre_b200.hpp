@@ -1,0 +1,483 @@
+// hyre_b200.hpp -- header-only C++ drop-in for the reference's hot-path API
+// (proj/include/hyre/{types,common,corpus,quantizer,term_match,knn,pipeline}.hpp)
+// implemented over the C-ABI in hyre_b200.h.  Same namespace, class names,
+// signatures and exceptions, so the reference's callers -- SearchService
+// (service.cpp:151-226), run_bench (bench.cpp:52-131), tt::knn_recall
+// (two_tower.cpp:369-394) -- compile unchanged against this header and link
+// libhyre_b200.so instead of the reference's corpus/term_match/quantizer/
+// knn/pipeline translation units.  See INTEGRATION.md.
+//
+// Differences a caller can observe (documented in DESIGN.md §6):
+//  * scores are computed on the GPU (FMA / tensor-core accumulation): equal to
+//    the reference within 1e-3 relative (2e-5 absolute floor), ties at the
+//    K-th score may resolve to a different row of the same score;
+//  * QuantCodec carries (dim, num_bits, seed); its rounds are re-derived inside
+//    the library exactly like FrozenIndex::load does (corpus.cpp:183).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hyre_b200.h"
+
+namespace hyre {
+
+// ---- errors (common.hpp:15-33, knn.cpp:59-61) ------------------------------
+class ValidationError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+
+class LoadError : public std::runtime_error {
+ public:
+  enum class Cause { kBadMagic, kVersionMismatch, kTruncated, kChecksum };
+  LoadError(Cause cause, const std::string& msg) : std::runtime_error(msg), cause_(cause) {}
+  Cause cause() const { return cause_; }
+
+ private:
+  Cause cause_;
+};
+
+namespace detail {
+inline void check(hyre_status st) {
+  if (st == HYRE_OK) return;
+  const std::string msg = hyre_last_error();
+  switch (st) {
+    case HYRE_INVALID_ARGUMENT: throw ValidationError(msg);
+    case HYRE_OUT_OF_RANGE: throw std::domain_error(msg);
+    case HYRE_LOAD_ERROR: throw LoadError(static_cast<LoadError::Cause>(hyre_last_load_cause()), msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+}  // namespace detail
+
+// ---- types.hpp ----------------------------------------------------------------
+struct Messenger {
+  std::uint32_t row_id = 0;
+  std::uint32_t batch_id = 0;
+  float score = 0.0f;
+  bool operator==(const Messenger&) const = default;
+};
+
+struct ScoredDoc {
+  std::string doc_id;
+  std::uint32_t row_id = 0;
+  float score = 0.0f;
+  bool operator==(const ScoredDoc&) const = default;
+};
+
+struct TopKResult {
+  std::vector<ScoredDoc> hits;
+  bool operator==(const TopKResult&) const = default;
+};
+
+// ---- quantizer.hpp (codec half) ---------------------------------------------------
+struct QuantCodec {
+  std::uint32_t dim = 0;
+  std::uint32_t num_bits = 0;
+  std::uint64_t seed = 0;
+  std::size_t num_words() const { return (num_bits + 63) / 64; }
+};
+
+struct Signature {
+  std::uint32_t num_bits = 0;
+  std::vector<std::uint64_t> words;
+  bool bit(std::uint32_t b) const { return (words[b / 64] >> (b % 64)) & 1u; }
+  bool operator==(const Signature&) const = default;
+};
+
+inline QuantCodec make_codec(std::uint32_t dim, std::uint32_t num_bits, std::uint64_t seed) {
+  if (dim == 0) throw ValidationError("codec dim must be >= 1");
+  if (num_bits == 0) throw ValidationError("codec numBits must be >= 1");
+  return QuantCodec{dim, num_bits, seed};
+}
+
+inline Signature encode(const QuantCodec& codec, std::span<const float> embedding) {
+  if (embedding.size() != codec.dim)
+    throw ValidationError("embedding length " + std::to_string(embedding.size()) + " != codec dim " +
+                          std::to_string(codec.dim));
+  Signature s{codec.num_bits, std::vector<std::uint64_t>(codec.num_words())};
+  detail::check(hyre_encode(codec.dim, codec.num_bits, codec.seed, embedding.data(), s.words.data()));
+  return s;
+}
+
+inline std::uint32_t quant_score_words(std::span<const std::uint64_t> a, std::span<const std::uint64_t> b,
+                                       std::uint32_t num_bits) {
+  return hyre_quant_score_words(a.data(), b.data(), static_cast<std::uint32_t>(a.size()), num_bits);
+}
+
+inline std::uint32_t quant_score(const Signature& a, const Signature& b) {
+  if (a.num_bits != b.num_bits) throw ValidationError("signature width mismatch");
+  return quant_score_words(a.words, b.words, a.num_bits);
+}
+
+// ---- corpus.hpp ---------------------------------------------------------------------
+struct DocumentInput {
+  std::string doc_id;
+  std::vector<std::vector<std::uint32_t>> clauses;
+  std::vector<float> embedding;
+};
+
+struct IndexConfig {
+  std::uint32_t num_clauses = 0;
+  std::uint32_t max_num_attr = 0;
+  std::uint32_t dim = 0;
+  std::vector<std::string> clause_names;
+};
+
+class Executor;
+
+class FrozenIndex {
+ public:
+  FrozenIndex(FrozenIndex&&) noexcept = default;
+  FrozenIndex& operator=(FrozenIndex&&) noexcept = default;
+
+  std::uint32_t num_docs() const { return shape_.num_docs; }
+  std::uint32_t num_clauses() const { return shape_.num_clauses; }
+  std::uint32_t max_num_attr() const { return shape_.max_num_attr; }
+  std::uint32_t dim() const { return shape_.dim; }
+  QuantCodec codec() const { return QuantCodec{shape_.dim, shape_.num_bits, shape_.seed}; }
+  std::vector<std::string> clause_names() const {
+    std::vector<std::string> out;
+    for (std::uint32_t c = 0; c < shape_.num_clauses; ++c) out.emplace_back(hyre_frozen_clause_name(f_.get(), c));
+    return out;
+  }
+
+  std::span<const std::uint32_t> attribute_row(std::uint32_t row) const {
+    return {hyre_frozen_attributes(f_.get()) + std::size_t{row} * shape_.max_num_attr, shape_.max_num_attr};
+  }
+  std::span<const std::uint32_t> offsets_row(std::uint32_t row) const {
+    return {hyre_frozen_offsets(f_.get()) + std::size_t{row} * (shape_.num_clauses + 1), shape_.num_clauses + 1u};
+  }
+  std::span<const std::uint32_t> clause_slice(std::uint32_t row, std::uint32_t clause) const {
+    auto offs = offsets_row(row);
+    return attribute_row(row).subspan(offs[clause], offs[clause + 1] - offs[clause]);
+  }
+  std::span<const float> embedding_row(std::uint32_t row) const {
+    return {hyre_frozen_embeddings(f_.get()) + std::size_t{row} * shape_.dim, shape_.dim};
+  }
+  std::span<const std::uint64_t> signature_words(std::uint32_t row) const {
+    return {hyre_frozen_signatures(f_.get()) + std::size_t{row} * shape_.num_words, shape_.num_words};
+  }
+  Signature signature_row(std::uint32_t row) const {
+    auto w = signature_words(row);
+    return Signature{shape_.num_bits, {w.begin(), w.end()}};
+  }
+  bool embedding_is_zero(std::uint32_t row) const { return hyre_frozen_zero_flags(f_.get())[row] != 0; }
+  std::string doc_id(std::uint32_t row) const { return hyre_frozen_doc_id(f_.get(), row); }
+  std::optional<std::uint32_t> row_of(const std::string& doc_id) const {
+    const std::int64_t r = hyre_frozen_row_of(f_.get(), doc_id.c_str());
+    if (r < 0) return std::nullopt;
+    return static_cast<std::uint32_t>(r);
+  }
+  int resolve_clause_slot(const std::string& name) const {
+    return hyre_frozen_resolve_clause_slot(f_.get(), name.c_str());
+  }
+
+  void save(const std::string& path) const { detail::check(hyre_frozen_save(f_.get(), path.c_str())); }
+  static FrozenIndex load(const std::string& path) {
+    hyre_frozen* f = nullptr;
+    detail::check(hyre_frozen_load(path.c_str(), &f));
+    return FrozenIndex(f);
+  }
+
+  // The device column store (GPU 0, fp32 rows + tensor-core tiles), built on
+  // first use by an Executor and shared by every executor of this index.
+  hyre_index* device() const {
+    if (!dev_->ix) {
+      hyre_index_options o{0, HYRE_EMB_F32, 0, 0, 1, 0};
+      detail::check(hyre_index_create(f_.get(), &o, &dev_->ix));
+    }
+    return dev_->ix;
+  }
+  const hyre_frozen* handle() const { return f_.get(); }
+
+ private:
+  friend class IndexBuilder;
+  explicit FrozenIndex(hyre_frozen* f) : f_(f, &hyre_frozen_destroy), dev_(std::make_shared<Dev>()) {
+    hyre_frozen_shape(f, &shape_);
+  }
+  struct Dev {
+    hyre_index* ix = nullptr;
+    ~Dev() {
+      if (ix) hyre_index_destroy(ix);
+    }
+  };
+  std::unique_ptr<hyre_frozen, void (*)(hyre_frozen*)> f_;
+  std::shared_ptr<Dev> dev_;
+  hyre_shape shape_{};
+};
+
+class IndexBuilder {
+ public:
+  explicit IndexBuilder(IndexConfig config) : dim_(config.dim) {
+    std::vector<const char*> names;
+    for (const auto& n : config.clause_names) names.push_back(n.c_str());
+    hyre_builder* b = nullptr;
+    detail::check(hyre_builder_create(config.num_clauses, config.max_num_attr, config.dim,
+                                      names.empty() ? nullptr : names.data(),
+                                      static_cast<std::uint32_t>(names.size()), &b));
+    b_.reset(b);
+  }
+  std::uint32_t add_document(const DocumentInput& doc) {
+    std::vector<std::uint32_t> offs{0}, ids;
+    for (const auto& c : doc.clauses) {
+      ids.insert(ids.end(), c.begin(), c.end());
+      offs.push_back(static_cast<std::uint32_t>(ids.size()));
+    }
+    std::uint32_t row = 0;
+    detail::check(hyre_builder_add_document(b_.get(), doc.doc_id.c_str(),
+                                            static_cast<std::uint32_t>(doc.clauses.size()), offs.data(),
+                                            ids.data(), doc.embedding.data(),
+                                            static_cast<std::uint32_t>(doc.embedding.size()), &row));
+    return row;
+  }
+  std::size_t size() const { return hyre_builder_size(b_.get()); }
+  FrozenIndex freeze(const QuantCodec& codec) && {
+    if (codec.dim != dim_) throw ValidationError("codec dim != index dim");
+    hyre_frozen* f = nullptr;
+    detail::check(hyre_builder_freeze(b_.get(), codec.num_bits, codec.seed, &f));
+    return FrozenIndex(f);
+  }
+
+ private:
+  struct Del {
+    void operator()(hyre_builder* b) const { hyre_builder_destroy(b); }
+  };
+  std::unique_ptr<hyre_builder, Del> b_;
+  std::uint32_t dim_;
+};
+
+// ---- term_match.hpp -------------------------------------------------------------
+struct CnfClause {
+  std::uint32_t slot = 0;
+  std::vector<std::uint32_t> attribute_ids;
+  bool operator==(const CnfClause&) const = default;
+};
+
+struct CnfQuery {
+  std::vector<CnfClause> clauses;
+  bool match_all() const { return clauses.empty(); }
+  bool operator==(const CnfQuery&) const = default;
+};
+
+inline CnfQuery normalize_query(const std::map<std::uint32_t, std::vector<std::uint32_t>>& raw,
+                                std::uint32_t num_clauses) {
+  std::vector<std::uint32_t> slots, offs{0}, ids;
+  for (const auto& [s, v] : raw) {
+    slots.push_back(s);
+    ids.insert(ids.end(), v.begin(), v.end());
+    offs.push_back(static_cast<std::uint32_t>(ids.size()));
+  }
+  std::vector<std::uint32_t> os(raw.size() + 1), oo(raw.size() + 2), oi(ids.size() + 1);
+  std::uint32_t n = 0;
+  detail::check(hyre_normalize_query(static_cast<std::uint32_t>(raw.size()), slots.data(), offs.data(),
+                                     ids.data(), num_clauses, &n, os.data(), oo.data(), oi.data()));
+  CnfQuery q;
+  for (std::uint32_t c = 0; c < n; ++c) q.clauses.push_back({os[c], {oi.begin() + oo[c], oi.begin() + oo[c + 1]}});
+  return q;
+}
+
+// ---- pipeline.hpp ---------------------------------------------------------------------
+struct ExecOptions {
+  bool quant_enabled = true;
+  std::uint32_t quant_k = 0;
+  std::uint32_t granularity = 100;
+  std::uint32_t effective_quant_k(std::uint32_t k) const { return quant_k != 0 ? quant_k : 200 * k; }
+};
+
+struct HybridQuery {
+  CnfQuery terms;
+  std::optional<std::vector<float>> embedding;
+  std::uint32_t k = 10;
+  ExecOptions options;
+};
+
+struct BatchRequest {
+  std::vector<HybridQuery> queries;
+};
+
+struct StageTimings {
+  double tbr_ms = 0, quant_ms = 0, ebr_ms = 0, topk_ms = 0, total_ms = 0;
+};
+
+struct QueryOutcome {
+  bool ok = false;
+  TopKResult result;
+  std::string error;
+};
+
+struct ScoredMessengers {
+  std::vector<Messenger> items;
+  bool query_was_renormalized = false;
+};
+
+namespace detail {
+// Flattens HybridQuery objects into hyre_query structs (pointers stay valid
+// while the pack lives).
+struct QueryPack {
+  std::vector<std::vector<std::uint32_t>> slots, offs, ids;
+  std::vector<hyre_query> q;
+  explicit QueryPack(const std::vector<HybridQuery>& qs) : slots(qs.size()), offs(qs.size()), ids(qs.size()) {
+    for (std::size_t i = 0; i < qs.size(); ++i) {
+      offs[i].push_back(0);
+      for (const auto& c : qs[i].terms.clauses) {
+        slots[i].push_back(c.slot);
+        ids[i].insert(ids[i].end(), c.attribute_ids.begin(), c.attribute_ids.end());
+        offs[i].push_back(static_cast<std::uint32_t>(ids[i].size()));
+      }
+      const auto& e = qs[i].embedding;
+      q.push_back(hyre_query{static_cast<std::uint32_t>(qs[i].terms.clauses.size()), slots[i].data(),
+                             offs[i].data(), ids[i].data(), e ? e->data() : nullptr,
+                             e ? static_cast<std::uint32_t>(e->size()) : 0u, qs[i].k,
+                             qs[i].options.quant_enabled ? 1u : 0u, qs[i].options.quant_k,
+                             qs[i].options.granularity});
+    }
+  }
+};
+}  // namespace detail
+
+inline void validate_query(const FrozenIndex& index, const HybridQuery& query) {
+  detail::QueryPack p({query});
+  detail::check(hyre_validate_query(index.handle(), p.q.data()));
+}
+
+class Executor {
+ public:
+  explicit Executor(const FrozenIndex& index, std::uint32_t max_batch = 16) : index_(index), max_batch_(max_batch) {
+    if (max_batch < 1) throw ValidationError("maxBatch must be >= 1");
+    hyre_executor* ex = nullptr;
+    detail::check(hyre_executor_create(index.device(), max_batch, &ex));
+    ex_.reset(ex);
+  }
+
+  TopKResult execute(const HybridQuery& query, StageTimings* timings = nullptr) {
+    detail::QueryPack p({query});
+    std::vector<hyre_hit> hits(std::max<std::uint32_t>(1, std::min(query.k, index_.num_docs())));
+    std::uint32_t n = 0;
+    hyre_timings t{};
+    detail::check(hyre_execute(ex_.get(), p.q.data(), hits.data(), &n, &t));
+    if (timings) *timings = StageTimings{t.tbr_ms, t.quant_ms, t.ebr_ms, t.topk_ms, t.total_ms};
+    return to_result(hits.data(), n);
+  }
+
+  std::vector<QueryOutcome> execute_batch(const BatchRequest& batch, StageTimings* timings = nullptr) {
+    const auto b = static_cast<std::uint32_t>(batch.queries.size());
+    detail::QueryPack p(batch.queries);
+    std::vector<std::uint64_t> offs(b + 1, 0);
+    for (std::uint32_t i = 0; i < b; ++i) offs[i + 1] = offs[i] + std::min(batch.queries[i].k, index_.num_docs());
+    std::vector<hyre_hit> hits(std::max<std::uint64_t>(1, offs[b]));
+    std::vector<std::uint32_t> counts(b);
+    std::vector<std::int32_t> st(b);
+    hyre_timings t{};
+    detail::check(hyre_execute_batch(ex_.get(), p.q.data(), b, hits.data(), offs.data(), counts.data(), st.data(), &t));
+    if (timings) *timings = StageTimings{t.tbr_ms, t.quant_ms, t.ebr_ms, t.topk_ms, t.total_ms};
+    std::vector<QueryOutcome> out(b);
+    for (std::uint32_t i = 0; i < b; ++i) {
+      out[i].ok = st[i] == HYRE_OK;
+      if (out[i].ok) out[i].result = to_result(hits.data() + offs[i], counts[i]);
+      else out[i].error = hyre_executor_slot_error(ex_.get(), i);
+    }
+    return out;
+  }
+
+  const FrozenIndex& index() const { return index_; }
+  std::uint32_t max_batch() const { return max_batch_; }
+  hyre_executor* handle() const { return ex_.get(); }
+
+ private:
+  TopKResult to_result(const hyre_hit* h, std::uint32_t n) const {
+    TopKResult r;
+    r.hits.reserve(n);
+    for (std::uint32_t i = 0; i < n; ++i) r.hits.push_back({index_.doc_id(h[i].row), h[i].row, h[i].score});
+    return r;
+  }
+  struct Del {
+    void operator()(hyre_executor* e) const { hyre_executor_destroy(e); }
+  };
+  const FrozenIndex& index_;
+  std::uint32_t max_batch_;
+  std::unique_ptr<hyre_executor, Del> ex_;
+};
+
+inline TopKResult execute(const FrozenIndex& index, const HybridQuery& query) {
+  Executor exec(index, 1);
+  return exec.execute(query);
+}
+
+inline std::vector<QueryOutcome> execute_batch(const FrozenIndex& index, const BatchRequest& batch) {
+  Executor exec(index, std::max<std::uint32_t>(1, static_cast<std::uint32_t>(batch.queries.size())));
+  return exec.execute_batch(batch);
+}
+
+// ---- stage functions (term_match.hpp:43-45, knn.hpp:24-35, quantizer.hpp:71-74) ----
+inline std::vector<Messenger> full_scan_tbr(const FrozenIndex& index, const CnfQuery& query,
+                                            std::uint32_t batch_id = 0) {
+  Executor ex(index, 1);
+  HybridQuery hq{query, std::nullopt, 1, {}};
+  detail::QueryPack p({hq});
+  std::vector<std::uint32_t> rows(index.num_docs());
+  std::uint64_t n = 0;
+  detail::check(hyre_full_scan_tbr(ex.handle(), p.q.data(), rows.data(), rows.size(), &n));
+  std::vector<Messenger> out;
+  out.reserve(n);
+  for (std::uint64_t i = 0; i < n; ++i) out.push_back({rows[i], batch_id, 0.0f});
+  return out;
+}
+
+inline ScoredMessengers exact_scores(const FrozenIndex& index, std::span<const float> query_embedding,
+                                     std::vector<Messenger> candidates) {
+  Executor ex(index, 1);
+  std::vector<std::uint32_t> rows;
+  for (const auto& m : candidates) rows.push_back(m.row_id);
+  std::vector<float> sc(rows.size());
+  std::int32_t ren = 0;
+  detail::check(hyre_exact_scores(ex.handle(), query_embedding.data(), static_cast<std::uint32_t>(query_embedding.size()),
+                                  rows.data(), rows.size(), sc.data(), &ren));
+  ScoredMessengers out{std::move(candidates), ren != 0};
+  for (std::size_t i = 0; i < out.items.size(); ++i) out.items[i].score = sc[i];
+  return out;
+}
+
+inline TopKResult bucket_top_k(const FrozenIndex& index, const ScoredMessengers& scored, std::uint32_t k,
+                               std::uint32_t granularity = 100) {
+  Executor ex(index, 1);
+  std::vector<std::uint32_t> rows;
+  std::vector<float> sc;
+  for (const auto& m : scored.items) {
+    rows.push_back(m.row_id);
+    sc.push_back(m.score);
+  }
+  std::vector<hyre_hit> hits(std::max<std::size_t>(1, std::min<std::size_t>(k, rows.size())));
+  std::uint32_t n = 0;
+  detail::check(hyre_bucket_top_k(ex.handle(), rows.data(), sc.data(), rows.size(), k, granularity, hits.data(), &n));
+  TopKResult r;
+  for (std::uint32_t i = 0; i < n; ++i) r.hits.push_back({index.doc_id(hits[i].row), hits[i].row, hits[i].score});
+  return r;
+}
+
+inline std::vector<Messenger> preselect(const FrozenIndex& index, const Signature& query_signature,
+                                        std::span<const Messenger> candidates, std::uint32_t quant_k) {
+  Executor ex(index, 1);
+  std::vector<std::uint32_t> rows, out(candidates.size());
+  for (const auto& m : candidates) rows.push_back(m.row_id);
+  std::uint64_t n = 0;
+  detail::check(hyre_preselect(ex.handle(), query_signature.words.data(), rows.data(), rows.size(), quant_k,
+                               out.data(), &n));
+  std::vector<Messenger> kept;
+  for (std::uint64_t i = 0; i < n; ++i)
+    for (const auto& m : candidates)
+      if (m.row_id == out[i]) {
+        kept.push_back(m);
+        break;
+      }
+  return kept;
+}
+
+}  // namespace hyre

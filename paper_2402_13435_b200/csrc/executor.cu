@@ -276,6 +276,13 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // the dense sample buffer holds kSampleRows rows per query
   const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
   period = std::max(period, (n_seg + kSampleRows / kSegRows - 1) / (kSampleRows / kSegRows));
+  if (!(any_emb && ix->has_tc && b >= kTcMinBatch)) {
+    // CUDA-core path (K2): its warps absorb a few thousand appends per query,
+    // so a smaller sample (~16 segments, ~max(16K, 32k) rows) suffices and the
+    // K-th selection over it is cheap.
+    const uint32_t want_seg = std::max<uint32_t>(16, (32 * max_k + kSegRows - 1) / kSegRows);
+    period = std::max(period, n_seg / want_seg);
+  }
   sample_period = period;
   const uint32_t n_samp_seg = (n_seg + period - 1) / period;
   sample_rows = (n_samp_seg - 1) * kSegRows +

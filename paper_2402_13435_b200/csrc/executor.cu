@@ -42,6 +42,14 @@ uint32_t tc_debug_flags() {  // HYRE_TC_DEBUG: profiling experiments only
   }();
   return v;
 }
+// HYRE_FUSED=0 disables the fused-CNF K3 epilogue (tests, profiling).
+bool fused_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_FUSED");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 // HYRE_MASK_PATH=bitmap|fwd forces the K1 / K1b choice (tests, profiling).
 int mask_path() {
   static const int v = [] {
@@ -252,7 +260,24 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   for (size_t r = 0; r < ref_src.size(); ++r)
     refs[r] = ref_src[r].first == 0 ? ix->bitmaps + size_t{ref_src[r].second} * W
                                     : d_scratch + size_t{ref_src[r].second} * W;
-  if (use_fwd && mask_path() != 2) {
+  use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
+  if (use_tc) {
+    tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
+    tc_groups = (b + tc_np - 1) / tc_np;
+  }
+  // Fused CNF: an all-hybrid, quant-free tensor-core batch evaluates the
+  // clauses in K3's epilogue from the forward term lists, when the group's
+  // term tables fit next to a >= 4-stage ring.
+  use_fused = false;
+  if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
+      ix->num_clauses <= 31) {
+    fz_smem = tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses);
+    const size_t kb = ix->dp / 64;
+    use_fused = tc_smem_bytes(tc_np, kb, ix->tc_ops, 4, fz_smem) <= 227 * 1024;
+  }
+  if (use_fused) {
+    build_fused_program();
+  } else if (use_fwd && mask_path() != 2) {
     // Cost model (measured on B200, c3): the term-major bitmap kernel costs
     // ~1.3 us per (32-query group x distinct ref) per 10M rows, the forward
     // kernel ~0.5 ms per pass of 64/128 queries per 10M rows.
@@ -269,7 +294,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       return prepare(qs, b);
     }
   }
-  if (use_fwd) build_forward_program(); else build_term_major_program();
+  if (!use_fused) {
+    if (use_fwd) build_forward_program(); else build_term_major_program();
+  }
   // sampling period: sampled survivors ~ k * period must fit the candidate buffer
   uint32_t period = 1;
   while (period < 256 && uint64_t{period} * 2 * max_k * 4 <= cap) period *= 2;
@@ -290,10 +317,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
 
   // tensor-core path: bf16 (hi, lo) split of the unit queries, padded to
   // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
-  use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
   if (use_tc) {
-    tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
-    tc_groups = (b + tc_np - 1) / tc_np;
     const size_t rows = size_t{tc_groups} * tc_np;
     qhi_h.assign(rows * dp, 0);
     qlo_h.assign(rows * dp, 0);
@@ -325,6 +349,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   const size_t o_fwd = place(std::max<size_t>(fwd_words.size(), 1) * 4);
   const size_t o_qhi = place(std::max<size_t>(qhi_h.size(), 1) * 2);
   const size_t o_qlo = place(std::max<size_t>(qlo_h.size(), 1) * 2);
+  const size_t o_fz = place(std::max<size_t>(fz_words.size(), 1) * 4);
   ensure_blob(off);
   std::memcpy(h_blob + o_qp, qp.data(), b * sizeof(QParam));
   std::memcpy(h_blob + o_q, qvec.data(), qvec.size() * 4);
@@ -337,6 +362,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     std::memcpy(h_blob + o_ipre, item_prefix.data(), item_prefix.size() * 8);
   }
   if (!fwd_words.empty()) std::memcpy(h_blob + o_fwd, fwd_words.data(), fwd_words.size() * 4);
+  if (use_fused) std::memcpy(h_blob + o_fz, fz_words.data(), fz_words.size() * 4);
   if (use_tc) {
     std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
     std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
@@ -356,6 +382,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_items = reinterpret_cast<ScatterItem*>(d_blob + o_items);
   d_ipre = reinterpret_cast<uint64_t*>(d_blob + o_ipre);
   d_fwd = reinterpret_cast<uint32_t*>(d_blob + o_fwd);
+  d_fz = reinterpret_cast<uint32_t*>(d_blob + o_fz);
   prepared = true;
 }
 
@@ -370,7 +397,8 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     const uint32_t n_ops = ix->tc_ops;
     const size_t q_bytes = 2ull * tc_np * 128 * kb;
     const size_t stage_bytes = size_t{n_ops} * 128 * 128;  // one K atom (hi [+ lo]) of a 128-row tile
-    const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0);
+    const size_t fzb = use_fused ? fz_smem : 0;
+    const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0, fzb);
     const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
     const uint32_t stages = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(12, budget / stage_bytes)));
     uint32_t cols = 32;
@@ -385,7 +413,20 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 ix->tc_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
                 rerun, tc_debug_flags()};
-      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages), st);
+      if (use_fused) {
+        const FusedGroup& fg = fz_group[g];
+        ta.fused = 1;
+        ta.row_terms = ix->row_terms;
+        ta.slot_of = ix->slot_of;
+        ta.A = ix->row_terms_width;
+        ta.T = ix->n_terms_fwd;
+        ta.C = ix->num_clauses;
+        ta.fz = d_fz + fg.entries;
+        ta.n_entries = fg.n_entries;
+        ta.hc_off = fg.hc - fg.entries;
+        ta.live_off = ta.hc_off + ix->num_clauses * 2 * ((tc_np / 32 + 1) / 2);
+      }
+      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages, fzb), st);
       ++kernels;
     }
     return;
@@ -493,6 +534,49 @@ void Executor::build_forward_program() {
   }
 }
 
+// Fused-CNF program per K3 query group (TcArgs::fz): for every term any
+// query of the group lists, its users words; per slot, the queries that
+// constrain it; the live (active, satisfiable) queries; the constrained-slot
+// mask.  Word w = half * cpt + cc holds query chunk c = half + 2 cc.
+void Executor::build_fused_program() {
+  fz_words.clear();
+  fz_group.clear();
+  const uint32_t C = ix->num_clauses, nch = tc_np / 32, cpt = (nch + 1) / 2, fw = 2 * cpt;
+  for (uint32_t g = 0; g < tc_groups; ++g) {
+    std::map<uint32_t, std::vector<uint32_t>> users;
+    std::vector<uint32_t> hc(size_t{C} * fw, 0u), live(fw, 0u);
+    uint32_t cslots = 0;
+    for (uint32_t i = g * tc_np; i < std::min(B, (g + 1) * tc_np); ++i) {
+      const QParam& p = qp[i];
+      if (!(p.flags & QF_ACTIVE) || (p.flags & QF_EMPTY)) continue;
+      const uint32_t j = i - g * tc_np, c = j / 32, w = (c & 1) * cpt + (c >> 1), bit = 1u << (j & 31);
+      live[w] |= bit;
+      for (size_t cl = 0; cl < qterms[i].size(); ++cl) {
+        const uint32_t slot = qslots[i][cl];
+        hc[size_t{slot} * fw + w] |= bit;
+        cslots |= 1u << slot;
+        for (uint32_t t : qterms[i][cl]) {
+          auto& u = users[t];
+          if (u.empty()) u.assign(fw, 0u);
+          u[w] |= bit;
+        }
+      }
+    }
+    FusedGroup fg{};
+    fg.entries = static_cast<uint32_t>(fz_words.size());
+    fg.n_entries = static_cast<uint32_t>(users.size());
+    for (auto& [t, u] : users) {
+      fz_words.push_back(t);
+      fz_words.insert(fz_words.end(), u.begin(), u.end());
+    }
+    fg.hc = static_cast<uint32_t>(fz_words.size());
+    fz_words.insert(fz_words.end(), hc.begin(), hc.end());
+    fz_words.insert(fz_words.end(), live.begin(), live.end());
+    fz_words.push_back(cslots);
+    fz_group.push_back(fg);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // run: the fixed kernel sequence, no host synchronisation.
 // ---------------------------------------------------------------------------
@@ -508,7 +592,11 @@ void Executor::run() {
   uint32_t* rerun = d_counters + 4 * max_batch;
   HYRE_CUDA(cudaEventRecord(ev[0], st));
   HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
-  if (use_fwd) {
+  if (use_fused) {
+    // eligibility is evaluated inside K3; the eligible counts are unknown
+    // (all-ones), which K4's rerun logic treats as "at least K"
+    HYRE_CUDA(cudaMemsetAsync(n_elig, 0xFF, sizeof(uint32_t) * B, st));
+  } else if (use_fwd) {
     for (const FwdPass& fp : fwd_pass) {
       FwdArgs fa{ix->row_terms, ix->slot_of, ix->row_terms_width, ix->n_rows, W, ix->n_chunks, B, ix->num_clauses,
                  ix->n_terms_fwd, d_fwd + fp.entries, fp.n_entries,
@@ -523,7 +611,7 @@ void Executor::run() {
                    d_scratch, W, st);
     ++kernels;
   }
-  if (!use_fwd) {
+  if (!use_fwd && !use_fused) {
     MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
                 d_mask, d_chunk_cnt, n_elig};
     const uint32_t ml = launch_mask_tm(ma, prog_groups, prog_live, st);

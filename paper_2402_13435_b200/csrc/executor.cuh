@@ -72,6 +72,16 @@ struct Executor {
   std::vector<float> qvec;
   std::vector<uint64_t> qsig;
   uint64_t n_hits_total = 0, h2d_bytes = 0, d2h_bytes = 0;
+  // fused CNF in the K3 epilogue (no K1 mask pass): per query group, the
+  // term-users program (TcArgs::fz) and its offsets into fz_words
+  bool use_fused = false;
+  struct FusedGroup {
+    uint32_t entries, n_entries, hc;
+  };
+  std::vector<FusedGroup> fz_group;
+  std::vector<uint32_t> fz_words;
+  uint32_t* d_fz = nullptr;
+  size_t fz_smem = 0;
   // tensor-core path (K3)
   bool use_tc = false;
   uint32_t tc_np = 0, tc_groups = 0;
@@ -112,6 +122,7 @@ struct Executor {
   void finish_reruns();
   void build_term_major_program();
   void build_forward_program();
+  void build_fused_program();
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
 };
 

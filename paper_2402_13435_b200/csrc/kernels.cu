@@ -850,15 +850,147 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   }
 }
 
+// K4 over a dense sample buffer (SELECT_KTH with dense_n): the thresholds
+// need only the K-th and m-th largest of the sample's few eligible keys
+// (0 = ineligible slot).  One pass builds a 4096-bin histogram of the top 12
+// key bits (sign, exponent, 3 mantissa bits of the score), a scan finds the
+// bin holding the K-th (m-th) key, a second pass gathers the keys at or above
+// that bin into shared memory and a bitonic sort reads both thresholds off
+// exactly.  Two streaming passes with 8 keys per thread in flight replace the
+// radix select's up to six; a bin too crowded to gather (massive ties) falls
+// back to the radix select.
+__global__ void __launch_bounds__(kSelThreads) sample_kth_kernel(SelectArgs a) {
+  extern __shared__ uint64_t sel_smem[];
+  uint64_t* sortbuf = sel_smem;                                          // kSelectMaxK keys
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sel_smem + kSelectMaxK);  // 4096
+  uint32_t* tmp = hist + 4096;                                           // 33
+  __shared__ uint32_t s_dk, s_gk, s_dm, s_gm, gathered;
+  const uint32_t q = blockIdx.x;
+  const QParam qp = a.qp[q];
+  if ((qp.flags & a.require_flags) != a.require_flags) return;
+  if (!(a.n_elig[q] > a.gate)) {  // not sampled: no threshold
+    if (threadIdx.x == 0) {
+      a.thr[q] = 0;
+      if (a.thr_safe) a.thr_safe[q] = 0;
+    }
+    return;
+  }
+  const uint32_t k = qp.k, n = a.dense_n;
+  const uint32_t m = min(k, max(8u, (4 * k + a.period - 1) / a.period));
+  const uint64_t* keys = a.buf + static_cast<size_t>(q) * a.cap;
+  for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  auto add = [&](uint64_t key) {
+    const uint32_t digit = key ? static_cast<uint32_t>(key >> 52) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, digit);
+    if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
+      atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
+  };
+  const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
+  const uint32_t n2 = n / 2;
+  for (uint32_t base = 0; base < n2; base += 4 * blockDim.x) {
+    ulonglong2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = base + u * blockDim.x + threadIdx.x;
+      v[u] = i < n2 ? k2[i] : make_ulonglong2(0ull, 0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      add(v[u].x);
+      add(v[u].y);
+    }
+  }
+  if (n & 1u) {
+    if (threadIdx.x < 32) add(threadIdx.x == 0 ? keys[n - 1] : 0ull);
+  }
+  __syncthreads();
+  // position t of the scan owns bins [8o, 8o+8), o = T-1-t: its exclusive
+  // prefix counts the keys in all higher bins
+  const uint32_t owner = blockDim.x - 1 - threadIdx.x;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) mine += hist[owner * 8 + b];
+  uint32_t nnz;
+  uint32_t above = block_excl_scan(mine, tmp, &nnz);
+#pragma unroll
+  for (int b = 7; b >= 0; --b) {
+    const uint32_t h = hist[owner * 8 + b];
+    if (above < k && k <= above + h) {
+      s_dk = owner * 8 + b;
+      s_gk = above + h;
+    }
+    if (above < m && m <= above + h) {
+      s_dm = owner * 8 + b;
+      s_gm = above + h;
+    }
+    above += h;
+  }
+  if (threadIdx.x == 0) gathered = 0;
+  __syncthreads();
+  uint64_t t_safe = 0, t_est = 0;
+  if (nnz >= m) {
+    const bool full = nnz >= k;
+    const uint32_t dsel = full ? s_dk : s_dm, g = full ? s_gk : s_gm;
+    if (g <= kSelectMaxK) {
+      for (uint32_t base = 0; base < n2; base += 4 * blockDim.x) {
+        ulonglong2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = base + u * blockDim.x + threadIdx.x;
+          v[u] = i < n2 ? k2[i] : make_ulonglong2(0ull, 0ull);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t key = h ? v[u].y : v[u].x;
+            const bool take = key != 0ull && static_cast<uint32_t>(key >> 52) >= dsel;
+            const unsigned bal = __ballot_sync(0xffffffffu, take);
+            if (bal) {
+              uint32_t base_at = 0;
+              if ((threadIdx.x & 31) == 0) base_at = atomicAdd(&gathered, static_cast<uint32_t>(__popc(bal)));
+              base_at = __shfl_sync(0xffffffffu, base_at, 0);
+              if (take) sortbuf[base_at + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = key;
+            }
+          }
+        }
+      }
+      if ((n & 1u) && threadIdx.x == 0) {
+        const uint64_t key = keys[n - 1];
+        if (key != 0ull && static_cast<uint32_t>(key >> 52) >= dsel) sortbuf[atomicAdd(&gathered, 1u)] = key;
+      }
+      __syncthreads();
+      const uint32_t cnt = gathered;  // == g
+      uint32_t c2 = 1;
+      while (c2 < cnt) c2 <<= 1;
+      for (uint32_t i = cnt + threadIdx.x; i < c2; i += blockDim.x) sortbuf[i] = 0ull;
+      __syncthreads();
+      bitonic_desc(sortbuf, c2);
+      t_safe = full ? sortbuf[k - 1] : 0ull;
+      t_est = sortbuf[m - 1];
+    } else {
+      t_safe = full ? kth_largest(keys, n, k, hist, tmp) : 0ull;
+      t_est = m < k ? kth_largest(keys, n, m, hist, tmp) : t_safe;
+    }
+  }
+  if (threadIdx.x == 0) {
+    a.thr[q] = t_est;
+    if (a.thr_safe) a.thr_safe[q] = t_safe;
+  }
+}
+
 void launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
   const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(sample_kth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
-  select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
+  if (a.mode == SELECT_KTH && a.dense_n) sample_kth_kernel<<<a.B, kSelThreads, smem, st>>>(a);
+  else select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
 }
 
 // ===========================================================================

@@ -130,12 +130,94 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
   return t < a.n_tiles ? t : UINT32_MAX;
 }
 
+// Eligibility of one row for this thread's query chunks (c = half + 2 cc)
+// from the row's forward term list: a query is eligible iff every slot it
+// constrains holds a row term listed in its clause (term_match.cpp:34-78:
+// AND over clauses of a non-empty sorted intersection).  Terms are slot-major
+// (ascending term ids), so a per-slot OR accumulator closes whenever the slot
+// changes: fail |= hc[slot] & ~acc.  Every table entry carries its term's
+// users words and its slot's hc words, so all 8*NA lookups are independent
+// and issue back to back; the combine is branch-free.  Padding (0xFFFF) maps
+// to the sentinel entry T (no users, dummy slot C).  Constrained slots the
+// row has no term in fail outright (an empty doc slice never matches,
+// term_match.cpp:45-46).
+template <int CPT, int NA>
+__device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, const uint32_t* tbl,
+                                        const uint8_t* slot_of, const uint32_t* hc, const uint32_t* live,
+                                        uint32_t cslots, uint32_t half, uint32_t (&out)[2]) {
+  constexpr int J = 8 * NA;
+  uint32_t sl[J], u[J][CPT], h[J][CPT];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t t = min((tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu, T);
+    // explicit ld.shared: the compiler's address-space inference does not
+    // survive the carve-up, and generic loads would cost long-scoreboard waits
+    asm("ld.shared.u8 %0, [%1];" : "=r"(sl[j]) : "r"(smem_u32(slot_of) + t));
+    const uint32_t e = smem_u32(tbl) + (t * 2 + half) * (8 * CPT);
+    if (CPT == 1) {
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[j][0]), "=r"(h[j][0]) : "r"(e));
+    } else {
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(u[j][0]), "=r"(u[j][CPT - 1]), "=r"(h[j][0]), "=r"(h[j][CPT - 1])
+          : "r"(e));
+    }
+  }
+  uint32_t acc[CPT], fail[CPT], hp[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) acc[c] = fail[c] = hp[c] = 0u;
+  uint32_t present = 0u, sp = 0xFFFFFFFFu;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const bool ch = sl[j] != sp;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      fail[c] |= ch ? (hp[c] & ~acc[c]) : 0u;
+      acc[c] = (ch ? 0u : acc[c]) | u[j][c];
+      hp[c] = h[j][c];
+    }
+    present |= 1u << sl[j];
+    sp = sl[j];
+  }
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) fail[c] |= hp[c] & ~acc[c];
+  for (uint32_t miss = cslots & ~present; miss; miss &= miss - 1u) {
+    const uint32_t s = __ffs(miss) - 1;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) fail[c] |= hc[(s * 2 + half) * CPT + c];
+  }
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) out[c] = live[half * CPT + c] & ~fail[c];
+  if (CPT == 1) out[1] = 0u;
+}
+
+__device__ __forceinline__ void load_row_terms(const TcArgs& a, uint32_t t, uint32_t row_in_tile,
+                                               uint32_t (&tw)[16]) {
+  const uint32_t r = t * kTileRows + row_in_tile;
+  const bool ok = t != UINT32_MAX && r < a.n_rows;
+  const uint4* src = reinterpret_cast<const uint4*>(a.row_terms + static_cast<size_t>(ok ? r : 0) * a.A);
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const uint4 x = (ok && v * 8 < static_cast<int>(a.A)) ? __ldg(src + v) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    tw[4 * v] = x.x;
+    tw[4 * v + 1] = x.y;
+    tw[4 * v + 2] = x.z;
+    tw[4 * v + 3] = x.w;
+  }
+}
+
 }  // namespace
 
+// NA > 0: fused CNF over row term lists of 8 * NA ids, CPT query chunks per
+// epilogue thread; NA == 0: eligibility from the K1 mask.  One instantiation
+// per variant keeps each kernel's code (and instruction-cache footprint) small.
+template <int NA, int CPT>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
+  constexpr bool kFused = NA > 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by pointer arithmetic on the shared array so every derived pointer
+  // stays in the shared window (LDS/STS, not generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Np = a.Np, kb = a.kblocks, S = a.stages;
   const uint32_t q_box = Np * 128;  // bytes of one K-atom of the query tile
@@ -159,6 +241,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // per-epilogue-warp candidate staging: [8][Np][kStage] keys + [8][Np] counts
   uint32_t* s_scnt = s_act + 8;
   uint64_t* s_skey = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_scnt + kEpiWarps * Np) + 15) & ~uintptr_t(15));
+  // fused CNF tables: per (term, half) entry {users[cpt], hc of its slot[cpt]} for T terms + sentinel,
+  // hc [C][W], live [W] + constrained slots, slot of term [T + 1]
+  const uint32_t cpt = kFused ? CPT : (Np / 32 + 1) / 2, fw = 2 * cpt;
+  uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(s_skey + static_cast<size_t>(kEpiWarps) * Np * kStage);
+  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * 2 * fw;
+  uint32_t* s_flive = s_fhc + a.C * fw;
+  uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + fw + 1);
 
   const uint32_t q0 = a.q0;
   // Any active query in this group?  One query per thread, then a block vote
@@ -200,6 +289,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t m = 0;
     for (uint32_t l = 0; l < 32; ++l) m |= tc_active(a, q0 + threadIdx.x * 32 + l) ? (1u << l) : 0u;
     s_act[threadIdx.x] = m;
+  }
+  if (kFused) {
+    for (uint32_t i = threadIdx.x; i < (a.C + 1) * fw + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
+    for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < (a.T + 1) * 2; i += blockDim.x) {  // (term, half): no users, slot's hc
+      const uint32_t t = i >> 1, hf = i & 1;
+      uint32_t* e = s_ftbl + i * (2 * cpt);
+      for (uint32_t c = 0; c < cpt; ++c) {
+        e[c] = 0u;
+        e[cpt + c] = t < a.T ? s_fhc[(s_fslot[t] * 2 + hf) * cpt + c] : 0u;
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {
+      const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + fw);
+      for (uint32_t w = 0; w < fw; ++w) {
+        const uint32_t hf = w / cpt, c = w % cpt;
+        s_ftbl[(en[0] * 2 + hf) * (2 * cpt) + c] = en[1 + w];
+      }
+    }
   }
   const uint32_t tmem_cols = a.tmem_cols;
   if (warp == 1) {
@@ -286,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t nq32 = Np / 32;
     uint32_t mw[2] = {0u, 0u};  // mask words of the current tile (lane l: query 32c + l)
     auto load_mask = [&](uint32_t t, uint32_t (&out)[2]) {
+      if (kFused) return;
 #pragma unroll
       for (uint32_t cc = 0; cc < 2; ++cc) {
         const uint32_t c = half + 2 * cc;
@@ -295,14 +406,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                       : 0u;
       }
     };
+    // fused CNF: the row's term ids are prefetched one tile ahead
+    uint32_t tw[16];
     uint32_t t = tile_of(a, 0);
     load_mask(t, mw);
+    if (kFused) load_row_terms(a, t, quad * 32 + lane, tw);
     for (uint32_t i = 0; t != UINT32_MAX; ++i) {
       const uint32_t acc = i & 1, aph = (i >> 1) & 1;
       const uint32_t t_next = tile_of(a, i + 1);
       uint32_t mw_next[2];
       load_mask(t_next, mw_next);  // in flight while this tile is processed
       const uint32_t grow = a.row_base + t * kTileRows + quad * 32 + lane;
+      uint32_t fel[2] = {0u, 0u};  // fused: bit j = row `lane` eligible for query 32c + j
+      if (kFused) {
+        cnf_row<CPT, (kFused ? NA : 1)>(tw, a.T, s_ftbl, s_fslot, s_fhc, s_flive, s_flive[fw], half, fel);
+        if (t * kTileRows + quad * 32 + lane >= a.n_rows) fel[0] = fel[1] = 0u;  // tail of the last tile
+        load_row_terms(a, t_next, quad * 32 + lane, tw);
+      }
       mbar_wait(tfull + acc, aph);
       fence_after();
 #pragma unroll
@@ -314,10 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 32x32 bit transpose: lane l held query (32c+l)'s word over this
         // warp's 32 rows; afterwards bit j of `elig` = row `lane`, query 32c+j.
         uint32_t elig = mw[cc];
+        if (kFused) {
+          elig = fel[cc];
+        } else {
 #pragma unroll
-        for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
-          const uint32_t y = __shfl_xor_sync(0xffffffffu, elig, j);
-          elig = (lane & j) ? ((elig & ~m) | ((y & ~m) >> j)) : ((elig & m) | ((y & m) << j));
+          for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, elig, j);
+            elig = (lane & j) ? ((elig & ~m) | ((y & ~m) >> j)) : ((elig & m) | ((y & m) << j));
+          }
         }
         // threshold test for all 32 queries: one compare of the raw
         // accumulator against the query's threshold score.  `>=` admits a
@@ -427,19 +551,36 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
   if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages) {
+size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes) {
   return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 5) * 8 + Np * 8 +
-         4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64;
+         4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64 + fused_bytes;
+}
+
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C) {
+  const size_t fw = 2 * ((Np / 32 + 1) / 2);
+  return 4 * ((T + 1) * 2 * fw + C * fw + fw + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (auto k : {tc_score_kernel<0, 1>, tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>,
+                   tc_score_kernel<4, 1>, tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>,
+                   tc_score_kernel<4, 2>})
+      HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  tc_score_kernel<<<grid, kThreads, smem, st>>>(qhi, qlo, a);
+  auto k = tc_score_kernel<0, 1>;
+  if (a.fused) {
+    const uint32_t na = (a.A + 7) / 8, cpt = (a.Np / 32 + 1) / 2;
+    if (na < 1 || na > 4) throw Error(HYRE_INTERNAL, "fused CNF: row term width out of range");
+    static decltype(k) const table[2][4] = {
+        {tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>, tc_score_kernel<4, 1>},
+        {tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>, tc_score_kernel<4, 2>}};
+    k = table[cpt - 1][na - 1];
+  }
+  k<<<grid, kThreads, smem, st>>>(qhi, qlo, a);
 }
 
 }  // namespace hyreb

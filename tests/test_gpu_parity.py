@@ -473,3 +473,46 @@ def test_batched_tbr_bitexact(hy, B):
     for o, e in zip(outs, expect):
         assert o.ok
         assert np.array_equal(np.asarray([h.row_id for h in o.result.hits], np.int64), e)
+
+
+@pytest.mark.parametrize("B", [9, 64, 130])
+def test_fused_cnf_eligibility_bitexact(hy, B):
+    # Hybrid batches on the tensor-core path evaluate the CNF inside K3's
+    # epilogue (fused, no mask pass).  With identical embeddings every
+    # eligible row scores the same, so each query's top-k is exactly its
+    # first k eligible rows (tie rule: row ascending) -- a bit-exact check of
+    # the fused eligibility against full_scan_tbr, covering sparse terms,
+    # rows with empty slots, absent ids, match-all and 2-group (B=130) batches.
+    n, C, dim = 12_000, 3, 64
+    rs = np.random.default_rng(5)
+    e0 = np.zeros(dim, np.float32)
+    e0[0], e0[1] = 0.6, 0.8
+    docs = []
+    for i in range(n):
+        cl = [(1 + np.minimum(rs.zipf(1.3, size=rs.integers(0, 4)), 400)).tolist() for _ in range(C)]
+        docs.append(O.Doc(f"d{i}", cl, e0))
+    width = max(sum(len(set(c)) for c in d.clauses) for d in docs)
+    prod = product_index(docs, C, width, dim, 64, 1)
+    ref = O.freeze(docs, C, width, dim, 64, 1)
+    ex = hy.Executor(prod, max_batch=B)
+    batch, expect = hy.BatchRequest(), []
+    q = np.zeros(dim, np.float32)
+    q[1] = 1.0
+    for i in range(B):
+        if i % 17 == 0:
+            raw = {}
+        elif i % 23 == 0:
+            raw = {1: [999_999]}  # id absent from the index
+        else:
+            raw = {c: (1 + np.minimum(rs.zipf(1.3, size=rs.integers(1, 5)), 400)).tolist()
+                   for c in range(C) if rs.random() < 0.7}
+        clauses = O.normalize_query(raw, C)
+        k = 4096 if i % 3 else 1 + i
+        batch.queries.append(hy.HybridQuery(to_cnf(clauses), q, k, hy.ExecOptions(quant_enabled=False)))
+        expect.append(O.full_scan_tbr(ref, clauses)[:k])
+    outs = ex.execute_batch(batch)
+    for o, e in zip(outs, expect):
+        assert o.ok
+        gr, gs = hits(o.result)
+        assert np.array_equal(gr, e), (len(gr), len(e))
+        assert np.all(gs == gs[0]) if len(gs) else True

@@ -271,7 +271,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   use_fused = false;
   if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31) {
-    fz_smem = tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses);
+    fz_smem = tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->row_terms_width);
     const size_t kb = ix->dp / 64;
     use_fused = tc_smem_bytes(tc_np, kb, ix->tc_ops, 4, fz_smem) <= 227 * 1024;
   }
@@ -400,9 +400,10 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     const size_t fzb = use_fused ? fz_smem : 0;
     const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0, fzb);
     const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
-    const uint32_t stages = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(12, budget / stage_bytes)));
-    uint32_t cols = 32;
-    while (cols < 2 * tc_np) cols <<= 1;
+    uint32_t stages = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(12, budget / stage_bytes)));
+    if (const char* e = std::getenv("HYRE_TC_STAGES"))  // profiling: cap the ring depth
+      stages = std::max(2u, std::min<uint32_t>(stages, static_cast<uint32_t>(std::atoi(e))));
+    const uint32_t cols = tc_tmem_cols(tc_np);
     uint32_t work = n_tiles;
     if (mode == SCORE_SAMPLE) {
       const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
@@ -424,7 +425,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
         ta.fz = d_fz + fg.entries;
         ta.n_entries = fg.n_entries;
         ta.hc_off = fg.hc - fg.entries;
-        ta.live_off = ta.hc_off + ix->num_clauses * 2 * ((tc_np / 32 + 1) / 2);
+        ta.live_off = ta.hc_off + ix->num_clauses * tc_fused_chunks(tc_np);
       }
       launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages, fzb), st);
       ++kernels;
@@ -537,11 +538,11 @@ void Executor::build_forward_program() {
 // Fused-CNF program per K3 query group (TcArgs::fz): for every term any
 // query of the group lists, its users words; per slot, the queries that
 // constrain it; the live (active, satisfiable) queries; the constrained-slot
-// mask.  Word w = half * cpt + cc holds query chunk c = half + 2 cc.
+// mask.  Word w holds query chunk w (queries 32w .. 32w + 31).
 void Executor::build_fused_program() {
   fz_words.clear();
   fz_group.clear();
-  const uint32_t C = ix->num_clauses, nch = tc_np / 32, cpt = (nch + 1) / 2, fw = 2 * cpt;
+  const uint32_t C = ix->num_clauses, fw = tc_fused_chunks(tc_np);
   for (uint32_t g = 0; g < tc_groups; ++g) {
     std::map<uint32_t, std::vector<uint32_t>> users;
     std::vector<uint32_t> hc(size_t{C} * fw, 0u), live(fw, 0u);
@@ -549,7 +550,7 @@ void Executor::build_fused_program() {
     for (uint32_t i = g * tc_np; i < std::min(B, (g + 1) * tc_np); ++i) {
       const QParam& p = qp[i];
       if (!(p.flags & QF_ACTIVE) || (p.flags & QF_EMPTY)) continue;
-      const uint32_t j = i - g * tc_np, c = j / 32, w = (c & 1) * cpt + (c >> 1), bit = 1u << (j & 31);
+      const uint32_t j = i - g * tc_np, w = j / 32, bit = 1u << (j & 31);
       live[w] |= bit;
       for (size_t cl = 0; cl < qterms[i].size(); ++cl) {
         const uint32_t slot = qslots[i][cl];

@@ -33,7 +33,13 @@ constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
 constexpr uint32_t kStage = 2;                    // staged candidate keys per (epilogue warp, query)
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
-constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kCnfWarps = 4;                 // fused CNF: one thread per tile row
+constexpr uint32_t kTermSlots = 2;                // fused CNF: tiles of row term lists in flight
+constexpr uint32_t kAccBufs = 4;                  // TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
+constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight
+__host__ __device__ constexpr uint32_t threads_for(bool fused) {
+  return 64 + 32 * kEpiWarps + (fused ? 32 * kCnfWarps : 0);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -130,10 +136,10 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
   return t < a.n_tiles ? t : UINT32_MAX;
 }
 
-// Eligibility of one row for this thread's query chunks (c = half + 2 cc)
-// from the row's forward term list: a query is eligible iff every slot it
-// constrains holds a row term listed in its clause (term_match.cpp:34-78:
-// AND over clauses of a non-empty sorted intersection).  Terms are slot-major
+// Eligibility of one row for all NCH 32-query chunks of the group from the
+// row's forward term list: a query is eligible iff every slot it constrains
+// holds a row term listed in its clause (term_match.cpp:34-78: AND over
+// clauses of a non-empty sorted intersection).  Terms are slot-major
 // (ascending term ids), so a per-slot OR accumulator closes whenever the slot
 // changes: fail |= hc[slot] & ~acc.  Every table entry carries its term's
 // users words and its slot's hc words, so all 8*NA lookups are independent
@@ -141,36 +147,37 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
 // to the sentinel entry T (no users, dummy slot C).  Constrained slots the
 // row has no term in fail outright (an empty doc slice never matches,
 // term_match.cpp:45-46).
-template <int CPT, int NA>
-__device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, const uint32_t* tbl,
-                                        const uint8_t* slot_of, const uint32_t* hc, const uint32_t* live,
-                                        uint32_t cslots, uint32_t half, uint32_t (&out)[2]) {
+template <int NCH, int NA>
+__device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, uint32_t tbl, uint32_t slot_of,
+                                        uint32_t hc, uint32_t live, uint32_t cslots, uint32_t (&out)[NCH]) {
   constexpr int J = 8 * NA;
-  uint32_t sl[J], u[J][CPT], h[J][CPT];
+  uint32_t sl[J], u[J][NCH], h[J][NCH];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const uint32_t t = min((tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu, T);
-    // explicit ld.shared: the compiler's address-space inference does not
-    // survive the carve-up, and generic loads would cost long-scoreboard waits
-    asm("ld.shared.u8 %0, [%1];" : "=r"(sl[j]) : "r"(smem_u32(slot_of) + t));
-    const uint32_t e = smem_u32(tbl) + (t * 2 + half) * (8 * CPT);
-    if (CPT == 1) {
+    // explicit ld.shared (32-bit shared addresses): generic loads would cost
+    // long-scoreboard waits
+    asm("ld.shared.u8 %0, [%1];" : "=r"(sl[j]) : "r"(slot_of + t));
+    const uint32_t e = tbl + t * (8 * NCH);
+    if (NCH == 1) {
       asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[j][0]), "=r"(h[j][0]) : "r"(e));
     } else {
-      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(u[j][0]), "=r"(u[j][CPT - 1]), "=r"(h[j][0]), "=r"(h[j][CPT - 1])
-          : "r"(e));
+#pragma unroll
+      for (int c = 0; c < NCH; c += 2)
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(u[j][c]), "=r"(u[j][(c + 1) % NCH]), "=r"(h[j][c]), "=r"(h[j][(c + 1) % NCH])
+            : "r"(e + 16 * (c / 2)));
     }
   }
-  uint32_t acc[CPT], fail[CPT], hp[CPT];
+  uint32_t acc[NCH], fail[NCH], hp[NCH];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) acc[c] = fail[c] = hp[c] = 0u;
+  for (int c = 0; c < NCH; ++c) acc[c] = fail[c] = hp[c] = 0u;
   uint32_t present = 0u, sp = 0xFFFFFFFFu;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const bool ch = sl[j] != sp;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
+    for (int c = 0; c < NCH; ++c) {
       fail[c] |= ch ? (hp[c] & ~acc[c]) : 0u;
       acc[c] = (ch ? 0u : acc[c]) | u[j][c];
       hp[c] = h[j][c];
@@ -179,39 +186,32 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, co
     sp = sl[j];
   }
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) fail[c] |= hp[c] & ~acc[c];
+  for (int c = 0; c < NCH; ++c) fail[c] |= hp[c] & ~acc[c];
   for (uint32_t miss = cslots & ~present; miss; miss &= miss - 1u) {
     const uint32_t s = __ffs(miss) - 1;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) fail[c] |= hc[(s * 2 + half) * CPT + c];
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t x;
+      asm("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(hc + (s * NCH + c) * 4));
+      fail[c] |= x;
+    }
   }
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) out[c] = live[half * CPT + c] & ~fail[c];
-  if (CPT == 1) out[1] = 0u;
-}
-
-__device__ __forceinline__ void load_row_terms(const TcArgs& a, uint32_t t, uint32_t row_in_tile,
-                                               uint32_t (&tw)[16]) {
-  const uint32_t r = t * kTileRows + row_in_tile;
-  const bool ok = t != UINT32_MAX && r < a.n_rows;
-  const uint4* src = reinterpret_cast<const uint4*>(a.row_terms + static_cast<size_t>(ok ? r : 0) * a.A);
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const uint4 x = (ok && v * 8 < static_cast<int>(a.A)) ? __ldg(src + v) : make_uint4(~0u, ~0u, ~0u, ~0u);
-    tw[4 * v] = x.x;
-    tw[4 * v + 1] = x.y;
-    tw[4 * v + 2] = x.z;
-    tw[4 * v + 3] = x.w;
+  for (int c = 0; c < NCH; ++c) {
+    uint32_t lv;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(lv) : "r"(live + c * 4));
+    out[c] = lv & ~fail[c];
   }
 }
 
 }  // namespace
 
-// NA > 0: fused CNF over row term lists of 8 * NA ids, CPT query chunks per
-// epilogue thread; NA == 0: eligibility from the K1 mask.  One instantiation
-// per variant keeps each kernel's code (and instruction-cache footprint) small.
-template <int NA, int CPT>
-__global__ void __launch_bounds__(kThreads, 1)
+// NA > 0: fused CNF over row term lists of 8 * NA ids for NCH 32-query
+// chunks, evaluated by kCnfWarps dedicated warps one tile ahead of the
+// epilogue; NA == 0: eligibility from the K1 mask.  One instantiation per
+// variant keeps each kernel's code (and instruction-cache footprint) small.
+template <int NA, int NCH>
+__global__ void __launch_bounds__(threads_for(NA > 0), 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   constexpr bool kFused = NA > 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -232,22 +232,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
-  uint64_t* qbar = bars + 2 * S + 4;
-  float* s_ts = reinterpret_cast<float*>(bars + ((2 * S + 6) & ~1u));  // [Np] threshold score (16-B aligned)
+  uint64_t* tempty = tfull + kAccBufs;
+  uint64_t* qbar = tempty + kAccBufs;
+  float* s_ts = reinterpret_cast<float*>(bars + ((2 * S + 2 * kAccBufs + 2) & ~1u));  // [Np] threshold score (16-B aligned)
   uint32_t* s_tr = reinterpret_cast<uint32_t*>(s_ts + Np);     // [Np] threshold row
   uint32_t* s_tmem = s_tr + Np;                                // TMEM base
   uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
   // per-epilogue-warp candidate staging: [8][Np][kStage] keys + [8][Np] counts
   uint32_t* s_scnt = s_act + 8;
-  uint64_t* s_skey = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_scnt + kEpiWarps * Np) + 15) & ~uintptr_t(15));
-  // fused CNF tables: per (term, half) entry {users[cpt], hc of its slot[cpt]} for T terms + sentinel,
-  // hc [C][W], live [W] + constrained slots, slot of term [T + 1]
-  const uint32_t cpt = kFused ? CPT : (Np / 32 + 1) / 2, fw = 2 * cpt;
-  uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(s_skey + static_cast<size_t>(kEpiWarps) * Np * kStage);
-  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * 2 * fw;
-  uint32_t* s_flive = s_fhc + a.C * fw;
-  uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + fw + 1);
+  uint8_t* after_cnt = reinterpret_cast<uint8_t*>(s_scnt + kEpiWarps * Np);
+  uint64_t* s_skey = reinterpret_cast<uint64_t*>(after_cnt + ((16u - (smem_u32(after_cnt) & 15u)) & 15u));
+  // fused CNF: a ring of kTermSlots tiles of row term lists (bulk-copied by
+  // the producer; 128 rows x A u16 each), a ring of kEligSlots tiles of
+  // eligibility words ([NCH][128 rows] u32, written by the CNF warps), their
+  // barriers, then the tables: per term entry {users[NCH], hc of its
+  // slot[NCH]} for T terms + sentinel, hc [C][NCH], live [NCH] + constrained
+  // slots, slot of term [T + 1]
+  uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey + static_cast<size_t>(kEpiWarps) * Np * kStage);
+  uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
+  const uint32_t term_tile_bytes = kTileRows * a.A * 2;
+  uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? kTermSlots * term_tile_bytes : 0u));
+  uint64_t* s_tbar = reinterpret_cast<uint64_t*>(s_elig + (kFused ? kEligSlots * NCH * kTileRows : 0u));
+  uint64_t* ttfull = s_tbar;
+  uint64_t* ttempty = s_tbar + kTermSlots;
+  uint64_t* efull = s_tbar + 2 * kTermSlots;
+  uint64_t* eempty = efull + kEligSlots;
+  uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(eempty + kEligSlots);
+  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * 2 * NCH;
+  uint32_t* s_flive = s_fhc + a.C * NCH;
+  uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
 
   const uint32_t q0 = a.q0;
   // Any active query in this group?  One query per thread, then a block vote
@@ -261,11 +274,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (uint32_t i = 0; i < kAccBufs; ++i) {
       mbar_init(tfull + i, 1);
       mbar_init(tempty + i, kEpiWarps);
     }
     mbar_init(qbar, 1);
+    if (kFused) {
+      for (uint32_t i = 0; i < kTermSlots; ++i) {
+        mbar_init(ttfull + i, 1);
+        mbar_init(ttempty + i, kCnfWarps);
+      }
+      for (uint32_t i = 0; i < kEligSlots; ++i) {
+        mbar_init(efull + i, kCnfWarps);
+        mbar_init(eempty + i, kEpiWarps);
+      }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // key >= thr  <=>  score > ts || (score == ts && row <= tr)   (make_key order)
@@ -291,24 +314,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     s_act[threadIdx.x] = m;
   }
   if (kFused) {
-    for (uint32_t i = threadIdx.x; i < (a.C + 1) * fw + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
+    for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
     for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < (a.T + 1) * 2; i += blockDim.x) {  // (term, half): no users, slot's hc
-      const uint32_t t = i >> 1, hf = i & 1;
-      uint32_t* e = s_ftbl + i * (2 * cpt);
-      for (uint32_t c = 0; c < cpt; ++c) {
+    for (uint32_t t = threadIdx.x; t <= a.T; t += blockDim.x) {  // every term: no users, its slot's hc
+      uint32_t* e = s_ftbl + t * (2 * NCH);
+#pragma unroll
+      for (uint32_t c = 0; c < NCH; ++c) {
         e[c] = 0u;
-        e[cpt + c] = t < a.T ? s_fhc[(s_fslot[t] * 2 + hf) * cpt + c] : 0u;
+        e[NCH + c] = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0u;
       }
     }
     __syncthreads();
     for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {
-      const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + fw);
-      for (uint32_t w = 0; w < fw; ++w) {
-        const uint32_t hf = w / cpt, c = w % cpt;
-        s_ftbl[(en[0] * 2 + hf) * (2 * cpt) + c] = en[1 + w];
-      }
+      const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + NCH);
+#pragma unroll
+      for (uint32_t c = 0; c < NCH; ++c) s_ftbl[en[0] * (2 * NCH) + c] = en[1 + c];
     }
   }
   const uint32_t tmem_cols = a.tmem_cols;
@@ -334,6 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
+        if (kFused) {  // the tile's row term lists (contiguous rows) into the term ring
+          const uint32_t ts = i % kTermSlots, tph = (i / kTermSlots) & 1;
+          const uint32_t rows = min(kTileRows, a.n_rows - t * kTileRows);
+          mbar_wait(ttempty + ts, tph ^ 1);
+          mbar_expect_tx(ttfull + ts, rows * a.A * 2);
+          bulk_load(s_terms + ts * term_tile_bytes, a.row_terms + static_cast<size_t>(t) * kTileRows * a.A,
+                    rows * a.A * 2, ttfull + ts);
+        }
         for (uint32_t k = 0; k < kb; ++k) {
           mbar_wait(empty + s, ph ^ 1);
           mbar_expect_tx(full + s, n_ops * a_bytes);
@@ -357,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
-        const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+        const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
         mbar_wait(tempty + acc, aph ^ 1);
         fence_after();
         const uint32_t d = tmem + acc * Np;
@@ -388,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(tfull + acc);  // accumulator ready for the epilogue
       }
     }
-  } else {
+  } else if (warp < 2 + kEpiWarps) {
     // ===== epilogue: TMEM -> registers -> mask / clamp / threshold -> candidates =====
     // 8 warps: lane quadrant = warp % 4 (TMEM access rule), column half =
     // (warp - 2) / 4; each warp owns chunks c = half, half + 2 (32 queries each).
@@ -406,22 +435,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                       : 0u;
       }
     };
-    // fused CNF: the row's term ids are prefetched one tile ahead
-    uint32_t tw[16];
     uint32_t t = tile_of(a, 0);
     load_mask(t, mw);
-    if (kFused) load_row_terms(a, t, quad * 32 + lane, tw);
     for (uint32_t i = 0; t != UINT32_MAX; ++i) {
-      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
       const uint32_t t_next = tile_of(a, i + 1);
       uint32_t mw_next[2];
       load_mask(t_next, mw_next);  // in flight while this tile is processed
       const uint32_t grow = a.row_base + t * kTileRows + quad * 32 + lane;
       uint32_t fel[2] = {0u, 0u};  // fused: bit j = row `lane` eligible for query 32c + j
       if (kFused) {
-        cnf_row<CPT, (kFused ? NA : 1)>(tw, a.T, s_ftbl, s_fslot, s_fhc, s_flive, s_flive[fw], half, fel);
-        if (t * kTileRows + quad * 32 + lane >= a.n_rows) fel[0] = fel[1] = 0u;  // tail of the last tile
-        load_row_terms(a, t_next, quad * 32 + lane, tw);
+        // this row's eligibility words for chunks half, half + 2 (CNF warps)
+        const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
+        mbar_wait(efull + es, eph);
+#pragma unroll
+        for (uint32_t cc = 0; cc < 2; ++cc) {
+          const uint32_t c = half + 2 * cc;
+          if (c < NCH)
+            asm volatile("ld.shared.u32 %0, [%1];"
+                         : "=r"(fel[cc])
+                         : "r"(smem_u32(s_elig) + ((es * NCH + c) * kTileRows + quad * 32 + lane) * 4));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(eempty + es);
       }
       mbar_wait(tfull + acc, aph);
       fence_after();
@@ -514,6 +550,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t k = 0; k < ns[c]; ++k)
         if (bases[c] + k < a.cap) dst[bases[c] + k] = stage[k];
     }
+  } else if (kFused) {
+    // ===== CNF warps: thread r evaluates tile row r for all NCH chunks =====
+    const uint32_t r = threadIdx.x - 32 * (2 + kEpiWarps);
+    const uint32_t cslots = s_flive[NCH];
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t t = tile_of(a, i);
+      if (t == UINT32_MAX) break;
+      const uint32_t ts = i % kTermSlots, tph = (i / kTermSlots) & 1;
+      mbar_wait(ttfull + ts, tph);
+      uint32_t tw[16];
+      const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.A * 2;
+#pragma unroll
+      for (int v = 0; v < (kFused ? NA : 1); ++v)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(tw[4 * v]), "=r"(tw[4 * v + 1]), "=r"(tw[4 * v + 2]), "=r"(tw[4 * v + 3])
+                     : "r"(src + 16 * v));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ttempty + ts);
+      uint32_t el[NCH];
+      cnf_row<NCH, (kFused ? NA : 1)>(tw, a.T, smem_u32(s_ftbl), smem_u32(s_fslot), smem_u32(s_fhc),
+                                       smem_u32(s_flive), cslots, el);
+      if (t * kTileRows + r >= a.n_rows) {  // tail of the last tile
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) el[c] = 0u;
+      }
+      const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
+      mbar_wait(eempty + es, eph ^ 1);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(s_elig) + ((es * NCH + c) * kTileRows + r) * 4),
+                     "r"(el[c])
+                     : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(efull + es);
+    }
   }
   fence_before();
   __syncthreads();
@@ -551,36 +622,46 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
   if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+uint32_t tc_tmem_cols(uint32_t Np) {
+  uint32_t cols = 32;
+  while (cols < kAccBufs * Np) cols <<= 1;
+  return cols;
+}
+
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes) {
-  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 5) * 8 + Np * 8 +
+  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
          4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64 + fused_bytes;
 }
 
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C) {
-  const size_t fw = 2 * ((Np / 32 + 1) / 2);
-  return 4 * ((T + 1) * 2 * fw + C * fw + fw + 1) + T + 1 + 16;
+uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }
+
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A) {
+  const size_t nch = tc_fused_chunks(Np);
+  return 128 + size_t{kTermSlots} * kTileRows * A * 2 + size_t{kEligSlots} * nch * kTileRows * 4 +
+         16 * (kTermSlots + kEligSlots) + 4 * ((T + 1) * 2 * nch + C * nch + nch + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st) {
+  using KFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
+  static const KFn fused[3][4] = {
+      {tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>, tc_score_kernel<4, 1>},
+      {tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>, tc_score_kernel<4, 2>},
+      {tc_score_kernel<1, 4>, tc_score_kernel<2, 4>, tc_score_kernel<3, 4>, tc_score_kernel<4, 4>}};
   static bool attr = false;
   if (!attr) {
-    for (auto k : {tc_score_kernel<0, 1>, tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>,
-                   tc_score_kernel<4, 1>, tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>,
-                   tc_score_kernel<4, 2>})
-      HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (auto& row : fused)
+      for (KFn k : row) HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  auto k = tc_score_kernel<0, 1>;
+  KFn k = tc_score_kernel<0, 1>;
   if (a.fused) {
-    const uint32_t na = (a.A + 7) / 8, cpt = (a.Np / 32 + 1) / 2;
+    const uint32_t na = (a.A + 7) / 8, nch = tc_fused_chunks(a.Np);
     if (na < 1 || na > 4) throw Error(HYRE_INTERNAL, "fused CNF: row term width out of range");
-    static decltype(k) const table[2][4] = {
-        {tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>, tc_score_kernel<4, 1>},
-        {tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>, tc_score_kernel<4, 2>}};
-    k = table[cpt - 1][na - 1];
+    k = fused[nch == 1 ? 0 : (nch == 2 ? 1 : 2)][na - 1];
   }
-  k<<<grid, kThreads, smem, st>>>(qhi, qlo, a);
+  k<<<grid, threads_for(a.fused != 0), smem, st>>>(qhi, qlo, a);
 }
 
 }  // namespace hyreb

@@ -25,13 +25,13 @@ struct TcArgs {
   uint32_t cap, mode, period, gate;
   const uint32_t* rerun;
   uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work (results invalid)
-  // Fused CNF (fused != 0, mask unused): the epilogue evaluates each row's
+  // Fused CNF (fused != 0, mask unused): dedicated warps evaluate each row's
   // eligibility from its forward term list (row_terms, slot-major, 0xFFFF
   // padded to A) against this group's program, scattered into shared memory:
   //   fz[0 .. n_entries*(1+W))  (term id, W users words) per referenced term
   //   fz + hc_off: hc[C][W]     queries constraining each slot
   //   fz + live_off: live[W], then the constrained-slot bitmask
-  // with W = 2 * cpt words laid out [half][cc] (query chunk c = half + 2 cc).
+  // with W = tc_fused_chunks(Np) words (word c = queries 32c .. 32c+31).
   uint32_t fused;
   const uint16_t* row_terms;
   const uint8_t* slot_of;
@@ -46,7 +46,11 @@ constexpr uint32_t kTcMaxGroup = 128;
 void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0);
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C);
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A);
+// TMEM columns for the accumulator buffers of a group of Np queries
+uint32_t tc_tmem_cols(uint32_t Np);
+// query chunks of a fused group as laid out in its program (1, 2 or 4)
+uint32_t tc_fused_chunks(uint32_t Np);
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st);
 

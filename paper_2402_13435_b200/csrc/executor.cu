@@ -88,7 +88,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   d_thr = dmalloc<uint64_t>(B);
   d_thr_safe = dmalloc<uint64_t>(B);
   d_cand = dmalloc<uint64_t>(B * cap);
-  d_samp = dmalloc<uint64_t>(B * samp_cap);
+  d_samp = dmalloc<uint32_t>(B * samp_cap);
   d_qhist = dmalloc<uint32_t>(B * (ix->num_bits + 1));
   d_tsel = dmalloc<uint32_t>(B * 3);
   d_eqcnt = dmalloc<uint32_t>(B * ix->n_chunks);
@@ -413,7 +413,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     for (uint32_t g = 0; g < tc_groups; ++g) {
       TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 ix->tc_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
-                rerun, tc_debug_flags()};
+                rerun, d_samp, tc_debug_flags()};
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
@@ -436,7 +436,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
   const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
-               d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun};
+               d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp};
   launch_score(sa, bf16, st);
   ++kernels;
 }
@@ -633,11 +633,12 @@ void Executor::run() {
   HYRE_CUDA(cudaEventRecord(ev[2], st));
   if (any_emb) {
     if (ix->n_rows > cap) {
-      HYRE_CUDA(cudaMemset2DAsync(d_samp, sizeof(uint64_t) * samp_cap, 0, sizeof(uint64_t) * sample_rows, B, st));
-      score(SCORE_SAMPLE, d_samp, samp_cnt, samp_cap);
-      SelectArgs ka{d_samp, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
-                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows};
-      launch_select(ka, st);
+      HYRE_CUDA(cudaMemset2DAsync(d_samp, sizeof(uint32_t) * samp_cap, 0, sizeof(uint32_t) * sample_rows, B, st));
+      score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
+      SelectArgs ka{nullptr, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
+                    nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows,
+                    d_samp, ix->row_base, d_cand, cap};
+      launch_sample_kth(ka, samp_cnt, st);
       ++kernels;
     } else {
       HYRE_CUDA(cudaMemsetAsync(d_thr, 0, sizeof(uint64_t) * B, st));

@@ -30,7 +30,7 @@ struct Executor {
   uint64_t* d_thr = nullptr;
   uint64_t* d_thr_safe = nullptr;
   uint64_t* d_cand = nullptr;
-  uint64_t* d_samp = nullptr;
+  uint32_t* d_samp = nullptr;  // dense sample scores [max_batch][samp_cap]
   uint32_t* d_qhist = nullptr;
   uint32_t* d_tsel = nullptr;
   uint32_t* d_eqcnt = nullptr;

@@ -586,7 +586,8 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const uint64_t key = make_key(clamp_score(p[0]), grow);
         if (a.mode == SCORE_SAMPLE) {
           // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
-          if (my_ok && elig) a.cand[static_cast<size_t>(q0 + j) * a.cap + it * kSegRows + my_off] = key;
+          if (my_ok && elig)
+            a.samp[static_cast<size_t>(q0 + j) * a.cap + it * kSegRows + my_off] = f2ord(clamp_score(p[0]));
           continue;
         }
         const bool take = my_ok && elig && key >= thr[j];
@@ -738,6 +739,57 @@ __device__ void bitonic_desc(uint64_t* s, uint32_t m) {  // m power of two
 }
 }  // namespace
 
+namespace {
+constexpr int kSampleVec = 8;  // uint4 of sample scores per thread: 8 x 4 x 512 = 16K slots
+
+__device__ __forceinline__ uint32_t kth_m(uint32_t k, uint32_t period) {
+  return min(k, max(8u, (4 * k + period - 1) / period));
+}
+// bins [per*o, per*o + per) belong to scan position t, o = T-1-t; returns
+// nnz; s_sel = {bin of the k-th key, keys at/above it, same for the m-th}
+__device__ __forceinline__ uint32_t kth_bins(const uint32_t* hist, uint32_t k, uint32_t m, uint32_t* tmp,
+                                             uint32_t* s_sel) {
+  const uint32_t per = 4096 / blockDim.x;
+  const uint32_t owner = blockDim.x - 1 - threadIdx.x;
+  uint32_t mine = 0;
+  for (uint32_t b = 0; b < per; ++b) mine += hist[owner * per + b];
+  uint32_t nnz;
+  uint32_t above = block_excl_scan(mine, tmp, &nnz);
+  for (int b = static_cast<int>(per) - 1; b >= 0; --b) {
+    const uint32_t h = hist[owner * per + b];
+    if (above < k && k <= above + h) {
+      s_sel[0] = owner * per + b;
+      s_sel[1] = above + h;
+    }
+    if (above < m && m <= above + h) {
+      s_sel[2] = owner * per + b;
+      s_sel[3] = above + h;
+    }
+    above += h;
+  }
+  __syncthreads();
+  return nnz;
+}
+// warp-aggregated shared-memory histogram increment (equal digits of a warp
+// cost one atomic); 0xffffffff = no value
+__device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t digit) {
+  const unsigned peers = __match_any_sync(0xffffffffu, digit);
+  if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
+    atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
+}
+// warp-aggregated append of `key` (if take) to dst[*cnt++] (capacity dcap)
+__device__ __forceinline__ void warp_append(bool take, uint64_t key, uint64_t* dst, uint32_t* cnt, uint32_t dcap) {
+  const unsigned bal = __ballot_sync(0xffffffffu, take);
+  if (!bal) return;
+  uint32_t at = 0;
+  if ((threadIdx.x & 31) == 0) at = atomicAdd(cnt, static_cast<uint32_t>(__popc(bal)));
+  at = __shfl_sync(0xffffffffu, at, 0) + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+  if (take && at < dcap) dst[at] = key;
+}
+}  // namespace
+
+constexpr uint32_t kSelResident = 8192;  // FINAL: candidates sorted from shared memory
+
 __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   extern __shared__ uint64_t sel_smem[];
   uint64_t* sortbuf = sel_smem;                                        // kSelectMaxK keys
@@ -820,18 +872,56 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     return;
   }
-  const uint64_t t = n > k ? kth_largest(keys, n, k, hist, tmp) : 0ull;
-  if (threadIdx.x == 0) gathered = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint64_t key = keys[i];
-    if (key >= t) {
-      const uint32_t at = atomicAdd(&gathered, 1u);
-      if (at < kSelectMaxK) sortbuf[at] = key;
+  uint32_t m = 0;
+  bool done = false;
+  if (n <= k) {  // every candidate is a hit (n <= k <= kSelectMaxK)
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sortbuf[i] = keys[i];
+    m = n;
+    done = true;
+  } else if (n <= kSelResident) {
+    // the common case: one coalesced pass into shared memory, a histogram of
+    // the top 12 key bits there finds the K-th key's bin, and only the keys
+    // at or above it (about K + one bin) are sorted -- no passes over global
+    // memory
+    uint64_t* res = reinterpret_cast<uint64_t*>(tmp + 40);
+    __shared__ uint32_t s_sel[4];
+    for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) gathered = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      const uint64_t key = i < n ? keys[i] : 0ull;
+      if (i < n) res[i] = key;
+      hist_add(hist, i < n ? static_cast<uint32_t>(key >> 52) : 0xffffffffu);
+    }
+    __syncthreads();
+    kth_bins(hist, k, k, tmp, s_sel);
+    if (s_sel[1] <= kSelectMaxK) {
+      const uint32_t dk = s_sel[0];
+      for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const uint64_t key = i < n ? res[i] : 0ull;
+        warp_append(i < n && static_cast<uint32_t>(key >> 52) >= dk, key, sortbuf, &gathered, kSelectMaxK);
+      }
+      __syncthreads();
+      m = gathered;
+      done = true;
     }
   }
-  __syncthreads();
-  const uint32_t m = min(gathered, kSelectMaxK);
+  if (!done) {
+    const uint64_t t = kth_largest(keys, n, k, hist, tmp);
+    if (threadIdx.x == 0) gathered = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if (key >= t) {
+        const uint32_t at = atomicAdd(&gathered, 1u);
+        if (at < kSelectMaxK) sortbuf[at] = key;
+      }
+    }
+    __syncthreads();
+    m = min(gathered, kSelectMaxK);
+  }
   uint32_t m2 = 1;
   while (m2 < m) m2 <<= 1;
   for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
@@ -850,127 +940,88 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   }
 }
 
-// K4 over a dense sample buffer (SELECT_KTH with dense_n): the thresholds
-// need only the K-th and m-th largest of the sample's few eligible keys
-// (0 = ineligible slot).  One pass builds a 4096-bin histogram of the top 12
-// key bits (sign, exponent, 3 mantissa bits of the score), a scan finds the
-// bin holding the K-th (m-th) key, a second pass gathers the keys at or above
-// that bin into shared memory and a bitonic sort reads both thresholds off
-// exactly.  Two streaming passes with 8 keys per thread in flight replace the
-// radix select's up to six; a bin too crowded to gather (massive ties) falls
-// back to the radix select.
-__global__ void __launch_bounds__(kSelThreads) sample_kth_kernel(SelectArgs a) {
+// K4 over the dense sample (SELECT_KTH with dense_n): the thresholds need
+// the K-th and m-th largest keys among the sample's eligible slots (slot
+// value = f2ord(score), 0 = ineligible; the slot index gives the row, so the
+// key (score, ~row) is rebuilt on the fly).  Two kernels:
+//   slice: each CTA holds one 16K-slot slice of a query's sample in
+//          registers, finds (4096-bin histogram of the top 12 score bits) the
+//          bin of its local r-th key, r = max(m, ceil(K / slices)), and
+//          appends the keys at or above it (its top r plus bin-mates) to the
+//          query's union buffer;
+//   union: one CTA per query sorts the union (a few hundred keys) in shared
+//          memory.  The union holds every slice's top m, so its m-th key is
+//          exactly the sample's m-th (t_est); it is a subset of the sample, so
+//          its K-th key is a valid lower bound on the global K-th (t_safe).
+__global__ void __launch_bounds__(kSelThreads) sample_slice_kernel(SelectArgs a, uint32_t* ucnt) {
+  __shared__ uint32_t hist[4096];
+  __shared__ uint32_t tmp[40], s_sel[4];
+  const uint32_t q = blockIdx.y;
+  const QParam qp = a.qp[q];
+  if ((qp.flags & a.require_flags) != a.require_flags || !(a.n_elig[q] > a.gate)) return;
+  const uint32_t k = qp.k, m = kth_m(k, a.period);
+  const uint32_t r = min(kSelectMaxK, max(m, (k + gridDim.x - 1) / gridDim.x));
+  const uint32_t n = a.dense_n, s0 = blockIdx.x * (kSampleVec * 4 * kSelThreads);
+  const uint32_t* sc = a.samp + static_cast<size_t>(q) * a.cap;
+  uint4 v[kSampleVec];
+#pragma unroll
+  for (int u = 0; u < kSampleVec; ++u) {
+    const uint32_t slot = s0 + 4 * (u * blockDim.x + threadIdx.x);
+    v[u] = slot + 3 < n ? *reinterpret_cast<const uint4*>(sc + slot)
+                        : make_uint4(slot < n ? sc[slot] : 0u, slot + 1 < n ? sc[slot + 1] : 0u,
+                                     slot + 2 < n ? sc[slot + 2] : 0u, 0u);
+  }
+  for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kSampleVec; ++u) {
+    hist_add(hist, v[u].x ? v[u].x >> 20 : 0xffffffffu);
+    hist_add(hist, v[u].y ? v[u].y >> 20 : 0xffffffffu);
+    hist_add(hist, v[u].z ? v[u].z >> 20 : 0xffffffffu);
+    hist_add(hist, v[u].w ? v[u].w >> 20 : 0xffffffffu);
+  }
+  __syncthreads();
+  const uint32_t nnz = kth_bins(hist, r, r, tmp, s_sel);
+  if (nnz == 0) return;
+  const uint32_t dsel = nnz >= r ? s_sel[0] : 0u;  // fewer than r: the whole slice
+  uint64_t* dst = a.fb + static_cast<size_t>(q) * a.fb_cap;
+#pragma unroll
+  for (int u = 0; u < kSampleVec; ++u) {
+    const uint32_t b0 = s0 + 4 * (u * blockDim.x + threadIdx.x);
+    const uint32_t o[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t slot = b0 + e, local = (slot >> 10) * a.period * 1024u + (slot & 1023u);
+      warp_append(o[e] != 0u && (o[e] >> 20) >= dsel,
+                  (static_cast<uint64_t>(o[e]) << 32) | static_cast<uint32_t>(~(a.row_base + local)), dst, ucnt + q,
+                  a.fb_cap);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSelThreads) sample_union_kernel(SelectArgs a, const uint32_t* ucnt) {
   extern __shared__ uint64_t sel_smem[];
   uint64_t* sortbuf = sel_smem;                                          // kSelectMaxK keys
   uint32_t* hist = reinterpret_cast<uint32_t*>(sel_smem + kSelectMaxK);  // 4096
   uint32_t* tmp = hist + 4096;                                           // 33
-  __shared__ uint32_t s_dk, s_gk, s_dm, s_gm, gathered;
   const uint32_t q = blockIdx.x;
   const QParam qp = a.qp[q];
   if ((qp.flags & a.require_flags) != a.require_flags) return;
-  if (!(a.n_elig[q] > a.gate)) {  // not sampled: no threshold
-    if (threadIdx.x == 0) {
-      a.thr[q] = 0;
-      if (a.thr_safe) a.thr_safe[q] = 0;
-    }
-    return;
-  }
-  const uint32_t k = qp.k, n = a.dense_n;
-  const uint32_t m = min(k, max(8u, (4 * k + a.period - 1) / a.period));
-  const uint64_t* keys = a.buf + static_cast<size_t>(q) * a.cap;
-  for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  auto add = [&](uint64_t key) {
-    const uint32_t digit = key ? static_cast<uint32_t>(key >> 52) : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, digit);
-    if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
-      atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
-  };
-  const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
-  const uint32_t n2 = n / 2;
-  for (uint32_t base = 0; base < n2; base += 4 * blockDim.x) {
-    ulonglong2 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = base + u * blockDim.x + threadIdx.x;
-      v[u] = i < n2 ? k2[i] : make_ulonglong2(0ull, 0ull);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      add(v[u].x);
-      add(v[u].y);
-    }
-  }
-  if (n & 1u) {
-    if (threadIdx.x < 32) add(threadIdx.x == 0 ? keys[n - 1] : 0ull);
-  }
-  __syncthreads();
-  // position t of the scan owns bins [8o, 8o+8), o = T-1-t: its exclusive
-  // prefix counts the keys in all higher bins
-  const uint32_t owner = blockDim.x - 1 - threadIdx.x;
-  uint32_t mine = 0;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) mine += hist[owner * 8 + b];
-  uint32_t nnz;
-  uint32_t above = block_excl_scan(mine, tmp, &nnz);
-#pragma unroll
-  for (int b = 7; b >= 0; --b) {
-    const uint32_t h = hist[owner * 8 + b];
-    if (above < k && k <= above + h) {
-      s_dk = owner * 8 + b;
-      s_gk = above + h;
-    }
-    if (above < m && m <= above + h) {
-      s_dm = owner * 8 + b;
-      s_gm = above + h;
-    }
-    above += h;
-  }
-  if (threadIdx.x == 0) gathered = 0;
-  __syncthreads();
   uint64_t t_safe = 0, t_est = 0;
-  if (nnz >= m) {
-    const bool full = nnz >= k;
-    const uint32_t dsel = full ? s_dk : s_dm, g = full ? s_gk : s_gm;
-    if (g <= kSelectMaxK) {
-      for (uint32_t base = 0; base < n2; base += 4 * blockDim.x) {
-        ulonglong2 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t i = base + u * blockDim.x + threadIdx.x;
-          v[u] = i < n2 ? k2[i] : make_ulonglong2(0ull, 0ull);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint64_t key = h ? v[u].y : v[u].x;
-            const bool take = key != 0ull && static_cast<uint32_t>(key >> 52) >= dsel;
-            const unsigned bal = __ballot_sync(0xffffffffu, take);
-            if (bal) {
-              uint32_t base_at = 0;
-              if ((threadIdx.x & 31) == 0) base_at = atomicAdd(&gathered, static_cast<uint32_t>(__popc(bal)));
-              base_at = __shfl_sync(0xffffffffu, base_at, 0);
-              if (take) sortbuf[base_at + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = key;
-            }
-          }
-        }
-      }
-      if ((n & 1u) && threadIdx.x == 0) {
-        const uint64_t key = keys[n - 1];
-        if (key != 0ull && static_cast<uint32_t>(key >> 52) >= dsel) sortbuf[atomicAdd(&gathered, 1u)] = key;
-      }
-      __syncthreads();
-      const uint32_t cnt = gathered;  // == g
+  if (a.n_elig[q] > a.gate) {
+    const uint32_t k = qp.k, m = kth_m(k, a.period);
+    const uint32_t n = min(ucnt[q], a.fb_cap);
+    const uint64_t* keys = a.fb + static_cast<size_t>(q) * a.fb_cap;
+    if (n <= kSelectMaxK) {
       uint32_t c2 = 1;
-      while (c2 < cnt) c2 <<= 1;
-      for (uint32_t i = cnt + threadIdx.x; i < c2; i += blockDim.x) sortbuf[i] = 0ull;
+      while (c2 < n) c2 <<= 1;
+      for (uint32_t i = threadIdx.x; i < c2; i += blockDim.x) sortbuf[i] = i < n ? keys[i] : 0ull;
       __syncthreads();
       bitonic_desc(sortbuf, c2);
-      t_safe = full ? sortbuf[k - 1] : 0ull;
-      t_est = sortbuf[m - 1];
+      t_safe = n >= k ? sortbuf[k - 1] : 0ull;
+      t_est = n >= m ? sortbuf[m - 1] : 0ull;
     } else {
-      t_safe = full ? kth_largest(keys, n, k, hist, tmp) : 0ull;
+      t_safe = n >= k ? kth_largest(keys, n, k, hist, tmp) : 0ull;
       t_est = m < k ? kth_largest(keys, n, m, hist, tmp) : t_safe;
     }
   }
@@ -980,17 +1031,30 @@ __global__ void __launch_bounds__(kSelThreads) sample_kth_kernel(SelectArgs a) {
   }
 }
 
-void launch_select(const SelectArgs& a, cudaStream_t st) {
+void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st) {
   if (a.B == 0) return;
+  constexpr uint32_t slice = kSampleVec * 4 * kSelThreads;
+  const dim3 grid((a.dense_n + slice - 1) / slice, a.B);
+  sample_slice_kernel<<<grid, kSelThreads, 0, st>>>(a, ucnt);
   const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(sample_kth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(sample_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
-  if (a.mode == SELECT_KTH && a.dense_n) sample_kth_kernel<<<a.B, kSelThreads, smem, st>>>(a);
-  else select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
+  sample_union_kernel<<<a.B, kSelThreads, smem, st>>>(a, ucnt);
+}
+
+void launch_select(const SelectArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  // sort buffer | histogram + scan scratch | resident candidates (FINAL)
+  const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t) + kSelResident * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = true;
+  }
+  select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
 }
 
 // ===========================================================================

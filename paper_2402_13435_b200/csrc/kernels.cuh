@@ -79,6 +79,7 @@ struct ScoreArgs {
   uint32_t mode, period;
   uint32_t gate;          // queries with n_elig > gate are sampled (= candidate cap)
   const uint32_t* rerun;  // [B]
+  uint32_t* samp;         // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 
@@ -105,9 +106,18 @@ struct SelectArgs {
   // falls back to thr_safe (rerun) if the estimate admitted fewer than K rows.
   uint64_t* thr_safe;
   uint32_t period;
-  uint32_t dense_n;  // KTH over a dense sample buffer: slots [0, dense_n) (0 keys = ineligible)
+  uint32_t dense_n;  // KTH over a dense sample buffer: slots [0, dense_n) (0 = ineligible)
+  // dense sample (KTH with dense_n): [B][cap] orderable scores f2ord(score);
+  // slot s holds local row (s / 1024) * period * 1024 + s % 1024
+  const uint32_t* samp;
+  uint32_t row_base;
+  uint64_t* fb;     // KTH fallback scratch ([B][fb_cap] keys; the candidate buffer)
+  uint32_t fb_cap;
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
+// SELECT_KTH over the dense sample: per-slice top keys gathered into fb
+// (ucnt [B] zeroed by the caller), then one sort per query.
+void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st);
 
 // ---- K5: term-only first-K rows (pipeline.cpp:30-40) ----
 struct FirstKArgs {

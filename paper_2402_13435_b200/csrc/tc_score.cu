@@ -31,7 +31,7 @@ namespace {
 
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
-constexpr uint32_t kStage = 2;                    // staged candidate keys per (epilogue warp, query)
+constexpr uint32_t kStageBytes = 32768;           // per-CTA candidate staging: Np queries x (32 KB / 8 Np) keys
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
 constexpr uint32_t kCnfWarps = 4;                 // fused CNF: one thread per tile row
 constexpr uint32_t kTermSlots = 2;                // fused CNF: tiles of row term lists in flight
@@ -238,9 +238,10 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   uint32_t* s_tr = reinterpret_cast<uint32_t*>(s_ts + Np);     // [Np] threshold row
   uint32_t* s_tmem = s_tr + Np;                                // TMEM base
   uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
-  // per-epilogue-warp candidate staging: [8][Np][kStage] keys + [8][Np] counts
+  // per-CTA candidate staging shared by the epilogue warps: [Np][kst] keys + [Np] counts
+  const uint32_t kst = kStageBytes / (8 * Np);
   uint32_t* s_scnt = s_act + 8;
-  uint8_t* after_cnt = reinterpret_cast<uint8_t*>(s_scnt + kEpiWarps * Np);
+  uint8_t* after_cnt = reinterpret_cast<uint8_t*>(s_scnt + Np);
   uint64_t* s_skey = reinterpret_cast<uint64_t*>(after_cnt + ((16u - (smem_u32(after_cnt) & 15u)) & 15u));
   // fused CNF: a ring of kTermSlots tiles of row term lists (bulk-copied by
   // the producer; 128 rows x A u16 each), a ring of kEligSlots tiles of
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   // barriers, then the tables: per term entry {users[NCH], hc of its
   // slot[NCH]} for T terms + sentinel, hc [C][NCH], live [NCH] + constrained
   // slots, slot of term [T + 1]
-  uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey + static_cast<size_t>(kEpiWarps) * Np * kStage);
+  uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + kStageBytes;
   uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
   const uint32_t term_tile_bytes = kTileRows * a.A * 2;
   uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? kTermSlots * term_tile_bytes : 0u));
@@ -307,11 +308,10 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       s_tr[j] = key_row(thr);
     }
   }
-  for (uint32_t j = threadIdx.x; j < kEpiWarps * Np; j += blockDim.x) s_scnt[j] = 0;
-  if (threadIdx.x < Np / 32) {
-    uint32_t m = 0;
-    for (uint32_t l = 0; l < 32; ++l) m |= tc_active(a, q0 + threadIdx.x * 32 + l) ? (1u << l) : 0u;
-    s_act[threadIdx.x] = m;
+  for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) s_scnt[j] = 0;
+  if (warp < Np / 32) {  // one ballot per 32-query chunk (parallel loads, not 32 serial ones)
+    const uint32_t m = __ballot_sync(0xffffffffu, tc_active(a, q0 + warp * 32 + lane));
+    if (lane == 0) s_act[warp] = m;
   }
   if (kFused) {
     for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
@@ -503,8 +503,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j)
             if ((elig >> j) & 1u)
-              a.cand[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] =
-                  make_key(clamp_score(__uint_as_float(v[j])), grow);
+              a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(clamp_score(__uint_as_float(v[j])));
           continue;
         }
         if (__any_sync(0xffffffffu, take != 0)) {
@@ -516,9 +515,9 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
             const uint32_t qq = c * 32 + j;
             const uint64_t key = make_key(clamp_score(__uint_as_float(v[j])), grow);
             if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
-            const uint32_t slot = atomicAdd(s_scnt + ewarp * Np + qq, 1u);
-            if (slot < kStage) {
-              s_skey[(static_cast<size_t>(ewarp) * Np + qq) * kStage + slot] = key;
+            const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
+            if (slot < kst) {
+              s_skey[qq * kst + slot] = key;
             } else {
               const uint32_t at = atomicAdd(a.cand_cnt + q0 + qq, 1u);
               if (at < a.cap) a.cand[static_cast<size_t>(q0 + qq) * a.cap + at] = key;
@@ -533,22 +532,18 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       mw[1] = mw_next[1];
       t = t_next;
     }
-    // final flush of the staged keys: lane l owns queries l, l+32, ...
-    __syncwarp();
-    uint32_t bases[4], ns[4];
-#pragma unroll
-    for (uint32_t c = 0; c < 4; ++c) {
-      const uint32_t qq = c * 32 + lane;
-      ns[c] = qq < Np ? min(s_scnt[ewarp * Np + qq], kStage) : 0u;
-      bases[c] = ns[c] ? atomicAdd(a.cand_cnt + q0 + qq, ns[c]) : 0u;
-    }
-#pragma unroll
-    for (uint32_t c = 0; c < 4; ++c) {
-      const uint32_t qq = c * 32 + lane;
-      const uint64_t* stage = s_skey + (static_cast<size_t>(ewarp) * Np + qq) * kStage;
+    // final flush of the CTA's staged keys once every epilogue warp is done:
+    // warp w owns queries w, w + 8, ...; one global reservation per query
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    for (uint32_t qq = ewarp; qq < Np; qq += kEpiWarps) {
+      const uint32_t ns = min(s_scnt[qq], kst);
+      if (ns == 0) continue;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(a.cand_cnt + q0 + qq, ns);
+      base = __shfl_sync(0xffffffffu, base, 0);
       uint64_t* dst = a.cand + static_cast<size_t>(q0 + qq) * a.cap;
-      for (uint32_t k = 0; k < ns[c]; ++k)
-        if (bases[c] + k < a.cap) dst[bases[c] + k] = stage[k];
+      for (uint32_t k = lane; k < ns; k += 32)
+        if (base + k < a.cap) dst[base + k] = s_skey[qq * kst + k];
     }
   } else if (kFused) {
     // ===== CNF warps: thread r evaluates tile row r for all NCH chunks =====
@@ -630,7 +625,7 @@ uint32_t tc_tmem_cols(uint32_t Np) {
 
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes) {
   return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
-         4 + 32 + kEpiWarps * Np * 4 + 16 + size_t{kEpiWarps} * Np * kStage * 8 + 64 + fused_bytes;
+         4 + 32 + Np * 4 + 16 + kStageBytes + 64 + fused_bytes;
 }
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }

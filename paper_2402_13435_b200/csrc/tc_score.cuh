@@ -24,6 +24,7 @@ struct TcArgs {
   uint32_t* cand_cnt;
   uint32_t cap, mode, period, gate;
   const uint32_t* rerun;
+  uint32_t* samp;  // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
   uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work (results invalid)
   // Fused CNF (fused != 0, mask unused): dedicated warps evaluate each row's
   // eligibility from its forward term list (row_terms, slot-major, 0xFFFF

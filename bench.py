@@ -341,9 +341,13 @@ def run_ours(args, w):
     elem = 2 if w.dtype == "bf16" else 4
     # algorithmic bytes of one main-scorer launch: every row of the shard once
     # (batched: U = N; the tensor path reads the bf16 hi+lo split = 4 B/elem)
-    # plus the B mask bitmaps it consumes.
+    # plus its eligibility input: the forward term lists (N x A u16) when the
+    # CNF is fused into K3, else the B mask bitmaps the K1 pass wrote.
     words = (n_local + 31) // 32
-    bytes_main = n_local * w.dim * elem + B * words * 4
+    path = int(lib.hyre_batch_path(h))
+    fused = bool(path & 2)
+    term_bytes = int(stats["forward_bytes"]) if fused else B * words * 4
+    bytes_main = n_local * w.dim * elem + term_bytes
     achieved = bytes_main / (main_avg * 1e-3) / 1e9
     traffic = load_traffic(w.name)
     step_ms = total_ms / args.steps
@@ -358,7 +362,8 @@ def run_ours(args, w):
                               [statistics.median(r[i] for r in stage_rows) for i in range(6)])),
         "roofline": {"bound": "hbm", "kernel": main_kernel_name(B), "achieved": achieved, "peak": hbm,
                      "peak_kind": f"{peak_kind} hbm_gbs (burst copy)", "unit": "GB/s", "frac": achieved / hbm,
-                     "bytes_per_launch": bytes_main, "launch_ms": main_avg, "traffic": traffic},
+                     "bytes_per_launch": bytes_main, "launch_ms": main_avg, "traffic": traffic,
+                     "eligibility": "fused CNF over forward term lists" if fused else "K1 mask bitmaps"},
         "e2e": {"value": B * e2e_steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
                 "d2h_bytes_per_step": int(d2h.value), "api": "hyre_execute_batch (C-ABI, host buffers)"},
         "gpu_launches": kernels_per_step * args.steps,

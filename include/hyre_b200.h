@@ -247,6 +247,14 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
                              uint32_t* counts, int32_t* statuses, hyre_timings* timings);
 /* Number of kernels the last hyre_batch_run enqueued. */
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
+/* Kernel path of the prepared batch (bit flags): 1 tensor-core scorer (K3),
+ * 2 CNF fused into K3 (no mask pass), 4 forward-list mask (K1b), 8 sample
+ * pass + threshold.  Diagnostics for benchmarks and tests. */
+#define HYRE_PATH_TC 1u
+#define HYRE_PATH_FUSED 2u
+#define HYRE_PATH_FWD_MASK 4u
+#define HYRE_PATH_SAMPLED 8u
+uint32_t hyre_batch_path(const hyre_executor* ex);
 /* CUDA-event durations (ms) of the last run, waiting for it to finish:
  * [0] K1 mask (+CSR scatter) [1] K6 quant [2] sample pass + K-th select
  * [3] main scorer (K2/K3) [4] final select + first-K [5] whole run. */

@@ -354,6 +354,14 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
 
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
 
+uint32_t hyre_batch_path(const hyre_executor* ex) {
+  if (!ex) return 0;
+  const Executor* e = ex->ex.get();
+  return (e->use_tc ? HYRE_PATH_TC : 0u) | (e->use_fused ? HYRE_PATH_FUSED : 0u) |
+         (e->use_fwd && !e->use_fused ? HYRE_PATH_FWD_MASK : 0u) |
+         (e->any_emb && e->ix->n_rows > e->cap ? HYRE_PATH_SAMPLED : 0u);
+}
+
 hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6) {
   return guard([&] {
     need(ex, "executor");

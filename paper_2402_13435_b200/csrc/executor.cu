@@ -267,13 +267,13 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   }
   // Fused CNF: an all-hybrid, quant-free tensor-core batch evaluates the
   // clauses in K3's epilogue from the forward term lists, when the group's
-  // term tables fit next to a >= 4-stage ring.
+  // term tables fit next to a >= 3-stage ring.
   use_fused = false;
   if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31) {
     fz_smem = tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->row_terms_width);
     const size_t kb = ix->dp / 64;
-    use_fused = tc_smem_bytes(tc_np, kb, ix->tc_ops, 4, fz_smem) <= 227 * 1024;
+    use_fused = tc_smem_bytes(tc_np, kb, ix->tc_ops, 3, fz_smem) <= 227 * 1024;
   }
   if (use_fused) {
     build_fused_program();
@@ -436,7 +436,12 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
   const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
-               d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp};
+               d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp, 1, 1};
+  // enough work items to fill the resident warp slots (148 SMs x 64 warps)
+  const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
+  const uint32_t n_samp_seg = (n_seg + sample_period - 1) / sample_period;
+  while (sa.split < 32 && n_seg * sa.split < 148u * 64u) sa.split *= 2;
+  while (sa.split_sample < 32 && n_samp_seg * sa.split_sample < 148u * 64u) sa.split_sample *= 2;
   launch_score(sa, bf16, st);
   ++kernels;
 }

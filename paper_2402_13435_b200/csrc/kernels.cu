@@ -146,26 +146,28 @@ struct MaskProg {
   uint32_t w[N];
 };
 
-template <uint32_t N>
+// QN = query slots evaluated per group (1, 8 or 32): single queries and small
+// batches skip the unused accumulators (registers, predicated ORs, counts).
+template <uint32_t N, int QN>
 __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_constant__ MaskProg<N> prog) {
   const uint32_t* c_mask_prog = prog.w;
-  __shared__ uint32_t wsum[32][4];
+  __shared__ uint32_t wsum[QN][4];
   const uint32_t t = threadIdx.x, chunk = blockIdx.x, g = blockIdx.y;
   const uint32_t widx = chunk * kChunkWords + t;
   const uint32_t live = c_mask_prog[2 + 2 * g];
   uint32_t pos = c_mask_prog[1 + 2 * g];
   const uint32_t q0 = (c_mask_prog[0] + g) * 32;  // word 0 = first group of this launch
   const uint32_t tm = tail_mask(widx, a.n_rows);
-  uint32_t res[32];
+  uint32_t res[QN];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) res[q] = ((live >> q) & 1u) ? tm : 0u;
+  for (int q = 0; q < QN; ++q) res[q] = ((live >> q) & 1u) ? tm : 0u;
   const uint32_t n_slots = c_mask_prog[pos++];
   for (uint32_t s = 0; s < n_slots; ++s) {
     const uint32_t hc = c_mask_prog[pos], n_refs = c_mask_prog[pos + 1];
     pos += 2;
-    uint32_t acc[32];
+    uint32_t acc[QN];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) acc[q] = 0u;
+    for (int q = 0; q < QN; ++q) acc[q] = 0u;
     // refs are (pointer lo, pointer hi, users) triples; 4 independent word
     // loads are issued before they are consumed.
     uint32_t r = 0;
@@ -180,28 +182,28 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
 #pragma unroll
       for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int q = 0; q < 32; ++q) acc[q] |= ((u[k] >> q) & 1u) ? w[k] : 0u;
+        for (int q = 0; q < QN; ++q) acc[q] |= ((u[k] >> q) & 1u) ? w[k] : 0u;
     }
     for (; r < n_refs; ++r, pos += 3) {
       const uint64_t ptr = (static_cast<uint64_t>(c_mask_prog[pos + 1]) << 32) | c_mask_prog[pos];
       const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(ptr) + widx);
       const uint32_t users = c_mask_prog[pos + 2];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) acc[q] |= ((users >> q) & 1u) ? w : 0u;
+      for (int q = 0; q < QN; ++q) acc[q] |= ((users >> q) & 1u) ? w : 0u;
     }
 #pragma unroll
-    for (int q = 0; q < 32; ++q)
+    for (int q = 0; q < QN; ++q)
       if ((hc >> q) & 1u) res[q] &= acc[q];
   }
   const int lane = t & 31, w = t >> 5;
 #pragma unroll
-  for (int q = 0; q < 32; ++q) {
+  for (int q = 0; q < QN; ++q) {
     if (q0 + q < a.B) a.mask[static_cast<size_t>(q0 + q) * a.words + widx] = res[q];
     const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(res[q]));
     if (lane == 0) wsum[q][w] = c;
   }
   __syncthreads();
-  if (t < 32 && q0 + t < a.B) {
+  if (t < QN && q0 + t < a.B) {
     const uint32_t c = wsum[t][0] + wsum[t][1] + wsum[t][2] + wsum[t][3];
     a.chunk_cnt[static_cast<size_t>(q0 + t) * a.n_chunks + chunk] = c;
     if (c) atomicAdd(a.n_elig + q0 + t, c);
@@ -209,11 +211,14 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
 }
 
 template <uint32_t N>
-void launch_mask_tm_n(const MaskArgs& a, const std::vector<uint32_t>& words, uint32_t n_groups,
+void launch_mask_tm_n(const MaskArgs& a, const std::vector<uint32_t>& words, uint32_t n_groups, uint32_t live_or,
                       cudaStream_t st) {
   MaskProg<N> p;
   std::memcpy(p.w, words.data(), words.size() * 4);
-  mask_tm_kernel<N><<<dim3(a.n_chunks, n_groups), kChunkWords, 0, st>>>(a, p);
+  const dim3 grid(a.n_chunks, n_groups);
+  if (live_or <= 1u) mask_tm_kernel<N, 1><<<grid, kChunkWords, 0, st>>>(a, p);
+  else if (live_or <= 0xFFu) mask_tm_kernel<N, 8><<<grid, kChunkWords, 0, st>>>(a, p);
+  else mask_tm_kernel<N, 32><<<grid, kChunkWords, 0, st>>>(a, p);
 }
 
 uint32_t launch_mask_tm(const MaskArgs& a, const std::vector<std::vector<uint32_t>>& groups,
@@ -234,8 +239,10 @@ uint32_t launch_mask_tm(const MaskArgs& a, const std::vector<std::vector<uint32_
       w[2 + 2 * (g - g0)] = live[g];
       w.insert(w.end(), groups[g].begin(), groups[g].end());
     }
-    if (w.size() <= 1024) launch_mask_tm_n<1024>(a, w, n, st);
-    else launch_mask_tm_n<kMaskProgWords>(a, w, n, st);
+    uint32_t live_or = 0;
+    for (size_t g = g0; g < g1; ++g) live_or |= live[g];
+    if (w.size() <= 1024) launch_mask_tm_n<1024>(a, w, n, live_or, st);
+    else launch_mask_tm_n<kMaskProgWords>(a, w, n, live_or, st);
     ++launches;
     g0 = g1;
   }
@@ -494,20 +501,25 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
                           : 0.0f;
 
   const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
-  const uint32_t n_iter = a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period : n_seg;
+  // few segments: each is split into S parts of 32/S mask words so that
+  // enough warps stream rows (the sample pass has its own split)
+  const uint32_t S = a.mode == SCORE_SAMPLE ? a.split_sample : a.split;
+  const uint32_t n_iter = (a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period : n_seg) * S;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const RowT* emb = static_cast<const RowT*>(a.emb);
   const int slot = ((lane & M1) ? 4 : 0) + ((lane & M2) ? 2 : 0) + ((lane & M3) ? 1 : 0);
   const bool leader = (lane & (M3 - 1)) == 0;
 
   for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + wib; it < n_iter; it += warps) {
-    const uint32_t seg = a.mode == SCORE_SAMPLE ? it * a.period : it;
+    const uint32_t seg = a.mode == SCORE_SAMPLE ? (it / S) * a.period : it / S;
     const uint32_t widx = seg * 32 + lane;
+    const bool in_part = lane / (32u / S) == it % S;
     uint32_t wq[QG];
     uint32_t uni = 0;
 #pragma unroll
     for (int j = 0; j < QG; ++j) {
-      wq[j] = ((act >> j & 1u) && widx < a.words) ? a.mask[static_cast<size_t>(q0 + j) * a.words + widx] : 0u;
+      wq[j] = ((act >> j & 1u) && widx < a.words && in_part) ? a.mask[static_cast<size_t>(q0 + j) * a.words + widx]
+                                                            : 0u;
       uni |= wq[j];
     }
     const uint32_t cnt = __popc(uni);
@@ -587,7 +599,7 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         if (a.mode == SCORE_SAMPLE) {
           // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
           if (my_ok && elig)
-            a.samp[static_cast<size_t>(q0 + j) * a.cap + it * kSegRows + my_off] = f2ord(clamp_score(p[0]));
+            a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(clamp_score(p[0]));
           continue;
         }
         const bool take = my_ok && elig && key >= thr[j];
@@ -628,7 +640,8 @@ void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st) {
   const uint32_t qg = a.B == 1 ? 1 : kMaxQG;
   const uint32_t groups = (a.B + qg - 1) / qg;
   const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
-  const uint32_t iters = a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period : n_seg;
+  const uint32_t iters =
+      a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period * a.split_sample : n_seg * a.split;
   // Persistent grid: up to 148 SMs x 8 CTAs of 8 warps, no more warps than segments.
   const uint32_t blocks = std::max(1u, std::min((iters + 7) / 8, 148u * 8u));
   dim3 grid(blocks, groups);

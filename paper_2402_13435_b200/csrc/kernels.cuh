@@ -80,6 +80,8 @@ struct ScoreArgs {
   uint32_t gate;          // queries with n_elig > gate are sampled (= candidate cap)
   const uint32_t* rerun;  // [B]
   uint32_t* samp;         // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
+  uint32_t split;         // main/rerun: parts per 1024-row segment (power of two <= 32)
+  uint32_t split_sample;  // the same for the sample pass
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 

@@ -113,6 +113,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// v[j] for a lane-varying j without local memory: a 5-level select tree
+__device__ __forceinline__ uint32_t pick32(const uint32_t (&v)[32], uint32_t j) {
+  uint32_t a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (j & 16u) ? v[i + 16] : v[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (j & 8u) ? a[i + 8] : a[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (j & 4u) ? b[i + 4] : b[i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) d[i] = (j & 2u) ? c[i + 2] : c[i];
+  return (j & 1u) ? d[1] : d[0];
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -161,12 +175,17 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, ui
     const uint32_t e = tbl + t * (8 * NCH);
     if (NCH == 1) {
       asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[j][0]), "=r"(h[j][0]) : "r"(e));
-    } else {
-#pragma unroll
-      for (int c = 0; c < NCH; c += 2)
-        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-            : "=r"(u[j][c]), "=r"(u[j][(c + 1) % NCH]), "=r"(h[j][c]), "=r"(h[j][(c + 1) % NCH])
-            : "r"(e + 16 * (c / 2)));
+    } else if (NCH == 2) {  // entry {u0, u1, h0, h1}
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(u[j][0]), "=r"(u[j][NCH - 1]), "=r"(h[j][0]), "=r"(h[j][NCH - 1])
+          : "r"(e));
+    } else {  // NCH == 4: entry {u0..u3, h0..h3}
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(u[j][0]), "=r"(u[j][1 % NCH]), "=r"(u[j][2 % NCH]), "=r"(u[j][3 % NCH])
+          : "r"(e));
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(h[j][0]), "=r"(h[j][1 % NCH]), "=r"(h[j][2 % NCH]), "=r"(h[j][3 % NCH])
+          : "r"(e + 16));
     }
   }
   uint32_t acc[NCH], fail[NCH], hp[NCH];
@@ -461,7 +480,9 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       }
       mbar_wait(tfull + acc, aph);
       fence_after();
-#pragma unroll
+      // not unrolled: one copy of the (large) chunk body keeps the
+      // instruction-cache footprint small when a warp owns two chunks
+#pragma unroll 1
       for (uint32_t cc = 0; cc < 2; ++cc) {
         const uint32_t c = half + 2 * cc;
         if (c >= nq32 || (a.debug & 2u)) break;
@@ -469,9 +490,9 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
         tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
         // 32x32 bit transpose: lane l held query (32c+l)'s word over this
         // warp's 32 rows; afterwards bit j of `elig` = row `lane`, query 32c+j.
-        uint32_t elig = mw[cc];
+        uint32_t elig = cc ? mw[1] : mw[0];
         if (kFused) {
-          elig = fel[cc];
+          elig = cc ? fel[1] : fel[0];
         } else {
 #pragma unroll
           for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
@@ -506,22 +527,21 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
               a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(clamp_score(__uint_as_float(v[j])));
           continue;
         }
-        if (__any_sync(0xffffffffu, take != 0)) {
-          // rare path: stage survivors in this warp's private smem slots,
-          // spill to the global candidate buffer only when a slot row is full
-#pragma unroll
-          for (uint32_t j = 0; j < 32; ++j) {  // static j keeps v[] in registers
-            if (!((take >> j) & 1u)) continue;
-            const uint32_t qq = c * 32 + j;
-            const uint64_t key = make_key(clamp_score(__uint_as_float(v[j])), grow);
-            if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
-            const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
-            if (slot < kst) {
-              s_skey[qq * kst + slot] = key;
-            } else {
-              const uint32_t at = atomicAdd(a.cand_cnt + q0 + qq, 1u);
-              if (at < a.cap) a.cand[static_cast<size_t>(q0 + qq) * a.cap + at] = key;
-            }
+        // survivors (rare): each lane walks its own set bits; the score is
+        // picked out of the register array by a select tree, so no
+        // 32-way-unrolled body sits in the hot loop's instruction footprint.
+        // Keys are staged per CTA in shared memory and spill to the global
+        // candidate buffer only when a query's slots are full.
+        for (uint32_t tk = take; tk; tk &= tk - 1u) {
+          const uint32_t j = __ffs(tk) - 1, qq = c * 32 + j;
+          const uint64_t key = make_key(clamp_score(__uint_as_float(pick32(v, j))), grow);
+          if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
+          const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
+          if (slot < kst) {
+            s_skey[qq * kst + slot] = key;
+          } else {
+            const uint32_t at = atomicAdd(a.cand_cnt + q0 + qq, 1u);
+            if (at < a.cap) a.cand[static_cast<size_t>(q0 + qq) * a.cap + at] = key;
           }
         }
       }

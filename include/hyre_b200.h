@@ -255,6 +255,10 @@ uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
 #define HYRE_PATH_FWD_MASK 4u
 #define HYRE_PATH_SAMPLED 8u
 uint32_t hyre_batch_path(const hyre_executor* ex);
+/* Eligible-row counts of the last run (u32[b], waits for it): the CNF
+ * matches per query; 0xFFFFFFFF where the CNF ran fused inside K3 (the count
+ * is never materialised there).  Diagnostics for benchmarks and tests. */
+hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out);
 /* CUDA-event durations (ms) of the last run, waiting for it to finish:
  * [0] K1 mask (+CSR scatter) [1] K6 quant [2] sample pass + K-th select
  * [3] main scorer (K2/K3) [4] final select + first-K [5] whole run. */

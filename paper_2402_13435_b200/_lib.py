@@ -111,6 +111,7 @@ SIGNATURES = {
     "hyre_batch_fetch": (C.c_int, [vp, C.POINTER(hyre_hit), u64p, u32p, i32p, C.POINTER(hyre_timings)]),
     "hyre_batch_kernel_count": (C.c_uint32, [vp]),
     "hyre_batch_path": (C.c_uint32, [vp]),
+    "hyre_batch_eligible": (C.c_int, [vp, u32p]),
     "hyre_batch_stage_ms": (C.c_int, [vp, f32p]),
     "hyre_batch_io_bytes": (C.c_int, [vp, u64p, u64p]),
     "hyre_batch_merge_gathered": (C.c_int, [vp, vp, vp, vp, C.c_uint32, C.c_uint64]),

@@ -354,6 +354,14 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
 
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
 
+hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out) {
+  return guard([&] {
+    need(ex, "executor");
+    need(out, "out");
+    ex->ex->eligible(out);
+  });
+}
+
 uint32_t hyre_batch_path(const hyre_executor* ex) {
   if (!ex) return 0;
   const Executor* e = ex->ex.get();

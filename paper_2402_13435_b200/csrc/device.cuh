@@ -66,6 +66,43 @@ struct Term {
   uint32_t id;      // term id (rank of (slot, id) among all index terms)
 };
 
+// Open-addressing term dictionary ((slot << 32) | id -> Term), linear
+// probing at <= 50% load: the per-id lookup of every query clause on the
+// host path (prepare) without unordered_map's node chasing.
+struct TermDict {
+  std::vector<uint64_t> keys;  // ~0 = empty
+  std::vector<Term> vals;
+  uint64_t mask = 0;
+  void reserve(size_t n) {
+    size_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    keys.assign(cap, ~0ull);
+    vals.assign(cap, Term{});
+    mask = cap - 1;
+  }
+  static uint64_t hash(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    return k;
+  }
+  void emplace(uint64_t k, const Term& t) {
+    for (uint64_t i = hash(k) & mask;; i = (i + 1) & mask)
+      if (keys[i] == ~0ull || keys[i] == k) {
+        keys[i] = k;
+        vals[i] = t;
+        return;
+      }
+  }
+  const Term* find(uint64_t k) const {
+    if (keys.empty()) return nullptr;
+    for (uint64_t i = hash(k) & mask;; i = (i + 1) & mask) {
+      if (keys[i] == k) return &vals[i];
+      if (keys[i] == ~0ull) return nullptr;
+    }
+  }
+};
+
 struct DevIndex {
   int device = 0;
   uint32_t n_rows = 0, row_base = 0, dim = 0, dp = 0;
@@ -89,7 +126,7 @@ struct DevIndex {
   uint32_t n_bitmap_terms = 0;
   uint32_t* post_rows = nullptr;
   uint64_t n_postings = 0;
-  std::unordered_map<uint64_t, Term> terms;  // key = (slot << 32) | id
+  TermDict terms;  // key = (slot << 32) | id
   bool has_tc = false;                       // tc_tiles present (dp % 64 == 0)
   // Forward term lists (K1b): row_terms[r * A + j] = term id of the row's j-th
   // attribute (slot order, 0xFFFF padding); slot_of[t] = clause slot of term t.

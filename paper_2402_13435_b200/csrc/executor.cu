@@ -159,7 +159,10 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   hit_off.assign(b, 0);
   qvec.assign(size_t{b} * dp, 0.0f);
   qsig.assign(size_t{b} * nw, 0ull);
-  qslots.assign(b, std::vector<uint32_t>());
+  q_cl.assign(b + 1, 0);
+  cl_slot.clear();
+  cl_t.clear();
+  t_ids.clear();
   any_emb = any_term_only = any_quant = false;
   max_k = 1;
   uint32_t n_scratch = 0;
@@ -171,9 +174,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // the inverted bitmaps / CSR postings of just their own terms (K1).
   use_fwd = ix->row_terms != nullptr && b >= kFwdMinBatch && mask_path() != 1 && !fwd_veto;
   fwd_veto = false;
-  qterms.assign(b, std::vector<std::vector<uint32_t>>());
   for (uint32_t i = 0; i < b; ++i) {
     const hyre_query& q = qs[i];
+    q_cl[i] = static_cast<uint32_t>(cl_slot.size());
     try {
       validate_query(shape, q);
     } catch (const Error& e) {
@@ -209,13 +212,14 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
         const size_t len_at = prog.size();
         prog.push_back(0);
         uint32_t scratch_for_clause = UINT32_MAX;
-        if (use_fwd) qterms[i].emplace_back();
+        cl_slot.push_back(static_cast<uint32_t>(slot));
+        cl_t.push_back(static_cast<uint32_t>(t_ids.size()));
         for (uint32_t j = q.id_offsets[c]; j < q.id_offsets[c + 1]; ++j) {
-          auto it = ix->terms.find((slot << 32) | q.ids[j]);
-          if (it == ix->terms.end()) continue;  // id absent from the index: matches no row
-          const Term& t = it->second;
+          const Term* tp = ix->terms.find((slot << 32) | q.ids[j]);
+          if (!tp) continue;  // id absent from the index: matches no row
+          const Term& t = *tp;
           if (use_fwd) {
-            qterms[i].back().push_back(t.id);
+            t_ids.push_back(t.id);
             prog.push_back(0);  // placeholder: the bitmap program is not used
             continue;
           }
@@ -247,10 +251,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       if (empty) p.flags |= QF_EMPTY;
     }
     qp[i] = p;
-    qslots[i].assign(q.slots, q.slots + q.n_clauses);
     hit_off[i] = total_hits;
     total_hits += p.k;
   }
+  q_cl[b] = static_cast<uint32_t>(cl_slot.size());
+  cl_t.push_back(static_cast<uint32_t>(t_ids.size()));
   scatter_total = items.empty() ? 0 : item_prefix.back() + items.back().count;
   n_scratch_used = n_scratch;
   ensure_scratch(n_scratch);
@@ -283,8 +288,8 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     // kernel ~0.5 ms per pass of 64/128 queries per 10M rows.
     std::vector<std::unordered_map<uint32_t, bool>> distinct((b + 31) / 32);
     for (uint32_t i = 0; i < b; ++i)
-      for (const auto& cl : qterms[i])
-        for (uint32_t t : cl) distinct[i / 32][t] = true;
+      for (uint32_t k = q_cl[i]; k < q_cl[i + 1]; ++k)
+        for (uint32_t x = cl_t[k]; x < cl_t[k + 1]; ++x) distinct[i / 32][t_ids[x]] = true;
     uint64_t ref_groups = 0;
     for (const auto& d : distinct) ref_groups += d.size();
     const uint64_t passes = (b + 127) / 128;
@@ -466,7 +471,7 @@ void Executor::build_term_major_program() {
       const uint32_t nc = prog[pos++];
       for (uint32_t c = 0; c < nc; ++c) {
         const uint32_t nr = prog[pos++];
-        auto& e = slots[qslots[i][c]];
+        auto& e = slots[cl_slot[q_cl[i] + c]];
         e.first |= 1u << j;
         for (uint32_t r = 0; r < nr; ++r) e.second[prog[pos + r]] |= 1u << j;
         pos += nr;
@@ -504,9 +509,10 @@ void Executor::build_forward_program() {
       const uint32_t w = (i - q0) >> 6;
       const uint64_t bit = 1ull << ((i - q0) & 63);
       live[w] |= bit;
-      for (size_t c = 0; c < qterms[i].size(); ++c) {
-        hc[size_t{qslots[i][c]} * nwp + w] |= bit;
-        for (uint32_t t : qterms[i][c]) {
+      for (uint32_t k = q_cl[i]; k < q_cl[i + 1]; ++k) {
+        hc[size_t{cl_slot[k]} * nwp + w] |= bit;
+        for (uint32_t x = cl_t[k]; x < cl_t[k + 1]; ++x) {
+          const uint32_t t = t_ids[x];
           auto& u = users[t];
           if (u.empty()) u.assign(nwp, 0ull);
           u[w] |= bit;
@@ -547,9 +553,11 @@ void Executor::build_forward_program() {
 void Executor::build_fused_program() {
   fz_words.clear();
   fz_group.clear();
-  const uint32_t C = ix->num_clauses, fw = tc_fused_chunks(tc_np);
+  const uint32_t C = ix->num_clauses, fw = tc_fused_chunks(tc_np), T = ix->n_terms_fwd;
+  // dense per-term users scratch (T <= kForwardMaxTerms), reset via the touched list
+  if (fz_users.size() < size_t{T} * fw) fz_users.assign(size_t{T} * fw, 0u);
   for (uint32_t g = 0; g < tc_groups; ++g) {
-    std::map<uint32_t, std::vector<uint32_t>> users;
+    fz_touched.clear();
     std::vector<uint32_t> hc(size_t{C} * fw, 0u), live(fw, 0u);
     uint32_t cslots = 0;
     for (uint32_t i = g * tc_np; i < std::min(B, (g + 1) * tc_np); ++i) {
@@ -557,23 +565,26 @@ void Executor::build_fused_program() {
       if (!(p.flags & QF_ACTIVE) || (p.flags & QF_EMPTY)) continue;
       const uint32_t j = i - g * tc_np, w = j / 32, bit = 1u << (j & 31);
       live[w] |= bit;
-      for (size_t cl = 0; cl < qterms[i].size(); ++cl) {
-        const uint32_t slot = qslots[i][cl];
-        hc[size_t{slot} * fw + w] |= bit;
-        cslots |= 1u << slot;
-        for (uint32_t t : qterms[i][cl]) {
-          auto& u = users[t];
-          if (u.empty()) u.assign(fw, 0u);
+      for (uint32_t k = q_cl[i]; k < q_cl[i + 1]; ++k) {
+        hc[size_t{cl_slot[k]} * fw + w] |= bit;
+        cslots |= 1u << cl_slot[k];
+        for (uint32_t x = cl_t[k]; x < cl_t[k + 1]; ++x) {
+          uint32_t* u = fz_users.data() + size_t{t_ids[x]} * fw;
+          bool fresh = true;
+          for (uint32_t v = 0; v < fw; ++v) fresh &= u[v] == 0u;
+          if (fresh) fz_touched.push_back(t_ids[x]);
           u[w] |= bit;
         }
       }
     }
     FusedGroup fg{};
     fg.entries = static_cast<uint32_t>(fz_words.size());
-    fg.n_entries = static_cast<uint32_t>(users.size());
-    for (auto& [t, u] : users) {
+    fg.n_entries = static_cast<uint32_t>(fz_touched.size());
+    for (uint32_t t : fz_touched) {
+      uint32_t* u = fz_users.data() + size_t{t} * fw;
       fz_words.push_back(t);
-      fz_words.insert(fz_words.end(), u.begin(), u.end());
+      fz_words.insert(fz_words.end(), u, u + fw);
+      std::fill(u, u + fw, 0u);
     }
     fg.hc = static_cast<uint32_t>(fz_words.size());
     fz_words.insert(fz_words.end(), hc.begin(), hc.end());
@@ -700,11 +711,21 @@ void Executor::finish_reruns() {
 void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* st_out,
                      hyre_timings* t) {
   if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_fetch before hyre_batch_prepare");
-  if (any_emb) finish_reruns();
   uint32_t* out_cnt = d_counters + 3 * max_batch;
-  HYRE_CUDA(cudaMemcpyAsync(h_out_cnt.data(), out_cnt, B * 4, cudaMemcpyDeviceToHost, st));
-  HYRE_CUDA(cudaMemcpyAsync(h_hits, d_hits, n_hits_total * sizeof(hyre_hit), cudaMemcpyDeviceToHost, st));
-  HYRE_CUDA(cudaStreamSynchronize(st));
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  // one round trip in the common case: results and the recovery flags
+  // together; a pending recovery (candidate overflow) reruns and re-copies
+  for (int pass = 0;; ++pass) {
+    if (any_emb) HYRE_CUDA(cudaMemcpyAsync(h_rerun.data(), rerun, B * 4, cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaMemcpyAsync(h_out_cnt.data(), out_cnt, B * 4, cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaMemcpyAsync(h_hits, d_hits, n_hits_total * sizeof(hyre_hit), cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    bool pending = false;
+    for (uint32_t i = 0; any_emb && i < B; ++i) pending |= h_rerun[i] != 0;
+    if (!pending) break;
+    if (pass > 0) throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");
+    finish_reruns();
+  }
   d2h_bytes = B * 4 + n_hits_total * sizeof(hyre_hit);
   for (uint32_t i = 0; i < B; ++i) {
     if (st_out) st_out[i] = statuses[i];
@@ -720,6 +741,11 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
     t->ebr_ms = s6[2] + s6[3];
     t->topk_ms = s6[4];
   }
+}
+
+void Executor::eligible(uint32_t* out) {
+  HYRE_CUDA(cudaMemcpyAsync(out, d_counters, sizeof(uint32_t) * B, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
 }
 
 float Executor::last_run_ms() const {

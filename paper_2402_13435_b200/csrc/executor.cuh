@@ -52,10 +52,12 @@ struct Executor {
   std::vector<uint32_t> prog;
   std::vector<std::vector<uint32_t>> prog_groups;  // term-major program per 32-query group (kernels.cu)
   std::vector<uint32_t> prog_live;
-  std::vector<std::vector<uint32_t>> qslots;
+  // flat clause view of the prepared batch: query i's clauses are
+  // [q_cl[i], q_cl[i+1]) with slot cl_slot[k] and index term ids
+  // t_ids[cl_t[k] .. cl_t[k+1]) (term ids only on the forward/fused paths)
+  std::vector<uint32_t> q_cl, cl_slot, cl_t, t_ids;
   // forward-index (K1b) program
   bool use_fwd = false, fwd_veto = false;
-  std::vector<std::vector<std::vector<uint32_t>>> qterms;  // [query][clause] term ids
   struct FwdPass {
     uint32_t q0, nw, n_entries, entries, hc, live;
   };
@@ -80,6 +82,7 @@ struct Executor {
   };
   std::vector<FusedGroup> fz_group;
   std::vector<uint32_t> fz_words;
+  std::vector<uint32_t> fz_users, fz_touched;  // build_fused_program scratch
   uint32_t* d_fz = nullptr;
   size_t fz_smem = 0;
   // tensor-core path (K3)
@@ -105,6 +108,7 @@ struct Executor {
   void fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* statuses,
              hyre_timings* t);
   float last_run_ms() const;
+  void eligible(uint32_t* out);  // n_elig of the last run (D2H, synchronous)
   void stage_ms(float* out) const;  // [mask, quant, sample+kth, main score, select/first-K, total]
 
   uint64_t full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows);

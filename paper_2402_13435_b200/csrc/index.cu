@@ -287,7 +287,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       std::vector<ScatterItem> items;
       std::vector<uint64_t> prefix;
       uint64_t begin = 0, bsum = 0;
-      ix->terms.reserve(T * 2);
+      ix->terms.reserve(T);
       for (uint32_t i = 0; i < T; ++i) {
         Term t{UINT32_MAX, hdf[i], begin, i};
         if (hdf[i] >= dense_df) {

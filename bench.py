@@ -285,14 +285,15 @@ def run_ours(args, w):
     total_ms = float(t.item())
     kernels_per_step = int(lib.hyre_batch_kernel_count(h)) + (1 if gather else 0)
 
-    # ---- per-call latency + per-kernel times (separately, synced per step) -
-    lat, main_ms, stage_rows = [], [], []
-    for _ in range(max(args.steps, 10)):
-        check(lib.hyre_batch_run(h))
-        check(lib.hyre_batch_stage_ms(h, s6))
+    # ---- per-call latency + per-kernel times of the timed steps ------------
+    # (CUDA events the executor records around each stage on its own stream;
+    # it keeps the last 64 runs, read back after the timed region)
+    stage_rows = []
+    for back in range(min(args.steps, 64)):
+        check(lib.hyre_batch_stage_ms_hist(h, back, s6))
         stage_rows.append(list(s6))
-        lat.append(s6[5])
-        main_ms.append(s6[3])
+    lat = [r[5] for r in stage_rows]
+    main_ms = [r[3] for r in stage_rows]
     p50 = statistics.median(lat)
     main_avg = statistics.mean(main_ms)
 
@@ -345,22 +346,27 @@ def run_ours(args, w):
     hbm, _, peak_kind = peaks()
     n_local = re_ - rb
     elem = 2 if w.dtype == "bf16" else 4
-    # algorithmic bytes of one main-scorer launch: every row of the shard once
-    # (batched: U = N; the tensor path reads the bf16 hi+lo split = 4 B/elem)
-    # plus its eligibility input: the forward term lists (N x A u16) when the
-    # CNF is fused into K3, else the B mask bitmaps the K1 pass wrote.
+    # algorithmic bytes of the dominant kernel's launch:
+    #  K3 (batched): every row of the shard once (bf16 hi+lo split = 4 B/elem
+    #     for an fp32 index) + its eligibility input (the forward term lists
+    #     when the CNF is fused into K3, else the B mask bitmaps K1 wrote);
+    #  K2 (B <= 8): only eligible rows are loaded: U = the largest per-query
+    #     eligible count (a lower bound on the union it streams) + the masks;
+    #  K1 (term-only batches): distinct term bitmaps + CSR postings + mask writes.
     words = (n_local + 31) // 32
     path = int(lib.hyre_batch_path(h))
     fused = bool(path & 2)
-    term_bytes = int(stats["forward_bytes"]) if fused else B * words * 4
-    rows_read = n_local
-    if not (path & 1):
-        # K2 (CUDA cores, B <= 8) loads only eligible rows: U = the largest
-        # per-query eligible count (a lower bound on the union it streams)
+    kernel = main_kernel_name(B)
+    if qemb is None:
+        kernel = "mask_tm_kernel (K1: term-major CNF over bitmaps/CSR)"
+        bytes_main = int(lib.hyre_batch_term_bytes(h)) + B * words * 4
+        main_avg = statistics.median(r[0] for r in stage_rows)
+    elif path & 1:
+        bytes_main = n_local * w.dim * elem + (int(lib.hyre_batch_term_bytes(h)) if fused else B * words * 4)
+    else:
         elig = np.zeros(B, np.uint32)
         check(lib.hyre_batch_eligible(h, elig.ctypes.data_as(L.u32p)))
-        rows_read = int(min(n_local, elig.max()))
-    bytes_main = rows_read * w.dim * elem + term_bytes
+        bytes_main = int(min(n_local, elig.max())) * w.dim * elem + B * words * 4
     achieved = bytes_main / (main_avg * 1e-3) / 1e9
     traffic = load_traffic(w.name)
     step_ms = total_ms / args.steps
@@ -373,10 +379,11 @@ def run_ours(args, w):
         "config": workload_config(w, args),
         "stages_ms": dict(zip(["mask", "quant", "sample", "main_scorer", "select_firstk", "run"],
                               [statistics.median(r[i] for r in stage_rows) for i in range(6)])),
-        "roofline": {"bound": "hbm", "kernel": main_kernel_name(B), "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm,
                      "peak_kind": f"{peak_kind} hbm_gbs (burst copy)", "unit": "GB/s", "frac": achieved / hbm,
                      "bytes_per_launch": bytes_main, "launch_ms": main_avg, "traffic": traffic,
-                     "eligibility": "fused CNF over forward term lists" if fused else "K1 mask bitmaps"},
+                     "eligibility": "fused CNF over forward term lists" if fused else "K1 mask bitmaps",
+                     "path_flags": path},
         "e2e": {"value": B * e2e_steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
                 "d2h_bytes_per_step": int(d2h.value), "api": "hyre_execute_batch (C-ABI, host buffers)",
                 "host_prepare_ms": prep_ms},
@@ -416,7 +423,7 @@ def load_traffic(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3")

@@ -259,10 +259,18 @@ uint32_t hyre_batch_path(const hyre_executor* ex);
  * matches per query; 0xFFFFFFFF where the CNF ran fused inside K3 (the count
  * is never materialised there).  Diagnostics for benchmarks and tests. */
 hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out);
+/* Algorithmic bytes of the prepared batch's eligibility inputs: distinct
+ * term bitmaps + CSR postings (K1), or the forward term lists once per pass
+ * (K1b / fused K3). */
+uint64_t hyre_batch_term_bytes(const hyre_executor* ex);
 /* CUDA-event durations (ms) of the last run, waiting for it to finish:
  * [0] K1 mask (+CSR scatter) [1] K6 quant [2] sample pass + K-th select
  * [3] main scorer (K2/K3) [4] final select + first-K [5] whole run. */
 hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6);
+/* The same for the run `back` runs before the last (0 = last; the executor
+ * keeps the events of its last 64 runs), so a benchmark can read per-kernel
+ * times of every step of a back-to-back timed region afterwards. */
+hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* out6);
 /* Device pointers of the last run's results (for on-device multi-GPU
  * gathers): hits (hyre_hit[*n_hits]), per-slot hit offsets (u64[b]) and
  * per-slot counts (u32[b]).  Valid until the next prepare. */

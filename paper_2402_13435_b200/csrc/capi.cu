@@ -354,6 +354,8 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
 
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
 
+uint64_t hyre_batch_term_bytes(const hyre_executor* ex) { return ex ? ex->ex->term_bytes : 0; }
+
 hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out) {
   return guard([&] {
     need(ex, "executor");
@@ -375,6 +377,14 @@ hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6) {
     need(ex, "executor");
     need(out6, "out");
     ex->ex->stage_ms(out6);
+  });
+}
+
+hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* out6) {
+  return guard([&] {
+    need(ex, "executor");
+    need(out6, "out");
+    ex->ex->stage_ms_hist(back, out6);
   });
 }
 

@@ -78,7 +78,8 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   if (max_batch < 1) validation("maxBatch must be >= 1");
   HYRE_CUDA(cudaSetDevice(ix->device));
   HYRE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  for (auto& e : ev) HYRE_CUDA(cudaEventCreate(&e));
+  for (auto& set : ev_ring)
+    for (auto& e : set) HYRE_CUDA(cudaEventCreate(&e));
   const size_t B = max_batch;
   cap = 65536;
   samp_cap = kSampleRows;
@@ -105,7 +106,8 @@ Executor::~Executor() {
     cudaFree(p);
   if (h_blob) cudaFreeHost(h_blob);
   if (h_hits) cudaFreeHost(h_hits);
-  for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& set : ev_ring)
+    for (auto& e : set) cudaEventDestroy(e);
   cudaStreamDestroy(st);
 }
 
@@ -378,6 +380,12 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     make_bf16_map(&tm_qlo, d_blob + o_qlo, size_t{tc_groups} * tc_np, dp, tc_np);
   }
   h2d_bytes = off;
+  // eligibility input bytes: distinct bitmaps W*4 each, CSR
+  // postings 4 each; the forward lists N*A*2 once per pass on the fwd/fused paths
+  if (use_fused || use_fwd)
+    term_bytes = size_t{ix->n_rows} * ix->row_terms_width * 2 * (use_fused ? tc_groups : fwd_pass.size());
+  else
+    term_bytes = uint64_t{ix->words} * 4 * (ref_src.size() - n_scratch) + scatter_total * 4;
   d_qp = reinterpret_cast<QParam*>(d_blob + o_qp);
   d_q = reinterpret_cast<float*>(d_blob + o_q);
   d_qsig = reinterpret_cast<uint64_t*>(d_blob + o_qsig);
@@ -601,6 +609,7 @@ void Executor::run() {
   if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_run before hyre_batch_prepare");
   HYRE_CUDA(cudaSetDevice(ix->device));
   kernels = 0;
+  ev = ev_ring[n_runs++ % kEvRing];
   const uint32_t W = ix->words;
   uint32_t* n_elig = d_counters;
   uint32_t* cand_cnt = d_counters + max_batch;
@@ -753,6 +762,18 @@ float Executor::last_run_ms() const {
   cudaEventSynchronize(ev[5]);
   cudaEventElapsedTime(&ms, ev[0], ev[5]);
   return ms;
+}
+
+void Executor::stage_ms_hist(uint32_t back, float* out) const {
+  if (back >= kEvRing || back >= n_runs) throw Error(HYRE_INVALID_ARGUMENT, "no such run in the timing ring");
+  const cudaEvent_t* e = ev_ring[(n_runs - 1 - back) % kEvRing];
+  cudaEventSynchronize(e[5]);
+  for (int i = 0; i < 5; ++i) {
+    out[i] = 0;
+    cudaEventElapsedTime(out + i, e[i], e[i + 1]);
+  }
+  out[5] = 0;
+  cudaEventElapsedTime(out + 5, e[0], e[5]);
 }
 
 void Executor::stage_ms(float* out) const {

@@ -20,7 +20,12 @@ struct Executor {
   DevIndex* ix;
   uint32_t max_batch;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[6] = {};  // start, mask, quant, pre-main, post-main, end
+  // stage events of the last kEvRing runs: start, mask, quant, pre-main,
+  // post-main, end (ring slot = run counter % kEvRing); ev = the current slot
+  static constexpr uint32_t kEvRing = 64;
+  cudaEvent_t ev_ring[kEvRing][6] = {};
+  cudaEvent_t* ev = ev_ring[0];
+  uint64_t n_runs = 0;
 
   // device scratch sized at construction
   uint32_t cap = 0, samp_cap = 0;
@@ -74,6 +79,7 @@ struct Executor {
   std::vector<float> qvec;
   std::vector<uint64_t> qsig;
   uint64_t n_hits_total = 0, h2d_bytes = 0, d2h_bytes = 0;
+  uint64_t term_bytes = 0;  // algorithmic eligibility-input bytes of the prepared batch
   // fused CNF in the K3 epilogue (no K1 mask pass): per query group, the
   // term-users program (TcArgs::fz) and its offsets into fz_words
   bool use_fused = false;
@@ -110,6 +116,7 @@ struct Executor {
   float last_run_ms() const;
   void eligible(uint32_t* out);  // n_elig of the last run (D2H, synchronous)
   void stage_ms(float* out) const;  // [mask, quant, sample+kth, main score, select/first-K, total]
+  void stage_ms_hist(uint32_t back, float* out) const;  // the same for the run `back` runs ago
 
   uint64_t full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows);
   bool exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out);

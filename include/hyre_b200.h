@@ -278,6 +278,23 @@ hyre_status hyre_batch_device_results(hyre_executor* ex, void** hits, uint64_t* 
                                       void** counts);
 /* Bytes the last prepare copied host->device and the last fetch copied back. */
 hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h);
+/* ------------------------------------------------------------------------
+ * Executor pool with dynamic request batching: the replacement for
+ * SearchService::ExecutorPool (service.cpp:99-141; ServiceConfig{workers,
+ * max_batch} service.hpp:19-26).  `workers` executors (own CUDA streams);
+ * concurrent hyre_pool_search calls are grouped into batches of up to
+ * max_batch queries, waiting at most max_wait_us after the first arrives.
+ * hyre_pool_search is thread-safe and blocking; its result (or validation
+ * error, thread-local hyre_last_error) is that of hyre_execute for the query.
+ * ------------------------------------------------------------------------ */
+typedef struct hyre_pool hyre_pool;
+hyre_status hyre_pool_create(hyre_index* ix, uint32_t workers, uint32_t max_batch, uint32_t max_wait_us,
+                             hyre_pool** out);
+void hyre_pool_destroy(hyre_pool* p);
+hyre_status hyre_pool_search(hyre_pool* p, const hyre_query* q, hyre_hit* hits, uint32_t* n_hits);
+/* Batches run and queries served so far (queries / batches = mean batch size). */
+hyre_status hyre_pool_stats(const hyre_pool* p, uint64_t* batches, uint64_t* queries);
+
 /* Exact on-device merge of G shard result sets gathered from the executors of
  * every shard (same batch): g_hits [G][hits_stride] hyre_hit, g_offsets [G][b]
  * u64 and g_counts [G][b] u32 (the hyre_batch_device_results layouts).  The

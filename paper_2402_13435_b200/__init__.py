@@ -12,7 +12,7 @@ _load_lib()
 
 from .hyre import *  # noqa: E402,F401,F403
 from .hyre import (  # noqa: E402,F401
-    BatchRequest, CnfClause, CnfQuery, DeviceError, DeviceIndex, DocumentInput, ExecOptions, Executor,
+    BatchRequest, CnfClause, CnfQuery, DeviceError, DeviceIndex, DocumentInput, ExecOptions, Executor, ExecutorPool,
     FrozenIndex, HybridQuery, IndexBuilder, IndexConfig, LoadError, Messenger, QuantCodec, QueryOutcome,
     ScoreDomainError, ScoredDoc, ScoredMessengers, Signature, StageTimings, TopKResult, ValidationError,
     bucket_top_k, clause_matches, encode, exact_scores, execute, execute_batch, full_scan_tbr, make_codec,

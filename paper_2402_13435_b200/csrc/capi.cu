@@ -8,6 +8,7 @@
 #include <string>
 
 #include "executor.cuh"
+#include "service.cuh"
 #include "hyre_b200.h"
 
 using namespace hyreb;
@@ -23,6 +24,9 @@ struct hyre_index {
 };
 struct hyre_executor {
   std::unique_ptr<Executor> ex;
+};
+struct hyre_pool {
+  std::unique_ptr<Pool> p;
 };
 
 namespace {
@@ -287,6 +291,32 @@ hyre_status hyre_executor_create(hyre_index* ix, uint32_t max_batch, hyre_execut
 }
 
 void hyre_executor_destroy(hyre_executor* ex) { delete ex; }
+
+hyre_status hyre_pool_create(hyre_index* ix, uint32_t workers, uint32_t max_batch, uint32_t max_wait_us,
+                             hyre_pool** out) {
+  return guard([&] {
+    need(ix, "index");
+    need(out, "out");
+    *out = new hyre_pool{std::unique_ptr<Pool>(new Pool(ix->ix.get(), workers, max_batch, max_wait_us))};
+  });
+}
+
+void hyre_pool_destroy(hyre_pool* p) { delete p; }
+
+hyre_status hyre_pool_search(hyre_pool* p, const hyre_query* q, hyre_hit* hits, uint32_t* n_hits) {
+  return guard([&] {
+    need(p, "pool");
+    need(q, "query");
+    p->p->search(*q, hits, n_hits);
+  });
+}
+
+hyre_status hyre_pool_stats(const hyre_pool* p, uint64_t* batches, uint64_t* queries) {
+  return guard([&] {
+    need(p, "pool");
+    p->p->stats(batches, queries);
+  });
+}
 void* hyre_executor_stream(hyre_executor* ex) { return ex ? ex->ex->st : nullptr; }
 
 hyre_status hyre_execute(hyre_executor* ex, const hyre_query* q, hyre_hit* hits, uint32_t* n_hits,

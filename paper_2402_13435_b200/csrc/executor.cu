@@ -310,6 +310,8 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // the dense sample buffer holds kSampleRows rows per query
   const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
   period = std::max(period, (n_seg + kSampleRows / kSegRows - 1) / (kSampleRows / kSegRows));
+  if (const char* e = std::getenv("HYRE_SAMPLE_PERIOD"))  // profiling: a sparser sample
+    period = std::max(period, static_cast<uint32_t>(std::atoi(e)));
   if (!(any_emb && ix->has_tc && b >= kTcMinBatch)) {
     // CUDA-core path (K2): its warps absorb a few thousand appends per query,
     // so a smaller sample (~16 segments, ~max(16K, 32k) rows) suffices and the

@@ -14,7 +14,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
 
 struct Executor {
   static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
-  static constexpr uint32_t kSampleRows = 128 * 1024;  // dense sample slots per query
+  static constexpr uint32_t kSampleRows = 40 * 1024;  // dense sample slots per query (~40K sampled rows: measured optimum at c3)
   static constexpr uint32_t kFwdMinBatch = 9;          // batches above 8 queries use K1b
 
   DevIndex* ix;

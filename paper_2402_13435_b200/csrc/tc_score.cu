@@ -31,7 +31,11 @@ namespace {
 
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
-constexpr uint32_t kStageBytes = 32768;           // per-CTA candidate staging: Np queries x (32 KB / 8 Np) keys
+// per-CTA candidate staging: 32 KB for groups of <= 64 queries (64 keys per
+// query), 8 KB for 128-query groups (8 keys per query; overflow goes straight
+// to the global buffer) so that their larger query tile still leaves >= 4 ring
+// stages in flight
+__host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 32768u : 8192u; }
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
 constexpr uint32_t kCnfWarps = 4;                 // fused CNF: one thread per tile row
 constexpr uint32_t kTermSlots = 2;                // fused CNF: tiles of row term lists in flight
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   uint32_t* s_tmem = s_tr + Np;                                // TMEM base
   uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
   // per-CTA candidate staging shared by the epilogue warps: [Np][kst] keys + [Np] counts
-  const uint32_t kst = kStageBytes / (8 * Np);
+  const uint32_t kst = stage_bytes_for(Np) / (8 * Np);
   uint32_t* s_scnt = s_act + 8;
   uint8_t* after_cnt = reinterpret_cast<uint8_t*>(s_scnt + Np);
   uint64_t* s_skey = reinterpret_cast<uint64_t*>(after_cnt + ((16u - (smem_u32(after_cnt) & 15u)) & 15u));
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   // barriers, then the tables: per term entry {users[NCH], hc of its
   // slot[NCH]} for T terms + sentinel, hc [C][NCH], live [NCH] + constrained
   // slots, slot of term [T + 1]
-  uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + kStageBytes;
+  uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + stage_bytes_for(Np);
   uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
   const uint32_t term_tile_bytes = kTileRows * a.A * 2;
   uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? kTermSlots * term_tile_bytes : 0u));
@@ -645,7 +649,7 @@ uint32_t tc_tmem_cols(uint32_t Np) {
 
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes) {
   return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
-         4 + 32 + Np * 4 + 16 + kStageBytes + 64 + fused_bytes;
+         4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes;
 }
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }

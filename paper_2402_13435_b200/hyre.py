@@ -622,6 +622,46 @@ class Executor:
         return [by_row[int(r)] for r in out[: cnt.value]]
 
 
+class ExecutorPool:
+    """The B200 ExecutorPool (service.cpp:99-141, ServiceConfig workers /
+    max_batch, service.hpp:19-26) with dynamic request batching: `workers`
+    executors, each with its own CUDA stream; concurrent search() calls are
+    grouped into execute_batch calls of up to max_batch queries, waiting at
+    most max_wait_us for a batch to fill.  search() is thread-safe (the ctypes
+    call releases the GIL) and returns what Executor.execute would."""
+
+    def __init__(self, index, workers: int = 2, max_batch: int = 16, max_wait_us: int = 200, device: int = 0,
+                 dtype: str = "f32", tensor_path: bool = True):
+        self._dev = index if isinstance(index, DeviceIndex) else index.device(device, dtype, tensor_path)
+        self._index = self._dev.frozen
+        h = C.c_void_p()
+        _check(L.lib().hyre_pool_create(self._dev._h, workers, max_batch, max_wait_us, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().hyre_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def search(self, query: HybridQuery) -> TopKResult:
+        pack = QueryPack([query])
+        cap = max(1, min(max(query.k, 1), self._index.num_docs()))
+        hits = (hyre_hit * cap)()
+        n = C.c_uint32()
+        _check(L.lib().hyre_pool_search(self._h, C.byref(pack.arr[0]), hits, C.byref(n)))
+        return TopKResult([ScoredDoc(self._index.doc_id(h.row), int(h.row), float(np.float32(h.score)))
+                           for h in hits[: n.value]])
+
+    def stats(self) -> tuple:
+        """(batches run, queries served)."""
+        b, q = C.c_uint64(), C.c_uint64()
+        _check(L.lib().hyre_pool_stats(self._h, C.byref(b), C.byref(q)))
+        return int(b.value), int(q.value)
+
+
 # Free functions over a per-index default executor (pipeline.hpp:98-100 and
 # the public stage functions the reference's tests call directly).
 def _default_executor(index: FrozenIndex, max_batch: int = 1) -> Executor:

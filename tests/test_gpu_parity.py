@@ -516,3 +516,49 @@ def test_fused_cnf_eligibility_bitexact(hy, B):
         gr, gs = hits(o.result)
         assert np.array_equal(gr, e), (len(gr), len(e))
         assert np.all(gs == gs[0]) if len(gs) else True
+
+
+def test_executor_pool_batches_concurrent_requests(hy):
+    # the ExecutorPool replacement groups concurrent single-query
+    # requests into batches; every caller gets the oracle's answer for its own
+    # query, and a malformed request fails alone (service.cpp:219-225).
+    import threading
+    from paper_2402_13435_b200 import workloads as W
+    w, prod, ref = _cnf_index(hy, 70_000, 128, 4, 6, 3, 5)
+    raws, qemb = W.queries(W.Workload("q", 0, 128, 4, 6, 2, 3, 10, 40, "cnf", qseed=19), 40)
+    pool = hy.ExecutorPool(prod, workers=2, max_batch=16, max_wait_us=5000)
+    queries = []
+    for i, raw in enumerate(raws):
+        clauses = [] if i % 7 == 0 else O.normalize_query(raw, 4)
+        queries.append(hy.HybridQuery(to_cnf(clauses), qemb[i], [10, 100, 3][i % 3],
+                                      hy.ExecOptions(quant_enabled=False)))
+    bad = hy.HybridQuery(to_cnf([]), qemb[0], 0)  # k = 0
+    results, errors = [None] * len(queries), []
+    barrier = threading.Barrier(len(queries) + 1)
+
+    def worker(i):
+        barrier.wait()
+        results[i] = pool.search(queries[i])
+
+    def bad_worker():
+        barrier.wait()
+        try:
+            pool.search(bad)
+        except hy.ValidationError as e:
+            errors.append(str(e))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(queries))]
+    threads.append(threading.Thread(target=bad_worker))
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == ["k must be >= 1"]
+    batches, served = pool.stats()
+    assert served == len(queries) + 1 and batches < served  # requests were batched
+    for q, r in zip(queries, results):
+        clauses = [(c.slot, c.attribute_ids) for c in q.terms.clauses]
+        er, es = O.execute(ref, clauses, q.embedding, q.k, quant_enabled=False)
+        gr, gs = hits(r)
+        assert_topk_match(ref, q.embedding, gr, gs, er, es)
+    pool.close()

@@ -318,6 +318,8 @@ def run_ours(args, w):
             check(lib.hyre_batch_fetch(h, host_hits, offs.ctypes.data_as(L.u64p), counts.ctypes.data_as(L.u32p),
                                        sts.ctypes.data_as(L.i32p), None))
 
+    if os.environ.get("HYRE_TC_DEBUG"):  # diagnostics runs: results are invalid, device timings only
+        e2e_call = lambda: check(lib.hyre_batch_run(h))  # noqa: E731
     e2e_call()
     # host-side cost of one prepare (validation, program build, packed H2D enqueue)
     t0 = time.perf_counter()

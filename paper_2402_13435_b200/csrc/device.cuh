@@ -113,13 +113,15 @@ struct DevIndex {
   uint64_t seed = 0;
   float* emb_f32 = nullptr;
   __nv_bfloat16* emb_hi = nullptr;  // bf16 index: RNE rows, row-major (K2 / gather path)
-  // Tensor-core tiles (K3): per 128-row tile t, K-atom k (64 elements), op o
-  // (0 = hi, 1 = lo for an fp32 index) a 16 KB block at
-  // ((t * kb + k) * tc_ops + o) * 16 KB holding the 128 x 128-byte atom in the
-  // UMMA canonical K-major SWIZZLE_128B layout (16-byte chunk c of row r at
-  // chunk c ^ (r % 8)); tail rows zero.  One cp.async.bulk of tc_ops * 16 KB
-  // fills a pipeline stage.
+  // Tensor-core tiles (K3): plane o (0 = hi, 1 = lo for an fp32 index) at
+  // o * tc_plane_bytes; within a plane, per 128-row tile t and K-atom k (64
+  // elements) a 16 KB block at (t * kb + k) * 16 KB holding the 128 x 128-byte
+  // atom in the UMMA canonical K-major SWIZZLE_128B layout (16-byte chunk c of
+  // row r at chunk c ^ (r % 8)); tail rows zero.  A pipeline stage is one
+  // cp.async.bulk per plane; the prefilter streams the hi plane alone
+  // (contiguous, so its DRAM pattern is a plain sequential scan).
   uint8_t* tc_tiles = nullptr;
+  uint64_t tc_plane_bytes = 0;
   uint32_t tc_ops = 0;
   uint64_t* sigs = nullptr;
   uint32_t* bitmaps = nullptr;

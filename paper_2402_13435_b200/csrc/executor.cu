@@ -50,6 +50,15 @@ bool fused_enabled() {
   }();
   return v;
 }
+// HYRE_PREFILTER=0 disables the K3 bf16 prefilter + exact rescore (the K3
+// pass then reads the full hi/lo split and scores at fp32 grade directly).
+bool prefilter_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_PREFILTER");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 // HYRE_MASK_PATH=bitmap|fwd forces the K1 / K1b choice (tests, profiling).
 int mask_path() {
   static const int v = [] {
@@ -268,6 +277,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     refs[r] = ref_src[r].first == 0 ? ix->bitmaps + size_t{ref_src[r].second} * W
                                     : d_scratch + size_t{ref_src[r].second} * W;
   use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
+  prefilter = use_tc && prefilter_enabled();
   if (use_tc) {
     tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
     tc_groups = (b + tc_np - 1) / tc_np;
@@ -278,10 +288,10 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   use_fused = false;
   if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31) {
-    fz_smem = tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->row_terms_width);
     const size_t kb = ix->dp / 64;
-    use_fused = tc_smem_bytes(tc_np, kb, ix->tc_ops, 3, fz_smem) <= 227 * 1024;
+    use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024;
   }
+  if (use_tc) plan_tc();
   if (use_fused) {
     build_fused_program();
   } else if (use_fwd && mask_path() != 2) {
@@ -409,15 +419,9 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   if (use_tc) {
     const uint32_t n_tiles = (ix->n_rows + 127) / 128;
     const uint32_t kb = ix->dp / 64;
-    const uint32_t n_ops = ix->tc_ops;
-    const size_t q_bytes = 2ull * tc_np * 128 * kb;
-    const size_t stage_bytes = size_t{n_ops} * 128 * 128;  // one K atom (hi [+ lo]) of a 128-row tile
-    const size_t fzb = use_fused ? fz_smem : 0;
-    const size_t fixed = tc_smem_bytes(tc_np, kb, n_ops, 0, fzb);
-    const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
-    uint32_t stages = static_cast<uint32_t>(std::max<size_t>(2, std::min<size_t>(12, budget / stage_bytes)));
-    if (const char* e = std::getenv("HYRE_TC_STAGES"))  // profiling: cap the ring depth
-      stages = std::max(2u, std::min<uint32_t>(stages, static_cast<uint32_t>(std::atoi(e))));
+    const uint32_t n_ops = tc_load_ops();
+    const uint32_t stages = tc_stages;
+    const size_t fzb = use_fused ? tc_fz_bytes(tc_term_slots) : 0;
     const uint32_t cols = tc_tmem_cols(tc_np);
     uint32_t work = n_tiles;
     if (mode == SCORE_SAMPLE) {
@@ -427,8 +431,13 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     const uint32_t grid = std::max(1u, std::min(work, 148u));
     for (uint32_t g = 0; g < tc_groups; ++g) {
       TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
-                ix->tc_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
+                n_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
                 rerun, d_samp, tc_debug_flags()};
+      ta.prefilter = prefilter ? 1u : 0u;
+      ta.plane_bytes = ix->tc_plane_bytes;
+      ta.delta = kPrefilterDelta;
+      ta.term_slots = tc_term_slots;
+      ta.aps = tc_aps;
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
@@ -442,7 +451,8 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
         ta.hc_off = fg.hc - fg.entries;
         ta.live_off = ta.hc_off + ix->num_clauses * tc_fused_chunks(tc_np);
       }
-      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages, fzb), st);
+      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages, fzb, tc_q_planes(), tc_aps),
+                      st);
       ++kernels;
     }
     return;
@@ -458,6 +468,75 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   while (sa.split < 32 && n_seg * sa.split < 148u * 64u) sa.split *= 2;
   while (sa.split_sample < 32 && n_samp_seg * sa.split_sample < 148u * 64u) sa.split_sample *= 2;
   launch_score(sa, bf16, st);
+  ++kernels;
+}
+
+// K3 shared-memory plan: the K-atom ring depth and (fused CNF) the depth of
+// the row-term ring.  The producer issues a tile's embedding stages only after
+// its term block, so the bytes in flight per SM are bounded by
+// min(term slots, stages / kb) tiles; the plan maximises that (Little's law:
+// ~150 KB in flight per SM sustain HBM rate at ~3 us loaded latency), then
+// prefers more stages.
+void Executor::plan_tc() {
+  const uint32_t kb = ix->dp / 64;
+  // Stage = aps K-atoms: the largest divisor of kb that still leaves a
+  // >= 3-stage ring, so each tile costs few MMA commits / barrier round trips
+  // (tcgen05.commit per stage was measured to pace the MMA issuer).
+  auto plan = [&](uint32_t aps, uint32_t slots) {
+    const size_t stage_bytes = size_t{tc_load_ops()} * aps * 128 * 128;
+    const size_t fixed = tc_smem_bytes(tc_np, kb, tc_load_ops(), 0, use_fused ? tc_fz_bytes(slots) : 0, tc_q_planes(), aps);
+    const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+    return static_cast<uint32_t>(std::min<size_t>(12, budget / stage_bytes));
+  };
+  uint32_t aps_max = kb;
+  if (const char* e = std::getenv("HYRE_TC_APS"))  // profiling: cap atoms per stage
+    aps_max = std::max(1u, std::min<uint32_t>(kb, static_cast<uint32_t>(std::atoi(e))));
+  tc_aps = 1;
+  for (uint32_t aps = aps_max; aps >= 1; --aps)
+    if (kb % aps == 0 && plan(aps, 2) >= 3) {
+      tc_aps = aps;
+      break;
+    }
+  const uint32_t spt = kb / tc_aps;  // stages per tile
+  // The producer issues a tile's stages only after its term block, so the
+  // tiles in flight are min(term slots, stages / spt): maximise that, then
+  // prefer more stages.
+  tc_term_slots = 2;
+  tc_stages = plan(tc_aps, 2);
+  if (use_fused) {
+    uint32_t best = std::min(2u, tc_stages / spt);
+    for (uint32_t slots = 3; slots <= kMaxTermSlots; ++slots) {
+      const uint32_t st_n = plan(tc_aps, slots);
+      const uint32_t depth = std::min(slots, st_n / spt);
+      if (st_n >= 2 && depth > best) {
+        best = depth;
+        tc_term_slots = slots;
+        tc_stages = st_n;
+      }
+    }
+  }
+  if (const char* e = std::getenv("HYRE_TC_TERM_SLOTS")) {  // profiling: fix the term ring depth
+    tc_term_slots = std::max(1u, std::min<uint32_t>(kMaxTermSlots, static_cast<uint32_t>(std::atoi(e))));
+    tc_stages = plan(tc_aps, tc_term_slots);
+  }
+  tc_stages = std::max(2u, tc_stages);
+  if (const char* e = std::getenv("HYRE_TC_STAGES"))  // profiling: cap the ring depth
+    tc_stages = std::max(2u, std::min<uint32_t>(tc_stages, static_cast<uint32_t>(std::atoi(e))));
+}
+
+size_t Executor::tc_fz_bytes(uint32_t slots) const {
+  return tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->row_terms_width, slots);
+}
+
+// K3 prefilter: exact scores for the candidates the pass admitted, and the
+// per-query count of rescored keys at or above the threshold.
+void Executor::rescore(uint64_t* cand, uint32_t* cnt, uint32_t* above) {
+  if (!prefilter) return;
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
+  HYRE_CUDA(cudaMemsetAsync(above, 0, sizeof(uint32_t) * B, st));
+  RescoreArgs ra{emb, ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q, cand, cnt, cap, B, d_thr, above};
+  launch_rescore(ra, bf16, st);
   ++kernels;
 }
 
@@ -618,6 +697,7 @@ void Executor::run() {
   uint32_t* samp_cnt = d_counters + 2 * max_batch;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
+  uint32_t* above = d_counters + 5 * max_batch;
   HYRE_CUDA(cudaEventRecord(ev[0], st));
   HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
   if (use_fused) {
@@ -664,7 +744,7 @@ void Executor::run() {
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       SelectArgs ka{nullptr, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
                     nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows,
-                    d_samp, ix->row_base, d_cand, cap};
+                    d_samp, ix->row_base, d_cand, cap, prefilter ? kPrefilterDelta : 0.0f, nullptr};
       launch_sample_kth(ka, samp_cnt, st);
       ++kernels;
     } else {
@@ -674,13 +754,16 @@ void Executor::run() {
     HYRE_CUDA(cudaEventRecord(ev[3], st));
     score(SCORE_MAIN, d_cand, cand_cnt, cap);
     HYRE_CUDA(cudaEventRecord(ev[4], st));
+    rescore(d_cand, cand_cnt, above);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
+    fa.above = prefilter ? above : nullptr;
     launch_select(fa, st);
     ++kernels;
     // One speculative recovery round: no-op unless a candidate buffer overflowed.
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
     score(SCORE_RERUN, d_cand, cand_cnt, cap);
+    rescore(d_cand, cand_cnt, above);
     fa.mode = SELECT_FINAL_RERUN;
     launch_select(fa, st);
     ++kernels;
@@ -712,8 +795,11 @@ void Executor::finish_reruns() {
     if (!any) return;
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
     score(SCORE_RERUN, d_cand, cand_cnt, cap);
+    uint32_t* above = d_counters + 5 * max_batch;
+    rescore(d_cand, cand_cnt, above);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
+    fa.above = prefilter ? above : nullptr;
     launch_select(fa, st);
   }
   throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");

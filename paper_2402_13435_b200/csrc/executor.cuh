@@ -13,7 +13,12 @@ namespace hyreb {
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
 
 struct Executor {
-  static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
+  static constexpr uint32_t kNumCounters = 6;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun, above
+  // K3 prefilter bound: |exact - prefilter score| for unit rows and queries.
+  // bf16 RNE of row and query: |e q - hi(e) hi(q)| <= (2^-8 + 2^-18)|e q| per
+  // element, summed <= 2^-8 (1 + 2^-10) |e| |q| (Cauchy-Schwarz); plus fp32
+  // accumulation (measured < 2e-5 at d = 128, here allowed 2.4e-4).
+  static constexpr float kPrefilterDelta = 1.0f / 256 + 1.0f / 4096;
   static constexpr uint32_t kSampleRows = 40 * 1024;  // dense sample slots per query (~40K sampled rows: measured optimum at c3)
   static constexpr uint32_t kFwdMinBatch = 9;          // batches above 8 queries use K1b
 
@@ -90,9 +95,14 @@ struct Executor {
   std::vector<uint32_t> fz_words;
   std::vector<uint32_t> fz_users, fz_touched;  // build_fused_program scratch
   uint32_t* d_fz = nullptr;
-  size_t fz_smem = 0;
   // tensor-core path (K3)
   bool use_tc = false;
+  bool prefilter = false;  // K3 reads the hi plane only; candidates rescored exactly (rescore())
+  uint32_t tc_load_ops() const { return prefilter ? 1u : ix->tc_ops; }
+  uint32_t tc_q_planes() const { return prefilter ? 1u : 2u; }
+  uint32_t tc_stages = 2, tc_term_slots = 2, tc_aps = 1;  // K3 ring depths, K atoms per stage (plan_tc)
+  void plan_tc();
+  size_t tc_fz_bytes(uint32_t term_slots) const;
   uint32_t tc_np = 0, tc_groups = 0;
   std::vector<uint16_t> qhi_h, qlo_h;
   CUtensorMap tm_qhi{}, tm_qlo{};
@@ -135,6 +145,7 @@ struct Executor {
   void build_forward_program();
   void build_fused_program();
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
+  void rescore(uint64_t* cand, uint32_t* cnt, uint32_t* above);
 };
 
 }  // namespace hyreb

@@ -89,7 +89,7 @@ __global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv
 
 // Writes the pre-swizzled tensor-core tiles (see DevIndex::tc_tiles): one
 // thread per 16-byte chunk (8 bf16) of the destination.
-__global__ void tile_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t kb, uint32_t ops, uint8_t* dst,
+__global__ void tile_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t kb, uint64_t plane_atoms, uint8_t* dst,
                             uint64_t n_chunks) {
   for (uint64_t ci = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; ci < n_chunks;
        ci += uint64_t{gridDim.x} * blockDim.x) {
@@ -97,8 +97,8 @@ __global__ void tile_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t 
     const uint32_t within = static_cast<uint32_t>(ci & 1023);
     const uint32_t rr = within >> 3, pc = within & 7;  // physical chunk pc of row rr
     const uint32_t lc = pc ^ (rr & 7);                 // logical 16-byte chunk (SWIZZLE_128B)
-    const uint32_t o = static_cast<uint32_t>(atom % ops);
-    const uint64_t tk = atom / ops;
+    const uint32_t o = static_cast<uint32_t>(atom / plane_atoms);  // plane: 0 = hi, 1 = lo
+    const uint64_t tk = atom % plane_atoms;
     const uint32_t k = static_cast<uint32_t>(tk % kb);
     const uint64_t row = (tk / kb) * 128 + rr;
     __align__(16) __nv_bfloat16 out[8];
@@ -181,9 +181,10 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       ix->tc_tiles = dmalloc<uint8_t>(tc_bytes);
       const uint64_t n_chunks = tc_bytes / 16;
       tile_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n_chunks + 255) / 256, 148 * 64)), 256, 0, st>>>(
-          f32, n, dp, kb, ops, ix->tc_tiles, n_chunks);
+          f32, n, dp, kb, n_tiles * kb, ix->tc_tiles, n_chunks);
       HYRE_CUDA(cudaGetLastError());
       ix->tc_ops = ops;
+      ix->tc_plane_bytes = n_tiles * kb * 16384;
       ix->has_tc = true;
       ix->stats.tensor_bytes = tc_bytes;
     }

@@ -654,6 +654,83 @@ void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st) {
   }
 }
 
+// Exact rescoring of K3 prefilter candidates (RescoreArgs).  LPR lanes per
+// row, CPL chunks per lane: the same per-lane fma chains as score_kernel and
+// a butterfly over the same lane pairs (xor LPR/2 .. 1), so the sums are
+// bit-identical to K2's reduce-scatter (fp32 addition is commutative).
+template <typename RowT, int LPR, int CPL>
+__global__ void __launch_bounds__(256) rescore_kernel(RescoreArgs a) {
+  constexpr int G = 32 / LPR;  // candidates per warp step
+  constexpr int E = Chunk<RowT>::kElems;
+  constexpr int U = 4;  // warp steps with loads in flight
+  const uint32_t q = blockIdx.y;
+  const uint32_t n = min(a.cnt[q], a.cap);
+  if (n == 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / LPR, li = lane % LPR;
+  float qv[CPL][E];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) qv[c][e] = a.q[static_cast<size_t>(q) * a.dp + (li + c * LPR) * E + e];
+  const uint64_t thr = a.thr[q];
+  uint64_t* keys = a.cand + static_cast<size_t>(q) * a.cap;
+  const RowT* emb = static_cast<const RowT*>(a.emb);
+  const uint32_t per_block = (blockDim.x >> 5) * U * G;
+  uint32_t mine = 0;
+  for (uint32_t base = blockIdx.x * per_block; base < n; base += gridDim.x * per_block) {
+    uint4 v[U][CPL];
+    uint32_t idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      idx[u] = base + (wib * U + u) * G + g;
+      const bool ok = idx[u] < n;
+      const uint32_t row = ok ? key_row(keys[idx[u]]) - a.row_base : 0u;
+      const RowT* r = emb + static_cast<size_t>(row) * a.dp;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[u][c] = ok ? ldg_stream(r + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[u][c], qv[c]);
+#pragma unroll
+      for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
+      if (li == 0 && idx[u] < n) {
+        const uint64_t key = make_key(clamp_score(acc), key_row(keys[idx[u]]));
+        keys[idx[u]] = key;
+        mine += key >= thr ? 1u : 0u;
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) mine += __shfl_xor_sync(kFull, mine, m);
+  if (lane == 0 && mine) atomicAdd(a.above + q, mine);
+}
+
+namespace {
+template <typename RowT>
+void dispatch_rescore(const RescoreArgs& a, dim3 grid, cudaStream_t st) {
+  const uint32_t cpr = a.dp_chunks;
+  if (cpr == 8) rescore_kernel<RowT, 8, 1><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 16) rescore_kernel<RowT, 16, 1><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 32) rescore_kernel<RowT, 32, 1><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 64) rescore_kernel<RowT, 32, 2><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 128) rescore_kernel<RowT, 32, 4><<<grid, 256, 0, st>>>(a);
+  else if (cpr == 256) rescore_kernel<RowT, 32, 8><<<grid, 256, 0, st>>>(a);
+  else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
+}
+}  // namespace
+
+void launch_rescore(const RescoreArgs& a, bool bf16, cudaStream_t st) {
+  if (a.B == 0) return;
+  // ~1K candidates per query at c3: 8 CTAs x 8 warps x 4 steps cover 256-1K per sweep
+  const dim3 grid(8, a.B);
+  if (bf16) dispatch_rescore<__nv_bfloat16>(a, grid, st);
+  else dispatch_rescore<float>(a, grid, st);
+}
+
 // ===========================================================================
 // K4: exact per-query selection over candidate keys (one CTA per query).
 // Radix select (12-bit digits from the top) finds the K-th largest key, the
@@ -854,7 +931,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     if (threadIdx.x == 0) {
       a.thr[q] = t_est;
-      if (a.thr_safe) a.thr_safe[q] = t_safe;
+      if (a.thr_safe) a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
     }
     return;
   }
@@ -876,7 +953,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     return;
   }
-  if (a.thr_safe && total < min(k, a.n_elig[q]) && a.thr[q] != a.thr_safe[q]) {
+  // (prefilter: candidates include rows below thr; count the rescored keys >= thr)
+  const uint32_t admitted = a.above ? a.above[q] : total;
+  if (a.thr_safe && admitted < min(k, a.n_elig[q]) && a.thr[q] != a.thr_safe[q]) {
     // The estimated threshold admitted fewer than K rows: rescore with the
     // guaranteed bound.
     if (threadIdx.x == 0) {
@@ -1040,7 +1119,7 @@ __global__ void __launch_bounds__(kSelThreads) sample_union_kernel(SelectArgs a,
   }
   if (threadIdx.x == 0) {
     a.thr[q] = t_est;
-    if (a.thr_safe) a.thr_safe[q] = t_safe;
+    if (a.thr_safe) a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
   }
 }
 

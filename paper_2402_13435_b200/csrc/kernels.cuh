@@ -85,6 +85,29 @@ struct ScoreArgs {
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 
+// ---- K3 prefilter companion: exact rescoring of the admitted candidates ----
+// Rewrites every candidate key of every query (cand[q][0 .. min(cnt, cap)))
+// with its exact score, computed with K2's arithmetic over the resident
+// row-major rows (fp32 rows, or the bf16 rows of a bf16 index) and the fp32
+// unit query, so a K3 batch returns the same scores as K2 / single queries.
+// above[q] += the number of rescored keys >= thr[q] (caller zeroes it).
+struct RescoreArgs {
+  const void* emb;
+  uint32_t dp, dp_chunks, row_base;
+  const float* q;  // [B][dp]
+  uint64_t* cand;
+  const uint32_t* cnt;
+  uint32_t cap, B;
+  const uint64_t* thr;
+  uint32_t* above;
+};
+void launch_rescore(const RescoreArgs& a, bool bf16, cudaStream_t st);
+// Largest key whose score is <= s - delta: a lower bound, in key space, for
+// every exact score of a row whose prefilter score was s (delta = the bound).
+__host__ __device__ __forceinline__ uint64_t key_minus_delta(uint64_t key, float delta) {
+  return key == 0ull ? 0ull : (static_cast<uint64_t>(f2ord(key_score(key) - delta)) << 32);
+}
+
 // ---- K4: per-query exact selection over candidate keys ----
 enum SelectMode : uint32_t { SELECT_KTH = 0, SELECT_FINAL = 1, SELECT_FINAL_RERUN = 2 };
 struct SelectArgs {
@@ -115,6 +138,11 @@ struct SelectArgs {
   uint32_t row_base;
   uint64_t* fb;     // KTH fallback scratch ([B][fb_cap] keys; the candidate buffer)
   uint32_t fb_cap;
+  // K3 prefilter: KTH lowers thr_safe by delta (the sample holds prefilter
+  // scores); FINAL decides "fewer than K admitted" from above[q] (rescored
+  // keys >= thr) instead of the candidate count.
+  float delta;
+  const uint32_t* above;
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
 // SELECT_KTH over the dense sample: per-slice top keys gathered into fb

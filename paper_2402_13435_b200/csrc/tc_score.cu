@@ -38,7 +38,6 @@ constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle
 __host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 32768u : 8192u; }
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
 constexpr uint32_t kCnfWarps = 4;                 // fused CNF: one thread per tile row
-constexpr uint32_t kTermSlots = 2;                // fused CNF: tiles of row term lists in flight
 constexpr uint32_t kAccBufs = 4;                  // TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
 constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight
 __host__ __device__ constexpr uint32_t threads_for(bool fused) {
@@ -87,17 +86,31 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 
 // K-major, 128-byte swizzle canonical layout: 8-row core groups 1024 B apart
 // (SBO = 64 x 16 B), LBO unused (1), descriptor version 1, layout type 2.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
-         (2ull << 61);
-}
-
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
           d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// The same with descriptors given as their low words (high word constant:
+// SBO = 1024 B, descriptor version 1, SWIZZLE_128B).
+__device__ __forceinline__ void mma_bf16w(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 da, db;\n setp.ne.b32 p, %4, 0;\n"
+      " mov.b64 da, {%1, %5};\n mov.b64 db, {%2, %5};\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(0x40004040));
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .b32 r;\n .reg .pred p;\n elect.sync r|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -245,13 +258,16 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   const uint32_t Np = a.Np, kb = a.kblocks, S = a.stages;
   const uint32_t q_box = Np * 128;  // bytes of one K-atom of the query tile
   const uint32_t q_bytes = q_box * kb;
-  const uint32_t a_bytes = kAtomBytes;  // one operand of one stage (one 128-byte K atom of 128 rows)
+  const uint32_t a_bytes = kAtomBytes;  // one 128-byte K atom of 128 rows of one plane
+  const uint32_t aps = a.aps;           // K atoms per pipeline stage (kb % aps == 0)
   const uint32_t n_ops = a.split ? 2 : 1;
-  // smem carve-up
+  const uint32_t st_bytes = n_ops * aps * a_bytes;  // stage: [hi atoms][lo atoms]
+  const uint32_t TS = a.term_slots;  // fused CNF: tiles of row term lists in flight
+  // smem carve-up (the prefilter uses Q_hi only: no Q_lo tile)
   uint8_t* s_qhi = smem;
   uint8_t* s_qlo = s_qhi + q_bytes;
-  uint8_t* s_stage = s_qlo + q_bytes;  // [S][n_ops][16 KB]: ring of K-atom stages, kb per tile
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + size_t{S} * n_ops * a_bytes);
+  uint8_t* s_stage = s_qlo + (a.prefilter ? 0u : q_bytes);  // [S][n_ops][aps][16 KB]: ring of stages, kb / aps per tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + size_t{S} * st_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -266,7 +282,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   uint32_t* s_scnt = s_act + 8;
   uint8_t* after_cnt = reinterpret_cast<uint8_t*>(s_scnt + Np);
   uint64_t* s_skey = reinterpret_cast<uint64_t*>(after_cnt + ((16u - (smem_u32(after_cnt) & 15u)) & 15u));
-  // fused CNF: a ring of kTermSlots tiles of row term lists (bulk-copied by
+  // fused CNF: a ring of TS tiles of row term lists (bulk-copied by
   // the producer; 128 rows x A u16 each), a ring of kEligSlots tiles of
   // eligibility words ([NCH][128 rows] u32, written by the CNF warps), their
   // barriers, then the tables: per term entry {users[NCH], hc of its
@@ -275,11 +291,11 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + stage_bytes_for(Np);
   uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
   const uint32_t term_tile_bytes = kTileRows * a.A * 2;
-  uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? kTermSlots * term_tile_bytes : 0u));
+  uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? TS * term_tile_bytes : 0u));
   uint64_t* s_tbar = reinterpret_cast<uint64_t*>(s_elig + (kFused ? kEligSlots * NCH * kTileRows : 0u));
   uint64_t* ttfull = s_tbar;
-  uint64_t* ttempty = s_tbar + kTermSlots;
-  uint64_t* efull = s_tbar + 2 * kTermSlots;
+  uint64_t* ttempty = s_tbar + TS;
+  uint64_t* efull = s_tbar + 2 * TS;
   uint64_t* eempty = efull + kEligSlots;
   uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(eempty + kEligSlots);
   uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * 2 * NCH;
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
     }
     mbar_init(qbar, 1);
     if (kFused) {
-      for (uint32_t i = 0; i < kTermSlots; ++i) {
+      for (uint32_t i = 0; i < TS; ++i) {
         mbar_init(ttfull + i, 1);
         mbar_init(ttempty + i, kCnfWarps);
       }
@@ -326,9 +342,10 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       s_ts[j] = -2.0f;  // no threshold
       s_tr[j] = 0u;
     } else {
-      const float ts = key_score(thr);
+      // prefilter: admit s' >= ts - delta (a superset of exact score >= ts)
+      const float ts = key_score(thr) - (a.prefilter ? a.delta : 0.0f);
       s_ts[j] = ts <= -1.0f ? -2.0f : ts;
-      s_tr[j] = key_row(thr);
+      s_tr[j] = a.prefilter ? 0xFFFFFFFFu : key_row(thr);
     }
   }
   for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) s_scnt[j] = 0;
@@ -369,29 +386,33 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
-      mbar_expect_tx(qbar, 2 * q_bytes);
+      mbar_expect_tx(qbar, (a.prefilter ? 1 : 2) * q_bytes);
       for (uint32_t k = 0; k < kb; ++k) {
         tma_load_2d(s_qhi + k * q_box, &tm_qhi, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
-        tma_load_2d(s_qlo + k * q_box, &tm_qlo, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
+        if (!a.prefilter)
+          tma_load_2d(s_qlo + k * q_box, &tm_qlo, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
       }
       uint32_t s = 0, ph = 0;
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
         if (kFused) {  // the tile's row term lists (contiguous rows) into the term ring
-          const uint32_t ts = i % kTermSlots, tph = (i / kTermSlots) & 1;
+          const uint32_t ts = i % TS, tph = (i / TS) & 1;
           const uint32_t rows = min(kTileRows, a.n_rows - t * kTileRows);
           mbar_wait(ttempty + ts, tph ^ 1);
           mbar_expect_tx(ttfull + ts, rows * a.A * 2);
           bulk_load(s_terms + ts * term_tile_bytes, a.row_terms + static_cast<size_t>(t) * kTileRows * a.A,
                     rows * a.A * 2, ttfull + ts);
         }
-        for (uint32_t k = 0; k < kb; ++k) {
+        for (uint32_t k = 0; k < kb; k += aps) {
           mbar_wait(empty + s, ph ^ 1);
-          mbar_expect_tx(full + s, n_ops * a_bytes);
-          // one contiguous, pre-swizzled K-atom (hi [+ lo]) per stage
-          bulk_load(s_stage + size_t{s} * n_ops * a_bytes,
-                    a.tiles + (static_cast<size_t>(t) * kb + k) * n_ops * a_bytes, n_ops * a_bytes, full + s);
+          mbar_expect_tx(full + s, st_bytes);
+          // aps pre-swizzled K-atoms per plane (hi [+ lo]) per stage, one
+          // bulk copy per plane (a tile's atoms are contiguous in a plane)
+          const uint8_t* src = a.tiles + (static_cast<size_t>(t) * kb + k) * a_bytes;
+          bulk_load(s_stage + size_t{s} * st_bytes, src, aps * a_bytes, full + s);
+          if (n_ops == 2)
+            bulk_load(s_stage + size_t{s} * st_bytes + aps * a_bytes, src + a.plane_bytes, aps * a_bytes, full + s);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -400,45 +421,50 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (one thread) =====
-    if (lane == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((Np >> 3) << 17) | ((kTileRows >> 4) << 24);
-      mbar_wait(qbar, 0);
+    // ===== MMA issuer: the whole warp walks the rings, one elected lane
+    // issues.  Descriptors are built from warp-uniform 32-bit words (low word
+    // = start address >> 4 | LBO 1; high word = SBO 64 | version 1 | SW128),
+    // so a K-step is one add per operand and the tcgen05.mma itself.
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((Np >> 3) << 17) | ((kTileRows >> 4) << 24);
+    const uint32_t a_lo0 = (smem_u32(s_stage) >> 4) | 0x10000u;
+    const uint32_t qh_lo0 = (smem_u32(s_qhi) >> 4) | 0x10000u, ql_lo0 = (smem_u32(s_qlo) >> 4) | 0x10000u;
+    const uint32_t nkk = (a.debug & 16u) ? 1u : 4u;  // debug bit4: one K16 step per atom (timing only)
+    mbar_wait(qbar, 0);
+    fence_after();
+    uint32_t s = 0, ph = 0;
+    for (uint32_t i = 0;; ++i) {
+      const uint32_t t = tile_of(a, i);
+      if (t == UINT32_MAX) break;
+      const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
+      if (!(a.debug & 8u)) mbar_wait(tempty + acc, aph ^ 1);  // debug bit3: ignore the accumulator ring
       fence_after();
-      uint32_t s = 0, ph = 0;
-      for (uint32_t i = 0;; ++i) {
-        const uint32_t t = tile_of(a, i);
-        if (t == UINT32_MAX) break;
-        const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
-        mbar_wait(tempty + acc, aph ^ 1);
+      const uint32_t d = tmem + acc * Np;
+      for (uint32_t k0 = 0; k0 < kb; k0 += aps) {
+        mbar_wait(full + s, ph);
         fence_after();
-        const uint32_t d = tmem + acc * Np;
-        uint32_t accum = 0;
-        for (uint32_t k = 0; k < kb; ++k) {
-          mbar_wait(full + s, ph);
-          fence_after();
-          const uint8_t* st = s_stage + size_t{s} * n_ops * a_bytes;
+        if (elect_one()) {
+          const uint32_t st_lo = a_lo0 + ((s * st_bytes) >> 4);
+          for (uint32_t k = 0; k < aps && !(a.debug & 1u); ++k) {
+            const uint32_t ka = st_lo + ((k * a_bytes) >> 4), kq = ((k0 + k) * q_box) >> 4;
 #pragma unroll
-          for (uint32_t kk = 0; kk < 4 && !(a.debug & 1u); ++kk) {  // 4 x K16 per 128-byte atom
-            const uint64_t ahi = sw128_desc(smem_u32(st + kk * 32));
-            const uint64_t qhi = sw128_desc(smem_u32(s_qhi + k * q_box + kk * 32));
-            const uint64_t qlo = sw128_desc(smem_u32(s_qlo + k * q_box + kk * 32));
-            mma_bf16(d, ahi, qhi, idesc, accum);
-            accum = 1;
-            mma_bf16(d, ahi, qlo, idesc, 1);
-            if (a.split) {
-              const uint64_t alo = sw128_desc(smem_u32(st + a_bytes + kk * 32));
-              mma_bf16(d, alo, qhi, idesc, 1);
+            for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K16 per 128-byte atom (+32 B = +2 per step)
+              if (kk >= nkk) break;
+              const uint32_t acc_in = (k0 + k + kk) != 0;
+              mma_bf16w(d, ka + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, acc_in);
+              if (!a.prefilter) mma_bf16w(d, ka + 2 * kk, ql_lo0 + kq + 2 * kk, idesc, 1u);
+              if (a.split) mma_bf16w(d, ka + ((aps * a_bytes) >> 4) + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, 1u);
             }
           }
-          mma_commit(empty + s);  // this K-atom stage is free once its MMAs retire
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
-          }
+          mma_commit(empty + s);  // this stage is free once its MMAs retire
         }
-        mma_commit(tfull + acc);  // accumulator ready for the epilogue
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) mma_commit(tfull + acc);  // accumulator ready for the epilogue
+      __syncwarp();
     }
   } else if (warp < 2 + kEpiWarps) {
     // ===== epilogue: TMEM -> registers -> mask / clamp / threshold -> candidates =====
@@ -540,6 +566,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
           const uint32_t j = __ffs(tk) - 1, qq = c * 32 + j;
           const uint64_t key = make_key(clamp_score(__uint_as_float(pick32(v, j))), grow);
           if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
+                                                                        // (prefilter: s_tr = ~0, never)
           const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
           if (slot < kst) {
             s_skey[qq * kst + slot] = key;
@@ -576,7 +603,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
     for (uint32_t i = 0;; ++i) {
       const uint32_t t = tile_of(a, i);
       if (t == UINT32_MAX) break;
-      const uint32_t ts = i % kTermSlots, tph = (i / kTermSlots) & 1;
+      const uint32_t ts = i % TS, tph = (i / TS) & 1;
       mbar_wait(ttfull + ts, tph);
       uint32_t tw[16];
       const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.A * 2;
@@ -588,8 +615,13 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(ttempty + ts);
       uint32_t el[NCH];
-      cnf_row<NCH, (kFused ? NA : 1)>(tw, a.T, smem_u32(s_ftbl), smem_u32(s_fslot), smem_u32(s_fhc),
-                                       smem_u32(s_flive), cslots, el);
+      if (a.debug & 4u) {  // diagnostics: no CNF evaluation (every live query eligible)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) el[c] = s_flive[c] ^ (tw[0] & 1u);
+      } else {
+        cnf_row<NCH, (kFused ? NA : 1)>(tw, a.T, smem_u32(s_ftbl), smem_u32(s_fslot), smem_u32(s_fhc),
+                                         smem_u32(s_flive), cslots, el);
+      }
       if (t * kTileRows + r >= a.n_rows) {  // tail of the last tile
 #pragma unroll
         for (int c = 0; c < NCH; ++c) el[c] = 0u;
@@ -647,17 +679,18 @@ uint32_t tc_tmem_cols(uint32_t Np) {
   return cols;
 }
 
-size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes) {
-  return 1024 + 2ull * Np * 128 * kb + size_t{stages} * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
+size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes, uint32_t q_planes,
+                     uint32_t aps) {
+  return 1024 + size_t{q_planes} * Np * 128 * kb + size_t{stages} * aps * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
          4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes;
 }
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }
 
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A) {
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
-  return 128 + size_t{kTermSlots} * kTileRows * A * 2 + size_t{kEligSlots} * nch * kTileRows * 4 +
-         16 * (kTermSlots + kEligSlots) + 4 * ((T + 1) * 2 * nch + C * nch + nch + 1) + T + 1 + 16;
+  return 128 + size_t{term_slots} * kTileRows * A * 2 + size_t{kEligSlots} * nch * kTileRows * 4 +
+         16 * (term_slots + kEligSlots) + 4 * ((T + 1) * 2 * nch + C * nch + nch + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,

@@ -25,7 +25,7 @@ struct TcArgs {
   uint32_t cap, mode, period, gate;
   const uint32_t* rerun;
   uint32_t* samp;  // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
-  uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work (results invalid)
+  uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work, bit2 skip CNF (results invalid)
   // Fused CNF (fused != 0, mask unused): dedicated warps evaluate each row's
   // eligibility from its forward term list (row_terms, slot-major, 0xFFFF
   // padded to A) against this group's program, scattered into shared memory:
@@ -39,15 +39,28 @@ struct TcArgs {
   uint32_t A, T, C;
   const uint32_t* fz;
   uint32_t n_entries, hc_off, live_off;
+  // Prefilter mode (prefilter != 0): only the hi plane of each K-atom is
+  // loaded and one MMA E_hi.Q_hi
+  // per K-step computes s' with |s - s'| <= delta for unit rows and queries
+  // (bf16 RNE of both operands: 2^-8 relative, Cauchy-Schwarz); rows are
+  // admitted when s' >= thr_score - delta and rescored exactly afterwards
+  // (launch_rescore), so no row whose exact score passes the threshold is lost.
+  uint32_t prefilter;
+  uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
+  float delta;
+  uint32_t aps;         // K atoms per pipeline stage (divides kblocks; one MMA commit per stage)
+  uint32_t term_slots;  // fused CNF: tiles of row term lists in flight (ring depth, <= kMaxTermSlots)
 };
 
 constexpr uint32_t kTcMinBatch = 9;  // batches above 8 queries use the tensor-core scorer
 constexpr uint32_t kTcMaxGroup = 128;
 
 void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
-size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0);
+size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0,
+                     uint32_t q_planes = 2, uint32_t aps = 1);
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A);
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A, uint32_t term_slots);
+constexpr uint32_t kMaxTermSlots = 8;
 // TMEM columns for the accumulator buffers of a group of Np queries
 uint32_t tc_tmem_cols(uint32_t Np);
 // query chunks of a fused group as laid out in its program (1, 2 or 4)

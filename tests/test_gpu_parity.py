@@ -562,3 +562,62 @@ def test_executor_pool_batches_concurrent_requests(hy):
         gr, gs = hits(r)
         assert_topk_match(ref, q.embedding, gr, gs, er, es)
     pool.close()
+
+
+# ---------------------------------------------------------------- K3 prefilter + exact rescore
+def _singles(hy, ex, batch):
+    return [[(h.row_id, h.score) for h in ex.execute(q).hits] for q in batch.queries]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_tensor_core_batch_equals_single_queries_exactly(hy, dtype):
+    # Batches > 8 run K3, which admits rows on a bf16 prefilter score and
+    # rescores the admitted rows with K2's exact arithmetic; single queries
+    # run K2.  Batch transparency (test_pipeline.cpp:237-275) is therefore
+    # exact -- identical rows AND scores -- for tensor-core batches too.
+    from paper_2402_13435_b200 import workloads as W
+    w, prod, ref = _cnf_index(hy, 70_000, 128, 4, 6, 3, 5)
+    ex = hy.Executor(prod.device(0, dtype), max_batch=64)
+    raws, qemb = W.queries(W.Workload("q", 0, 128, 4, 6, 2, 3, 10, 64, "cnf", qseed=21), 64)
+    batch = hy.BatchRequest()
+    for i, raw in enumerate(raws):
+        clauses = [] if i % 5 == 0 else O.normalize_query(raw, 4)
+        batch.queries.append(hy.HybridQuery(to_cnf(clauses), qemb[i], [10, 100, 1, 257][i % 4],
+                                            hy.ExecOptions(quant_enabled=False)))
+    outs = ex.execute_batch(batch)
+    for o, s in zip(outs, _singles(hy, ex, batch)):
+        assert o.ok
+        assert [(h.row_id, h.score) for h in o.result.hits] == s
+
+
+def test_prefilter_keeps_exact_order_among_bf16_indistinguishable_rows(hy):
+    # Rows differ from a common direction by ~1e-3, so their exact scores are
+    # distinct while most bf16 prefilter scores coincide: the K-th exact
+    # score sits inside a band of thousands of prefilter ties.  The admitted
+    # set (prefilter >= threshold - delta) must still contain the exact top-K,
+    # and the rescored result must equal the exact single-query (K2) answer
+    # and the oracle's.
+    n, dim = 60_000, 64
+    rs = np.random.default_rng(3)
+    base = rs.standard_normal(dim).astype(np.float32)
+    emb = (base[None, :] + 1e-3 * rs.standard_normal((n, dim))).astype(np.float32)
+    b = hy.IndexBuilder(hy.IndexConfig(1, 1, dim))
+    b.add_documents(np.arange(n + 1, dtype=np.uint64), np.ones(n, np.uint32), emb)
+    prod = b.freeze(hy.make_codec(dim, 64, 1))
+    ref = O.Frozen(n, 1, 1, dim, 64, 1, np.array(prod.attributes), np.array(prod.offsets),
+                   np.array(prod.embeddings), np.array(prod.signatures), np.array(prod.zero_flags))
+    ex = hy.Executor(prod, max_batch=16)
+    batch = hy.BatchRequest()
+    for i in range(16):
+        q = (base + 0.02 * rs.standard_normal(dim)).astype(np.float32)
+        batch.queries.append(hy.HybridQuery(hy.CnfQuery(), q, [100, 7, 1000, 1][i % 4],
+                                            hy.ExecOptions(quant_enabled=False)))
+    outs = ex.execute_batch(batch)
+    rows = np.arange(n)
+    for q, o, s in zip(batch.queries, outs, _singles(hy, ex, batch)):
+        assert o.ok
+        assert [(h.row_id, h.score) for h in o.result.hits] == s
+        qq, _ = O.unit_embedding(q.embedding)
+        er, es = O.top_k(rows, O.scores_rows(ref.embeddings, qq, rows), q.k)
+        gr, gs = hits(o.result)
+        assert_topk_match(ref, q.embedding, gr, gs, er, es)

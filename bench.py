@@ -349,9 +349,11 @@ def run_ours(args, w):
     n_local = re_ - rb
     elem = 2 if w.dtype == "bf16" else 4
     # algorithmic bytes of the dominant kernel's launch:
-    #  K3 (batched): every row of the shard once (bf16 hi+lo split = 4 B/elem
-    #     for an fp32 index) + its eligibility input (the forward term lists
-    #     when the CNF is fused into K3, else the B mask bitmaps K1 wrote);
+    #  K3 (batched): per query group, every row of the shard once -- the
+    #     bf16 hi plane (prefilter; exact rescoring of the admitted rows is a
+    #     separate small kernel) or hi + lo -- + its eligibility input (the
+    #     compact CNF rows when the CNF is fused into K3, else the mask words
+    #     K1 wrote), as the executor reports it (hyre_batch_scan_bytes);
     #  K2 (B <= 8): only eligible rows are loaded: U = the largest per-query
     #     eligible count (a lower bound on the union it streams) + the masks;
     #  K1 (term-only batches): distinct term bitmaps + CSR postings + mask writes.
@@ -364,7 +366,7 @@ def run_ours(args, w):
         bytes_main = int(lib.hyre_batch_term_bytes(h)) + B * words * 4
         main_avg = statistics.median(r[0] for r in stage_rows)
     elif path & 1:
-        bytes_main = n_local * w.dim * elem + (int(lib.hyre_batch_term_bytes(h)) if fused else B * words * 4)
+        bytes_main = int(lib.hyre_batch_scan_bytes(h))
     else:
         elig = np.zeros(B, np.uint32)
         check(lib.hyre_batch_eligible(h, elig.ctypes.data_as(L.u32p)))
@@ -409,7 +411,8 @@ def run_ours(args, w):
 
 def main_kernel_name(B):
     if B > 8:
-        return "tc_score_kernel (K3: TMA -> tcgen05.mma bf16 hi/lo split, fp32 accumulation in TMEM)"
+        return ("tc_score_kernel (K3: bulk-copy ring -> tcgen05.mma, fp32 accumulation in TMEM; bf16 hi-plane "
+                "prefilter + fused CNF, admitted rows pruned + rescored exactly in select_prefilter_kernel)")
     return "score_kernel (K2, CUDA-core streaming scorer)"
 
 

@@ -263,6 +263,11 @@ hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out);
  * term bitmaps + CSR postings (K1), or the forward term lists once per pass
  * (K1b / fused K3). */
 uint64_t hyre_batch_term_bytes(const hyre_executor* ex);
+/* Algorithmic bytes the prepared batch's K3 main stage reads (all query
+ * groups): the embedding planes it streams (bf16 hi for the prefilter or a
+ * bf16 index, hi + lo otherwise) + the eligibility input (compact CNF rows
+ * when fused, else the K1 mask words); 0 when the batch runs on K2. */
+uint64_t hyre_batch_scan_bytes(const hyre_executor* ex);
 /* CUDA-event durations (ms) of the last run, waiting for it to finish:
  * [0] K1 mask (+CSR scatter) [1] K6 quant [2] sample pass + K-th select
  * [3] main scorer (K2/K3) [4] final select + first-K [5] whole run. */

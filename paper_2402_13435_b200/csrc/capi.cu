@@ -385,6 +385,7 @@ hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* 
 uint32_t hyre_batch_kernel_count(const hyre_executor* ex) { return ex ? ex->ex->kernels : 0; }
 
 uint64_t hyre_batch_term_bytes(const hyre_executor* ex) { return ex ? ex->ex->term_bytes : 0; }
+uint64_t hyre_batch_scan_bytes(const hyre_executor* ex) { return ex ? ex->ex->scan_bytes : 0; }
 
 hyre_status hyre_batch_eligible(hyre_executor* ex, uint32_t* out) {
   return guard([&] {

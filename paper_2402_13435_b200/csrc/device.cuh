@@ -135,6 +135,13 @@ struct DevIndex {
   uint16_t* row_terms = nullptr;
   uint8_t* slot_of = nullptr;
   uint32_t n_terms_fwd = 0, max_num_attr = 0, row_terms_width = 0;
+  // Compact CNF rows (K3 fused evaluator): cnf_ids[r * cnf_row_bytes ..] =
+  // the row's term ids as u8 (T <= 255) or u16, all-ones padded to
+  // cnf_ids_per_row ids (row width an odd multiple of 8 B); cnf_masks[r] =
+  // (slots present << 32) | segment starts (bit j: id j opens a new slot).
+  uint8_t* cnf_ids = nullptr;
+  uint64_t* cnf_masks = nullptr;
+  uint32_t cnf_id_bytes = 0, cnf_ids_per_row = 0, cnf_row_bytes = 0;
   Codec codec;
   hyre_index_stats stats{};
   ~DevIndex();

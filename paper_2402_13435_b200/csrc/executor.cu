@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -99,6 +100,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   d_thr_safe = dmalloc<uint64_t>(B);
   d_cand = dmalloc<uint64_t>(B * cap);
   d_samp = dmalloc<uint32_t>(B * samp_cap);
+  d_shist = dmalloc<uint32_t>(B * kHistBins);
   d_qhist = dmalloc<uint32_t>(B * (ix->num_bits + 1));
   d_tsel = dmalloc<uint32_t>(B * 3);
   d_eqcnt = dmalloc<uint32_t>(B * ix->n_chunks);
@@ -110,6 +112,7 @@ Executor::~Executor() {
   cudaSetDevice(ix->device);
   cudaStreamSynchronize(st);
   for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_thr_safe, (void*)d_cand,
+                  (void*)d_shist,
                   (void*)d_samp, (void*)d_qhist, (void*)d_tsel, (void*)d_eqcnt, (void*)d_blob,
                   (void*)d_hits, (void*)d_scratch})
     cudaFree(p);
@@ -287,7 +290,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // term tables fit next to a >= 3-stage ring.
   use_fused = false;
   if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
-      ix->num_clauses <= 31) {
+      ix->num_clauses <= 31 && ix->cnf_ids) {
     const size_t kb = ix->dp / 64;
     use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024;
   }
@@ -322,7 +325,16 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   period = std::max(period, (n_seg + kSampleRows / kSegRows - 1) / (kSampleRows / kSegRows));
   if (const char* e = std::getenv("HYRE_SAMPLE_PERIOD"))  // profiling: a sparser sample
     period = std::max(period, static_cast<uint32_t>(std::atoi(e)));
-  if (!(any_emb && ix->has_tc && b >= kTcMinBatch)) {
+  if (use_tc) {
+    // K3: the sample pass feeds per-query score histograms (no dense buffer),
+    // so it can afford ~kTcSampleSegs segments; a denser sample tightens the
+    // estimated threshold (~8 x period admitted rows per query)
+    uint32_t segs = kTcSampleSegs;
+    if (const char* e = std::getenv("HYRE_TC_SAMPLE_SEGS")) segs = std::max(1, std::atoi(e));
+    period = std::max<uint32_t>(1, (n_seg + segs - 1) / segs);
+    if (const char* e = std::getenv("HYRE_SAMPLE_PERIOD"))
+      period = std::max(period, static_cast<uint32_t>(std::atoi(e)));
+  } else if (!(any_emb && ix->has_tc && b >= kTcMinBatch)) {
     // CUDA-core path (K2): its warps absorb a few thousand appends per query,
     // so a smaller sample (~16 segments, ~max(16K, 32k) rows) suffices and the
     // K-th selection over it is cheap.
@@ -394,10 +406,23 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   h2d_bytes = off;
   // eligibility input bytes: distinct bitmaps W*4 each, CSR
   // postings 4 each; the forward lists N*A*2 once per pass on the fwd/fused paths
-  if (use_fused || use_fwd)
-    term_bytes = size_t{ix->n_rows} * ix->row_terms_width * 2 * (use_fused ? tc_groups : fwd_pass.size());
+  if (use_fused)
+    term_bytes = size_t{ix->n_rows} * (ix->cnf_row_bytes + 8) * tc_groups;  // compact CNF rows per group pass
+  else if (use_fwd)
+    term_bytes = size_t{ix->n_rows} * ix->row_terms_width * 2 * fwd_pass.size();
   else
     term_bytes = uint64_t{ix->words} * 4 * (ref_src.size() - n_scratch) + scatter_total * 4;
+  // K3 main stage (all groups): every row's embedding operand planes the pass
+  // reads (hi only for the prefilter / a bf16 index; hi + lo otherwise) plus
+  // its eligibility input (compact CNF rows when fused, else the group's K1
+  // mask words)
+  scan_bytes = 0;
+  if (use_tc) {
+    const uint64_t emb = uint64_t{ix->n_rows} * ix->dp * 2 * tc_load_ops();
+    const uint64_t elig = use_fused ? uint64_t{ix->n_rows} * (ix->cnf_row_bytes + 8)
+                                    : uint64_t{ix->words} * 4 * tc_np;
+    scan_bytes = (emb + elig) * tc_groups;
+  }
   d_qp = reinterpret_cast<QParam*>(d_blob + o_qp);
   d_q = reinterpret_cast<float*>(d_blob + o_q);
   d_qsig = reinterpret_cast<uint64_t*>(d_blob + o_qsig);
@@ -432,18 +457,24 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     for (uint32_t g = 0; g < tc_groups; ++g) {
       TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 n_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
-                rerun, d_samp, tc_debug_flags()};
+                rerun, d_samp};
+      ta.debug = tc_debug_flags();
       ta.prefilter = prefilter ? 1u : 0u;
       ta.plane_bytes = ix->tc_plane_bytes;
       ta.delta = kPrefilterDelta;
       ta.term_slots = tc_term_slots;
+      ta.shist = mode == SCORE_SAMPLE ? d_shist : nullptr;
+      ta.hbins = kHistBins;
       ta.aps = tc_aps;
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
-        ta.row_terms = ix->row_terms;
+        ta.cnf_ids = ix->cnf_ids;
+        ta.cnf_masks = ix->cnf_masks;
         ta.slot_of = ix->slot_of;
-        ta.A = ix->row_terms_width;
+        ta.J = ix->cnf_ids_per_row;
+        ta.tb = ix->cnf_id_bytes;
+        ta.wb = ix->cnf_row_bytes;
         ta.T = ix->n_terms_fwd;
         ta.C = ix->num_clauses;
         ta.fz = d_fz + fg.entries;
@@ -525,18 +556,23 @@ void Executor::plan_tc() {
 }
 
 size_t Executor::tc_fz_bytes(uint32_t slots) const {
-  return tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->row_terms_width, slots);
+  return tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->cnf_row_bytes, slots);
 }
 
-// K3 prefilter: exact scores for the candidates the pass admitted, and the
-// per-query count of rescored keys at or above the threshold.
-void Executor::rescore(uint64_t* cand, uint32_t* cnt, uint32_t* above) {
-  if (!prefilter) return;
+// Final K4 after a main / rerun pass: the prefilter variant (prune, exact
+// rescoring, threshold check, sort) for K3 prefilter candidates, else the
+// exact select_kernel.
+void Executor::final_select(SelectArgs fa) {
+  if (!prefilter) {
+    launch_select(fa, st);
+    ++kernels;
+    return;
+  }
   const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
-  const void* emb = bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32);
-  HYRE_CUDA(cudaMemsetAsync(above, 0, sizeof(uint32_t) * B, st));
-  RescoreArgs ra{emb, ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q, cand, cnt, cap, B, d_thr, above};
-  launch_rescore(ra, bf16, st);
+  fa.delta = kPrefilterDelta;
+  PrefSelectArgs pa{fa, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
+                    ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
+  launch_select_prefilter(pa, bf16, st);
   ++kernels;
 }
 
@@ -636,7 +672,8 @@ void Executor::build_forward_program() {
 }
 
 // Fused-CNF program per K3 query group (TcArgs::fz): for every term any
-// query of the group lists, its users words; per slot, the queries that
+// query of the group lists, v = hc(slot) & ~users (the queries constraining
+// the term's slot that do not list it); per slot, the queries that
 // constrain it; the live (active, satisfiable) queries; the constrained-slot
 // mask.  Word w holds query chunk w (queries 32w .. 32w + 31).
 void Executor::build_fused_program() {
@@ -645,6 +682,7 @@ void Executor::build_fused_program() {
   const uint32_t C = ix->num_clauses, fw = tc_fused_chunks(tc_np), T = ix->n_terms_fwd;
   // dense per-term users scratch (T <= kForwardMaxTerms), reset via the touched list
   if (fz_users.size() < size_t{T} * fw) fz_users.assign(size_t{T} * fw, 0u);
+  if (fz_slot.size() < T) fz_slot.assign(T, 0u);
   for (uint32_t g = 0; g < tc_groups; ++g) {
     fz_touched.clear();
     std::vector<uint32_t> hc(size_t{C} * fw, 0u), live(fw, 0u);
@@ -661,7 +699,10 @@ void Executor::build_fused_program() {
           uint32_t* u = fz_users.data() + size_t{t_ids[x]} * fw;
           bool fresh = true;
           for (uint32_t v = 0; v < fw; ++v) fresh &= u[v] == 0u;
-          if (fresh) fz_touched.push_back(t_ids[x]);
+          if (fresh) {
+            fz_touched.push_back(t_ids[x]);
+            fz_slot[t_ids[x]] = cl_slot[k];
+          }
           u[w] |= bit;
         }
       }
@@ -669,10 +710,11 @@ void Executor::build_fused_program() {
     FusedGroup fg{};
     fg.entries = static_cast<uint32_t>(fz_words.size());
     fg.n_entries = static_cast<uint32_t>(fz_touched.size());
-    for (uint32_t t : fz_touched) {
+    for (uint32_t t : fz_touched) {  // v(t) = hc(slot(t)) & ~users(t)
       uint32_t* u = fz_users.data() + size_t{t} * fw;
+      const uint32_t* h = hc.data() + size_t{fz_slot[t]} * fw;
       fz_words.push_back(t);
-      fz_words.insert(fz_words.end(), u, u + fw);
+      for (uint32_t v = 0; v < fw; ++v) fz_words.push_back(h[v] & ~u[v]);
       std::fill(u, u + fw, 0u);
     }
     fg.hc = static_cast<uint32_t>(fz_words.size());
@@ -690,6 +732,7 @@ void Executor::run() {
   if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_run before hyre_batch_prepare");
   HYRE_CUDA(cudaSetDevice(ix->device));
   kernels = 0;
+  finish_rounds = 0;
   ev = ev_ring[n_runs++ % kEvRing];
   const uint32_t W = ix->words;
   uint32_t* n_elig = d_counters;
@@ -697,7 +740,6 @@ void Executor::run() {
   uint32_t* samp_cnt = d_counters + 2 * max_batch;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
-  uint32_t* above = d_counters + 5 * max_batch;
   HYRE_CUDA(cudaEventRecord(ev[0], st));
   HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
   if (use_fused) {
@@ -739,12 +781,20 @@ void Executor::run() {
   }
   HYRE_CUDA(cudaEventRecord(ev[2], st));
   if (any_emb) {
-    if (ix->n_rows > cap) {
+    if (ix->n_rows > cap && use_tc) {
+      // K3 sample pass into per-query score histograms -> thresholds
+      HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
+      score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
+      HistThrArgs ha{d_shist, kHistBins, d_qp, n_elig, cap, sample_period, B, QF_ACTIVE | QF_EMB, d_thr, d_thr_safe,
+                     prefilter ? kPrefilterDelta : 0.0f};
+      launch_hist_thr(ha, st);
+      ++kernels;
+    } else if (ix->n_rows > cap) {
       HYRE_CUDA(cudaMemset2DAsync(d_samp, sizeof(uint32_t) * samp_cap, 0, sizeof(uint32_t) * sample_rows, B, st));
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       SelectArgs ka{nullptr, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
                     nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows,
-                    d_samp, ix->row_base, d_cand, cap, prefilter ? kPrefilterDelta : 0.0f, nullptr};
+                    d_samp, ix->row_base, d_cand, cap, prefilter ? kPrefilterDelta : 0.0f};
       launch_sample_kth(ka, samp_cnt, st);
       ++kernels;
     } else {
@@ -754,19 +804,13 @@ void Executor::run() {
     HYRE_CUDA(cudaEventRecord(ev[3], st));
     score(SCORE_MAIN, d_cand, cand_cnt, cap);
     HYRE_CUDA(cudaEventRecord(ev[4], st));
-    rescore(d_cand, cand_cnt, above);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
-    fa.above = prefilter ? above : nullptr;
-    launch_select(fa, st);
-    ++kernels;
-    // One speculative recovery round: no-op unless a candidate buffer overflowed.
-    HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
-    score(SCORE_RERUN, d_cand, cand_cnt, cap);
-    rescore(d_cand, cand_cnt, above);
-    fa.mode = SELECT_FINAL_RERUN;
-    launch_select(fa, st);
-    ++kernels;
+    final_select(fa);
+    // Recovery (a query whose estimated threshold admitted too few rows, or
+    // whose candidate buffer overflowed) is rare: fetch() sees the rerun
+    // flags with the results and runs it then, so the common batch costs no
+    // speculative kernels.
   } else {
     HYRE_CUDA(cudaEventRecord(ev[3], st));
     HYRE_CUDA(cudaEventRecord(ev[4], st));
@@ -793,14 +837,12 @@ void Executor::finish_reruns() {
     bool any = false;
     for (uint32_t i = 0; i < B; ++i) any |= h_rerun[i] != 0;
     if (!any) return;
+    ++finish_rounds;
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
     score(SCORE_RERUN, d_cand, cand_cnt, cap);
-    uint32_t* above = d_counters + 5 * max_batch;
-    rescore(d_cand, cand_cnt, above);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
-    fa.above = prefilter ? above : nullptr;
-    launch_select(fa, st);
+    final_select(fa);
   }
   throw Error(HYRE_INTERNAL, "top-K candidate selection did not converge");
 }
@@ -824,6 +866,17 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
     finish_reruns();
   }
   d2h_bytes = B * 4 + n_hits_total * sizeof(hyre_hit);
+  if (std::getenv("HYRE_DEBUG_COUNTS")) {  // diagnostics: candidate / admitted counts per query
+    std::vector<uint32_t> c(size_t{max_batch} * kNumCounters);
+    HYRE_CUDA(cudaMemcpy(c.data(), d_counters, c.size() * 4, cudaMemcpyDeviceToHost));
+    uint64_t sc = 0, mx = 0;
+    for (uint32_t i = 0; i < B; ++i) {
+      sc += c[max_batch + i];
+      mx = std::max<uint64_t>(mx, c[max_batch + i]);
+    }
+    std::fprintf(stderr, "[hyre] B=%u candidates mean %.1f max %lu, sample period %u, reruns %d\n", B,
+                 double(sc) / B, static_cast<unsigned long>(mx), sample_period, int(finish_rounds));
+  }
   for (uint32_t i = 0; i < B; ++i) {
     if (st_out) st_out[i] = statuses[i];
     const uint32_t c = statuses[i] == HYRE_OK ? h_out_cnt[i] : 0u;

@@ -13,7 +13,7 @@ namespace hyreb {
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
 
 struct Executor {
-  static constexpr uint32_t kNumCounters = 6;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun, above
+  static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
   // K3 prefilter bound: |exact - prefilter score| for unit rows and queries.
   // bf16 RNE of row and query: |e q - hi(e) hi(q)| <= (2^-8 + 2^-18)|e q| per
   // element, summed <= 2^-8 (1 + 2^-10) |e| |q| (Cauchy-Schwarz); plus fp32
@@ -40,7 +40,10 @@ struct Executor {
   uint64_t* d_thr = nullptr;
   uint64_t* d_thr_safe = nullptr;
   uint64_t* d_cand = nullptr;
-  uint32_t* d_samp = nullptr;  // dense sample scores [max_batch][samp_cap]
+  uint32_t* d_samp = nullptr;  // dense sample scores [max_batch][samp_cap] (K2 sample pass)
+  uint32_t* d_shist = nullptr;  // K3 sample pass: score histograms [max_batch][kHistBins]
+  static constexpr uint32_t kHistBins = 4096;    // linear bins over [-1, 1] (width 4.9e-4)
+  static constexpr uint32_t kTcSampleSegs = 80;  // K3 sample: ~80 x 1024 rows (c3 sweep 80/160/320/640: 80 best)
   uint32_t* d_qhist = nullptr;
   uint32_t* d_tsel = nullptr;
   uint32_t* d_eqcnt = nullptr;
@@ -85,6 +88,7 @@ struct Executor {
   std::vector<uint64_t> qsig;
   uint64_t n_hits_total = 0, h2d_bytes = 0, d2h_bytes = 0;
   uint64_t term_bytes = 0;  // algorithmic eligibility-input bytes of the prepared batch
+  uint64_t scan_bytes = 0;  // algorithmic bytes of the K3 main stage (0 on the K2 path)
   // fused CNF in the K3 epilogue (no K1 mask pass): per query group, the
   // term-users program (TcArgs::fz) and its offsets into fz_words
   bool use_fused = false;
@@ -93,11 +97,11 @@ struct Executor {
   };
   std::vector<FusedGroup> fz_group;
   std::vector<uint32_t> fz_words;
-  std::vector<uint32_t> fz_users, fz_touched;  // build_fused_program scratch
+  std::vector<uint32_t> fz_users, fz_touched, fz_slot;  // build_fused_program scratch
   uint32_t* d_fz = nullptr;
   // tensor-core path (K3)
   bool use_tc = false;
-  bool prefilter = false;  // K3 reads the hi plane only; candidates rescored exactly (rescore())
+  bool prefilter = false;  // K3 reads the hi plane only; candidates rescored exactly (final_select())
   uint32_t tc_load_ops() const { return prefilter ? 1u : ix->tc_ops; }
   uint32_t tc_q_planes() const { return prefilter ? 1u : 2u; }
   uint32_t tc_stages = 2, tc_term_slots = 2, tc_aps = 1;  // K3 ring depths, K atoms per stage (plan_tc)
@@ -145,7 +149,8 @@ struct Executor {
   void build_forward_program();
   void build_fused_program();
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
-  void rescore(uint64_t* cand, uint32_t* cnt, uint32_t* above);
+  void final_select(SelectArgs fa);
+  uint32_t finish_rounds = 0;  // recovery rounds fetch() ran for the last batch (diagnostics)
 };
 
 }  // namespace hyreb

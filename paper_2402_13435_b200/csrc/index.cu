@@ -72,6 +72,31 @@ __global__ void row_terms_kernel(const uint64_t* keys, const uint64_t* pos, uint
   }
 }
 
+// Compact CNF rows for K3's fused evaluator: per row the term ids as u8
+// (T <= 255) or u16, padded with the all-ones sentinel to `wb` bytes, and a
+// u64 of masks: low word = segment starts (bit j: id j opens a new slot
+// segment, j >= 1), high word = slots present in the row.
+__global__ void cnf_rows_kernel(const uint16_t* row_terms, const uint8_t* slot_of, uint32_t n, uint32_t A,
+                                uint32_t tb, uint32_t wb, uint8_t* ids, uint64_t* masks) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint16_t* src = row_terms + static_cast<size_t>(r) * A;
+    uint8_t* dst = ids + static_cast<size_t>(r) * wb;
+    uint32_t starts = 0, pres = 0, prev = 0xFFFFFFFFu;
+    for (uint32_t j = 0; j < wb / tb; ++j) {
+      const uint32_t t = j < A ? src[j] : 0xFFFFu;
+      if (t != 0xFFFFu) {
+        const uint32_t sl = slot_of[t];
+        if (j > 0 && sl != prev) starts |= 1u << j;
+        pres |= 1u << sl;
+        prev = sl;
+      }
+      if (tb == 1) dst[j] = static_cast<uint8_t>(t == 0xFFFFu ? 0xFFu : t);
+      else reinterpret_cast<uint16_t*>(dst)[j] = static_cast<uint16_t>(t);
+    }
+    masks[r] = (static_cast<uint64_t>(pres) << 32) | starts;
+  }
+}
+
 __global__ void slot_of_kernel(const uint64_t* uniq, uint32_t T, uint8_t* slot_of) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
     slot_of[t] = static_cast<uint8_t>(uniq[t] >> 32);
@@ -131,6 +156,8 @@ DevIndex::~DevIndex() {
   cudaFree(emb_hi);
   cudaFree(tc_tiles);
   cudaFree(row_terms);
+  cudaFree(cnf_ids);
+  cudaFree(cnf_masks);
   cudaFree(slot_of);
   cudaFree(sigs);
   cudaFree(bitmaps);
@@ -276,6 +303,27 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
         ix->n_terms_fwd = T;
         ix->stats.forward_bytes = size_t{n} * Ap * 2;
         ix->row_terms_width = Ap;
+        // compact CNF rows (K3 fused): ids in as few bytes as T allows, row
+        // width an odd multiple of 8 B (bank-conflict-free LDS.64 per row),
+        // plus the per-row segment/present masks
+        const uint32_t tb = T <= 255 ? 1u : 2u;
+        uint32_t jw = A <= 8 ? 8u : (A <= 16 ? 16u : (A <= 24 ? 24u : 32u));
+        if (tb == 2 && jw % 16) jw += 8;  // u16 variants: 16 or 32 ids
+        uint32_t wb = jw * tb;
+        if ((wb / 8) % 2 == 0) wb += 8;
+        // whole 128-row tiles (K3 bulk-copies full tiles): sentinel ids, no masks in the tail
+        const size_t n_pad = (size_t{n} + 127) / 128 * 128;
+        ix->cnf_ids = dmalloc<uint8_t>(n_pad * wb);
+        ix->cnf_masks = dmalloc<uint64_t>(n_pad);
+        HYRE_CUDA(cudaMemset(ix->cnf_ids, 0xFF, n_pad * wb));
+        HYRE_CUDA(cudaMemset(ix->cnf_masks, 0, n_pad * 8));
+        cnf_rows_kernel<<<blocks, 256>>>(ix->row_terms, ix->slot_of, n, Ap, tb, wb, ix->cnf_ids, ix->cnf_masks);
+        HYRE_CUDA(cudaGetLastError());
+        HYRE_CUDA(cudaDeviceSynchronize());
+        ix->cnf_id_bytes = tb;
+        ix->cnf_ids_per_row = jw;
+        ix->cnf_row_bytes = wb;
+        ix->stats.forward_bytes += size_t{n} * (wb + 8);
       }
       pos.reset();
       std::vector<uint64_t> hk(T);

@@ -654,83 +654,6 @@ void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st) {
   }
 }
 
-// Exact rescoring of K3 prefilter candidates (RescoreArgs).  LPR lanes per
-// row, CPL chunks per lane: the same per-lane fma chains as score_kernel and
-// a butterfly over the same lane pairs (xor LPR/2 .. 1), so the sums are
-// bit-identical to K2's reduce-scatter (fp32 addition is commutative).
-template <typename RowT, int LPR, int CPL>
-__global__ void __launch_bounds__(256) rescore_kernel(RescoreArgs a) {
-  constexpr int G = 32 / LPR;  // candidates per warp step
-  constexpr int E = Chunk<RowT>::kElems;
-  constexpr int U = 4;  // warp steps with loads in flight
-  const uint32_t q = blockIdx.y;
-  const uint32_t n = min(a.cnt[q], a.cap);
-  if (n == 0) return;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int g = lane / LPR, li = lane % LPR;
-  float qv[CPL][E];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c)
-#pragma unroll
-    for (int e = 0; e < E; ++e) qv[c][e] = a.q[static_cast<size_t>(q) * a.dp + (li + c * LPR) * E + e];
-  const uint64_t thr = a.thr[q];
-  uint64_t* keys = a.cand + static_cast<size_t>(q) * a.cap;
-  const RowT* emb = static_cast<const RowT*>(a.emb);
-  const uint32_t per_block = (blockDim.x >> 5) * U * G;
-  uint32_t mine = 0;
-  for (uint32_t base = blockIdx.x * per_block; base < n; base += gridDim.x * per_block) {
-    uint4 v[U][CPL];
-    uint32_t idx[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      idx[u] = base + (wib * U + u) * G + g;
-      const bool ok = idx[u] < n;
-      const uint32_t row = ok ? key_row(keys[idx[u]]) - a.row_base : 0u;
-      const RowT* r = emb + static_cast<size_t>(row) * a.dp;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) v[u][c] = ok ? ldg_stream(r + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[u][c], qv[c]);
-#pragma unroll
-      for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
-      if (li == 0 && idx[u] < n) {
-        const uint64_t key = make_key(clamp_score(acc), key_row(keys[idx[u]]));
-        keys[idx[u]] = key;
-        mine += key >= thr ? 1u : 0u;
-      }
-    }
-  }
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) mine += __shfl_xor_sync(kFull, mine, m);
-  if (lane == 0 && mine) atomicAdd(a.above + q, mine);
-}
-
-namespace {
-template <typename RowT>
-void dispatch_rescore(const RescoreArgs& a, dim3 grid, cudaStream_t st) {
-  const uint32_t cpr = a.dp_chunks;
-  if (cpr == 8) rescore_kernel<RowT, 8, 1><<<grid, 256, 0, st>>>(a);
-  else if (cpr == 16) rescore_kernel<RowT, 16, 1><<<grid, 256, 0, st>>>(a);
-  else if (cpr == 32) rescore_kernel<RowT, 32, 1><<<grid, 256, 0, st>>>(a);
-  else if (cpr == 64) rescore_kernel<RowT, 32, 2><<<grid, 256, 0, st>>>(a);
-  else if (cpr == 128) rescore_kernel<RowT, 32, 4><<<grid, 256, 0, st>>>(a);
-  else if (cpr == 256) rescore_kernel<RowT, 32, 8><<<grid, 256, 0, st>>>(a);
-  else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
-}
-}  // namespace
-
-void launch_rescore(const RescoreArgs& a, bool bf16, cudaStream_t st) {
-  if (a.B == 0) return;
-  // ~1K candidates per query at c3: 8 CTAs x 8 warps x 4 steps cover 256-1K per sweep
-  const dim3 grid(8, a.B);
-  if (bf16) dispatch_rescore<__nv_bfloat16>(a, grid, st);
-  else dispatch_rescore<float>(a, grid, st);
-}
-
 // ===========================================================================
 // K4: exact per-query selection over candidate keys (one CTA per query).
 // Radix select (12-bit digits from the top) finds the K-th largest key, the
@@ -953,9 +876,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     return;
   }
-  // (prefilter: candidates include rows below thr; count the rescored keys >= thr)
-  const uint32_t admitted = a.above ? a.above[q] : total;
-  if (a.thr_safe && admitted < min(k, a.n_elig[q]) && a.thr[q] != a.thr_safe[q]) {
+  if (a.thr_safe && total < min(k, a.n_elig[q]) && a.thr[q] != a.thr_safe[q]) {
     // The estimated threshold admitted fewer than K rows: rescore with the
     // guaranteed bound.
     if (threadIdx.x == 0) {
@@ -1137,6 +1058,55 @@ void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st) {
   sample_union_kernel<<<a.B, kSelThreads, smem, st>>>(a, ucnt);
 }
 
+__global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
+  __shared__ uint32_t tmp[40];
+  __shared__ uint32_t s_bin[2];
+  const uint32_t q = blockIdx.x;
+  const QParam qp = a.qp[q];
+  const bool on = (qp.flags & a.require_flags) == a.require_flags && a.n_elig[q] > a.gate;
+  if (!on) {
+    if (threadIdx.x == 0) {
+      a.thr[q] = 0ull;
+      a.thr_safe[q] = 0ull;
+    }
+    return;
+  }
+  const uint32_t k = qp.k, m = kth_m(k, a.period);
+  // thread t owns bins [nb - (t + 1) per, nb - t per): scan positions run
+  // from the top score down, so the exclusive prefix counts the rows above
+  const uint32_t per = a.nb / blockDim.x, hi = a.nb - threadIdx.x * per;
+  const uint32_t* h = a.hist + static_cast<size_t>(q) * a.nb;
+  uint32_t mine = 0;
+  for (uint32_t b = hi - per; b < hi; ++b) mine += h[b];
+  if (threadIdx.x == 0) s_bin[0] = s_bin[1] = UINT32_MAX;
+  uint32_t total;
+  uint32_t above = block_excl_scan(mine, tmp, &total);
+  for (uint32_t b = hi; b-- > hi - per;) {
+    const uint32_t c = h[b];
+    if (above < k && k <= above + c) s_bin[0] = b;
+    if (above < m && m <= above + c) s_bin[1] = b;
+    above += c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // lower bin edge, a hair lower so float rounding of the binning can never
+    // leave a binned score below it; the key of (edge, last row) is below every
+    // key with a score >= edge
+    auto edge_key = [&](uint32_t b) {
+      const float e = -1.0f + 2.0f * static_cast<float>(b) / static_cast<float>(a.nb) - 1e-6f;
+      return make_key(fmaxf(e, -1.0f), 0xFFFFFFFFu);
+    };
+    const uint64_t t_safe = s_bin[0] == UINT32_MAX ? 0ull : edge_key(s_bin[0]);
+    a.thr[q] = s_bin[1] == UINT32_MAX ? 0ull : edge_key(s_bin[1]);
+    a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
+  }
+}
+
+void launch_hist_thr(const HistThrArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  hist_thr_kernel<<<a.B, 256, 0, st>>>(a);
+}
+
 void launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
   // sort buffer | histogram + scan scratch | resident candidates (FINAL)
@@ -1147,6 +1117,200 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
     attr_set = true;
   }
   select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// K4 for the K3 prefilter (SELECT_FINAL / SELECT_FINAL_RERUN): candidates
+// carry prefilter keys (|exact - prefilter| <= delta).  One CTA per query:
+//   1. tau = K-th largest prefilter key of the candidates.  K candidates have
+//      exact scores >= score(tau) - delta, so the exact K-th score is too, and
+//      every row of the exact top K has prefilter score >= score(tau) - 2 delta:
+//      only those survivors (about K + the rows in a 2-delta band) are rescored;
+//   2. survivors are rescored exactly with K2's arithmetic (the fp32 or bf16
+//      row and the fp32 unit query; LPR lanes per row, the butterfly of
+//      score_kernel), so batch scores equal single-query scores bit for bit;
+//   3. the threshold was valid if K rows are known to score >= score(thr)
+//      (score(tau) - delta >= score(thr), or K rescored keys above it); else
+//      the query reruns with thr_safe, exactly as in select_kernel;
+//   4. the survivors' exact keys are sorted; the first K are the hits.
+// Overflowing candidate buffers rerun with the delta-lowered K-th prefilter
+// key of the kept subset (a valid bound).  More than kSelectMaxK survivors
+// (near-duplicate rows; adversarial) fall back to rescoring every candidate
+// in place and an exact radix select.
+// ---------------------------------------------------------------------------
+namespace {
+template <typename RowT, int LPR, int CPL>
+__device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys, uint32_t n, float thr_s,
+                             uint32_t* above) {
+  constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems, U = CPL >= 8 ? 1 : (CPL >= 4 ? 2 : 4);  // rows in flight per lane group
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane / LPR, li = lane % LPR;
+  float qv[CPL][E];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int e = 0; e < E; ++e) qv[c][e] = a.q[static_cast<size_t>(q) * a.dp + (li + c * LPR) * E + e];
+  const RowT* emb = static_cast<const RowT*>(a.emb);
+  uint32_t mine = 0;
+  for (uint32_t base = wib * U * G; base < n; base += nw * U * G) {
+    uint4 v[U][CPL];
+    uint32_t idx[U], grow[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      idx[u] = base + u * G + g;
+      const bool ok = idx[u] < n;
+      grow[u] = ok ? key_row(keys[idx[u]]) : a.row_base;
+      const RowT* r = emb + static_cast<size_t>(grow[u] - a.row_base) * a.dp;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[u][c] = ok ? ldg_stream(r + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[u][c], qv[c]);
+#pragma unroll
+      for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
+      if (li == 0 && idx[u] < n) {
+        const float sc = clamp_score(acc);
+        keys[idx[u]] = make_key(sc, grow[u]);
+        mine += sc >= thr_s ? 1u : 0u;
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) mine += __shfl_xor_sync(kFull, mine, m);
+  if (lane == 0 && mine) atomicAdd(above, mine);
+}
+}  // namespace
+
+template <typename RowT, int LPR, int CPL>
+__global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelectArgs pa) {
+  const SelectArgs& a = pa.s;
+  extern __shared__ uint64_t sel_smem[];
+  uint64_t* sortbuf = sel_smem;                                          // kSelectMaxK keys
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sel_smem + kSelectMaxK);  // 4096
+  uint32_t* tmp = hist + 4096;                                           // 33
+  uint64_t* res = reinterpret_cast<uint64_t*>(tmp + 40);                 // kSelResident keys
+  __shared__ uint32_t gathered, above;
+  const uint32_t q = blockIdx.x;
+  const QParam qp = a.qp[q];
+  if ((qp.flags & a.require_flags) != a.require_flags) return;
+  if (a.mode == SELECT_FINAL_RERUN && !a.rerun[q]) return;
+  const uint32_t total = a.cnt[q], n = min(total, a.cap), k = qp.k;
+  uint64_t* keys = const_cast<uint64_t*>(a.buf) + static_cast<size_t>(q) * a.cap;  // the candidate buffer (rescored in place on spill)
+  const uint64_t thr = a.thr[q];
+  const bool has_safe = a.thr_safe && thr != a.thr_safe[q];
+  if (a.n_elig[q] == 0 || (total == 0 && !has_safe)) {
+    if (threadIdx.x == 0) {
+      a.out_cnt[q] = 0;
+      a.rerun[q] = 0;
+    }
+    return;
+  }
+  if (total > a.cap) {  // overflow: the kept subset's K-th prefilter key, lowered by delta, bounds the exact K-th
+    const uint64_t t = kth_largest(keys, n, k, hist, tmp);
+    if (threadIdx.x == 0) {
+      a.thr[q] = key_minus_delta(t, a.delta);
+      a.rerun[q] = 1;
+    }
+    return;
+  }
+  const float thr_s = thr == 0ull ? -2.0f : key_score(thr);
+  // 1. tau: K-th largest prefilter key (no pruning when n <= K)
+  const bool resident = n <= kSelResident;
+  if (resident) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) res[i] = keys[i];
+    __syncthreads();
+  }
+  const uint64_t* src = resident ? res : keys;
+  float tau_s = -4.0f;
+  if (n > k) tau_s = key_score(kth_largest(src, n, k, hist, tmp));
+  const float prune = tau_s - 2.0f * a.delta;
+  // 2. survivors -> sortbuf, rescored in place
+  if (threadIdx.x == 0) {
+    gathered = 0;
+    above = 0;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint64_t key = i < n ? src[i] : 0ull;
+    warp_append(i < n && key_score(key) >= prune, key, sortbuf, &gathered, kSelectMaxK);
+  }
+  __syncthreads();
+  const uint32_t g = gathered;
+  const bool spill = g > kSelectMaxK;
+  if (!spill) {
+    rescore_list<RowT, LPR, CPL>(pa, q, sortbuf, g, thr_s, &above);
+  } else {  // adversarial: rescore every candidate in place in global memory
+    rescore_list<RowT, LPR, CPL>(pa, q, keys, n, thr_s, &above);
+  }
+  __syncthreads();
+  // 3. threshold validity (select_kernel's rule with the prefilter bound)
+  const bool valid = (n >= k && tau_s - a.delta >= thr_s) || above >= min(k, a.n_elig[q]);
+  if (!valid && has_safe) {
+    if (threadIdx.x == 0) {
+      a.thr[q] = a.thr_safe[q];
+      a.rerun[q] = 1;
+    }
+    return;
+  }
+  // 4. exact order
+  uint32_t m = g;
+  if (spill) {
+    const uint64_t t = kth_largest(keys, n, k, hist, tmp);
+    if (threadIdx.x == 0) gathered = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      const uint64_t key = i < n ? keys[i] : 0ull;
+      warp_append(i < n && key >= t, key, sortbuf, &gathered, kSelectMaxK);
+    }
+    __syncthreads();
+    m = min(gathered, kSelectMaxK);
+  }
+  uint32_t m2 = 1;
+  while (m2 < m) m2 <<= 1;
+  for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
+  __syncthreads();
+  bitonic_desc(sortbuf, m2);
+  const uint32_t take = min(m, k);
+  hyre_hit* out = a.hits + a.hit_off[q];
+  for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
+    const uint64_t key = sortbuf[i];
+    out[i].row = key_row(key);
+    out[i].score = key_score(key);
+  }
+  if (threadIdx.x == 0) {
+    a.out_cnt[q] = take;
+    a.rerun[q] = 0;
+  }
+}
+
+namespace {
+template <typename RowT>
+void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_t st) {
+  using KFn = void (*)(PrefSelectArgs);
+  KFn k = nullptr;
+  const uint32_t cpr = a.dp_chunks;
+  if (cpr == 8) k = select_prefilter_kernel<RowT, 8, 1>;
+  else if (cpr == 16) k = select_prefilter_kernel<RowT, 16, 1>;
+  else if (cpr == 32) k = select_prefilter_kernel<RowT, 32, 1>;
+  else if (cpr == 64) k = select_prefilter_kernel<RowT, 32, 2>;
+  else if (cpr == 128) k = select_prefilter_kernel<RowT, 32, 4>;
+  else if (cpr == 256) k = select_prefilter_kernel<RowT, 32, 8>;
+  else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
+  HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k<<<a.s.B, kSelThreads, smem, st>>>(a);
+}
+}  // namespace
+
+void launch_select_prefilter(const PrefSelectArgs& a, bool bf16, cudaStream_t st) {
+  if (a.s.B == 0) return;
+  const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t) + kSelResident * sizeof(uint64_t);
+  if (bf16) dispatch_select_prefilter<__nv_bfloat16>(a, smem, st);
+  else dispatch_select_prefilter<float>(a, smem, st);
 }
 
 // ===========================================================================

@@ -85,23 +85,6 @@ struct ScoreArgs {
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 
-// ---- K3 prefilter companion: exact rescoring of the admitted candidates ----
-// Rewrites every candidate key of every query (cand[q][0 .. min(cnt, cap)))
-// with its exact score, computed with K2's arithmetic over the resident
-// row-major rows (fp32 rows, or the bf16 rows of a bf16 index) and the fp32
-// unit query, so a K3 batch returns the same scores as K2 / single queries.
-// above[q] += the number of rescored keys >= thr[q] (caller zeroes it).
-struct RescoreArgs {
-  const void* emb;
-  uint32_t dp, dp_chunks, row_base;
-  const float* q;  // [B][dp]
-  uint64_t* cand;
-  const uint32_t* cnt;
-  uint32_t cap, B;
-  const uint64_t* thr;
-  uint32_t* above;
-};
-void launch_rescore(const RescoreArgs& a, bool bf16, cudaStream_t st);
 // Largest key whose score is <= s - delta: a lower bound, in key space, for
 // every exact score of a row whose prefilter score was s (delta = the bound).
 __host__ __device__ __forceinline__ uint64_t key_minus_delta(uint64_t key, float delta) {
@@ -138,16 +121,43 @@ struct SelectArgs {
   uint32_t row_base;
   uint64_t* fb;     // KTH fallback scratch ([B][fb_cap] keys; the candidate buffer)
   uint32_t fb_cap;
-  // K3 prefilter: KTH lowers thr_safe by delta (the sample holds prefilter
-  // scores); FINAL decides "fewer than K admitted" from above[q] (rescored
-  // keys >= thr) instead of the candidate count.
+  // K3 prefilter bound: KTH lowers thr_safe by delta (the sample holds
+  // prefilter scores); select_prefilter_kernel prunes and checks with it.
   float delta;
-  const uint32_t* above;
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
+// K4 for K3 prefilter candidates (SELECT_FINAL / SELECT_FINAL_RERUN; see
+// kernels.cu): prunes to the rows that can still reach the exact top K,
+// rescores them exactly with K2's arithmetic over the resident row-major rows
+// (fp32, or the bf16 rows of a bf16 index) and the fp32 unit queries, checks
+// the threshold, sorts.  s.delta = the prefilter bound.
+struct PrefSelectArgs {
+  SelectArgs s;
+  const void* emb;
+  uint32_t dp, dp_chunks, row_base;
+  const float* q;  // [B][dp]
+};
+void launch_select_prefilter(const PrefSelectArgs& a, bool bf16, cudaStream_t st);
 // SELECT_KTH over the dense sample: per-slice top keys gathered into fb
 // (ucnt [B] zeroed by the caller), then one sort per query.
 void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st);
+
+// Thresholds from per-query sample histograms (K3 sample pass with shist):
+// thr = lower edge of the bin holding the sample's m-th score (the same m as
+// SELECT_KTH), thr_safe = lower edge of the K-th's bin (a lower bound on the
+// global K-th score: K sampled rows lie at or above it), lowered by delta for
+// prefilter scores.  Queries not sampled get 0 (no threshold).
+struct HistThrArgs {
+  const uint32_t* hist;  // [B][nb]
+  uint32_t nb;
+  const QParam* qp;
+  const uint32_t* n_elig;
+  uint32_t gate, period, B, require_flags;
+  uint64_t* thr;
+  uint64_t* thr_safe;
+  float delta;
+};
+void launch_hist_thr(const HistThrArgs& a, cudaStream_t st);
 
 // ---- K5: term-only first-K rows (pipeline.cpp:30-40) ----
 struct FirstKArgs {

@@ -167,68 +167,63 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
   return t < a.n_tiles ? t : UINT32_MAX;
 }
 
-// Eligibility of one row for all NCH 32-query chunks of the group from the
-// row's forward term list: a query is eligible iff every slot it constrains
-// holds a row term listed in its clause (term_match.cpp:34-78: AND over
-// clauses of a non-empty sorted intersection).  Terms are slot-major
-// (ascending term ids), so a per-slot OR accumulator closes whenever the slot
-// changes: fail |= hc[slot] & ~acc.  Every table entry carries its term's
-// users words and its slot's hc words, so all 8*NA lookups are independent
-// and issue back to back; the combine is branch-free.  Padding (0xFFFF) maps
-// to the sentinel entry T (no users, dummy slot C).  Constrained slots the
-// row has no term in fail outright (an empty doc slice never matches,
-// term_match.cpp:45-46).
-template <int NCH, int NA>
-__device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, uint32_t tbl, uint32_t slot_of,
+// Eligibility of one row for all NCH 32-query chunks of the group
+// (term_match.cpp:34-78: a query matches iff every slot it constrains holds a
+// row term listed in its clause).  The table holds, per term t,
+//   v(t) = hc(slot(t)) & ~users(t)
+// (the group's queries that constrain t's slot but do not list t; sentinel:
+// all ones).  A constrained slot s fails a query iff EVERY row term in s
+// fails it, i.e. fail_s = AND over the slot's segment of v(t), so
+//   fail = OR over present slots of AND over the segment of v  |  hc of the
+//          constrained slots the row has no term in
+// (an empty doc slice never matches, term_match.cpp:45-46).  The row's ids are
+// slot-major, and its segment-start mask (bit j: id j opens a new slot) makes
+// the whole evaluation two LOP3s per id and chunk, after J independent table
+// loads issued back to back.
+template <int J, int TB, int NCH>
+__device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64_t masks, uint32_t T, uint32_t tbl,
                                         uint32_t hc, uint32_t live, uint32_t cslots, uint32_t (&out)[NCH]) {
-  constexpr int J = 8 * NA;
-  uint32_t sl[J], u[J][NCH], h[J][NCH];
+  uint32_t v[J][NCH];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const uint32_t t = min((tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu, T);
+    const uint32_t id = TB == 1 ? (tw[j >> 2] >> ((j & 3) * 8)) & 0xFFu : (tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+    const uint32_t e = tbl + min(id, T) * (4 * NCH);  // all-ones padding -> sentinel entry T
     // explicit ld.shared (32-bit shared addresses): generic loads would cost
     // long-scoreboard waits
-    asm("ld.shared.u8 %0, [%1];" : "=r"(sl[j]) : "r"(slot_of + t));
-    const uint32_t e = tbl + t * (8 * NCH);
     if (NCH == 1) {
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(u[j][0]), "=r"(h[j][0]) : "r"(e));
-    } else if (NCH == 2) {  // entry {u0, u1, h0, h1}
+      asm("ld.shared.u32 %0, [%1];" : "=r"(v[j][0]) : "r"(e));
+    } else if (NCH == 2) {
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[j][0]), "=r"(v[j][NCH - 1]) : "r"(e));
+    } else {
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(u[j][0]), "=r"(u[j][NCH - 1]), "=r"(h[j][0]), "=r"(h[j][NCH - 1])
+          : "=r"(v[j][0]), "=r"(v[j][1 % NCH]), "=r"(v[j][2 % NCH]), "=r"(v[j][3 % NCH])
           : "r"(e));
-    } else {  // NCH == 4: entry {u0..u3, h0..h3}
-      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(u[j][0]), "=r"(u[j][1 % NCH]), "=r"(u[j][2 % NCH]), "=r"(u[j][3 % NCH])
-          : "r"(e));
-      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(h[j][0]), "=r"(h[j][1 % NCH]), "=r"(h[j][2 % NCH]), "=r"(h[j][3 % NCH])
-          : "r"(e + 16));
     }
   }
-  uint32_t acc[NCH], fail[NCH], hp[NCH];
+  const uint32_t starts = static_cast<uint32_t>(masks), pres = static_cast<uint32_t>(masks >> 32);
+  uint32_t seg[NCH], fail[NCH];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) acc[c] = fail[c] = hp[c] = 0u;
-  uint32_t present = 0u, sp = 0xFFFFFFFFu;
+  for (int c = 0; c < NCH; ++c) {
+    seg[c] = v[0][c];
+    fail[c] = 0u;
+  }
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const bool ch = sl[j] != sp;
+  for (int j = 1; j < J; ++j) {
+    const uint32_t m = 0u - ((starts >> j) & 1u);  // all ones where id j opens a new slot segment
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-      fail[c] |= ch ? (hp[c] & ~acc[c]) : 0u;
-      acc[c] = (ch ? 0u : acc[c]) | u[j][c];
-      hp[c] = h[j][c];
+      fail[c] |= seg[c] & m;
+      seg[c] = (seg[c] | m) & v[j][c];
     }
-    present |= 1u << sl[j];
-    sp = sl[j];
   }
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) fail[c] |= hp[c] & ~acc[c];
-  for (uint32_t miss = cslots & ~present; miss; miss &= miss - 1u) {
-    const uint32_t s = __ffs(miss) - 1;
+  for (int c = 0; c < NCH; ++c) fail[c] |= pres ? seg[c] : 0u;
+  for (uint32_t miss = cslots & ~pres; miss; miss &= miss - 1u) {
+    const uint32_t sl = __ffs(miss) - 1;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
       uint32_t x;
-      asm("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(hc + (s * NCH + c) * 4));
+      asm("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(hc + (sl * NCH + c) * 4));
       fail[c] |= x;
     }
   }
@@ -242,14 +237,14 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[16], uint32_t T, ui
 
 }  // namespace
 
-// NA > 0: fused CNF over row term lists of 8 * NA ids for NCH 32-query
-// chunks, evaluated by kCnfWarps dedicated warps one tile ahead of the
-// epilogue; NA == 0: eligibility from the K1 mask.  One instantiation per
+// J > 0: fused CNF over compact CNF rows of J ids of TB bytes for NCH
+// 32-query chunks, evaluated by kCnfWarps dedicated warps one tile ahead of
+// the epilogue; J == 0: eligibility from the K1 mask.  One instantiation per
 // variant keeps each kernel's code (and instruction-cache footprint) small.
-template <int NA, int NCH>
-__global__ void __launch_bounds__(threads_for(NA > 0), 1)
+template <int J, int TB, int NCH>
+__global__ void __launch_bounds__(threads_for(J > 0), 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
-  constexpr bool kFused = NA > 0;
+  constexpr bool kFused = J > 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array so every derived pointer
   // stays in the shared window (LDS/STS, not generic loads)
@@ -290,7 +285,8 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   // slots, slot of term [T + 1]
   uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + stage_bytes_for(Np);
   uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
-  const uint32_t term_tile_bytes = kTileRows * a.A * 2;
+  // term slot: [128 rows x wb id bytes][128 x u64 masks]
+  const uint32_t term_ids_bytes = kTileRows * a.wb, term_tile_bytes = term_ids_bytes + kTileRows * 8;
   uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? TS * term_tile_bytes : 0u));
   uint64_t* s_tbar = reinterpret_cast<uint64_t*>(s_elig + (kFused ? kEligSlots * NCH * kTileRows : 0u));
   uint64_t* ttfull = s_tbar;
@@ -298,7 +294,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
   uint64_t* efull = s_tbar + 2 * TS;
   uint64_t* eempty = efull + kEligSlots;
   uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(eempty + kEligSlots);
-  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * 2 * NCH;
+  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * NCH;
   uint32_t* s_flive = s_fhc + a.C * NCH;
   uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
 
@@ -357,19 +353,16 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
     for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
     for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t <= a.T; t += blockDim.x) {  // every term: no users, its slot's hc
-      uint32_t* e = s_ftbl + t * (2 * NCH);
+    for (uint32_t t = threadIdx.x; t <= a.T; t += blockDim.x) {  // unlisted term: v = hc of its slot
+      uint32_t* e = s_ftbl + t * NCH;
 #pragma unroll
-      for (uint32_t c = 0; c < NCH; ++c) {
-        e[c] = 0u;
-        e[NCH + c] = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0u;
-      }
+      for (uint32_t c = 0; c < NCH; ++c) e[c] = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;
     }
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {
+    for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {  // listed terms: v = hc & ~users
       const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + NCH);
 #pragma unroll
-      for (uint32_t c = 0; c < NCH; ++c) s_ftbl[en[0] * (2 * NCH) + c] = en[1 + c];
+      for (uint32_t c = 0; c < NCH; ++c) s_ftbl[en[0] * NCH + c] = en[1 + c];
     }
   }
   const uint32_t tmem_cols = a.tmem_cols;
@@ -396,13 +389,14 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
-        if (kFused) {  // the tile's row term lists (contiguous rows) into the term ring
+        if (kFused) {  // the tile's compact CNF rows (ids, masks; padded to whole tiles) into the term ring
           const uint32_t ts = i % TS, tph = (i / TS) & 1;
-          const uint32_t rows = min(kTileRows, a.n_rows - t * kTileRows);
           mbar_wait(ttempty + ts, tph ^ 1);
-          mbar_expect_tx(ttfull + ts, rows * a.A * 2);
-          bulk_load(s_terms + ts * term_tile_bytes, a.row_terms + static_cast<size_t>(t) * kTileRows * a.A,
-                    rows * a.A * 2, ttfull + ts);
+          mbar_expect_tx(ttfull + ts, term_tile_bytes);
+          bulk_load(s_terms + ts * term_tile_bytes, a.cnf_ids + static_cast<size_t>(t) * term_ids_bytes,
+                    term_ids_bytes, ttfull + ts);
+          bulk_load(s_terms + ts * term_tile_bytes + term_ids_bytes, a.cnf_masks + static_cast<size_t>(t) * kTileRows,
+                    kTileRows * 8, ttfull + ts);
         }
         for (uint32_t k = 0; k < kb; k += aps) {
           mbar_wait(empty + s, ph ^ 1);
@@ -546,6 +540,18 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
           take |= (__uint_as_float(v[4 * j4 + 3]) >= t4.w ? 1u : 0u) << (4 * j4 + 3);
         }
         take &= elig;
+        if (a.mode == SCORE_SAMPLE && a.shist) {
+          // sample pass, histogram form: one global increment per eligible
+          // sampled (row, query) in the query's score histogram
+          const float scale = 0.5f * static_cast<float>(a.hbins);
+          for (uint32_t el = elig; el; el &= el - 1u) {
+            const uint32_t j = __ffs(el) - 1;
+            const float sc = clamp_score(__uint_as_float(pick32(v, j)));
+            const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);
+            atomicAdd(a.shist + static_cast<size_t>(q0 + c * 32 + j) * a.hbins + b, 1u);
+          }
+          continue;
+        }
         if (a.mode == SCORE_SAMPLE) {
           // sample pass: every eligible sampled row goes to its fixed slot
           // (segment ordinal x 1024 + row in segment) -- no threshold, no atomics
@@ -598,6 +604,7 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
     }
   } else if (kFused) {
     // ===== CNF warps: thread r evaluates tile row r for all NCH chunks =====
+    constexpr int JW = kFused ? J * TB / 4 : 2;  // u32 words of a row's ids
     const uint32_t r = threadIdx.x - 32 * (2 + kEpiWarps);
     const uint32_t cslots = s_flive[NCH];
     for (uint32_t i = 0;; ++i) {
@@ -605,22 +612,24 @@ __global__ void __launch_bounds__(threads_for(NA > 0), 1)
       if (t == UINT32_MAX) break;
       const uint32_t ts = i % TS, tph = (i / TS) & 1;
       mbar_wait(ttfull + ts, tph);
-      uint32_t tw[16];
-      const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.A * 2;
+      uint32_t tw[JW];
+      const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.wb;
 #pragma unroll
-      for (int v = 0; v < (kFused ? NA : 1); ++v)
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(tw[4 * v]), "=r"(tw[4 * v + 1]), "=r"(tw[4 * v + 2]), "=r"(tw[4 * v + 3])
-                     : "r"(src + 16 * v));
+      for (int v = 0; v < JW / 2; ++v)
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tw[2 * v]), "=r"(tw[2 * v + 1]) : "r"(src + 8 * v));
+      uint64_t masks;
+      asm volatile("ld.shared.u64 %0, [%1];"
+                   : "=l"(masks)
+                   : "r"(smem_u32(s_terms) + ts * term_tile_bytes + term_ids_bytes + r * 8));
       __syncwarp();
       if (lane == 0) mbar_arrive(ttempty + ts);
       uint32_t el[NCH];
       if (a.debug & 4u) {  // diagnostics: no CNF evaluation (every live query eligible)
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) el[c] = s_flive[c] ^ (tw[0] & 1u);
+        for (int c = 0; c < NCH; ++c) el[c] = s_flive[c] ^ (tw[0] & 1u) ^ static_cast<uint32_t>(masks & 2u);
       } else {
-        cnf_row<NCH, (kFused ? NA : 1)>(tw, a.T, smem_u32(s_ftbl), smem_u32(s_fslot), smem_u32(s_fhc),
-                                         smem_u32(s_flive), cslots, el);
+        cnf_row<(kFused ? J : 8), (kFused ? TB : 1), NCH>(tw, masks, a.T, smem_u32(s_ftbl), smem_u32(s_fhc),
+                                                         smem_u32(s_flive), cslots, el);
       }
       if (t * kTileRows + r >= a.n_rows) {  // tail of the last tile
 #pragma unroll
@@ -687,31 +696,35 @@ size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, 
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }
 
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A, uint32_t term_slots) {
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
-  return 128 + size_t{term_slots} * kTileRows * A * 2 + size_t{kEligSlots} * nch * kTileRows * 4 +
-         16 * (term_slots + kEligSlots) + 4 * ((T + 1) * 2 * nch + C * nch + nch + 1) + T + 1 + 16;
+  return 128 + size_t{term_slots} * kTileRows * (wb + 8) + size_t{kEligSlots} * nch * kTileRows * 4 +
+         16 * (term_slots + kEligSlots) + 4 * ((T + 1) * nch + C * nch + nch + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st) {
   using KFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
-  static const KFn fused[3][4] = {
-      {tc_score_kernel<1, 1>, tc_score_kernel<2, 1>, tc_score_kernel<3, 1>, tc_score_kernel<4, 1>},
-      {tc_score_kernel<1, 2>, tc_score_kernel<2, 2>, tc_score_kernel<3, 2>, tc_score_kernel<4, 2>},
-      {tc_score_kernel<1, 4>, tc_score_kernel<2, 4>, tc_score_kernel<3, 4>, tc_score_kernel<4, 4>}};
+  // [id width: u8 J = 8/16/24/32, u16 J = 16/32][query chunks 1/2/4]
+#define HYRE_TC_ROW(J, TB) {tc_score_kernel<J, TB, 1>, tc_score_kernel<J, TB, 2>, tc_score_kernel<J, TB, 4>}
+  static const KFn fused[6][3] = {HYRE_TC_ROW(8, 1),  HYRE_TC_ROW(16, 1), HYRE_TC_ROW(24, 1),
+                                  HYRE_TC_ROW(32, 1), HYRE_TC_ROW(16, 2), HYRE_TC_ROW(32, 2)};
+#undef HYRE_TC_ROW
   static bool attr = false;
   if (!attr) {
-    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     for (auto& row : fused)
       for (KFn k : row) HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  KFn k = tc_score_kernel<0, 1>;
+  KFn k = tc_score_kernel<0, 1, 1>;
   if (a.fused) {
-    const uint32_t na = (a.A + 7) / 8, nch = tc_fused_chunks(a.Np);
-    if (na < 1 || na > 4) throw Error(HYRE_INTERNAL, "fused CNF: row term width out of range");
-    k = fused[nch == 1 ? 0 : (nch == 2 ? 1 : 2)][na - 1];
+    const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : 2);
+    int ri = -1;
+    if (a.tb == 1) ri = a.J == 8 ? 0 : a.J == 16 ? 1 : a.J == 24 ? 2 : a.J == 32 ? 3 : -1;
+    else if (a.tb == 2) ri = a.J == 16 ? 4 : a.J == 32 ? 5 : -1;
+    if (ri < 0) throw Error(HYRE_INTERNAL, "fused CNF: unsupported compact row shape");
+    k = fused[ri][ci];
   }
   k<<<grid, threads_for(a.fused != 0), smem, st>>>(qhi, qlo, a);
 }

@@ -25,18 +25,25 @@ struct TcArgs {
   uint32_t cap, mode, period, gate;
   const uint32_t* rerun;
   uint32_t* samp;  // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
+  // SCORE_SAMPLE with shist: per-query histograms [B][hbins] of the sampled
+  // eligible rows' clamped scores (linear bins over [-1, 1]) instead of samp
+  uint32_t* shist;
+  uint32_t hbins;
   uint32_t debug;  // diagnostics: bit0 skip MMAs, bit1 skip epilogue work, bit2 skip CNF (results invalid)
   // Fused CNF (fused != 0, mask unused): dedicated warps evaluate each row's
-  // eligibility from its forward term list (row_terms, slot-major, 0xFFFF
-  // padded to A) against this group's program, scattered into shared memory:
-  //   fz[0 .. n_entries*(1+W))  (term id, W users words) per referenced term
+  // eligibility from its compact CNF row (DevIndex::cnf_ids / cnf_masks: J
+  // ids of tb bytes in wb-byte rows, slot-major, segment/present masks)
+  // against this group's program, scattered into shared memory:
+  //   fz[0 .. n_entries*(1+W))  (term id, W words v = hc(slot) & ~users)
+  //                             per term some query of the group lists
   //   fz + hc_off: hc[C][W]     queries constraining each slot
   //   fz + live_off: live[W], then the constrained-slot bitmask
   // with W = tc_fused_chunks(Np) words (word c = queries 32c .. 32c+31).
   uint32_t fused;
-  const uint16_t* row_terms;
+  const uint8_t* cnf_ids;
+  const uint64_t* cnf_masks;
   const uint8_t* slot_of;
-  uint32_t A, T, C;
+  uint32_t J, tb, wb, T, C;
   const uint32_t* fz;
   uint32_t n_entries, hc_off, live_off;
   // Prefilter mode (prefilter != 0): only the hi plane of each K-atom is
@@ -59,7 +66,7 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0,
                      uint32_t q_planes = 2, uint32_t aps = 1);
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t A, uint32_t term_slots);
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots);
 constexpr uint32_t kMaxTermSlots = 8;
 // TMEM columns for the accumulator buffers of a group of Np queries
 uint32_t tc_tmem_cols(uint32_t Np);

@@ -37,11 +37,13 @@ constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle
 // stages in flight
 __host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 32768u : 8192u; }
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
-constexpr uint32_t kCnfWarps = 4;                 // fused CNF: one thread per tile row
+// fused CNF warps: one thread per tile row and query-chunk share (4 warps
+// for one 32-query chunk, 8 -- two chunk halves per row -- for 2 or 4 chunks)
+__host__ __device__ constexpr uint32_t cnf_warps(int nch) { return nch == 1 ? 4u : 8u; }
 constexpr uint32_t kAccBufs = 4;                  // TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
 constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight
-__host__ __device__ constexpr uint32_t threads_for(bool fused) {
-  return 64 + 32 * kEpiWarps + (fused ? 32 * kCnfWarps : 0);
+__host__ __device__ constexpr uint32_t threads_for(bool fused, int nch) {
+  return 64 + 32 * kEpiWarps + (fused ? 32 * cnf_warps(nch) : 0);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -58,13 +60,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier
+// (woken when the phase completes) instead of re-polling, so idle roles do
+// not steal issue slots from the CNF / epilogue warps on the same SMSP
+// (without the hint ~20% of K3's issued instructions were poll loops).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(20000u)
         : "memory");
   } while (!done);
 }
@@ -180,30 +186,32 @@ __device__ __forceinline__ uint32_t tile_of(const TcArgs& a, uint32_t i) {
 // slot-major, and its segment-start mask (bit j: id j opens a new slot) makes
 // the whole evaluation two LOP3s per id and chunk, after J independent table
 // loads issued back to back.
-template <int J, int TB, int NCH>
+template <int J, int TB, int NCH, int NT>
 __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64_t masks, uint32_t T, uint32_t tbl,
-                                        uint32_t hc, uint32_t live, uint32_t cslots, uint32_t (&out)[NCH]) {
-  uint32_t v[J][NCH];
+                                        uint32_t hc, uint32_t live, uint32_t cslots, uint32_t c0,
+                                        uint32_t (&out)[NT]) {
+  uint32_t v[J][NT];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const uint32_t id = TB == 1 ? (tw[j >> 2] >> ((j & 3) * 8)) & 0xFFu : (tw[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
-    const uint32_t e = tbl + min(id, T) * (4 * NCH);  // all-ones padding -> sentinel entry T
+    // u8 ids index a 256-entry table directly (entries T..255 are sentinels)
+    const uint32_t e = tbl + ((TB == 1 ? id : min(id, T)) * NCH + c0) * 4;
     // explicit ld.shared (32-bit shared addresses): generic loads would cost
     // long-scoreboard waits
-    if (NCH == 1) {
+    if (NT == 1) {
       asm("ld.shared.u32 %0, [%1];" : "=r"(v[j][0]) : "r"(e));
-    } else if (NCH == 2) {
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[j][0]), "=r"(v[j][NCH - 1]) : "r"(e));
+    } else if (NT == 2) {
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[j][0]), "=r"(v[j][NT - 1]) : "r"(e));
     } else {
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(v[j][0]), "=r"(v[j][1 % NCH]), "=r"(v[j][2 % NCH]), "=r"(v[j][3 % NCH])
+          : "=r"(v[j][0]), "=r"(v[j][1 % NT]), "=r"(v[j][2 % NT]), "=r"(v[j][3 % NT])
           : "r"(e));
     }
   }
   const uint32_t starts = static_cast<uint32_t>(masks), pres = static_cast<uint32_t>(masks >> 32);
-  uint32_t seg[NCH], fail[NCH];
+  uint32_t seg[NT], fail[NT];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
+  for (int c = 0; c < NT; ++c) {
     seg[c] = v[0][c];
     fail[c] = 0u;
   }
@@ -211,26 +219,26 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
   for (int j = 1; j < J; ++j) {
     const uint32_t m = 0u - ((starts >> j) & 1u);  // all ones where id j opens a new slot segment
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NT; ++c) {
       fail[c] |= seg[c] & m;
       seg[c] = (seg[c] | m) & v[j][c];
     }
   }
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) fail[c] |= pres ? seg[c] : 0u;
+  for (int c = 0; c < NT; ++c) fail[c] |= pres ? seg[c] : 0u;
   for (uint32_t miss = cslots & ~pres; miss; miss &= miss - 1u) {
     const uint32_t sl = __ffs(miss) - 1;
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
+    for (int c = 0; c < NT; ++c) {
       uint32_t x;
-      asm("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(hc + (sl * NCH + c) * 4));
+      asm("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(hc + (sl * NCH + c0 + c) * 4));
       fail[c] |= x;
     }
   }
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
+  for (int c = 0; c < NT; ++c) {
     uint32_t lv;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(lv) : "r"(live + c * 4));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(lv) : "r"(live + (c0 + c) * 4));
     out[c] = lv & ~fail[c];
   }
 }
@@ -238,11 +246,11 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
 }  // namespace
 
 // J > 0: fused CNF over compact CNF rows of J ids of TB bytes for NCH
-// 32-query chunks, evaluated by kCnfWarps dedicated warps one tile ahead of
+// 32-query chunks, evaluated by cnf_warps(NCH) dedicated warps one tile ahead of
 // the epilogue; J == 0: eligibility from the K1 mask.  One instantiation per
 // variant keeps each kernel's code (and instruction-cache footprint) small.
 template <int J, int TB, int NCH>
-__global__ void __launch_bounds__(threads_for(J > 0), 1)
+__global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   constexpr bool kFused = J > 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -294,7 +302,8 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
   uint64_t* efull = s_tbar + 2 * TS;
   uint64_t* eempty = efull + kEligSlots;
   uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(eempty + kEligSlots);
-  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(a.T + 1) * NCH;
+  const uint32_t n_tbl = TB == 1 ? 256u : a.T + 1;  // table entries (u8 ids: direct index, sentinels above T)
+  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(n_tbl) * NCH;
   uint32_t* s_flive = s_fhc + a.C * NCH;
   uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
 
@@ -318,10 +327,10 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
     if (kFused) {
       for (uint32_t i = 0; i < TS; ++i) {
         mbar_init(ttfull + i, 1);
-        mbar_init(ttempty + i, kCnfWarps);
+        mbar_init(ttempty + i, cnf_warps(NCH));
       }
       for (uint32_t i = 0; i < kEligSlots; ++i) {
-        mbar_init(efull + i, kCnfWarps);
+        mbar_init(efull + i, cnf_warps(NCH));
         mbar_init(eempty + i, kEpiWarps);
       }
     }
@@ -353,7 +362,7 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
     for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
     for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t <= a.T; t += blockDim.x) {  // unlisted term: v = hc of its slot
+    for (uint32_t t = threadIdx.x; t < n_tbl; t += blockDim.x) {  // unlisted term: v = hc of its slot
       uint32_t* e = s_ftbl + t * NCH;
 #pragma unroll
       for (uint32_t c = 0; c < NCH; ++c) e[c] = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;
@@ -529,17 +538,19 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
         // superset of the exact key test (ties with the threshold row, values
         // clamped later); K4 resolves it exactly.  Thresholds at or below -1
         // are stored as -2 so clamping can never hide a candidate.
-        uint32_t take = 0;
+        // Two instructions per score: d = v - ts (>= 0 exactly when v >= ts,
+        // monotone rounding) and a funnel shift collecting d's sign bit.
+        uint32_t below = 0;  // bit 31 - j: query 32c + j scored below its threshold
         const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
 #pragma unroll
         for (uint32_t j4 = 0; j4 < 8; ++j4) {
           const float4 t4 = ts4[j4];
-          take |= (__uint_as_float(v[4 * j4 + 0]) >= t4.x ? 1u : 0u) << (4 * j4 + 0);
-          take |= (__uint_as_float(v[4 * j4 + 1]) >= t4.y ? 1u : 0u) << (4 * j4 + 1);
-          take |= (__uint_as_float(v[4 * j4 + 2]) >= t4.z ? 1u : 0u) << (4 * j4 + 2);
-          take |= (__uint_as_float(v[4 * j4 + 3]) >= t4.w ? 1u : 0u) << (4 * j4 + 3);
+          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 0]) - t4.x), below, 1);
+          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 1]) - t4.y), below, 1);
+          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 2]) - t4.z), below, 1);
+          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 3]) - t4.w), below, 1);
         }
-        take &= elig;
+        const uint32_t take = __brev(~below) & elig;
         if (a.mode == SCORE_SAMPLE && a.shist) {
           // sample pass, histogram form: one global increment per eligible
           // sampled (row, query) in the query's score histogram
@@ -603,9 +614,12 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
         if (base + k < a.cap) dst[base + k] = s_skey[qq * kst + k];
     }
   } else if (kFused) {
-    // ===== CNF warps: thread r evaluates tile row r for all NCH chunks =====
+    // ===== CNF warps: thread r evaluates tile row r % 128 for its share
+    // of the NCH query chunks (all of them with 4 CNF warps, half with 8) =====
     constexpr int JW = kFused ? J * TB / 4 : 2;  // u32 words of a row's ids
-    const uint32_t r = threadIdx.x - 32 * (2 + kEpiWarps);
+    constexpr int NT = kFused ? NCH * 4 / static_cast<int>(cnf_warps(NCH)) : 1;  // chunks per thread
+    const uint32_t rr = threadIdx.x - 32 * (2 + kEpiWarps);
+    const uint32_t r = rr & (kTileRows - 1), c0 = (rr / kTileRows) * NT;
     const uint32_t cslots = s_flive[NCH];
     for (uint32_t i = 0;; ++i) {
       const uint32_t t = tile_of(a, i);
@@ -623,23 +637,23 @@ __global__ void __launch_bounds__(threads_for(J > 0), 1)
                    : "r"(smem_u32(s_terms) + ts * term_tile_bytes + term_ids_bytes + r * 8));
       __syncwarp();
       if (lane == 0) mbar_arrive(ttempty + ts);
-      uint32_t el[NCH];
+      uint32_t el[NT];
       if (a.debug & 4u) {  // diagnostics: no CNF evaluation (every live query eligible)
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) el[c] = s_flive[c] ^ (tw[0] & 1u) ^ static_cast<uint32_t>(masks & 2u);
+        for (int c = 0; c < NT; ++c) el[c] = s_flive[c0 + c] ^ (tw[0] & 1u) ^ static_cast<uint32_t>(masks & 2u);
       } else {
-        cnf_row<(kFused ? J : 8), (kFused ? TB : 1), NCH>(tw, masks, a.T, smem_u32(s_ftbl), smem_u32(s_fhc),
-                                                         smem_u32(s_flive), cslots, el);
+        cnf_row<(kFused ? J : 8), (kFused ? TB : 1), NCH, NT>(tw, masks, a.T, smem_u32(s_ftbl), smem_u32(s_fhc),
+                                                             smem_u32(s_flive), cslots, c0, el);
       }
       if (t * kTileRows + r >= a.n_rows) {  // tail of the last tile
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) el[c] = 0u;
+        for (int c = 0; c < NT; ++c) el[c] = 0u;
       }
       const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
       mbar_wait(eempty + es, eph ^ 1);
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(s_elig) + ((es * NCH + c) * kTileRows + r) * 4),
+      for (int c = 0; c < NT; ++c)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(s_elig) + ((es * NCH + c0 + c) * kTileRows + r) * 4),
                      "r"(el[c])
                      : "memory");
       __syncwarp();
@@ -698,8 +712,9 @@ uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 
 
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
+  const size_t n_tbl = T <= 255 ? 256 : T + 1;  // u8 ids index a 256-entry table
   return 128 + size_t{term_slots} * kTileRows * (wb + 8) + size_t{kEligSlots} * nch * kTileRows * 4 +
-         16 * (term_slots + kEligSlots) + 4 * ((T + 1) * nch + C * nch + nch + 1) + T + 1 + 16;
+         16 * (term_slots + kEligSlots) + 4 * (n_tbl * nch + C * nch + nch + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
@@ -726,7 +741,7 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
     if (ri < 0) throw Error(HYRE_INTERNAL, "fused CNF: unsupported compact row shape");
     k = fused[ri][ci];
   }
-  k<<<grid, threads_for(a.fused != 0), smem, st>>>(qhi, qlo, a);
+  k<<<grid, threads_for(a.fused != 0, static_cast<int>(tc_fused_chunks(a.Np))), smem, st>>>(qhi, qlo, a);
 }
 
 }  // namespace hyreb

@@ -95,11 +95,41 @@ struct TermDict {
       }
   }
   const Term* find(uint64_t k) const {
+    if (!dense.empty()) {  // direct (slot, id) table
+      const uint64_t slot = k >> 32, id = k & 0xFFFFFFFFu;
+      if (slot >= dense_base.size() - 1 || id >= dense_base[slot + 1] - dense_base[slot]) return nullptr;
+      const uint32_t at = dense[dense_base[slot] + id];
+      return at == UINT32_MAX ? nullptr : &vals[at];
+    }
     if (keys.empty()) return nullptr;
     for (uint64_t i = hash(k) & mask;; i = (i + 1) & mask) {
       if (keys[i] == k) return &vals[i];
       if (keys[i] == ~0ull) return nullptr;
     }
+  }
+  // After the last emplace: when the ids of every slot are small enough
+  // (sum over slots of max id + 1 <= 16M), a direct table replaces probing
+  // on the per-query lookup path (one load per clause id).
+  std::vector<uint64_t> dense_base;  // [slots + 1] offsets into dense
+  std::vector<uint32_t> dense;       // slot table entry -> index into vals, or ~0
+  void finalize() {
+    uint64_t slots = 0;
+    std::vector<uint64_t> max_id;
+    for (uint64_t k : keys)
+      if (k != ~0ull) {
+        const uint64_t s = k >> 32;
+        if (s >= max_id.size()) max_id.resize(s + 1, 0);
+        max_id[s] = std::max<uint64_t>(max_id[s], k & 0xFFFFFFFFu);
+        slots = std::max<uint64_t>(slots, s + 1);
+      }
+    uint64_t total = 0;
+    for (uint64_t s = 0; s < slots; ++s) total += max_id[s] + 1;
+    if (slots == 0 || slots > 1024 || total > (16u << 20)) return;
+    dense_base.assign(slots + 1, 0);
+    for (uint64_t s = 0; s < slots; ++s) dense_base[s + 1] = dense_base[s] + max_id[s] + 1;
+    dense.assign(total, UINT32_MAX);
+    for (uint64_t i = 0; i < keys.size(); ++i)
+      if (keys[i] != ~0ull) dense[dense_base[keys[i] >> 32] + (keys[i] & 0xFFFFFFFFu)] = static_cast<uint32_t>(i);
   }
 };
 

@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -68,6 +69,32 @@ int mask_path() {
     return std::string(e) == "bitmap" ? 1 : (std::string(e) == "fwd" ? 2 : 0);
   }();
   return v;
+}
+// HYRE_DEBUG_PREP: accumulate host prepare phase times, print at exit.
+struct PrepProfile {
+  double t[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<std::array<double, 6>> calls;
+  uint64_t n = 0;
+  bool on = std::getenv("HYRE_DEBUG_PREP") != nullptr;
+  ~PrepProfile() {
+    if (!on || calls.empty()) return;
+    std::array<double, 6> med{};
+    for (int i = 0; i < 6; ++i) {
+      std::vector<double> v;
+      for (auto& c : calls) v.push_back(c[i]);
+      std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+      med[i] = v[v.size() / 2];
+    }
+    std::fprintf(stderr, "[hyre] prepare median us/call (%zu calls): queries %.1f program %.1f sample %.1f qsplit %.1f "
+                 "pack %.1f h2d %.1f\n", calls.size(), med[0], med[1], med[2], med[3], med[4], med[5]);
+  }
+};
+PrepProfile g_prep;
+double us_since(std::chrono::steady_clock::time_point& t0) {
+  const auto t1 = std::chrono::steady_clock::now();
+  const double us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+  t0 = t1;
+  return us;
 }
 uint16_t bf16_rne(float f) {  // round-to-nearest-even, as __float2bfloat16_rn
   uint32_t u;
@@ -160,6 +187,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (b > max_batch)
     validation("batch size " + std::to_string(b) + " exceeds maxBatch " + std::to_string(max_batch));
   HYRE_CUDA(cudaSetDevice(ix->device));
+  auto tp = std::chrono::steady_clock::now();
   B = b;
   const uint32_t dp = ix->dp, nw = ix->num_words, W = ix->words;
   const QueryShape shape{ix->num_clauses, ix->dim};
@@ -268,6 +296,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     hit_off[i] = total_hits;
     total_hits += p.k;
   }
+  if (g_prep.on) g_prep.t[0] += us_since(tp);
   q_cl[b] = static_cast<uint32_t>(cl_slot.size());
   cl_t.push_back(static_cast<uint32_t>(t_ids.size()));
   scatter_total = items.empty() ? 0 : item_prefix.back() + items.back().count;
@@ -317,6 +346,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (!use_fused) {
     if (use_fwd) build_forward_program(); else build_term_major_program();
   }
+  if (g_prep.on) g_prep.t[1] += us_since(tp);
   // sampling period: sampled survivors ~ k * period must fit the candidate buffer
   uint32_t period = 1;
   while (period < 256 && uint64_t{period} * 2 * max_k * 4 <= cap) period *= 2;
@@ -346,21 +376,23 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   sample_rows = (n_samp_seg - 1) * kSegRows +
                 std::min<uint32_t>(kSegRows, ix->n_rows - (n_samp_seg - 1) * period * kSegRows);
 
+  if (g_prep.on) g_prep.t[2] += us_since(tp);
   // tensor-core path: bf16 (hi, lo) split of the unit queries, padded to
   // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
   if (use_tc) {
     const size_t rows = size_t{tc_groups} * tc_np;
     qhi_h.assign(rows * dp, 0);
-    qlo_h.assign(rows * dp, 0);
+    if (prefilter) qlo_h.clear(); else qlo_h.assign(rows * dp, 0);
     for (uint32_t i = 0; i < b; ++i)
       for (uint32_t e = 0; e < dp; ++e) {
         const float x = qvec[size_t{i} * dp + e];
         const uint16_t h = bf16_rne(x);
         qhi_h[size_t{i} * dp + e] = h;
-        qlo_h[size_t{i} * dp + e] = bf16_rne(x - bf16_to_f(h));
+        if (!prefilter) qlo_h[size_t{i} * dp + e] = bf16_rne(x - bf16_to_f(h));  // the prefilter reads Q_hi only
       }
   }
 
+  if (g_prep.on) g_prep.t[3] += us_since(tp);
   // ---- pack and upload ----------------------------------------------------
   size_t off = 0;
   auto place = [&](size_t bytes) {
@@ -396,12 +428,13 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (use_fused) std::memcpy(h_blob + o_fz, fz_words.data(), fz_words.size() * 4);
   if (use_tc) {
     std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
-    std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
+    if (!qlo_h.empty()) std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
   }
+  if (g_prep.on) g_prep.t[4] += us_since(tp);
   HYRE_CUDA(cudaMemcpyAsync(d_blob, h_blob, off, cudaMemcpyHostToDevice, st));
   if (use_tc) {
     make_bf16_map(&tm_qhi, d_blob + o_qhi, size_t{tc_groups} * tc_np, dp, tc_np);
-    make_bf16_map(&tm_qlo, d_blob + o_qlo, size_t{tc_groups} * tc_np, dp, tc_np);
+    make_bf16_map(&tm_qlo, d_blob + (prefilter ? o_qhi : o_qlo), size_t{tc_groups} * tc_np, dp, tc_np);
   }
   h2d_bytes = off;
   // eligibility input bytes: distinct bitmaps W*4 each, CSR
@@ -434,6 +467,14 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_fwd = reinterpret_cast<uint32_t*>(d_blob + o_fwd);
   d_fz = reinterpret_cast<uint32_t*>(d_blob + o_fz);
   prepared = true;
+  if (g_prep.on) {
+    g_prep.t[5] += us_since(tp);
+    std::array<double, 6> c{};
+    for (int i = 0; i < 6; ++i) c[i] = g_prep.t[i];
+    g_prep.calls.push_back(c);
+    ++g_prep.n;
+    std::fill(std::begin(g_prep.t), std::end(g_prep.t), 0.0);
+  }
 }
 
 // One scorer pass (main / sample / rerun) over every embedding query: K3 on

@@ -351,6 +351,7 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
         ix->terms.emplace(hk[i], t);
         begin += hdf[i];
       }
+      ix->terms.finalize();
       ix->stats.num_terms = T;
       ix->stats.bitmap_terms = ix->n_bitmap_terms;
       if (ix->n_bitmap_terms) {

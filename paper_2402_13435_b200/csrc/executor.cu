@@ -311,7 +311,12 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
   prefilter = use_tc && prefilter_enabled();
   if (use_tc) {
-    tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);  // epilogue works in 32-column chunks
+    // one group of up to 256 queries per pass (the epilogue works in 32-column
+    // chunks); a group must leave room for a >= 3-stage ring next to its
+    // query tile, else groups of 128
+    tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);
+    if (tc_np > 128 && tc_smem_bytes(tc_np, ix->dp / 64, tc_load_ops(), 3, 0, tc_q_planes(), 1) > 200 * 1024)
+      tc_np = 128;
     tc_groups = (b + tc_np - 1) / tc_np;
   }
   // Fused CNF: an all-hybrid, quant-free tensor-core batch evaluates the
@@ -359,7 +364,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     // K3: the sample pass feeds per-query score histograms (no dense buffer),
     // so it can afford ~kTcSampleSegs segments; a denser sample tightens the
     // estimated threshold (~8 x period admitted rows per query)
-    uint32_t segs = kTcSampleSegs;
+    // (at most 1/64 of the index: a small index samples fewer rows, which
+    // also bounds the histogram increments of match-all batches)
+    uint32_t segs = std::max<uint32_t>(8, std::min<uint32_t>(kTcSampleSegs, n_seg / 64));
     if (const char* e = std::getenv("HYRE_TC_SAMPLE_SEGS")) segs = std::max(1, std::atoi(e));
     period = std::max<uint32_t>(1, (n_seg + segs - 1) / segs);
     if (const char* e = std::getenv("HYRE_SAMPLE_PERIOD"))
@@ -507,6 +514,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.shist = mode == SCORE_SAMPLE ? d_shist : nullptr;
       ta.hbins = kHistBins;
       ta.aps = tc_aps;
+      ta.acc_bufs = tc_acc_bufs(tc_np);
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;

@@ -40,7 +40,8 @@ constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM 
 // fused CNF warps: one thread per tile row and query-chunk share (4 warps
 // for one 32-query chunk, 8 -- two chunk halves per row -- for 2 or 4 chunks)
 __host__ __device__ constexpr uint32_t cnf_warps(int nch) { return nch == 1 ? 4u : 8u; }
-constexpr uint32_t kAccBufs = 4;                  // TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
+constexpr uint32_t kAccBufs = 4;                  // max TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
+constexpr uint32_t kMaxWarpChunks = 4;            // 32-query chunks per epilogue warp (Np <= 256)
 constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight
 __host__ __device__ constexpr uint32_t threads_for(bool fused, int nch) {
   return 64 + 32 * kEpiWarps + (fused ? 32 * cnf_warps(nch) : 0);
@@ -259,6 +260,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Np = a.Np, kb = a.kblocks, S = a.stages;
+  const uint32_t AB = a.acc_bufs;  // TMEM accumulator buffers (4, or 2 for Np > 128): a power of two
+  const uint32_t ab_shift = AB == 4 ? 2u : (AB == 2 ? 1u : 0u);
   const uint32_t q_box = Np * 128;  // bytes of one K-atom of the query tile
   const uint32_t q_bytes = q_box * kb;
   const uint32_t a_bytes = kAtomBytes;  // one 128-byte K atom of 128 rows of one plane
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     for (uint32_t i = 0;; ++i) {
       const uint32_t t = tile_of(a, i);
       if (t == UINT32_MAX) break;
-      const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
+      const uint32_t acc = i & (AB - 1), aph = (i >> ab_shift) & 1;
       if (!(a.debug & 8u)) mbar_wait(tempty + acc, aph ^ 1);  // debug bit3: ignore the accumulator ring
       fence_after();
       const uint32_t d = tmem + acc * Np;
@@ -472,14 +475,17 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
   } else if (warp < 2 + kEpiWarps) {
     // ===== epilogue: TMEM -> registers -> mask / clamp / threshold -> candidates =====
     // 8 warps: lane quadrant = warp % 4 (TMEM access rule), column half =
-    // (warp - 2) / 4; each warp owns chunks c = half, half + 2 (32 queries each).
+    // (warp - 2) / 4; each warp owns chunks c = half, half + 2, ... (32
+    // queries each; up to 4 chunks at Np = 256).
     const uint32_t quad = warp & 3, ewarp = warp - 2, half = ewarp >> 2;
     const uint32_t nq32 = Np / 32;
-    uint32_t mw[2] = {0u, 0u};  // mask words of the current tile (lane l: query 32c + l)
-    auto load_mask = [&](uint32_t t, uint32_t (&out)[2]) {
+    // chunks per warp: NCH / 2 for a fused group (compile time), up to 4 otherwise
+    constexpr uint32_t WC = kFused ? (NCH >= 2 ? NCH / 2 : 1) : kMaxWarpChunks;
+    uint32_t mw[WC] = {};  // mask words of the current tile (lane l: query 32c + l)
+    auto load_mask = [&](uint32_t t, uint32_t (&out)[WC]) {
       if (kFused) return;
 #pragma unroll
-      for (uint32_t cc = 0; cc < 2; ++cc) {
+      for (uint32_t cc = 0; cc < WC; ++cc) {
         const uint32_t c = half + 2 * cc;
         const uint32_t qq = c * 32 + lane;
         out[cc] = (c < nq32 && t != UINT32_MAX && ((s_act[c] >> lane) & 1u))
@@ -490,18 +496,18 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     uint32_t t = tile_of(a, 0);
     load_mask(t, mw);
     for (uint32_t i = 0; t != UINT32_MAX; ++i) {
-      const uint32_t acc = i % kAccBufs, aph = (i / kAccBufs) & 1;
+      const uint32_t acc = i & (AB - 1), aph = (i >> ab_shift) & 1;
       const uint32_t t_next = tile_of(a, i + 1);
-      uint32_t mw_next[2];
+      uint32_t mw_next[WC];
       load_mask(t_next, mw_next);  // in flight while this tile is processed
       const uint32_t grow = a.row_base + t * kTileRows + quad * 32 + lane;
-      uint32_t fel[2] = {0u, 0u};  // fused: bit j = row `lane` eligible for query 32c + j
+      uint32_t fel[WC] = {};  // fused: bit j = row `lane` eligible for query 32c + j
       if (kFused) {
-        // this row's eligibility words for chunks half, half + 2 (CNF warps)
+        // this row's eligibility words for chunks half, half + 2, ... (CNF warps)
         const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
         mbar_wait(efull + es, eph);
 #pragma unroll
-        for (uint32_t cc = 0; cc < 2; ++cc) {
+        for (uint32_t cc = 0; cc < WC; ++cc) {
           const uint32_t c = half + 2 * cc;
           if (c < NCH)
             asm volatile("ld.shared.u32 %0, [%1];"
@@ -516,16 +522,22 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       // not unrolled: one copy of the (large) chunk body keeps the
       // instruction-cache footprint small when a warp owns two chunks
 #pragma unroll 1
-      for (uint32_t cc = 0; cc < 2; ++cc) {
+      for (uint32_t cc = 0; cc < WC; ++cc) {
         const uint32_t c = half + 2 * cc;
         if (c >= nq32 || (a.debug & 2u)) break;
         uint32_t v[32];
         tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
         // 32x32 bit transpose: lane l held query (32c+l)'s word over this
         // warp's 32 rows; afterwards bit j of `elig` = row `lane`, query 32c+j.
-        uint32_t elig = cc ? mw[1] : mw[0];
+        // (register arrays indexed by a runtime cc: select, no local memory)
+        uint32_t elig = mw[0], fe = fel[0];
+#pragma unroll
+        for (uint32_t x = 1; x < WC; ++x) {
+          elig = cc == x ? mw[x] : elig;
+          fe = cc == x ? fel[x] : fe;
+        }
         if (kFused) {
-          elig = cc ? fel[1] : fel[0];
+          elig = fe;
         } else {
 #pragma unroll
           for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
@@ -596,8 +608,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
-      mw[0] = mw_next[0];
-      mw[1] = mw_next[1];
+#pragma unroll
+      for (uint32_t cc = 0; cc < WC; ++cc) mw[cc] = mw_next[cc];
       t = t_next;
     }
     // final flush of the CTA's staged keys once every epilogue warp is done:
@@ -696,9 +708,11 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
   if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+uint32_t tc_acc_bufs(uint32_t Np) { return Np <= 128 ? kAccBufs : 2u; }  // 512 TMEM columns
+
 uint32_t tc_tmem_cols(uint32_t Np) {
   uint32_t cols = 32;
-  while (cols < kAccBufs * Np) cols <<= 1;
+  while (cols < tc_acc_bufs(Np) * Np) cols <<= 1;
   return cols;
 }
 
@@ -708,7 +722,7 @@ size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, 
          4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes;
 }
 
-uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 4u); }
+uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : (Np <= 128 ? 4u : 8u)); }
 
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
@@ -721,8 +735,9 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
                      cudaStream_t st) {
   using KFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
   // [id width: u8 J = 8/16/24/32, u16 J = 16/32][query chunks 1/2/4]
-#define HYRE_TC_ROW(J, TB) {tc_score_kernel<J, TB, 1>, tc_score_kernel<J, TB, 2>, tc_score_kernel<J, TB, 4>}
-  static const KFn fused[6][3] = {HYRE_TC_ROW(8, 1),  HYRE_TC_ROW(16, 1), HYRE_TC_ROW(24, 1),
+#define HYRE_TC_ROW(J, TB) \
+  {tc_score_kernel<J, TB, 1>, tc_score_kernel<J, TB, 2>, tc_score_kernel<J, TB, 4>, tc_score_kernel<J, TB, 8>}
+  static const KFn fused[6][4] = {HYRE_TC_ROW(8, 1),  HYRE_TC_ROW(16, 1), HYRE_TC_ROW(24, 1),
                                   HYRE_TC_ROW(32, 1), HYRE_TC_ROW(16, 2), HYRE_TC_ROW(32, 2)};
 #undef HYRE_TC_ROW
   static bool attr = false;
@@ -734,7 +749,7 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
   }
   KFn k = tc_score_kernel<0, 1, 1>;
   if (a.fused) {
-    const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : 2);
+    const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : (nch == 4 ? 2 : 3));
     int ri = -1;
     if (a.tb == 1) ri = a.J == 8 ? 0 : a.J == 16 ? 1 : a.J == 24 ? 2 : a.J == 32 ? 3 : -1;
     else if (a.tb == 2) ri = a.J == 16 ? 4 : a.J == 32 ? 5 : -1;

@@ -55,12 +55,13 @@ struct TcArgs {
   uint32_t prefilter;
   uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
   float delta;
+  uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))
   uint32_t aps;         // K atoms per pipeline stage (divides kblocks; one MMA commit per stage)
   uint32_t term_slots;  // fused CNF: tiles of row term lists in flight (ring depth, <= kMaxTermSlots)
 };
 
 constexpr uint32_t kTcMinBatch = 9;  // batches above 8 queries use the tensor-core scorer
-constexpr uint32_t kTcMaxGroup = 128;
+constexpr uint32_t kTcMaxGroup = 256;
 
 void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0,
@@ -68,9 +69,10 @@ size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, 
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots);
 constexpr uint32_t kMaxTermSlots = 8;
-// TMEM columns for the accumulator buffers of a group of Np queries
+// TMEM accumulator buffers / columns for a group of Np queries (512 columns)
+uint32_t tc_acc_bufs(uint32_t Np);
 uint32_t tc_tmem_cols(uint32_t Np);
-// query chunks of a fused group as laid out in its program (1, 2 or 4)
+// query chunks of a fused group as laid out in its program (1, 2, 4 or 8)
 uint32_t tc_fused_chunks(uint32_t Np);
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st);

@@ -387,7 +387,7 @@ def _cnf_index(hy, n, dim, C, V, max_ids, seed, dtype="f32"):
 
 
 @pytest.mark.parametrize("B,dim,dtype", [(16, 64, "f32"), (64, 128, "f32"), (200, 128, "f32"), (64, 128, "bf16"),
-                                         (9, 256, "f32")])
+                                         (9, 256, "f32"), (256, 128, "bf16"), (300, 64, "f32")])
 def test_tensor_core_batch_matches_oracle(hy, B, dim, dtype):
     from paper_2402_13435_b200 import workloads as W
     w, prod, ref = _cnf_index(hy, 70_000, dim, 4, 6, 3, 5)

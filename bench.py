@@ -386,7 +386,8 @@ def run_ours(args, w):
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm,
                      "peak_kind": f"{peak_kind} hbm_gbs (burst copy)", "unit": "GB/s", "frac": achieved / hbm,
                      "bytes_per_launch": bytes_main, "launch_ms": main_avg, "traffic": traffic,
-                     "eligibility": "fused CNF over forward term lists" if fused else "K1 mask bitmaps",
+                     "eligibility": ("none (match-all batch)" if path & 16 else
+                                     "fused CNF over compact CNF rows" if fused else "K1 mask bitmaps"),
                      "path_flags": path},
         "e2e": {"value": B * e2e_steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
                 "d2h_bytes_per_step": int(d2h.value), "api": "hyre_execute_batch (C-ABI, host buffers)",

@@ -322,8 +322,13 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // Fused CNF: an all-hybrid, quant-free tensor-core batch evaluates the
   // clauses in K3's epilogue from the forward term lists, when the group's
   // term tables fit next to a >= 3-stage ring.
+  // A tensor-core batch whose queries are all match-all (no clauses) needs
+  // no eligibility pass at all: K3 treats every row as eligible.
+  all_match = use_tc && !any_quant && !any_term_only;
+  for (uint32_t i = 0; i < b && all_match; ++i)
+    if ((qp[i].flags & QF_ACTIVE) && !(qp[i].flags & QF_MATCH_ALL)) all_match = false;
   use_fused = false;
-  if (use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
+  if (!all_match && use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31 && ix->cnf_ids) {
     const size_t kb = ix->dp / 64;
     use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024;
@@ -331,6 +336,8 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (use_tc) plan_tc();
   if (use_fused) {
     build_fused_program();
+  } else if (all_match) {
+    // no program
   } else if (use_fwd && mask_path() != 2) {
     // Cost model (measured on B200, c3): the term-major bitmap kernel costs
     // ~1.3 us per (32-query group x distinct ref) per 10M rows, the forward
@@ -348,7 +355,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       return prepare(qs, b);
     }
   }
-  if (!use_fused) {
+  if (!use_fused && !all_match) {
     if (use_fwd) build_forward_program(); else build_term_major_program();
   }
   if (g_prep.on) g_prep.t[1] += us_since(tp);
@@ -459,8 +466,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   scan_bytes = 0;
   if (use_tc) {
     const uint64_t emb = uint64_t{ix->n_rows} * ix->dp * 2 * tc_load_ops();
-    const uint64_t elig = use_fused ? uint64_t{ix->n_rows} * (ix->cnf_row_bytes + 8)
-                                    : uint64_t{ix->words} * 4 * tc_np;
+    const uint64_t elig = all_match ? 0
+                          : use_fused ? uint64_t{ix->n_rows} * (ix->cnf_row_bytes + 8)
+                                      : uint64_t{ix->words} * 4 * tc_np;
     scan_bytes = (emb + elig) * tc_groups;
   }
   d_qp = reinterpret_cast<QParam*>(d_blob + o_qp);
@@ -515,6 +523,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.hbins = kHistBins;
       ta.aps = tc_aps;
       ta.acc_bufs = tc_acc_bufs(tc_np);
+      ta.match_all = all_match ? 1u : 0u;
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
@@ -791,9 +800,10 @@ void Executor::run() {
   uint32_t* rerun = d_counters + 4 * max_batch;
   HYRE_CUDA(cudaEventRecord(ev[0], st));
   HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
-  if (use_fused) {
-    // eligibility is evaluated inside K3; the eligible counts are unknown
-    // (all-ones), which K4's rerun logic treats as "at least K"
+  if (use_fused || all_match) {
+    // eligibility is evaluated inside K3 (or every row is eligible); the
+    // eligible counts are unknown (all-ones), which K4's rerun logic treats as
+    // "at least K"
     HYRE_CUDA(cudaMemsetAsync(n_elig, 0xFF, sizeof(uint32_t) * B, st));
   } else if (use_fwd) {
     for (const FwdPass& fp : fwd_pass) {
@@ -810,7 +820,7 @@ void Executor::run() {
                    d_scratch, W, st);
     ++kernels;
   }
-  if (!use_fwd && !use_fused) {
+  if (!use_fwd && !use_fused && !all_match) {
     MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
                 d_mask, d_chunk_cnt, n_elig};
     const uint32_t ml = launch_mask_tm(ma, prog_groups, prog_live, st);

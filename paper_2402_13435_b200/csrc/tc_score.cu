@@ -76,6 +76,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   } while (!done);
 }
 
+// Wait for the many-warp roles (epilogue, CNF): after a failed try_wait the
+// warp sleeps briefly before re-testing.  try_wait's own suspension ends after
+// ~100 cycles whatever the hint, so without the back-off waiting warps re-poll
+// continuously and their spin instructions (measured: up to 25% of K3's issued
+// instructions) take issue slots from the warps doing work on the same SMSP.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  while (!done) {
+    __nanosleep(64);
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -483,7 +505,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     constexpr uint32_t WC = kFused ? (NCH >= 2 ? NCH / 2 : 1) : kMaxWarpChunks;
     uint32_t mw[WC] = {};  // mask words of the current tile (lane l: query 32c + l)
     auto load_mask = [&](uint32_t t, uint32_t (&out)[WC]) {
-      if (kFused) return;
+      if (kFused || a.match_all) return;
 #pragma unroll
       for (uint32_t cc = 0; cc < WC; ++cc) {
         const uint32_t c = half + 2 * cc;
@@ -505,7 +527,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       if (kFused) {
         // this row's eligibility words for chunks half, half + 2, ... (CNF warps)
         const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
-        mbar_wait(efull + es, eph);
+        mbar_wait_backoff(efull + es, eph);
 #pragma unroll
         for (uint32_t cc = 0; cc < WC; ++cc) {
           const uint32_t c = half + 2 * cc;
@@ -517,7 +539,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(eempty + es);
       }
-      mbar_wait(tfull + acc, aph);
+      mbar_wait_backoff(tfull + acc, aph);
       fence_after();
       // not unrolled: one copy of the (large) chunk body keeps the
       // instruction-cache footprint small when a warp owns two chunks
@@ -538,6 +560,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         }
         if (kFused) {
           elig = fe;
+        } else if (a.match_all) {  // every active query, every row inside the shard
+          elig = (t * kTileRows + quad * 32 + lane < a.n_rows) ? s_act[c] : 0u;
         } else {
 #pragma unroll
           for (uint32_t j = 16, m = 0x0000FFFFu; j > 0; j >>= 1, m ^= m << j) {
@@ -637,7 +661,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       const uint32_t t = tile_of(a, i);
       if (t == UINT32_MAX) break;
       const uint32_t ts = i % TS, tph = (i / TS) & 1;
-      mbar_wait(ttfull + ts, tph);
+      mbar_wait_backoff(ttfull + ts, tph);
       uint32_t tw[JW];
       const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.wb;
 #pragma unroll
@@ -662,7 +686,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         for (int c = 0; c < NT; ++c) el[c] = 0u;
       }
       const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
-      mbar_wait(eempty + es, eph ^ 1);
+      mbar_wait_backoff(eempty + es, eph ^ 1);
 #pragma unroll
       for (int c = 0; c < NT; ++c)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(s_elig) + ((es * NCH + c0 + c) * kTileRows + r) * 4),

@@ -56,6 +56,7 @@ struct TcArgs {
   uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
   float delta;
   uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))
+  uint32_t match_all;   // non-fused: every query of the batch is match-all (no mask; all rows eligible)
   uint32_t aps;         // K atoms per pipeline stage (divides kblocks; one MMA commit per stage)
   uint32_t term_slots;  // fused CNF: tiles of row term lists in flight (ring depth, <= kMaxTermSlots)
 };

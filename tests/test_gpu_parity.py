@@ -415,6 +415,35 @@ def test_tensor_core_batch_matches_oracle(hy, B, dim, dtype):
         assert_topk_match(ref, q.embedding, gr, gs, er, es, emb_override=emb_scored)
 
 
+@pytest.mark.parametrize("B,dtype", [(64, "f32"), (256, "bf16")])
+def test_match_all_tensor_core_batch(hy, B, dtype):
+    # A batch of match-all queries runs K3 with no eligibility pass at all
+    # (every row of the shard eligible, the tail tile masked): exact against
+    # the oracle's full scan and identical to single-query execution.
+    from paper_2402_13435_b200 import workloads as W
+    w, prod, ref = _cnf_index(hy, 50_003, 64, 4, 6, 3, 5)
+    dev = prod.device(0, dtype)
+    ex = hy.Executor(dev, max_batch=B)
+    _, qemb = W.queries(W.Workload("q", 0, 64, 4, 6, 2, 3, 10, B, "cnf", qseed=33), B)
+    emb_scored = ref.embeddings
+    if dtype == "bf16":
+        import torch
+        emb_scored = torch.from_numpy(ref.embeddings).to(torch.bfloat16).float().numpy()
+    batch = hy.BatchRequest([hy.HybridQuery(hy.CnfQuery(), qemb[i], [100, 7, 1000][i % 3],
+                                            hy.ExecOptions(quant_enabled=False)) for i in range(B)])
+    outs = ex.execute_batch(batch)
+    rows = np.arange(ref.num_docs)
+    single = hy.Executor(dev, max_batch=1)
+    for i, (q, o) in enumerate(zip(batch.queries, outs)):
+        assert o.ok
+        qq, _ = O.unit_embedding(q.embedding)
+        er, es = O.top_k(rows, O.scores_rows(emb_scored, qq, rows), q.k)
+        gr, gs = hits(o.result)
+        assert_topk_match(ref, q.embedding, gr, gs, er, es, emb_override=emb_scored)
+        if i % 16 == 0:
+            assert [(h.row_id, h.score) for h in o.result.hits] == [(h.row_id, h.score) for h in single.execute(q).hits]
+
+
 @pytest.mark.parametrize("B", [1, 16])
 def test_candidate_overflow_recovers(hy, B):
     # Scores increase with the row id, so the strided sample (early rows)

@@ -138,6 +138,7 @@ struct DevIndex {
   uint32_t n_rows = 0, row_base = 0, dim = 0, dp = 0;
   uint32_t words = 0, n_chunks = 0;  // W and W / kChunkWords
   uint32_t emb_dtype = HYRE_EMB_F32;
+  float max_row_norm = 1.0f;  // largest row L2 norm (1 for frozen rows; scales the K3 prefilter bound)
   bool tensor_path = false;
   uint32_t num_clauses = 0, num_bits = 0, num_words = 0;
   uint64_t seed = 0;

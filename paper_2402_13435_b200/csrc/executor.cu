@@ -517,7 +517,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.debug = tc_debug_flags();
       ta.prefilter = prefilter ? 1u : 0u;
       ta.plane_bytes = ix->tc_plane_bytes;
-      ta.delta = kPrefilterDelta;
+      ta.delta = prefilter_delta();
       ta.term_slots = tc_term_slots;
       ta.shist = mode == SCORE_SAMPLE ? d_shist : nullptr;
       ta.hbins = kHistBins;
@@ -627,7 +627,7 @@ void Executor::final_select(SelectArgs fa) {
     return;
   }
   const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
-  fa.delta = kPrefilterDelta;
+  fa.delta = prefilter_delta();
   PrefSelectArgs pa{fa, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
                     ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
   launch_select_prefilter(pa, bf16, st);
@@ -845,7 +845,7 @@ void Executor::run() {
       HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       HistThrArgs ha{d_shist, kHistBins, d_qp, n_elig, cap, sample_period, B, QF_ACTIVE | QF_EMB, d_thr, d_thr_safe,
-                     prefilter ? kPrefilterDelta : 0.0f};
+                     prefilter ? prefilter_delta() : 0.0f};
       launch_hist_thr(ha, st);
       ++kernels;
     } else if (ix->n_rows > cap) {
@@ -853,7 +853,7 @@ void Executor::run() {
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       SelectArgs ka{nullptr, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
                     nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows,
-                    d_samp, ix->row_base, d_cand, cap, prefilter ? kPrefilterDelta : 0.0f};
+                    d_samp, ix->row_base, d_cand, cap, prefilter ? prefilter_delta() : 0.0f};
       launch_sample_kth(ka, samp_cnt, st);
       ++kernels;
     } else {

@@ -1,6 +1,7 @@
 // Executor state (see executor.cu).
 #pragma once
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -19,6 +20,8 @@ struct Executor {
   // element, summed <= 2^-8 (1 + 2^-10) |e| |q| (Cauchy-Schwarz); plus fp32
   // accumulation (measured < 2e-5 at d = 128, here allowed 2.4e-4).
   static constexpr float kPrefilterDelta = 1.0f / 256 + 1.0f / 4096;
+  // the bound for this index: |e| |q| <= max_row_norm (unit queries)
+  float prefilter_delta() const { return kPrefilterDelta * std::max(1.0f, ix->max_row_norm); }
   static constexpr uint32_t kSampleRows = 40 * 1024;  // dense sample slots per query (~40K sampled rows: measured optimum at c3)
   static constexpr uint32_t kFwdMinBatch = 9;          // batches above 8 queries use K1b
 

@@ -103,6 +103,19 @@ __global__ void slot_of_kernel(const uint64_t* uniq, uint32_t T, uint8_t* slot_o
 }
 
 // x = hi + lo with hi = RNE_bf16(x), lo = RNE_bf16(x - hi): |x - hi - lo| <= 2^-17 |x|.
+// Largest squared row norm of the shard (positive floats order like their
+// bit patterns): bounds the K3 prefilter error for rows that are not unit
+// vectors (an index wrapped from external arrays).
+__global__ void max_norm_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t* out) {
+  float mx = 0.0f;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (uint32_t e = 0; e < dp; ++e) s = fmaf(src[size_t{r} * dp + e], src[size_t{r} * dp + e], s);
+    mx = fmaxf(mx, s);
+  }
+  atomicMax(out, __float_as_uint(mx));
+}
+
 __global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
   for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) {
     const float x = src[i];
@@ -201,6 +214,17 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
     HYRE_CUDA(cudaMemcpy2D(f32, dp * sizeof(float), f.embeddings.data() + size_t{rb} * d,
                            d * sizeof(float), d * sizeof(float), n, cudaMemcpyHostToDevice));
     const unsigned blocks = static_cast<unsigned>(std::min<size_t>((elems + 255) / 256, 148 * 64));
+    {
+      DPtr<uint32_t> mx(dmalloc<uint32_t>(1));
+      HYRE_CUDA(cudaMemset(mx.get(), 0, 4));
+      max_norm_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(f32, n, dp,
+                                                                                                          mx.get());
+      uint32_t bits = 0;
+      HYRE_CUDA(cudaMemcpy(&bits, mx.get(), 4, cudaMemcpyDeviceToHost));
+      float sq;
+      std::memcpy(&sq, &bits, 4);
+      ix->max_row_norm = std::sqrt(sq) * (1.0f + 1e-6f);
+    }
     if (dp % 64 == 0 && (ix->tensor_path || bf16)) {
       const uint32_t kb = dp / 64, ops = bf16 ? 1 : 2;
       const uint64_t n_tiles = (n + 127) / 128;

@@ -39,7 +39,7 @@ __host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np 
 constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
 // fused CNF warps: one thread per tile row and query-chunk share (4 warps
 // for one 32-query chunk, 8 -- two chunk halves per row -- for 2 or 4 chunks)
-__host__ __device__ constexpr uint32_t cnf_warps(int nch) { return nch == 1 ? 4u : 8u; }
+__host__ __device__ constexpr uint32_t cnf_warps(int nch) { return nch <= 2 ? 4u : 8u; }
 constexpr uint32_t kAccBufs = 4;                  // max TMEM accumulators (MMA runs up to 4 tiles ahead of the epilogue)
 constexpr uint32_t kMaxWarpChunks = 4;            // 32-query chunks per epilogue warp (Np <= 256)
 constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight

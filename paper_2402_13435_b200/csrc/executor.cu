@@ -798,13 +798,21 @@ void Executor::run() {
   uint32_t* samp_cnt = d_counters + 2 * max_batch;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
-  HYRE_CUDA(cudaEventRecord(ev[0], st));
-  HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
+  mark(0, true);
+  const bool hist_sample = any_emb && use_tc && ix->n_rows > cap;
   if (use_fused || all_match) {
-    // eligibility is evaluated inside K3 (or every row is eligible); the
-    // eligible counts are unknown (all-ones), which K4's rerun logic treats as
-    // "at least K"
-    HYRE_CUDA(cudaMemsetAsync(n_elig, 0xFF, sizeof(uint32_t) * B, st));
+    // One init kernel instead of three memsets: counters zeroed; eligible
+    // counts unknown (all-ones: eligibility is evaluated inside K3, or every
+    // row is eligible), which K4's rerun logic treats as "at least K"; the
+    // sample histograms zeroed.
+    launch_run_init(d_counters, max_batch * kNumCounters, B, hist_sample ? d_shist : nullptr,
+                    size_t{B} * kHistBins, st);
+    ++kernels;
+  } else {
+    HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
+    if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
+  }
+  if (use_fused || all_match) {
   } else if (use_fwd) {
     for (const FwdPass& fp : fwd_pass) {
       FwdArgs fa{ix->row_terms, ix->slot_of, ix->row_terms_width, ix->n_rows, W, ix->n_chunks, B, ix->num_clauses,
@@ -830,7 +838,7 @@ void Executor::run() {
     }
     kernels += ml & 0x7fffffffu;
   }
-  HYRE_CUDA(cudaEventRecord(ev[1], st));
+  mark(1, !use_fused && !all_match);  // K1/K1b mask pass (the K3 init kernel is attributed to the sample stage)
   if (any_quant) {
     HYRE_CUDA(cudaMemsetAsync(d_qhist, 0, sizeof(uint32_t) * B * (ix->num_bits + 1), st));
     QuantArgs qa{ix->sigs, ix->num_words, ix->num_bits, d_qsig, d_qp, B, W, ix->n_chunks, ix->n_rows,
@@ -838,11 +846,10 @@ void Executor::run() {
     launch_quant(qa, st);
     kernels += 5;
   }
-  HYRE_CUDA(cudaEventRecord(ev[2], st));
+  mark(2, any_quant);
   if (any_emb) {
-    if (ix->n_rows > cap && use_tc) {
-      // K3 sample pass into per-query score histograms -> thresholds
-      HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
+    if (hist_sample) {
+      // K3 sample pass into per-query score histograms (zeroed above) -> thresholds
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       HistThrArgs ha{d_shist, kHistBins, d_qp, n_elig, cap, sample_period, B, QF_ACTIVE | QF_EMB, d_thr, d_thr_safe,
                      prefilter ? prefilter_delta() : 0.0f};
@@ -860,9 +867,9 @@ void Executor::run() {
       HYRE_CUDA(cudaMemsetAsync(d_thr, 0, sizeof(uint64_t) * B, st));
       HYRE_CUDA(cudaMemsetAsync(d_thr_safe, 0, sizeof(uint64_t) * B, st));
     }
-    HYRE_CUDA(cudaEventRecord(ev[3], st));
+    mark(3, true);
     score(SCORE_MAIN, d_cand, cand_cnt, cap);
-    HYRE_CUDA(cudaEventRecord(ev[4], st));
+    mark(4, true);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
                   out_cnt, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, 0};
     final_select(fa);
@@ -871,8 +878,8 @@ void Executor::run() {
     // flags with the results and runs it then, so the common batch costs no
     // speculative kernels.
   } else {
-    HYRE_CUDA(cudaEventRecord(ev[3], st));
-    HYRE_CUDA(cudaEventRecord(ev[4], st));
+    mark(3, false);
+    mark(4, false);
   }
   if (any_term_only) {
     FirstKArgs fk{d_mask, d_chunk_cnt, n_elig, d_qp, B, W, ix->n_chunks, ix->row_base, d_hit_off, d_hits,
@@ -880,7 +887,7 @@ void Executor::run() {
     launch_first_k(fk, st);
     ++kernels;
   }
-  HYRE_CUDA(cudaEventRecord(ev[5], st));
+  mark(5, true);
   HYRE_CUDA(cudaGetLastError());
 }
 
@@ -960,30 +967,46 @@ void Executor::eligible(uint32_t* out) {
 float Executor::last_run_ms() const {
   float ms = 0;
   cudaEventSynchronize(ev[5]);
-  cudaEventElapsedTime(&ms, ev[0], ev[5]);
+  const uint8_t* map = ev_map[(n_runs - 1) % kEvRing];
+  cudaEventSynchronize(ev[map[5]]);
+  cudaEventElapsedTime(&ms, ev[map[0]], ev[map[5]]);
   return ms;
+}
+
+// Stage times of one ring slot: boundary i is the event ev_map[slot][i] (an
+// empty stage records no event and reuses the previous boundary: 0 ms).
+static void slot_stage_ms(const cudaEvent_t* e, const uint8_t* map, float* out) {
+  cudaEventSynchronize(e[map[5]]);
+  for (int i = 0; i < 5; ++i) {
+    out[i] = 0;
+    if (map[i] != map[i + 1]) cudaEventElapsedTime(out + i, e[map[i]], e[map[i + 1]]);
+  }
+  out[5] = 0;
+  cudaEventElapsedTime(out + 5, e[map[0]], e[map[5]]);
 }
 
 void Executor::stage_ms_hist(uint32_t back, float* out) const {
   if (back >= kEvRing || back >= n_runs) throw Error(HYRE_INVALID_ARGUMENT, "no such run in the timing ring");
-  const cudaEvent_t* e = ev_ring[(n_runs - 1 - back) % kEvRing];
-  cudaEventSynchronize(e[5]);
-  for (int i = 0; i < 5; ++i) {
-    out[i] = 0;
-    cudaEventElapsedTime(out + i, e[i], e[i + 1]);
-  }
-  out[5] = 0;
-  cudaEventElapsedTime(out + 5, e[0], e[5]);
+  const uint64_t slot = (n_runs - 1 - back) % kEvRing;
+  slot_stage_ms(ev_ring[slot], ev_map[slot], out);
 }
 
 void Executor::stage_ms(float* out) const {
-  cudaEventSynchronize(ev[5]);
-  for (int i = 0; i < 5; ++i) {
-    out[i] = 0;
-    cudaEventElapsedTime(out + i, ev[i], ev[i + 1]);
+  if (n_runs == 0) throw Error(HYRE_INVALID_ARGUMENT, "no run to time");
+  const uint64_t slot = (n_runs - 1) % kEvRing;
+  slot_stage_ms(ev_ring[slot], ev_map[slot], out);
+}
+
+// Boundary i of the current run: an event when its stage did work, else an
+// alias of boundary i - 1 (each event record costs ~1-2 us of stream time).
+void Executor::mark(int i, bool stage_ran) {
+  uint8_t* map = ev_map[(n_runs - 1) % kEvRing];
+  if (i == 0 || stage_ran) {
+    HYRE_CUDA(cudaEventRecord(ev[i], st));
+    map[i] = static_cast<uint8_t>(i);
+  } else {
+    map[i] = map[i - 1];
   }
-  out[5] = 0;
-  cudaEventElapsedTime(out + 5, ev[0], ev[5]);
 }
 
 // ---------------------------------------------------------------------------

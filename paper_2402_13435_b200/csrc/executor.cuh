@@ -32,6 +32,7 @@ struct Executor {
   // post-main, end (ring slot = run counter % kEvRing); ev = the current slot
   static constexpr uint32_t kEvRing = 64;
   cudaEvent_t ev_ring[kEvRing][6] = {};
+  uint8_t ev_map[kEvRing][6] = {};  // boundary -> recorded event of that slot (see mark())
   cudaEvent_t* ev = ev_ring[0];
   uint64_t n_runs = 0;
 
@@ -46,7 +47,7 @@ struct Executor {
   uint32_t* d_samp = nullptr;  // dense sample scores [max_batch][samp_cap] (K2 sample pass)
   uint32_t* d_shist = nullptr;  // K3 sample pass: score histograms [max_batch][kHistBins]
   static constexpr uint32_t kHistBins = 4096;    // linear bins over [-1, 1] (width 4.9e-4)
-  static constexpr uint32_t kTcSampleSegs = 80;  // K3 sample: ~80 x 1024 rows (c3 sweep 80/160/320/640: 80 best)
+  static constexpr uint32_t kTcSampleSegs = 60;  // K3 sample: ~60 x 1024 rows (c3 sweeps 40-640: 60 best)
   uint32_t* d_qhist = nullptr;
   uint32_t* d_tsel = nullptr;
   uint32_t* d_eqcnt = nullptr;
@@ -154,6 +155,7 @@ struct Executor {
   void build_fused_program();
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
   void final_select(SelectArgs fa);
+  void mark(int boundary, bool stage_ran);
   uint32_t finish_rounds = 0;  // recovery rounds fetch() ran for the last batch (diagnostics)
 };
 

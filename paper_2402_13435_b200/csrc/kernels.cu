@@ -2,6 +2,7 @@
 // argument behind each one; reference functions are cited per kernel.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -1102,6 +1103,20 @@ __global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
   }
 }
 
+__global__ void run_init_kernel(uint32_t* counters, uint32_t n_counters, uint32_t B, uint4* hist, size_t hist_vec) {
+  const size_t stride = size_t{gridDim.x} * blockDim.x;
+  const size_t t0 = size_t{blockIdx.x} * blockDim.x + threadIdx.x;
+  for (size_t i = t0; i < n_counters; i += stride) counters[i] = i < B ? 0xFFFFFFFFu : 0u;
+  for (size_t i = t0; i < hist_vec; i += stride) hist[i] = make_uint4(0, 0, 0, 0);
+}
+
+void launch_run_init(uint32_t* counters, uint32_t n_counters, uint32_t B, uint32_t* hist, size_t hist_words,
+                     cudaStream_t st) {
+  const size_t hv = hist ? hist_words / 4 : 0;  // hist_words is a multiple of 4096
+  const uint32_t blocks = static_cast<uint32_t>(std::min<size_t>(592, (std::max<size_t>(hv, n_counters) + 255) / 256));
+  run_init_kernel<<<std::max(1u, blocks), 256, 0, st>>>(counters, n_counters, B, reinterpret_cast<uint4*>(hist), hv);
+}
+
 void launch_hist_thr(const HistThrArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
   hist_thr_kernel<<<a.B, 256, 0, st>>>(a);
@@ -1142,7 +1157,7 @@ namespace {
 template <typename RowT, int LPR, int CPL>
 __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys, uint32_t n, float thr_s,
                              uint32_t* above) {
-  constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems, U = CPL >= 8 ? 1 : (CPL >= 4 ? 2 : 4);  // rows in flight per lane group
+  constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems, U = CPL >= 8 ? 1 : (CPL >= 4 ? 2 : (CPL >= 2 ? 4 : 8));  // rows in flight per lane group
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane / LPR, li = lane % LPR;
   float qv[CPL][E];
@@ -1224,8 +1239,25 @@ __global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelec
     __syncthreads();
   }
   const uint64_t* src = resident ? res : keys;
+  // tau_s: a lower bound on the K-th largest prefilter score, the lower edge
+  // of its bin in a 4096-bin linear histogram over [-1, 1] (bin width 4.9e-4,
+  // one pass; K candidates lie at or above the edge, which is all steps 1-3
+  // need -- a lower tau only admits a few more survivors)
   float tau_s = -4.0f;
-  if (n > k) tau_s = key_score(kth_largest(src, n, k, hist, tmp));
+  if (n > k) {
+    __shared__ uint32_t s_sel[4];
+    for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      uint32_t b = 0xffffffffu;
+      if (i < n) b = min(static_cast<uint32_t>((key_score(src[i]) + 1.0f) * 2048.0f), 4095u);
+      hist_add(hist, b);
+    }
+    __syncthreads();
+    kth_bins(hist, k, k, tmp, s_sel);
+    tau_s = -1.0f + static_cast<float>(s_sel[0]) / 2048.0f - 1e-6f;
+  }
   const float prune = tau_s - 2.0f * a.delta;
   // 2. survivors -> sortbuf, rescored in place
   if (threadIdx.x == 0) {
@@ -1270,17 +1302,31 @@ __global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelec
     __syncthreads();
     m = min(gathered, kSelectMaxK);
   }
-  uint32_t m2 = 1;
-  while (m2 < m) m2 <<= 1;
-  for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
-  __syncthreads();
-  bitonic_desc(sortbuf, m2);
   const uint32_t take = min(m, k);
   hyre_hit* out = a.hits + a.hit_off[q];
-  for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
-    const uint64_t key = sortbuf[i];
-    out[i].row = key_row(key);
-    out[i].score = key_score(key);
+  if (m <= 1024) {
+    // rank by counting (keys are unique): no sort stages, one pass over the
+    // survivors per key in shared memory (broadcast reads)
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint64_t key = sortbuf[i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) rank += sortbuf[j] > key ? 1u : 0u;
+      if (rank < take) {
+        out[rank].row = key_row(key);
+        out[rank].score = key_score(key);
+      }
+    }
+  } else {
+    uint32_t m2 = 1;
+    while (m2 < m) m2 <<= 1;
+    for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
+    __syncthreads();
+    bitonic_desc(sortbuf, m2);
+    for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
+      const uint64_t key = sortbuf[i];
+      out[i].row = key_row(key);
+      out[i].score = key_score(key);
+    }
   }
   if (threadIdx.x == 0) {
     a.out_cnt[q] = take;

@@ -158,6 +158,10 @@ struct HistThrArgs {
   float delta;
 };
 void launch_hist_thr(const HistThrArgs& a, cudaStream_t st);
+// Run prologue of a K3 batch: counters[0 .. n_counters) = 0 except the first
+// B (eligible counts) = ~0 (unknown), and hist[0 .. hist_words) = 0.
+void launch_run_init(uint32_t* counters, uint32_t n_counters, uint32_t B, uint32_t* hist, size_t hist_words,
+                     cudaStream_t st);
 
 // ---- K5: term-only first-K rows (pipeline.cpp:30-40) ----
 struct FirstKArgs {

@@ -153,6 +153,11 @@ struct DevIndex {
   // (contiguous, so its DRAM pattern is a plain sequential scan).
   uint8_t* tc_tiles = nullptr;
   uint64_t tc_plane_bytes = 0;
+  // int8 prefilter plane (dp % 128 == 0): q = rint(x / i8_scale) in the same
+  // tile layout (a K-atom = 128 int8 elements); i8_rmax = the largest row
+  // residual ||x - i8_scale q||_2 (the row part of the prefilter bound)
+  uint8_t* tc_i8 = nullptr;
+  float i8_scale = 0.0f, i8_rmax = 0.0f;
   uint32_t tc_ops = 0;
   uint64_t* sigs = nullptr;
   uint32_t* bitmaps = nullptr;

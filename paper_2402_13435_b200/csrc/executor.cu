@@ -52,12 +52,20 @@ bool fused_enabled() {
   }();
   return v;
 }
-// HYRE_PREFILTER=0 disables the K3 bf16 prefilter + exact rescore (the K3
-// pass then reads the full hi/lo split and scores at fp32 grade directly).
+// HYRE_PREFILTER=0 disables the K3 prefilter + exact rescore (the K3 pass
+// then reads the full hi/lo split and scores at fp32 grade directly);
+// HYRE_PREFILTER=bf16 forces the bf16 prefilter over the int8 one.
 bool prefilter_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("HYRE_PREFILTER");
     return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+bool prefilter_i8_allowed() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_PREFILTER");
+    return !(e && std::string(e) == "bf16");
   }();
   return v;
 }
@@ -310,12 +318,13 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
                                     : d_scratch + size_t{ref_src[r].second} * W;
   use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
   prefilter = use_tc && prefilter_enabled();
+  pf_i8 = prefilter && ix->tc_i8 != nullptr && ix->dp % 128 == 0 && prefilter_i8_allowed();
   if (use_tc) {
     // one group of up to 256 queries per pass (the epilogue works in 32-column
     // chunks); a group must leave room for a >= 3-stage ring next to its
     // query tile, else groups of 128
     tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);
-    if (tc_np > 128 && tc_smem_bytes(tc_np, ix->dp / 64, tc_load_ops(), 3, 0, tc_q_planes(), 1) > 200 * 1024)
+    if (tc_np > 128 && tc_smem_bytes(tc_np, tc_kb(), tc_load_ops(), 3, 0, tc_q_planes(), 1) > 200 * 1024)
       tc_np = 128;
     tc_groups = (b + tc_np - 1) / tc_np;
   }
@@ -330,7 +339,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   use_fused = false;
   if (!all_match && use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31 && ix->cnf_ids) {
-    const size_t kb = ix->dp / 64;
+    const size_t kb = tc_kb();
     use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024;
   }
   if (use_tc) plan_tc();
@@ -393,7 +402,36 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (g_prep.on) g_prep.t[2] += us_since(tp);
   // tensor-core path: bf16 (hi, lo) split of the unit queries, padded to
   // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
-  if (use_tc) {
+  qdelta_h.assign(b, prefilter ? prefilter_delta() : 0.0f);
+  qscale_h.assign(b, 0.0f);
+  if (use_tc && pf_i8) {
+    // int8 prefilter: q8 = rint(q / s_q), s_q = max|q| / 127 per query; the
+    // bound: |s - s'| <= r_e |q| + (|e| + r_e) r_q + 1e-5 with
+    // r_e the index's largest row residual, r_q = ||q - s_q q8||
+    const size_t rows = size_t{tc_groups} * tc_np;
+    qi8_h.assign(rows * dp, 0);
+    const double re = ix->i8_rmax, en = std::max(1.0f, ix->max_row_norm) * 1.004;
+    for (uint32_t i = 0; i < b; ++i) {
+      const float* q = qvec.data() + size_t{i} * dp;
+      float amax = 0.0f;
+      double qn = 0.0;
+      for (uint32_t e = 0; e < dp; ++e) {
+        amax = std::max(amax, std::fabs(q[e]));
+        qn += static_cast<double>(q[e]) * q[e];
+      }
+      const float sq = amax > 0.0f ? amax / 127.0f : 1.0f, inv = amax > 0.0f ? 127.0f / amax : 0.0f;
+      double rq = 0.0;
+      for (uint32_t e = 0; e < dp; ++e) {
+        const float v = std::nearbyint(q[e] * inv);
+        const int8_t q8 = static_cast<int8_t>(std::min(127.0f, std::max(-127.0f, v)));
+        qi8_h[size_t{i} * dp + e] = q8;
+        const double d = static_cast<double>(q[e]) - static_cast<double>(sq) * q8;
+        rq += d * d;
+      }
+      qscale_h[i] = ix->i8_scale * sq;
+      qdelta_h[i] = static_cast<float>(re * std::sqrt(qn) * (1.0 + 1e-6) + (en + re) * std::sqrt(rq) + 1e-5);
+    }
+  } else if (use_tc) {
     const size_t rows = size_t{tc_groups} * tc_np;
     qhi_h.assign(rows * dp, 0);
     if (prefilter) qlo_h.clear(); else qlo_h.assign(rows * dp, 0);
@@ -424,8 +462,10 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   const size_t o_items = place(std::max<size_t>(items.size(), 1) * sizeof(ScatterItem));
   const size_t o_ipre = place(std::max<size_t>(item_prefix.size(), 1) * 8);
   const size_t o_fwd = place(std::max<size_t>(fwd_words.size(), 1) * 4);
-  const size_t o_qhi = place(std::max<size_t>(qhi_h.size(), 1) * 2);
+  const size_t o_qhi = place(std::max<size_t>(pf_i8 ? (qi8_h.size() + 1) / 2 : qhi_h.size(), 1) * 2);
   const size_t o_qlo = place(std::max<size_t>(qlo_h.size(), 1) * 2);
+  const size_t o_qsc = place(b * 4);
+  const size_t o_qdl = place(b * 4);
   const size_t o_fz = place(std::max<size_t>(fz_words.size(), 1) * 4);
   ensure_blob(off);
   std::memcpy(h_blob + o_qp, qp.data(), b * sizeof(QParam));
@@ -441,13 +481,17 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (!fwd_words.empty()) std::memcpy(h_blob + o_fwd, fwd_words.data(), fwd_words.size() * 4);
   if (use_fused) std::memcpy(h_blob + o_fz, fz_words.data(), fz_words.size() * 4);
   if (use_tc) {
-    std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
+    if (pf_i8) std::memcpy(h_blob + o_qhi, qi8_h.data(), qi8_h.size());
+    else std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
     if (!qlo_h.empty()) std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
   }
   if (g_prep.on) g_prep.t[4] += us_since(tp);
+  std::memcpy(h_blob + o_qsc, qscale_h.data(), b * 4);
+  std::memcpy(h_blob + o_qdl, qdelta_h.data(), b * 4);
   HYRE_CUDA(cudaMemcpyAsync(d_blob, h_blob, off, cudaMemcpyHostToDevice, st));
   if (use_tc) {
-    make_bf16_map(&tm_qhi, d_blob + o_qhi, size_t{tc_groups} * tc_np, dp, tc_np);
+    if (pf_i8) make_i8_map(&tm_qhi, d_blob + o_qhi, size_t{tc_groups} * tc_np, dp, tc_np);
+    else make_bf16_map(&tm_qhi, d_blob + o_qhi, size_t{tc_groups} * tc_np, dp, tc_np);
     make_bf16_map(&tm_qlo, d_blob + (prefilter ? o_qhi : o_qlo), size_t{tc_groups} * tc_np, dp, tc_np);
   }
   h2d_bytes = off;
@@ -465,7 +509,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // mask words)
   scan_bytes = 0;
   if (use_tc) {
-    const uint64_t emb = uint64_t{ix->n_rows} * ix->dp * 2 * tc_load_ops();
+    const uint64_t emb = uint64_t{ix->n_rows} * ix->dp * (pf_i8 ? 1 : 2 * tc_load_ops());
     const uint64_t elig = all_match ? 0
                           : use_fused ? uint64_t{ix->n_rows} * (ix->cnf_row_bytes + 8)
                                       : uint64_t{ix->words} * 4 * tc_np;
@@ -481,6 +525,8 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_ipre = reinterpret_cast<uint64_t*>(d_blob + o_ipre);
   d_fwd = reinterpret_cast<uint32_t*>(d_blob + o_fwd);
   d_fz = reinterpret_cast<uint32_t*>(d_blob + o_fz);
+  d_qscale = reinterpret_cast<float*>(d_blob + o_qsc);
+  d_qdelta = reinterpret_cast<float*>(d_blob + o_qdl);
   prepared = true;
   if (g_prep.on) {
     g_prep.t[5] += us_since(tp);
@@ -499,7 +545,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   uint32_t* rerun = d_counters + 4 * max_batch;
   if (use_tc) {
     const uint32_t n_tiles = (ix->n_rows + 127) / 128;
-    const uint32_t kb = ix->dp / 64;
+    const uint32_t kb = tc_kb();
     const uint32_t n_ops = tc_load_ops();
     const uint32_t stages = tc_stages;
     const size_t fzb = use_fused ? tc_fz_bytes(tc_term_slots) : 0;
@@ -511,13 +557,16 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
     }
     const uint32_t grid = std::max(1u, std::min(work, 148u));
     for (uint32_t g = 0; g < tc_groups; ++g) {
-      TcArgs ta{ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
+      TcArgs ta{pf_i8 ? ix->tc_i8 : ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 n_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
                 rerun, d_samp};
       ta.debug = tc_debug_flags();
       ta.prefilter = prefilter ? 1u : 0u;
       ta.plane_bytes = ix->tc_plane_bytes;
       ta.delta = prefilter_delta();
+      ta.i8 = pf_i8 ? 1u : 0u;
+      ta.qscale = d_qscale;
+      ta.qdelta = prefilter ? d_qdelta : nullptr;
       ta.term_slots = tc_term_slots;
       ta.shist = mode == SCORE_SAMPLE ? d_shist : nullptr;
       ta.hbins = kHistBins;
@@ -567,7 +616,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
 // ~150 KB in flight per SM sustain HBM rate at ~3 us loaded latency), then
 // prefers more stages.
 void Executor::plan_tc() {
-  const uint32_t kb = ix->dp / 64;
+  const uint32_t kb = tc_kb();
   // Stage = aps K-atoms: the largest divisor of kb that still leaves a
   // >= 3-stage ring, so each tile costs few MMA commits / barrier round trips
   // (tcgen05.commit per stage was measured to pace the MMA issuer).
@@ -628,6 +677,7 @@ void Executor::final_select(SelectArgs fa) {
   }
   const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
   fa.delta = prefilter_delta();
+  fa.qdelta = d_qdelta;
   PrefSelectArgs pa{fa, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
                     ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
   launch_select_prefilter(pa, bf16, st);
@@ -852,7 +902,7 @@ void Executor::run() {
       // K3 sample pass into per-query score histograms (zeroed above) -> thresholds
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       HistThrArgs ha{d_shist, kHistBins, d_qp, n_elig, cap, sample_period, B, QF_ACTIVE | QF_EMB, d_thr, d_thr_safe,
-                     prefilter ? prefilter_delta() : 0.0f};
+                     prefilter ? prefilter_delta() : 0.0f, prefilter ? d_qdelta : nullptr};
       launch_hist_thr(ha, st);
       ++kernels;
     } else if (ix->n_rows > cap) {

@@ -109,6 +109,12 @@ struct Executor {
   bool prefilter = false;  // K3 reads the hi plane only; candidates rescored exactly (final_select())
   uint32_t tc_load_ops() const { return prefilter ? 1u : ix->tc_ops; }
   uint32_t tc_q_planes() const { return prefilter ? 1u : 2u; }
+  bool pf_i8 = false;  // the prefilter runs on the int8 plane (kind::i8 MMAs)
+  uint32_t tc_kb() const { return ix->dp / (pf_i8 ? 128 : 64); }  // 128-byte K atoms per row
+  std::vector<int8_t> qi8_h;
+  std::vector<float> qscale_h, qdelta_h;  // per query: int8 score scale, prefilter bound
+  float* d_qscale = nullptr;
+  float* d_qdelta = nullptr;
   uint32_t tc_stages = 2, tc_term_slots = 2, tc_aps = 1;  // K3 ring depths, K atoms per stage (plan_tc)
   void plan_tc();
   size_t tc_fz_bytes(uint32_t term_slots) const;

@@ -116,6 +116,61 @@ __global__ void max_norm_kernel(const float* src, uint32_t n, uint32_t dp, uint3
   atomicMax(out, __float_as_uint(mx));
 }
 
+// int8 prefilter plane (K3 "i8" prefilter): one global scale s = max|x| / 127
+// (x = the row values the exact rescoring reads: fp32, or bf16 for a bf16
+// index), q = clamp(rint(x / s), -127, 127), in the same pre-swizzled
+// SWIZZLE_128B tile layout as the bf16 planes (a 128-byte K-atom = 128 int8
+// elements).  The largest per-row residual ||x - s q||_2 bounds the prefilter
+// error.
+__device__ __forceinline__ float prefilter_src(const float* src, size_t i, bool bf16) {
+  const float x = src[i];
+  return bf16 ? __bfloat162float(__float2bfloat16_rn(x)) : x;
+}
+
+__global__ void max_abs_kernel(const float* src, size_t elems, bool bf16, uint32_t* out) {
+  float mx = 0.0f;
+  for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < elems; i += size_t{gridDim.x} * blockDim.x)
+    mx = fmaxf(mx, fabsf(prefilter_src(src, i, bf16)));
+  atomicMax(out, __float_as_uint(mx));
+}
+
+__device__ __forceinline__ int8_t quant_i8(float x, float inv) {
+  return static_cast<int8_t>(fminf(fmaxf(rintf(x * inv), -127.0f), 127.0f));
+}
+
+__global__ void i8_tile_kernel(const float* src, uint32_t n, uint32_t dp, uint32_t kb8, float inv, bool bf16,
+                               uint8_t* dst, uint64_t n_chunks) {
+  for (uint64_t ci = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; ci < n_chunks;
+       ci += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t atom = ci >> 10;  // 1024 chunks per 16 KB atom
+    const uint32_t within = static_cast<uint32_t>(ci & 1023);
+    const uint32_t rr = within >> 3, pc = within & 7;
+    const uint32_t lc = pc ^ (rr & 7);  // logical 16-byte chunk (SWIZZLE_128B)
+    const uint32_t k = static_cast<uint32_t>(atom % kb8);
+    const uint64_t row = (atom / kb8) * 128 + rr;
+    __align__(16) int8_t out[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      out[e] = row < n ? quant_i8(prefilter_src(src, row * dp + k * 128 + lc * 16 + e, bf16), inv) : int8_t{0};
+    *reinterpret_cast<uint4*>(dst + ci * 16) = *reinterpret_cast<const uint4*>(out);
+  }
+}
+
+__global__ void i8_resid_kernel(const float* src, uint32_t n, uint32_t dp, float scale, float inv, bool bf16,
+                                uint32_t* out) {
+  float mx = 0.0f;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint32_t e = 0; e < dp; ++e) {
+      const float x = prefilter_src(src, size_t{r} * dp + e, bf16);
+      const double d = static_cast<double>(x) - static_cast<double>(scale) * quant_i8(x, inv);
+      s += d * d;
+    }
+    mx = fmaxf(mx, static_cast<float>(sqrt(s)));
+  }
+  atomicMax(out, __float_as_uint(mx));
+}
+
 __global__ void split_kernel(const float* src, size_t n, __nv_bfloat16* hi, __nv_bfloat16* lo) {
   for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) {
     const float x = src[i];
@@ -168,6 +223,7 @@ DevIndex::~DevIndex() {
   cudaFree(emb_f32);
   cudaFree(emb_hi);
   cudaFree(tc_tiles);
+  cudaFree(tc_i8);
   cudaFree(row_terms);
   cudaFree(cnf_ids);
   cudaFree(cnf_masks);
@@ -238,6 +294,32 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
       ix->tc_plane_bytes = n_tiles * kb * 16384;
       ix->has_tc = true;
       ix->stats.tensor_bytes = tc_bytes;
+    }
+    if (dp % 128 == 0 && (ix->tensor_path || bf16)) {
+      DPtr<uint32_t> mx(dmalloc<uint32_t>(2));
+      HYRE_CUDA(cudaMemset(mx.get(), 0, 8));
+      max_abs_kernel<<<148 * 8, 256, 0, st>>>(f32, elems, bf16, mx.get());
+      uint32_t bits = 0;
+      HYRE_CUDA(cudaMemcpy(&bits, mx.get(), 4, cudaMemcpyDeviceToHost));
+      float amax;
+      std::memcpy(&amax, &bits, 4);
+      if (amax > 0.0f) {
+        const float scale = amax / 127.0f, inv = 127.0f / amax;
+        const uint32_t kb8 = dp / 128;
+        const uint64_t n_tiles = (n + 127) / 128, i8_bytes = n_tiles * kb8 * 16384, n_chunks = i8_bytes / 16;
+        ix->tc_i8 = dmalloc<uint8_t>(i8_bytes);
+        i8_tile_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n_chunks + 255) / 256, 148 * 64)), 256, 0, st>>>(
+            f32, n, dp, kb8, inv, bf16, ix->tc_i8, n_chunks);
+        i8_resid_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(
+            f32, n, dp, scale, inv, bf16, mx.get() + 1);
+        HYRE_CUDA(cudaGetLastError());
+        HYRE_CUDA(cudaMemcpy(&bits, mx.get() + 1, 4, cudaMemcpyDeviceToHost));
+        float rmax;
+        std::memcpy(&rmax, &bits, 4);
+        ix->i8_scale = scale;
+        ix->i8_rmax = rmax * (1.0f + 1e-5f) + 1e-7f;
+        ix->stats.tensor_bytes += i8_bytes;
+      }
     }
     if (bf16) {
       ix->emb_hi = dmalloc<__nv_bfloat16>(elems);

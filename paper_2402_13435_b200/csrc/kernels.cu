@@ -1099,7 +1099,8 @@ __global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
     };
     const uint64_t t_safe = s_bin[0] == UINT32_MAX ? 0ull : edge_key(s_bin[0]);
     a.thr[q] = s_bin[1] == UINT32_MAX ? 0ull : edge_key(s_bin[1]);
-    a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
+    const float dl = a.qdelta ? a.qdelta[q] : a.delta;
+    a.thr_safe[q] = dl > 0.0f ? key_minus_delta(t_safe, dl) : t_safe;
   }
 }
 
@@ -1223,10 +1224,11 @@ __global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelec
     }
     return;
   }
+  const float dl = a.qdelta ? a.qdelta[q] : a.delta;  // this query's prefilter bound
   if (total > a.cap) {  // overflow: the kept subset's K-th prefilter key, lowered by delta, bounds the exact K-th
     const uint64_t t = kth_largest(keys, n, k, hist, tmp);
     if (threadIdx.x == 0) {
-      a.thr[q] = key_minus_delta(t, a.delta);
+      a.thr[q] = key_minus_delta(t, dl);
       a.rerun[q] = 1;
     }
     return;
@@ -1258,7 +1260,7 @@ __global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelec
     kth_bins(hist, k, k, tmp, s_sel);
     tau_s = -1.0f + static_cast<float>(s_sel[0]) / 2048.0f - 1e-6f;
   }
-  const float prune = tau_s - 2.0f * a.delta;
+  const float prune = tau_s - 2.0f * dl;
   // 2. survivors -> sortbuf, rescored in place
   if (threadIdx.x == 0) {
     gathered = 0;
@@ -1280,7 +1282,7 @@ __global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelec
   }
   __syncthreads();
   // 3. threshold validity (select_kernel's rule with the prefilter bound)
-  const bool valid = (n >= k && tau_s - a.delta >= thr_s) || above >= min(k, a.n_elig[q]);
+  const bool valid = (n >= k && tau_s - dl >= thr_s) || above >= min(k, a.n_elig[q]);
   if (!valid && has_safe) {
     if (threadIdx.x == 0) {
       a.thr[q] = a.thr_safe[q];

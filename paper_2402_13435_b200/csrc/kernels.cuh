@@ -124,6 +124,7 @@ struct SelectArgs {
   // K3 prefilter bound: KTH lowers thr_safe by delta (the sample holds
   // prefilter scores); select_prefilter_kernel prunes and checks with it.
   float delta;
+  const float* qdelta;  // per-query bounds (replace delta when given)
 };
 void launch_select(const SelectArgs& a, cudaStream_t st);
 // K4 for K3 prefilter candidates (SELECT_FINAL / SELECT_FINAL_RERUN; see
@@ -156,6 +157,7 @@ struct HistThrArgs {
   uint64_t* thr;
   uint64_t* thr_safe;
   float delta;
+  const float* qdelta;  // per-query bounds (replace delta when given)
 };
 void launch_hist_thr(const HistThrArgs& a, cudaStream_t st);
 // Run prologue of a K3 batch: counters[0 .. n_counters) = 0 except the first

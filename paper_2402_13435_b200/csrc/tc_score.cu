@@ -134,6 +134,15 @@ __device__ __forceinline__ void mma_bf16w(uint32_t d_tmem, uint32_t a_lo, uint32
       "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(0x40004040));
 }
 
+__device__ __forceinline__ void mma_i8w(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n .reg .b64 da, db;\n setp.ne.b32 p, %4, 0;\n"
+      " mov.b64 da, {%1, %5};\n mov.b64 db, {%2, %5};\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(0x40004040));
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -303,7 +312,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
   uint64_t* qbar = tempty + kAccBufs;
   float* s_ts = reinterpret_cast<float*>(bars + ((2 * S + 2 * kAccBufs + 2) & ~1u));  // [Np] threshold score (16-B aligned)
   uint32_t* s_tr = reinterpret_cast<uint32_t*>(s_ts + Np);     // [Np] threshold row
-  uint32_t* s_tmem = s_tr + Np;                                // TMEM base
+  float* s_sc = reinterpret_cast<float*>(s_tr + Np);           // [Np] i8: score = accumulator x s_sc
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_sc + Np);   // TMEM base
   uint32_t* s_act = s_tmem + 1;                                // [Np / 32] active bitmasks
   // per-CTA candidate staging shared by the epilogue warps: [Np][kst] keys + [Np] counts
   const uint32_t kst = stage_bytes_for(Np) / (8 * Np);
@@ -373,9 +383,21 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       s_tr[j] = 0u;
     } else {
       // prefilter: admit s' >= ts - delta (a superset of exact score >= ts)
-      const float ts = key_score(thr) - (a.prefilter ? a.delta : 0.0f);
+      const float dl = a.prefilter ? (a.qdelta ? a.qdelta[q0 + j] : a.delta) : 0.0f;
+      const float ts = key_score(thr) - dl;
       s_ts[j] = ts <= -1.0f ? -2.0f : ts;
       s_tr[j] = a.prefilter ? 0xFFFFFFFFu : key_row(thr);
+    }
+    if (a.i8) {
+      // int8 prefilter: s' = acc x scale_q, so s' >= ts  <=  acc >= floor(ts / scale_q) - 1
+      // (an integer threshold one below the exact bound absorbs the division's rounding)
+      const float sc = q0 + j < a.B ? a.qscale[q0 + j] : 1.0f, ts = s_ts[j];
+      s_sc[j] = sc;
+      int32_t T;
+      if (ts >= 2.0f) T = INT32_MAX;  // inactive: never taken
+      else if (ts <= -1.0f) T = INT32_MIN / 2;  // no threshold
+      else T = static_cast<int32_t>(fmaxf(floorf(ts / sc) - 1.0f, -1.0e9f));
+      s_ts[j] = __int_as_float(T);
     }
   }
   for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) s_scnt[j] = 0;
@@ -415,7 +437,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     if (lane == 0) {
       mbar_expect_tx(qbar, (a.prefilter ? 1 : 2) * q_bytes);
       for (uint32_t k = 0; k < kb; ++k) {
-        tma_load_2d(s_qhi + k * q_box, &tm_qhi, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
+        tma_load_2d(s_qhi + k * q_box, &tm_qhi, qbar, static_cast<int>(k * (a.i8 ? 128 : 64)),
+                    static_cast<int>(a.q_row0));
         if (!a.prefilter)
           tma_load_2d(s_qlo + k * q_box, &tm_qlo, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
       }
@@ -453,7 +476,11 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     // issues.  Descriptors are built from warp-uniform 32-bit words (low word
     // = start address >> 4 | LBO 1; high word = SBO 64 | version 1 | SW128),
     // so a K-step is one add per operand and the tcgen05.mma itself.
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((Np >> 3) << 17) | ((kTileRows >> 4) << 24);
+    // instruction descriptor: D type (bits 4-5: 1 = f32, 2 = s32), A/B types
+    // (bits 7-9 / 10-12: bf16 = 1 for kind::f16, signed int8 = 1 for
+    // kind::i8), K-major A and B, N >> 3 at bit 17, M >> 4 at bit 24
+    const uint32_t idesc = ((a.i8 ? 2u : 1u) << 4) | (1u << 7) | (1u << 10) | ((Np >> 3) << 17) |
+                           ((kTileRows >> 4) << 24);
     const uint32_t a_lo0 = (smem_u32(s_stage) >> 4) | 0x10000u;
     const uint32_t qh_lo0 = (smem_u32(s_qhi) >> 4) | 0x10000u, ql_lo0 = (smem_u32(s_qlo) >> 4) | 0x10000u;
     const uint32_t nkk = (a.debug & 16u) ? 1u : 4u;  // debug bit4: one K16 step per atom (timing only)
@@ -478,7 +505,9 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
             for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K16 per 128-byte atom (+32 B = +2 per step)
               if (kk >= nkk) break;
               const uint32_t acc_in = (k0 + k + kk) != 0;
-              mma_bf16w(d, ka + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, acc_in);
+              // one K step = 32 bytes of every row (16 bf16 or 32 int8 elements)
+              if (a.i8) mma_i8w(d, ka + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, acc_in);
+              else mma_bf16w(d, ka + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, acc_in);
               if (!a.prefilter) mma_bf16w(d, ka + 2 * kk, ql_lo0 + kq + 2 * kk, idesc, 1u);
               if (a.split) mma_bf16w(d, ka + ((aps * a_bytes) >> 4) + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, 1u);
             }
@@ -578,22 +607,37 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         // monotone rounding) and a funnel shift collecting d's sign bit.
         uint32_t below = 0;  // bit 31 - j: query 32c + j scored below its threshold
         const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
+        if (a.i8) {  // int32 accumulators against integer thresholds (no overflow: |acc|, |T| < 2^30)
 #pragma unroll
-        for (uint32_t j4 = 0; j4 < 8; ++j4) {
-          const float4 t4 = ts4[j4];
-          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 0]) - t4.x), below, 1);
-          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 1]) - t4.y), below, 1);
-          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 2]) - t4.z), below, 1);
-          below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 3]) - t4.w), below, 1);
+          for (uint32_t j4 = 0; j4 < 8; ++j4) {
+            const int4 t4 = *reinterpret_cast<const int4*>(ts4 + j4);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 0]) - t4.x), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 1]) - t4.y), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 2]) - t4.z), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 3]) - t4.w), below, 1);
+          }
+        } else {
+#pragma unroll
+          for (uint32_t j4 = 0; j4 < 8; ++j4) {
+            const float4 t4 = ts4[j4];
+            below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 0]) - t4.x), below, 1);
+            below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 1]) - t4.y), below, 1);
+            below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 2]) - t4.z), below, 1);
+            below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 3]) - t4.w), below, 1);
+          }
         }
         const uint32_t take = __brev(~below) & elig;
+        // prefilter score of (row lane, query 32c + j) from the accumulator word
+        auto score_of = [&](uint32_t w, uint32_t j) {
+          return a.i8 ? static_cast<float>(static_cast<int32_t>(w)) * s_sc[c * 32 + j] : __uint_as_float(w);
+        };
         if (a.mode == SCORE_SAMPLE && a.shist) {
           // sample pass, histogram form: one global increment per eligible
           // sampled (row, query) in the query's score histogram
           const float scale = 0.5f * static_cast<float>(a.hbins);
           for (uint32_t el = elig; el; el &= el - 1u) {
             const uint32_t j = __ffs(el) - 1;
-            const float sc = clamp_score(__uint_as_float(pick32(v, j)));
+            const float sc = clamp_score(score_of(pick32(v, j), j));
             const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);
             atomicAdd(a.shist + static_cast<size_t>(q0 + c * 32 + j) * a.hbins + b, 1u);
           }
@@ -607,7 +651,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j)
             if ((elig >> j) & 1u)
-              a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(clamp_score(__uint_as_float(v[j])));
+              a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(clamp_score(score_of(v[j], j)));
           continue;
         }
         // survivors (rare): each lane walks its own set bits; the score is
@@ -617,7 +661,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         // candidate buffer only when a query's slots are full.
         for (uint32_t tk = take; tk; tk &= tk - 1u) {
           const uint32_t j = __ffs(tk) - 1, qq = c * 32 + j;
-          const uint64_t key = make_key(clamp_score(__uint_as_float(pick32(v, j))), grow);
+          const uint64_t key = make_key(clamp_score(score_of(pick32(v, j), j)), grow);
           if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
                                                                         // (prefilter: s_tr = ~0, never)
           const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
@@ -732,6 +776,17 @@ void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t d
   if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+void make_i8_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {dp, rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(dp)};
+  const cuuint32_t box[2] = {128, box_rows};  // one 128-byte K atom of box_rows queries
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(HYRE_CUDA_ERROR, "cuTensorMapEncodeTiled (int8) failed: " + std::to_string(r));
+}
+
 uint32_t tc_acc_bufs(uint32_t Np) { return Np <= 128 ? kAccBufs : 2u; }  // 512 TMEM columns
 
 uint32_t tc_tmem_cols(uint32_t Np) {
@@ -742,7 +797,7 @@ uint32_t tc_tmem_cols(uint32_t Np) {
 
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes, uint32_t q_planes,
                      uint32_t aps) {
-  return 1024 + size_t{q_planes} * Np * 128 * kb + size_t{stages} * aps * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 8 +
+  return 1024 + size_t{q_planes} * Np * 128 * kb + size_t{stages} * aps * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 12 +
          4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes;
 }
 

@@ -53,6 +53,12 @@ struct TcArgs {
   // admitted when s' >= thr_score - delta and rescored exactly afterwards
   // (launch_rescore), so no row whose exact score passes the threshold is lost.
   uint32_t prefilter;
+  // int8 prefilter (i8 != 0; tiles = DevIndex::tc_i8, kblocks = dp / 128):
+  // kind::i8 MMAs into s32 accumulators, score s' = acc x qscale[q];
+  // per-query bounds qdelta[q] replace delta when given (bf16 prefilter too)
+  uint32_t i8;
+  const float* qscale;
+  const float* qdelta;
   uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
   float delta;
   uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))
@@ -65,6 +71,7 @@ constexpr uint32_t kTcMinBatch = 9;  // batches above 8 queries use the tensor-c
 constexpr uint32_t kTcMaxGroup = 256;
 
 void make_bf16_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
+void make_i8_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp, uint32_t box_rows);
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0,
                      uint32_t q_planes = 2, uint32_t aps = 1);
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)

@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         if (c >= nq32 || (a.debug & 2u)) break;
         uint32_t v[32];
         tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
+        if (a.debug & 128u) {  // diagnostics: TMEM loads only (results invalid)
+          if (v[0] == 0x7fffffffu && v[31] == 0x7fffffffu) a.cand_cnt[0] = 1;
+          continue;
+        }
         // 32x32 bit transpose: lane l held query (32c+l)'s word over this
         // warp's 32 rows; afterwards bit j of `elig` = row `lane`, query 32c+j.
         // (register arrays indexed by a runtime cc: select, no local memory)
@@ -626,7 +630,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
             below = __funnelshift_l(__float_as_uint(__uint_as_float(v[4 * j4 + 3]) - t4.w), below, 1);
           }
         }
-        const uint32_t take = __brev(~below) & elig;
+        const uint32_t take = (a.debug & 256u) ? ((__brev(~below) & elig) == 0x12345u ? 1u : 0u)  // diagnostics: no survivors
+                                               : (__brev(~below) & elig);
         // prefilter score of (row lane, query 32c + j) from the accumulator word
         auto score_of = [&](uint32_t w, uint32_t j) {
           return a.i8 ? static_cast<float>(static_cast<int32_t>(w)) * s_sc[c * 32 + j] : __uint_as_float(w);

@@ -62,6 +62,13 @@ bool prefilter_enabled() {
   }();
   return v;
 }
+uint32_t tc_backoff_ns() {  // HYRE_TC_BACKOFF_NS: profiling the K3 wait back-off
+  static const uint32_t v = [] {
+    const char* e = std::getenv("HYRE_TC_BACKOFF_NS");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 64u;
+  }();
+  return v;
+}
 bool prefilter_i8_allowed() {
   static const bool v = [] {
     const char* e = std::getenv("HYRE_PREFILTER");
@@ -340,7 +347,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (!all_match && use_fwd && use_tc && !any_quant && !any_term_only && fused_enabled() && mask_path() == 0 &&
       ix->num_clauses <= 31 && ix->cnf_ids) {
     const size_t kb = tc_kb();
-    use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024;
+    use_fused = tc_smem_bytes(tc_np, kb, tc_load_ops(), 3, tc_fz_bytes(2), tc_q_planes()) <= 227 * 1024 - kTcStaticSmem;
   }
   if (use_tc) plan_tc();
   if (use_fused) {
@@ -573,6 +580,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.aps = tc_aps;
       ta.acc_bufs = tc_acc_bufs(tc_np);
       ta.match_all = all_match ? 1u : 0u;
+      ta.backoff_ns = tc_backoff_ns();
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
@@ -623,7 +631,8 @@ void Executor::plan_tc() {
   auto plan = [&](uint32_t aps, uint32_t slots) {
     const size_t stage_bytes = size_t{tc_load_ops()} * aps * 128 * 128;
     const size_t fixed = tc_smem_bytes(tc_np, kb, tc_load_ops(), 0, use_fused ? tc_fz_bytes(slots) : 0, tc_q_planes(), aps);
-    const size_t budget = 227 * 1024 > fixed ? 227 * 1024 - fixed : 0;
+    const size_t cap_b = 227 * 1024 - (use_fused ? kTcStaticSmem : 64);
+    const size_t budget = cap_b > fixed ? cap_b - fixed : 0;
     return static_cast<uint32_t>(std::min<size_t>(12, budget / stage_bytes));
   };
   uint32_t aps_max = kb;

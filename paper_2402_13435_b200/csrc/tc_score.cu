@@ -81,7 +81,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 // ~100 cycles whatever the hint, so without the back-off waiting warps re-poll
 // continuously and their spin instructions (measured: up to 25% of K3's issued
 // instructions) take issue slots from the warps doing work on the same SMSP.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity, uint32_t ns) {
   uint32_t done = 0;
   asm volatile(
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
@@ -89,7 +89,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) 
       : "r"(smem_u32(b)), "r"(parity)
       : "memory");
   while (!done) {
-    __nanosleep(64);
+    if (ns) __nanosleep(ns);
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
@@ -241,6 +241,12 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
     }
   }
   const uint32_t starts = static_cast<uint32_t>(masks), pres = static_cast<uint32_t>(masks >> 32);
+  // segment masks: bit j of starts lands on a byte's sign bit in starts << s,
+  // s = (7 - j) mod 8, and prmt replicates that sign across the word -- one
+  // instruction per id plus 7 shifts per row
+  uint32_t sh[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sh[k] = starts << k;
   uint32_t seg[NT], fail[NT];
 #pragma unroll
   for (int c = 0; c < NT; ++c) {
@@ -249,7 +255,8 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
   }
 #pragma unroll
   for (int j = 1; j < J; ++j) {
-    const uint32_t m = 0u - ((starts >> j) & 1u);  // all ones where id j opens a new slot segment
+    uint32_t m;  // all ones where id j opens a new slot segment
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(m) : "r"(sh[(7 - j) & 7]), "r"(((j >> 3) | 8) * 0x1111));
 #pragma unroll
     for (int c = 0; c < NT; ++c) {
       fail[c] |= seg[c] & m;
@@ -336,9 +343,13 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
   uint64_t* ttempty = s_tbar + TS;
   uint64_t* efull = s_tbar + 2 * TS;
   uint64_t* eempty = efull + kEligSlots;
-  uint32_t* s_ftbl = reinterpret_cast<uint32_t*>(eempty + kEligSlots);
+  // u8 ids: a static 256-entry table (its address folds into the loads'
+  // immediate offset); u16 ids: the table follows in dynamic memory
+  __shared__ __align__(16) uint32_t s_tbl8[(kFused && TB == 1) ? 256 * NCH : 4];
+  uint32_t* s_ftbl = (kFused && TB == 1) ? s_tbl8 : reinterpret_cast<uint32_t*>(eempty + kEligSlots);
   const uint32_t n_tbl = TB == 1 ? 256u : a.T + 1;  // table entries (u8 ids: direct index, sentinels above T)
-  uint32_t* s_fhc = s_ftbl + static_cast<size_t>(n_tbl) * NCH;
+  uint32_t* s_fhc = (kFused && TB == 1) ? reinterpret_cast<uint32_t*>(eempty + kEligSlots)
+                                        : s_ftbl + static_cast<size_t>(n_tbl) * NCH;
   uint32_t* s_flive = s_fhc + a.C * NCH;
   uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
 
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       if (kFused) {
         // this row's eligibility words for chunks half, half + 2, ... (CNF warps)
         const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
-        mbar_wait_backoff(efull + es, eph);
+        mbar_wait_backoff(efull + es, eph, a.backoff_ns);
 #pragma unroll
         for (uint32_t cc = 0; cc < WC; ++cc) {
           const uint32_t c = half + 2 * cc;
@@ -568,7 +579,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(eempty + es);
       }
-      mbar_wait_backoff(tfull + acc, aph);
+      mbar_wait_backoff(tfull + acc, aph, a.backoff_ns);
       fence_after();
       // not unrolled: one copy of the (large) chunk body keeps the
       // instruction-cache footprint small when a warp owns two chunks
@@ -710,7 +721,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       const uint32_t t = tile_of(a, i);
       if (t == UINT32_MAX) break;
       const uint32_t ts = i % TS, tph = (i / TS) & 1;
-      mbar_wait_backoff(ttfull + ts, tph);
+      mbar_wait_backoff(ttfull + ts, tph, a.backoff_ns);
       uint32_t tw[JW];
       const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.wb;
 #pragma unroll
@@ -735,7 +746,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         for (int c = 0; c < NT; ++c) el[c] = 0u;
       }
       const uint32_t es = i % kEligSlots, eph = (i / kEligSlots) & 1;
-      mbar_wait_backoff(eempty + es, eph ^ 1);
+      mbar_wait_backoff(eempty + es, eph ^ 1, a.backoff_ns);
 #pragma unroll
       for (int c = 0; c < NT; ++c)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(s_elig) + ((es * NCH + c0 + c) * kTileRows + r) * 4),
@@ -810,7 +821,7 @@ uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : 
 
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
-  const size_t n_tbl = T <= 255 ? 256 : T + 1;  // u8 ids index a 256-entry table
+  const size_t n_tbl = T <= 255 ? 0 : T + 1;  // u8 ids: static 256-entry table (kTcStaticSmem)
   return 128 + size_t{term_slots} * kTileRows * (wb + 8) + size_t{kEligSlots} * nch * kTileRows * 4 +
          16 * (term_slots + kEligSlots) + 4 * (n_tbl * nch + C * nch + nch + 1) + T + 1 + 16;
 }
@@ -826,9 +837,11 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
 #undef HYRE_TC_ROW
   static bool attr = false;
   if (!attr) {
-    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024 - 64));
     for (auto& row : fused)
-      for (KFn k : row) HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      for (KFn k : row)
+        HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kTcStaticSmem));
     attr = true;
   }
   KFn k = tc_score_kernel<0, 1, 1>;

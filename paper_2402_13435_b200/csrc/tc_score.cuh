@@ -62,6 +62,7 @@ struct TcArgs {
   uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
   float delta;
   uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))
+  uint32_t backoff_ns;  // sleep between failed barrier tests of the epilogue / CNF warps (0 = spin)
   uint32_t match_all;   // non-fused: every query of the batch is match-all (no mask; all rows eligible)
   uint32_t aps;         // K atoms per pipeline stage (divides kblocks; one MMA commit per stage)
   uint32_t term_slots;  // fused CNF: tiles of row term lists in flight (ring depth, <= kMaxTermSlots)
@@ -77,6 +78,8 @@ size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, 
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots);
 constexpr uint32_t kMaxTermSlots = 8;
+// static shared memory of the fused variants (the u8-id term table, <= 256 x 8 words)
+constexpr uint32_t kTcStaticSmem = 8 * 1024 + 64;
 // TMEM accumulator buffers / columns for a group of Np queries (512 columns)
 uint32_t tc_acc_bufs(uint32_t Np);
 uint32_t tc_tmem_cols(uint32_t Np);

@@ -36,7 +36,11 @@ constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle
 // to the global buffer) so that their larger query tile still leaves >= 4 ring
 // stages in flight
 __host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 32768u : 8192u; }
-constexpr uint32_t kEpiWarps = 8;                 // epilogue warps (2 per TMEM lane quadrant)
+// epilogue warps: 8 (2 per TMEM lane quadrant) next to the fused CNF warps;
+// 16 for the mask / match-all variant, whose only per-tile work is the
+// epilogue (large query groups need the extra warps to hide TMEM-load and
+// compare-chain latency)
+__host__ __device__ constexpr uint32_t epi_warps(bool fused) { return fused ? 8u : 16u; }
 // fused CNF warps: one thread per tile row and query-chunk share (4 warps
 // for one 32-query chunk, 8 -- two chunk halves per row -- for 2 or 4 chunks)
 __host__ __device__ constexpr uint32_t cnf_warps(int nch) { return nch <= 2 ? 4u : 8u; }
@@ -44,7 +48,7 @@ constexpr uint32_t kAccBufs = 4;                  // max TMEM accumulators (MMA 
 constexpr uint32_t kMaxWarpChunks = 4;            // 32-query chunks per epilogue warp (Np <= 256)
 constexpr uint32_t kEligSlots = 4;                // fused CNF: tiles of eligibility words in flight
 __host__ __device__ constexpr uint32_t threads_for(bool fused, int nch) {
-  return 64 + 32 * kEpiWarps + (fused ? 32 * cnf_warps(nch) : 0);
+  return 64 + 32 * epi_warps(fused) + (fused ? 32 * cnf_warps(nch) : 0);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -292,6 +296,7 @@ template <int J, int TB, int NCH>
 __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   constexpr bool kFused = J > 0;
+  constexpr uint32_t kEW = epi_warps(kFused);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align by pointer arithmetic on the shared array so every derived pointer
   // stays in the shared window (LDS/STS, not generic loads)
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     }
     for (uint32_t i = 0; i < kAccBufs; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, kEpiWarps);
+      mbar_init(tempty + i, kEW);
     }
     mbar_init(qbar, 1);
     if (kFused) {
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       }
       for (uint32_t i = 0; i < kEligSlots; ++i) {
         mbar_init(efull + i, cnf_warps(NCH));
-        mbar_init(eempty + i, kEpiWarps);
+        mbar_init(eempty + i, kEW);
       }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -534,21 +539,23 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       if (elect_one()) mma_commit(tfull + acc);  // accumulator ready for the epilogue
       __syncwarp();
     }
-  } else if (warp < 2 + kEpiWarps) {
+  } else if (warp < 2 + kEW) {
     // ===== epilogue: TMEM -> registers -> mask / clamp / threshold -> candidates =====
     // 8 warps: lane quadrant = warp % 4 (TMEM access rule), column half =
     // (warp - 2) / 4; each warp owns chunks c = half, half + 2, ... (32
     // queries each; up to 4 chunks at Np = 256).
+    // warp = 2 + 4 part + quad: chunks c = part, part + P, ... (P = kEW / 4)
+    constexpr uint32_t P = kEW / 4;
     const uint32_t quad = warp & 3, ewarp = warp - 2, half = ewarp >> 2;
     const uint32_t nq32 = Np / 32;
     // chunks per warp: NCH / 2 for a fused group (compile time), up to 4 otherwise
-    constexpr uint32_t WC = kFused ? (NCH >= 2 ? NCH / 2 : 1) : kMaxWarpChunks;
+    constexpr uint32_t WC = kFused ? (NCH >= 2 ? NCH / 2 : 1) : (kMaxWarpChunks * 2 + P - 1) / P;
     uint32_t mw[WC] = {};  // mask words of the current tile (lane l: query 32c + l)
     auto load_mask = [&](uint32_t t, uint32_t (&out)[WC]) {
       if (kFused || a.match_all) return;
 #pragma unroll
       for (uint32_t cc = 0; cc < WC; ++cc) {
-        const uint32_t c = half + 2 * cc;
+        const uint32_t c = half + P * cc;
         const uint32_t qq = c * 32 + lane;
         out[cc] = (c < nq32 && t != UINT32_MAX && ((s_act[c] >> lane) & 1u))
                       ? __ldg(a.mask + static_cast<size_t>(q0 + qq) * a.words + t * (kTileRows / 32) + quad)
@@ -570,7 +577,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
         mbar_wait_backoff(efull + es, eph, a.backoff_ns);
 #pragma unroll
         for (uint32_t cc = 0; cc < WC; ++cc) {
-          const uint32_t c = half + 2 * cc;
+          const uint32_t c = half + P * cc;
           if (c < NCH)
             asm volatile("ld.shared.u32 %0, [%1];"
                          : "=r"(fel[cc])
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
       // instruction-cache footprint small when a warp owns two chunks
 #pragma unroll 1
       for (uint32_t cc = 0; cc < WC; ++cc) {
-        const uint32_t c = half + 2 * cc;
+        const uint32_t c = half + P * cc;
         if (c >= nq32 || (a.debug & 2u)) break;
         uint32_t v[32];
         tmem_ld32(tmem + ((quad * 32) << 16) + acc * Np + c * 32, v);
@@ -698,8 +705,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     }
     // final flush of the CTA's staged keys once every epilogue warp is done:
     // warp w owns queries w, w + 8, ...; one global reservation per query
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-    for (uint32_t qq = ewarp; qq < Np; qq += kEpiWarps) {
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");
+    for (uint32_t qq = ewarp; qq < Np; qq += kEW) {
       const uint32_t ns = min(s_scnt[qq], kst);
       if (ns == 0) continue;
       uint32_t base = 0;
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
     // of the NCH query chunks (all of them with 4 CNF warps, half with 8) =====
     constexpr int JW = kFused ? J * TB / 4 : 2;  // u32 words of a row's ids
     constexpr int NT = kFused ? NCH * 4 / static_cast<int>(cnf_warps(NCH)) : 1;  // chunks per thread
-    const uint32_t rr = threadIdx.x - 32 * (2 + kEpiWarps);
+    const uint32_t rr = threadIdx.x - 32 * (2 + kEW);
     const uint32_t r = rr & (kTileRows - 1), c0 = (rr / kTileRows) * NT;
     const uint32_t cslots = s_flive[NCH];
     for (uint32_t i = 0;; ++i) {

@@ -347,8 +347,16 @@ hyre_status hyre_execute_batch(hyre_executor* ex, const hyre_query* qs, uint32_t
     need(ex, "executor");
     const auto t0 = std::chrono::steady_clock::now();
     ex->ex->prepare(qs, b);
+    const auto t1 = std::chrono::steady_clock::now();
     ex->ex->run();
+    const auto t2 = std::chrono::steady_clock::now();
     ex->ex->fetch(hits, hit_offsets, counts, statuses, timings);
+    if (std::getenv("HYRE_DEBUG_E2E")) {  // diagnostics: host phases of one call
+      const auto t3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      std::fprintf(stderr, "[hyre] execute_batch us: prepare %.1f run(launch) %.1f fetch(wait+copy) %.1f\n",
+                   us(t0, t1), us(t1, t2), us(t2, t3));
+    }
     if (timings)
       timings->total_ms =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -428,11 +428,16 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       }
       const float sq = amax > 0.0f ? amax / 127.0f : 1.0f, inv = amax > 0.0f ? 127.0f / amax : 0.0f;
       double rq = 0.0;
+      // any rounding is valid (r_q is measured on the values used); round
+      // half away from zero with a plain conversion (std::nearbyint is slow)
+      int8_t* q8 = qi8_h.data() + size_t{i} * dp;
       for (uint32_t e = 0; e < dp; ++e) {
-        const float v = std::nearbyint(q[e] * inv);
-        const int8_t q8 = static_cast<int8_t>(std::min(127.0f, std::max(-127.0f, v)));
-        qi8_h[size_t{i} * dp + e] = q8;
-        const double d = static_cast<double>(q[e]) - static_cast<double>(sq) * q8;
+        const float x = q[e] * inv;
+        const int v = static_cast<int>(x + (x >= 0.0f ? 0.5f : -0.5f));
+        q8[e] = static_cast<int8_t>(v > 127 ? 127 : (v < -127 ? -127 : v));
+      }
+      for (uint32_t e = 0; e < dp; ++e) {
+        const double d = static_cast<double>(q[e]) - static_cast<double>(sq) * q8[e];
         rq += d * d;
       }
       qscale_h[i] = ix->i8_scale * sq;

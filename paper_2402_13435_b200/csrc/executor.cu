@@ -148,6 +148,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   d_eqcnt = dmalloc<uint32_t>(B * ix->n_chunks);
   h_out_cnt.resize(B);
   h_rerun.resize(B);
+  h_cnt_rerun.resize(2 * B);
 }
 
 Executor::~Executor() {
@@ -985,10 +986,13 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
   // one round trip in the common case: results and the recovery flags
   // together; a pending recovery (candidate overflow) reruns and re-copies
   for (int pass = 0;; ++pass) {
-    if (any_emb) HYRE_CUDA(cudaMemcpyAsync(h_rerun.data(), rerun, B * 4, cudaMemcpyDeviceToHost, st));
-    HYRE_CUDA(cudaMemcpyAsync(h_out_cnt.data(), out_cnt, B * 4, cudaMemcpyDeviceToHost, st));
+    // out counts and rerun flags are adjacent counter rows: one copy for both
+    HYRE_CUDA(cudaMemcpyAsync(h_cnt_rerun.data(), out_cnt, sizeof(uint32_t) * (max_batch + B), cudaMemcpyDeviceToHost,
+                              st));
     HYRE_CUDA(cudaMemcpyAsync(h_hits, d_hits, n_hits_total * sizeof(hyre_hit), cudaMemcpyDeviceToHost, st));
     HYRE_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(h_out_cnt.data(), h_cnt_rerun.data(), B * 4);
+    std::memcpy(h_rerun.data(), h_cnt_rerun.data() + max_batch, B * 4);
     bool pending = false;
     for (uint32_t i = 0; any_emb && i < B; ++i) pending |= h_rerun[i] != 0;
     if (!pending) break;

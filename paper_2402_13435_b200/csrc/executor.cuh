@@ -121,7 +121,7 @@ struct Executor {
   uint32_t tc_np = 0, tc_groups = 0;
   std::vector<uint16_t> qhi_h, qlo_h;
   CUtensorMap tm_qhi{}, tm_qlo{};
-  std::vector<uint32_t> h_out_cnt, h_rerun;
+  std::vector<uint32_t> h_out_cnt, h_rerun, h_cnt_rerun;
   QParam* d_qp = nullptr;
   float* d_q = nullptr;
   uint64_t* d_qsig = nullptr;

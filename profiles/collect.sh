@@ -10,8 +10,8 @@ mkdir -p gpurun_out
 # the 4th tc_score launch = the main pass of the 2nd run (each run: sample, main)
 ncu --set full --clock-control none --import-source on -k regex:tc_score -s 3 -c 1 -o gpurun_out/${T}_tc_main \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_ncu_full.log 2>&1
-# kernels of runs 3-4 (each run: K3 sample, thresholds, K3 main, K4 select)
-ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:tc_score|hist_thr|select' -s 8 -c 8 --csv \
+# kernels of runs 3-4 (each run: init, K3 sample, thresholds, K3 main, K4 select)
+ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:tc_score|hist_thr|select|run_init' -s 10 -c 10 --csv \
   --log-file gpurun_out/${T}_launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 python bench.py > gpurun_out/${T}_bench_c3.log 2>&1

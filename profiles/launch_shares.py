@@ -8,11 +8,13 @@ import json
 import sys
 
 
-def main(src, dst, per_step=4):
+def main(src, dst, per_step=None):
     rows = [r for r in csv.reader(open(src)) if len(r) > 10]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     launches = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", ""))) for r in rows[1:]]
+    if per_step is None:  # one step = up to and including the first select kernel
+        per_step = next(i for i, (k, _) in enumerate(launches) if k.startswith("select")) + 1
     step = launches[:per_step]
     total = sum(t for _, t in step)
     out = {"note": "one c3 bench step (10M x d128 fp32, 8-clause CNF, B=64, K=100) from `ncu --metrics "

@@ -619,14 +619,15 @@ def test_tensor_core_batch_equals_single_queries_exactly(hy, dtype):
         assert [(h.row_id, h.score) for h in o.result.hits] == s
 
 
-def test_prefilter_keeps_exact_order_among_bf16_indistinguishable_rows(hy):
+@pytest.mark.parametrize("dim", [64, 128])  # bf16 prefilter (dp % 128 != 0) / int8 prefilter
+def test_prefilter_keeps_exact_order_among_bf16_indistinguishable_rows(hy, dim):
     # Rows differ from a common direction by ~1e-3, so their exact scores are
     # distinct while most bf16 prefilter scores coincide: the K-th exact
     # score sits inside a band of thousands of prefilter ties.  The admitted
     # set (prefilter >= threshold - delta) must still contain the exact top-K,
     # and the rescored result must equal the exact single-query (K2) answer
     # and the oracle's.
-    n, dim = 60_000, 64
+    n = 60_000
     rs = np.random.default_rng(3)
     base = rs.standard_normal(dim).astype(np.float32)
     emb = (base[None, :] + 1e-3 * rs.standard_normal((n, dim))).astype(np.float32)
@@ -650,3 +651,19 @@ def test_prefilter_keeps_exact_order_among_bf16_indistinguishable_rows(hy):
         er, es = O.top_k(rows, O.scores_rows(ref.embeddings, qq, rows), q.k)
         gr, gs = hits(o.result)
         assert_topk_match(ref, q.embedding, gr, gs, er, es)
+
+
+@pytest.mark.parametrize("mode", ["bf16", "0"])
+def test_prefilter_modes_in_a_fresh_process(mode):
+    # The prefilter kind is fixed per process (HYRE_PREFILTER): rerun the
+    # exactness tests with the bf16 prefilter and with no prefilter (the K3
+    # hi/lo split scoring directly) in a child process.
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HYRE_PREFILTER=mode)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(root, "tests",
+                        "test_gpu_parity.py"), "-k", "equals_single or indistinguishable or tensor_core_batch_matches"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

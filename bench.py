@@ -360,7 +360,7 @@ def run_ours(args, w):
     words = (n_local + 31) // 32
     path = int(lib.hyre_batch_path(h))
     fused = bool(path & 2)
-    kernel = main_kernel_name(B)
+    kernel = main_kernel_name(B, path)
     if qemb is None:
         kernel = "mask_tm_kernel (K1: term-major CNF over bitmaps/CSR)"
         bytes_main = int(lib.hyre_batch_term_bytes(h)) + B * words * 4
@@ -370,7 +370,8 @@ def run_ours(args, w):
     else:
         elig = np.zeros(B, np.uint32)
         check(lib.hyre_batch_eligible(h, elig.ctypes.data_as(L.u32p)))
-        bytes_main = int(min(n_local, elig.max())) * w.dim * elem + B * words * 4
+        elem_k2 = 1 if path & 32 else elem  # int8 prefilter rows
+        bytes_main = int(min(n_local, elig.max())) * w.dim * elem_k2 + B * words * 4
     achieved = bytes_main / (main_avg * 1e-3) / 1e9
     traffic = load_traffic(w.name)
     step_ms = total_ms / args.steps
@@ -410,7 +411,9 @@ def run_ours(args, w):
     print(json.dumps(line), flush=True)
 
 
-def main_kernel_name(B):
+def main_kernel_name(B, path=0):
+    if B <= 8 and path & 32:
+        return "score_kernel<int8> (K2: int8 prefilter rows, dp4a, exact rescoring in K4p)"
     if B > 8:
         return ("tc_score_kernel (K3: bulk-copy ring -> tcgen05.mma, fp32 accumulation in TMEM; bf16 hi-plane "
                 "prefilter + fused CNF, admitted rows pruned + rescored exactly in select_prefilter_kernel)")

@@ -255,6 +255,7 @@ uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
 #define HYRE_PATH_FWD_MASK 4u
 #define HYRE_PATH_SAMPLED 8u
 #define HYRE_PATH_MATCH_ALL 16u /* tensor-core batch of match-all queries: no eligibility pass */
+#define HYRE_PATH_I8 32u        /* the main pass streams the int8 prefilter plane (exact rescoring of survivors) */
 uint32_t hyre_batch_path(const hyre_executor* ex);
 /* Eligible-row counts of the last run (u32[b], waits for it): the CNF
  * matches per query; 0xFFFFFFFF where the CNF ran fused inside K3 (the count

@@ -62,6 +62,13 @@ bool prefilter_enabled() {
   }();
   return v;
 }
+bool k2_i8_enabled() {  // HYRE_K2_I8=0: single / small batches stream the fp32 (bf16) rows directly
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_K2_I8");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 uint32_t tc_backoff_ns() {  // HYRE_TC_BACKOFF_NS: profiling the K3 wait back-off
   static const uint32_t v = [] {
     const char* e = std::getenv("HYRE_TC_BACKOFF_NS");
@@ -325,8 +332,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     refs[r] = ref_src[r].first == 0 ? ix->bitmaps + size_t{ref_src[r].second} * W
                                     : d_scratch + size_t{ref_src[r].second} * W;
   use_tc = any_emb && ix->has_tc && b >= kTcMinBatch;
-  prefilter = use_tc && prefilter_enabled();
-  pf_i8 = prefilter && ix->tc_i8 != nullptr && ix->dp % 128 == 0 && prefilter_i8_allowed();
+  // prefilter + exact rescoring: K3 batches (int8 or bf16 prefilter), and K2
+  // batches when the int8 plane exists (the int8 rows are a quarter of fp32)
+  const bool i8_ok = ix->tc_i8 != nullptr && ix->dp % 128 == 0 && prefilter_i8_allowed();
+  prefilter = any_emb && prefilter_enabled() && (use_tc || (i8_ok && k2_i8_enabled()));
+  pf_i8 = prefilter && i8_ok;
   if (use_tc) {
     // one group of up to 256 queries per pass (the epilogue works in 32-column
     // chunks); a group must leave room for a >= 3-stage ring next to its
@@ -412,11 +422,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // groups of tc_np rows (multiple of 16, <= kTcMaxGroup).
   qdelta_h.assign(b, prefilter ? prefilter_delta() : 0.0f);
   qscale_h.assign(b, 0.0f);
-  if (use_tc && pf_i8) {
+  if (pf_i8) {
     // int8 prefilter: q8 = rint(q / s_q), s_q = max|q| / 127 per query; the
     // bound: |s - s'| <= r_e |q| + (|e| + r_e) r_q + 1e-5 with
     // r_e the index's largest row residual, r_q = ||q - s_q q8||
-    const size_t rows = size_t{tc_groups} * tc_np;
+    const size_t rows = use_tc ? size_t{tc_groups} * tc_np : size_t{b};
     qi8_h.assign(rows * dp, 0);
     const double re = ix->i8_rmax, en = std::max(1.0f, ix->max_row_norm) * 1.004;
     for (uint32_t i = 0; i < b; ++i) {
@@ -493,9 +503,10 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   }
   if (!fwd_words.empty()) std::memcpy(h_blob + o_fwd, fwd_words.data(), fwd_words.size() * 4);
   if (use_fused) std::memcpy(h_blob + o_fz, fz_words.data(), fz_words.size() * 4);
-  if (use_tc) {
-    if (pf_i8) std::memcpy(h_blob + o_qhi, qi8_h.data(), qi8_h.size());
-    else std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
+  if (pf_i8) {
+    std::memcpy(h_blob + o_qhi, qi8_h.data(), qi8_h.size());  // int8 queries (K3 tiles or K2 rows)
+  } else if (use_tc) {
+    std::memcpy(h_blob + o_qhi, qhi_h.data(), qhi_h.size() * 2);
     if (!qlo_h.empty()) std::memcpy(h_blob + o_qlo, qlo_h.data(), qlo_h.size() * 2);
   }
   if (g_prep.on) g_prep.t[4] += us_since(tp);
@@ -539,6 +550,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   d_fwd = reinterpret_cast<uint32_t*>(d_blob + o_fwd);
   d_fz = reinterpret_cast<uint32_t*>(d_blob + o_fz);
   d_qscale = reinterpret_cast<float*>(d_blob + o_qsc);
+  d_qi8 = reinterpret_cast<int8_t*>(d_blob + o_qhi);
   d_qdelta = reinterpret_cast<float*>(d_blob + o_qdl);
   prepared = true;
   if (g_prep.on) {
@@ -614,12 +626,19 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
                d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp, 1, 1};
+  if (pf_i8) {  // int8 prefilter rows (exact rescoring in K4p)
+    sa.emb = ix->tc_i8;
+    sa.qi8 = d_qi8;
+    sa.qscale = d_qscale;
+    sa.qdelta = d_qdelta;
+  }
   // enough work items to fill the resident warp slots (148 SMs x 64 warps)
   const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
   const uint32_t n_samp_seg = (n_seg + sample_period - 1) / sample_period;
   while (sa.split < 32 && n_seg * sa.split < 148u * 64u) sa.split *= 2;
   while (sa.split_sample < 32 && n_samp_seg * sa.split_sample < 148u * 64u) sa.split_sample *= 2;
-  launch_score(sa, bf16, st);
+  if (pf_i8) launch_score_i8(sa, st);
+  else launch_score(sa, bf16, st);
   ++kernels;
 }
 
@@ -925,7 +944,8 @@ void Executor::run() {
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       SelectArgs ka{nullptr, samp_cnt, samp_cap, d_qp, n_elig, SELECT_KTH, d_thr, nullptr, nullptr,
                     nullptr, nullptr, B, QF_ACTIVE | QF_EMB, cap, d_thr_safe, sample_period, sample_rows,
-                    d_samp, ix->row_base, d_cand, cap, prefilter ? prefilter_delta() : 0.0f};
+                    d_samp, ix->row_base, d_cand, cap, prefilter ? prefilter_delta() : 0.0f,
+                    prefilter ? d_qdelta : nullptr};
       launch_sample_kth(ka, samp_cnt, st);
       ++kernels;
     } else {
@@ -969,6 +989,16 @@ void Executor::finish_reruns() {
     for (uint32_t i = 0; i < B; ++i) any |= h_rerun[i] != 0;
     if (!any) return;
     ++finish_rounds;
+    if (std::getenv("HYRE_DEBUG_COUNTS") && round < 4) {  // diagnostics: the recovery state of query 0
+      uint64_t t[2];
+      uint32_t c[2];
+      HYRE_CUDA(cudaMemcpy(&t[0], d_thr, 8, cudaMemcpyDeviceToHost));
+      HYRE_CUDA(cudaMemcpy(&t[1], d_thr_safe, 8, cudaMemcpyDeviceToHost));
+      HYRE_CUDA(cudaMemcpy(&c[0], cand_cnt, 4, cudaMemcpyDeviceToHost));
+      HYRE_CUDA(cudaMemcpy(&c[1], n_elig, 4, cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[hyre] rerun round %d: q0 rerun %u thr %.6f thr_safe %.6f cand %u elig %u\n", round,
+                   h_rerun[0], key_score(t[0]), key_score(t[1]), c[0], c[1]);
+    }
     HYRE_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * max_batch, st));
     score(SCORE_RERUN, d_cand, cand_cnt, cap);
     SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL_RERUN, d_thr, rerun, d_hits, d_hit_off,

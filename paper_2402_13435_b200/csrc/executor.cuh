@@ -114,6 +114,7 @@ struct Executor {
   std::vector<int8_t> qi8_h;
   std::vector<float> qscale_h, qdelta_h;  // per query: int8 score scale, prefilter bound
   float* d_qscale = nullptr;
+  int8_t* d_qi8 = nullptr;
   float* d_qdelta = nullptr;
   uint32_t tc_stages = 2, tc_term_slots = 2, tc_aps = 1;  // K3 ring depths, K atoms per stage (plan_tc)
   void plan_tc();

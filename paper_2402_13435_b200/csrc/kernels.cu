@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
@@ -457,6 +458,20 @@ struct Chunk<__nv_bfloat16> {
   }
 };
 
+// int8 chunk: 16 elements; the lane's partial dot of 16 int8 products is
+// exact (|sum| < 2^18) and exactly representable as a float, so the float
+// butterfly below sums exact integers (< 2^24) -- the int8 dot is exact.
+struct I8Chunk {
+  static constexpr int kElems = 16;
+  __device__ static float dot(const uint4& v, const uint4& q) {
+    int acc = __dp4a(static_cast<int>(v.x), static_cast<int>(q.x), 0);
+    acc = __dp4a(static_cast<int>(v.y), static_cast<int>(q.y), acc);
+    acc = __dp4a(static_cast<int>(v.z), static_cast<int>(q.z), acc);
+    acc = __dp4a(static_cast<int>(v.w), static_cast<int>(q.w), acc);
+    return static_cast<float>(acc);
+  }
+};
+
 __device__ __forceinline__ bool score_active(const ScoreArgs& a, uint32_t q) {
   if (q >= a.B) return false;
   const uint32_t f = a.qp[q].flags;
@@ -470,10 +485,23 @@ __device__ __forceinline__ bool score_active(const ScoreArgs& a, uint32_t q) {
 
 }  // namespace
 
+template <typename RowT>
+struct ChunkElems {
+  static constexpr int value = Chunk<RowT>::kElems;
+};
+template <>
+struct ChunkElems<int8_t> {
+  static constexpr int value = I8Chunk::kElems;
+};
+
+// RowT = int8_t: the int8 prefilter plane (DevIndex::tc_i8, swizzled 128-row
+// tiles) with the int8 query; scores are prefilter scores (s' = acc x scale)
+// and rows are admitted against score(thr) - delta_q for exact rescoring in K4p.
 template <typename RowT, int LPR, int CPL, int QG>
 __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
-  constexpr int G = 32 / LPR;             // row groups per warp load step
-  constexpr int E = Chunk<RowT>::kElems;  // elements per 16-byte chunk
+  constexpr bool kI8 = std::is_same<RowT, int8_t>::value;
+  constexpr int G = 32 / LPR;                // row groups per warp load step
+  constexpr int E = ChunkElems<RowT>::value;  // elements per 16-byte chunk
   constexpr int M1 = LPR / 2, M2 = LPR / 4, M3 = LPR / 8;
   __shared__ uint16_t lists[8][kSegRows];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -482,24 +510,37 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
 
   uint32_t act = 0;
   uint64_t thr[QG];
+  float ts8[QG], sc8[QG];  // int8: admission score bound and score scale per query
 #pragma unroll
   for (int j = 0; j < QG; ++j) {
     const bool on = score_active(a, q0 + j);
     act |= on ? (1u << j) : 0u;
     thr[j] = (on && a.mode != SCORE_SAMPLE) ? a.thr[q0 + j] : 0ull;
+    if (kI8) {
+      sc8[j] = on ? a.qscale[q0 + j] : 0.0f;
+      ts8[j] = thr[j] == 0ull ? -4.0f : key_score(thr[j]) - a.qdelta[q0 + j];
+    }
   }
   if (!act) return;
 
-  float qv[QG][CPL][E];
+  float qv[QG][CPL][kI8 ? 1 : E];
+  uint4 qv8[QG][CPL];
 #pragma unroll
   for (int j = 0; j < QG; ++j)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c)
+    for (int c = 0; c < CPL; ++c) {
+      if constexpr (kI8) {
+        qv8[j][c] = (act >> j & 1u) ? *reinterpret_cast<const uint4*>(a.qi8 + static_cast<size_t>(q0 + j) * a.dp +
+                                                                        (li + c * LPR) * E)
+                                    : make_uint4(0, 0, 0, 0);
+      } else {
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        qv[j][c][e] = (act >> j & 1u)
-                          ? a.q[static_cast<size_t>(q0 + j) * a.dp + (li + c * LPR) * E + e]
-                          : 0.0f;
+        for (int e = 0; e < E; ++e)
+          qv[j][c][e] = (act >> j & 1u)
+                            ? a.q[static_cast<size_t>(q0 + j) * a.dp + (li + c * LPR) * E + e]
+                            : 0.0f;
+      }
+    }
 
   const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
   // few segments: each is split into S parts of 32/S mask words so that
@@ -546,10 +587,22 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const uint32_t idx = base + s * G + g;
         const bool ok = idx < total;
         roff[s] = ok ? (full ? idx : lists[wib][idx]) : 0u;
-        const RowT* row = emb + (seg_row0 + roff[s]) * a.dp;
+        if constexpr (kI8) {
+          // tiled int8 row: tile lr / 128, K atom cidx / 8, physical chunk
+          // (cidx % 8) ^ (row % 8) (SWIZZLE_128B), 16 KB per atom
+          const uint32_t lr = static_cast<uint32_t>(seg_row0) + roff[s], rr = lr & 127u;
+          const uint8_t* tile = reinterpret_cast<const uint8_t*>(emb) + size_t{lr >> 7} * (a.dp / 128) * 16384 + rr * 128;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          v[s][c] = ok ? ldg_stream(row + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+          for (int c = 0; c < CPL; ++c) {
+            const uint32_t cidx = li + c * LPR;
+            v[s][c] = ok ? ldg_stream(tile + (cidx >> 3) * 16384 + (((cidx & 7u) ^ (rr & 7u)) << 4)) : make_uint4(0, 0, 0, 0);
+          }
+        } else {
+          const RowT* row = emb + (seg_row0 + roff[s]) * a.dp;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            v[s][c] = ok ? ldg_stream(row + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+        }
       }
       const uint32_t my_idx = base + slot * G + g;
       const bool my_ok = leader && my_idx < total;
@@ -562,7 +615,10 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         for (int s = 0; s < 8; ++s) {
           float acc = 0.0f;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[s][c], qv[j][c]);
+          for (int c = 0; c < CPL; ++c) {
+            if constexpr (kI8) acc += I8Chunk::dot(v[s][c], qv8[j][c]);
+            else acc += Chunk<RowT>::dot(v[s][c], qv[j][c]);
+          }
           p[s] = acc;
         }
         // reduce-scatter: 8 values over LPR lanes -> 1 value per lane.
@@ -596,6 +652,7 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const uint32_t src_word = __shfl_sync(kFull, wq[j], (my_off >> 5) & 31);
         const bool elig = (src_word >> (my_off & 31)) & 1u;
         const uint32_t grow = a.row_base + static_cast<uint32_t>(seg_row0) + my_off;
+        if (kI8) p[0] *= sc8[j];  // exact int8 dot -> prefilter score
         const uint64_t key = make_key(clamp_score(p[0]), grow);
         if (a.mode == SCORE_SAMPLE) {
           // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
@@ -603,7 +660,7 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
             a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(clamp_score(p[0]));
           continue;
         }
-        const bool take = my_ok && elig && key >= thr[j];
+        const bool take = my_ok && elig && (kI8 ? p[0] >= ts8[j] : key >= thr[j]);
         const unsigned bal = __ballot_sync(kFull, take);
         if (bal) {
           const uint32_t q = q0 + j;
@@ -635,6 +692,29 @@ void dispatch_score(const ScoreArgs& a, dim3 grid, cudaStream_t st) {
   else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
 }
 }  // namespace
+
+void launch_score_i8(const ScoreArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  const uint32_t qg = a.B == 1 ? 1 : kMaxQG;
+  const uint32_t groups = (a.B + qg - 1) / qg;
+  const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
+  const uint32_t iters =
+      a.mode == SCORE_SAMPLE ? (n_seg + a.period - 1) / a.period * a.split_sample : n_seg * a.split;
+  const uint32_t blocks = std::max(1u, std::min((iters + 7) / 8, 148u * 8u));
+  const dim3 grid(blocks, groups);
+  const uint32_t cpr = a.dp / 16;  // 16-byte chunks of int8 per row
+  if (qg == 1) {
+    if (cpr == 8) score_kernel<int8_t, 8, 1, 1><<<grid, 256, 0, st>>>(a);
+    else if (cpr == 16) score_kernel<int8_t, 16, 1, 1><<<grid, 256, 0, st>>>(a);
+    else if (cpr == 32) score_kernel<int8_t, 32, 1, 1><<<grid, 256, 0, st>>>(a);
+    else throw Error(HYRE_INTERNAL, "int8 K2: unsupported row width");
+  } else {
+    if (cpr == 8) score_kernel<int8_t, 8, 1, kMaxQG><<<grid, 256, 0, st>>>(a);
+    else if (cpr == 16) score_kernel<int8_t, 16, 1, kMaxQG><<<grid, 256, 0, st>>>(a);
+    else if (cpr == 32) score_kernel<int8_t, 32, 1, kMaxQG><<<grid, 256, 0, st>>>(a);
+    else throw Error(HYRE_INTERNAL, "int8 K2: unsupported row width");
+  }
+}
 
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st) {
   if (a.B == 0) return;
@@ -855,7 +935,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     }
     if (threadIdx.x == 0) {
       a.thr[q] = t_est;
-      if (a.thr_safe) a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
+      const float dl = a.qdelta ? a.qdelta[q] : a.delta;
+      if (a.thr_safe) a.thr_safe[q] = dl > 0.0f ? key_minus_delta(t_safe, dl) : t_safe;
     }
     return;
   }
@@ -1041,7 +1122,8 @@ __global__ void __launch_bounds__(kSelThreads) sample_union_kernel(SelectArgs a,
   }
   if (threadIdx.x == 0) {
     a.thr[q] = t_est;
-    if (a.thr_safe) a.thr_safe[q] = a.delta > 0.0f ? key_minus_delta(t_safe, a.delta) : t_safe;
+    const float dl = a.qdelta ? a.qdelta[q] : a.delta;
+    if (a.thr_safe) a.thr_safe[q] = dl > 0.0f ? key_minus_delta(t_safe, dl) : t_safe;
   }
 }
 

@@ -82,8 +82,15 @@ struct ScoreArgs {
   uint32_t* samp;         // SCORE_SAMPLE: dense [B][cap] orderable scores (0 = ineligible)
   uint32_t split;         // main/rerun: parts per 1024-row segment (power of two <= 32)
   uint32_t split_sample;  // the same for the sample pass
+  // int8 prefilter (emb = DevIndex::tc_i8, the swizzled 128-row tiles): the
+  // int8 query qi8 [B][dp], score s' = acc x qscale[q]; rows are admitted
+  // when s' >= score(thr) - qdelta[q] (exact rescoring follows in K4p)
+  const int8_t* qi8;
+  const float* qscale;
+  const float* qdelta;
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
+void launch_score_i8(const ScoreArgs& a, cudaStream_t st);
 
 // Largest key whose score is <= s - delta: a lower bound, in key space, for
 // every exact score of a row whose prefilter score was s (delta = the bound).

@@ -342,6 +342,42 @@ def run_ours(args, w):
     check(lib.hyre_batch_io_bytes(h, C.byref(h2d), C.byref(d2h)))
     if not os.environ.get("HYRE_TC_DEBUG"):
         assert all(sts == 0) and int(counts.min()) > 0, "empty results in the e2e run"
+    single_e2e = B * e2e_steps / e2e_s
+
+    # ---- the same calls from two host threads, one executor each ----------
+    # (the reference's ExecutorPool model, service.cpp:99-141: one thread's
+    # host work -- validation, program build, copies -- overlaps the other
+    # executor's kernels; every call still copies its queries in and its
+    # hits out).  N = 1 only: the multi-GPU e2e keeps one caller per rank.
+    pooled = None
+    if world == 1 and not os.environ.get("HYRE_TC_DEBUG"):
+        ex2 = hy.Executor(dev, max_batch=args.batch)
+        pack2 = hy.QueryPack(hq)
+
+        def worker(hx, pk, n, out):
+            hh = (L.hyre_hit * sum(caps))()
+            cn = np.zeros(B, np.uint32)
+            st_ = np.zeros(B, np.int32)
+            for _ in range(n):
+                rc = lib.hyre_execute_batch(hx, pk.arr, B, hh, offs.ctypes.data_as(L.u64p), cn.ctypes.data_as(L.u32p),
+                                            st_.ctypes.data_as(L.i32p), None)
+                if rc != 0 or not all(st_ == 0):
+                    out.append(False)
+                    return
+            out.append(True)
+
+        n_each = max(3, e2e_steps)
+        worker(ex2._h, pack2, 1, [])  # warm the second executor
+        oks = []
+        threads = [threading.Thread(target=worker, args=(hx, pk, n_each, oks)) for hx, pk in ((h, pack), (ex2._h, pack2))]
+        t0 = time.perf_counter()
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        pooled_s = time.perf_counter() - t0
+        assert all(oks) and len(oks) == 2, "pooled e2e calls failed"
+        pooled = 2 * B * n_each / pooled_s
 
     if rank != 0:
         return
@@ -390,9 +426,11 @@ def run_ours(args, w):
                      "eligibility": ("none (match-all batch)" if path & 16 else
                                      "fused CNF over compact CNF rows" if fused else "K1 mask bitmaps"),
                      "path_flags": path},
-        "e2e": {"value": B * e2e_steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
-                "d2h_bytes_per_step": int(d2h.value), "api": "hyre_execute_batch (C-ABI, host buffers)",
-                "host_prepare_ms": prep_ms},
+        "e2e": {"value": pooled if pooled else single_e2e, "unit": "queries/s", "h2d_bytes_per_step": int(h2d.value),
+                "d2h_bytes_per_step": int(d2h.value),
+                "api": ("hyre_execute_batch (C-ABI, host buffers) from 2 host threads, one executor each "
+                        "(ExecutorPool model)" if pooled else "hyre_execute_batch (C-ABI, host buffers)"),
+                "single_caller_value": single_e2e, "host_prepare_ms": prep_ms},
         "gpu_launches": kernels_per_step * args.steps,
         "clocks": clocks.summary(),
         "index": {"build_s": t_frozen, **{k: stats[k] for k in ("num_terms", "bitmap_terms", "csr_terms")}},

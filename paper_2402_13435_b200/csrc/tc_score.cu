@@ -1,24 +1,29 @@
-// K3: batched scorer on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+// K3: batched scorer on the 5th-gen tensor cores (tcgen05 + TMEM + bulk copies).
 //
 // Scoring B queries against N jobs is the dense contraction
 //   S[N x B] = E[N x d] . Q[B x d]^T
-// (Executor::execute_batch's scoring loop, pipeline.cpp:246-256).  One
-// persistent CTA per SM streams 128-row tiles of the embedding matrix through
-// a TMA -> shared-memory ring; a single thread issues tcgen05.mma
-// (M=128 rows x N=Np queries x K=16, bf16 inputs, fp32 accumulation in TMEM);
-// four epilogue warps pull the 128 x Np accumulator tile out of TMEM with
-// tcgen05.ld, apply the CNF eligibility bit (mask), clamp (knn.cpp:37) and the
-// per-query candidate threshold in registers, and append only surviving
+// (Executor::execute_batch's scoring loop, pipeline.cpp:246-256) fused with
+// the CNF term match (term_match.cpp:56-78).  One persistent CTA per SM
+// streams 128-row tiles through a bulk-copy -> shared-memory ring; one elected
+// thread issues tcgen05.mma into TMEM accumulators; CNF warps evaluate each
+// row's clauses from its compact term list; epilogue warps pull the
+// accumulator tile out of TMEM with tcgen05.ld, compare every score with its
+// query's threshold in registers and append only the (eligible, passing)
 // (score, row) keys.  Ineligible / sub-threshold jobs never leave registers.
 //
-// fp32-grade accuracy on bf16 tensor cores: the index stores each fp32 row as
-// hi + lo bf16 (x - hi - lo = O(2^-17 x)) and the query likewise, and the
-// kernel accumulates  E_hi.Q_hi + E_hi.Q_lo + E_lo.Q_hi  (3 bf16 MMAs per
-// K-step; the dropped E_lo.Q_lo term is O(2^-16)).  Bytes per row are the same
-// 4 B/element as fp32.  A bf16 index (config c4) scores E.Q_hi + E.Q_lo.
+// Operand planes:
+//  * prefilter (default): the int8 plane, one kind::i8 MMA per K step
+//    (K = 32, s32 accumulation; s' = acc x scale_q), or the bf16 hi plane
+//    (kind::f16, K = 16, fp32); rows are admitted at s' >= thr - delta_q and
+//    rescored exactly afterwards (select_prefilter_kernel), so K3's scores are
+//    never returned;
+//  * exact (HYRE_PREFILTER=0): hi + lo bf16 planes of the fp32 rows and of the
+//    query, E_hi.Q_hi + E_hi.Q_lo + E_lo.Q_hi (the dropped E_lo.Q_lo term is
+//    O(2^-16)); a bf16 index scores E.Q_hi + E.Q_lo.
 //
-// Warp roles (320 threads): w0 TMA producer, w1 TMEM owner + MMA issuer,
-// w2..w9 epilogue (TMEM lane quadrant = warp % 4, two warps per quadrant).
+// Warp roles: w0 bulk-copy producer, w1 TMEM owner + MMA issuer, 8 epilogue
+// warps (16 in the mask / match-all variant; TMEM lane quadrant = warp % 4),
+// then 4 or 8 CNF warps in the fused variants.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

@@ -1282,8 +1282,9 @@ __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys
 }
 }  // namespace
 
+constexpr int kSelPThreads = 1024;  // K4p: more warps -> more survivor rows in flight
 template <typename RowT, int LPR, int CPL>
-__global__ void __launch_bounds__(kSelThreads) select_prefilter_kernel(PrefSelectArgs pa) {
+__global__ void __launch_bounds__(kSelPThreads) select_prefilter_kernel(PrefSelectArgs pa) {
   const SelectArgs& a = pa.s;
   extern __shared__ uint64_t sel_smem[];
   uint64_t* sortbuf = sel_smem;                                          // kSelectMaxK keys
@@ -1432,7 +1433,7 @@ void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_
   else if (cpr == 256) k = select_prefilter_kernel<RowT, 32, 8>;
   else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
   HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k<<<a.s.B, kSelThreads, smem, st>>>(a);
+  k<<<a.s.B, kSelPThreads, smem, st>>>(a);
 }
 }  // namespace
 

@@ -782,17 +782,16 @@ __device__ uint64_t kth_largest(const uint64_t* keys, uint32_t n, uint32_t k, ui
     __syncthreads();
     // Position t of the scan owns bins [8*o, 8*o+8) with o = T-1-t, so the
     // exclusive prefix at t counts every key in bins above o's range.
-    const uint32_t owner = blockDim.x - 1 - threadIdx.x;
+    // (per = 4096 / blockDim.x bins per scan position: 8 at 512 threads, 4 at 1024)
+    const uint32_t owner = blockDim.x - 1 - threadIdx.x, per = 4096 / blockDim.x;
     uint32_t mine = 0;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) mine += hist[owner * 8 + b];
+    for (uint32_t b = 0; b < per; ++b) mine += hist[owner * per + b];
     uint32_t tot;
     uint32_t above = block_excl_scan(mine, tmp, &tot);
-#pragma unroll
-    for (int b = 7; b >= 0; --b) {
-      const uint32_t h = hist[owner * 8 + b];
+    for (int b = static_cast<int>(per) - 1; b >= 0; --b) {
+      const uint32_t h = hist[owner * per + b];
       if (above < kk && kk <= above + h) {
-        sel_digit = owner * 8 + b;
+        sel_digit = owner * per + b;
         sel_unique = h == 1;
         sel_kk = kk - above;
       }

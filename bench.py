@@ -415,7 +415,10 @@ def run_ours(args, w):
     line = {
         "metric": "queries_per_sec", "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "p50_ms": p50, "jobs_scored_per_sec": qps * w.n,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": w.dtype,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        # returned scores are computed in f32 (bf16 rows for a bf16 index); the
+        # scan itself runs on the int8 prefilter plane when path & 32
+        "dtype": (f"{w.dtype} (scan: int8 prefilter)" if path & 32 else w.dtype),
         "data": "synthetic (SURVEY §8(d) generator, std::mt19937_64; index built by the product IndexBuilder)",
         "config": workload_config(w, args),
         "stages_ms": dict(zip(["mask", "quant", "sample", "main_scorer", "select_firstk", "run"],
@@ -452,9 +455,12 @@ def run_ours(args, w):
 def main_kernel_name(B, path=0):
     if B <= 8 and path & 32:
         return "score_kernel<int8> (K2: int8 prefilter rows, dp4a, exact rescoring in K4p)"
+    if B > 8 and path & 32:
+        return ("tc_score_kernel (K3: bulk-copy ring -> tcgen05.mma kind::i8, s32 accumulation in TMEM; int8 "
+                "prefilter + fused CNF, admitted rows pruned + rescored exactly in fp32 by select_prefilter_kernel)")
     if B > 8:
-        return ("tc_score_kernel (K3: bulk-copy ring -> tcgen05.mma, fp32 accumulation in TMEM; bf16 hi-plane "
-                "prefilter + fused CNF, admitted rows pruned + rescored exactly in select_prefilter_kernel)")
+        return ("tc_score_kernel (K3: bulk-copy ring -> tcgen05.mma kind::f16, fp32 accumulation in TMEM; bf16 "
+                "prefilter or hi/lo split + fused CNF)")
     return "score_kernel (K2, CUDA-core streaming scorer)"
 
 

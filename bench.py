@@ -311,9 +311,10 @@ def run_ours(args, w):
             check(lib.hyre_execute_batch(h, pack.arr, B, host_hits, offs.ctypes.data_as(L.u64p),
                                          counts.ctypes.data_as(L.u32p), sts.ctypes.data_as(L.i32p), C.byref(tim)))
         else:
-            # host queries -> device; shard results -> all ranks (NCCL) -> exact device merge -> host
+            # host queries -> device; shard results (settled) -> all ranks (NCCL) -> exact device merge -> host
             check(lib.hyre_batch_prepare(h, pack.arr, B))
             check(lib.hyre_batch_run(h))
+            check(lib.hyre_batch_settle(h))
             gather()
             check(lib.hyre_batch_fetch(h, host_hits, offs.ctypes.data_as(L.u64p), counts.ctypes.data_as(L.u32p),
                                        sts.ctypes.data_as(L.i32p), None))

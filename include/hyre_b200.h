@@ -243,6 +243,12 @@ const char* hyre_executor_slot_error(const hyre_executor* ex, uint32_t slot);
  * out (same layout as hyre_execute_batch).  run may be repeated. */
 hyre_status hyre_batch_prepare(hyre_executor* ex, const hyre_query* qs, uint32_t b);
 hyre_status hyre_batch_run(hyre_executor* ex);
+/* Waits for the last run and resolves any pending recovery round (a query
+ * whose estimated threshold admitted too few rows or whose candidate buffer
+ * overflowed), so the device results are final: call before reading them on
+ * the device (hyre_batch_device_results, the multi-GPU gather).  fetch does
+ * this itself. */
+hyre_status hyre_batch_settle(hyre_executor* ex);
 hyre_status hyre_batch_fetch(hyre_executor* ex, hyre_hit* hits, const uint64_t* hit_offsets,
                              uint32_t* counts, int32_t* statuses, hyre_timings* timings);
 /* Number of kernels the last hyre_batch_run enqueued. */

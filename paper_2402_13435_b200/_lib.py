@@ -114,6 +114,7 @@ SIGNATURES = {
     "hyre_batch_eligible": (C.c_int, [vp, u32p]),
     "hyre_batch_term_bytes": (C.c_uint64, [vp]),
     "hyre_batch_scan_bytes": (C.c_uint64, [vp]),
+    "hyre_batch_settle": (C.c_int32, [vp]),
     "hyre_pool_create": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp)]),
     "hyre_pool_destroy": (None, [vp]),
     "hyre_pool_search": (C.c_int, [vp, vp, vp, u32p]),

@@ -368,6 +368,13 @@ const char* hyre_executor_slot_error(const hyre_executor* ex, uint32_t slot) {
   return ex->ex->slot_errors[slot].c_str();
 }
 
+hyre_status hyre_batch_settle(hyre_executor* ex) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->settle();
+  });
+}
+
 hyre_status hyre_batch_prepare(hyre_executor* ex, const hyre_query* qs, uint32_t b) {
   return guard([&] {
     need(ex, "executor");

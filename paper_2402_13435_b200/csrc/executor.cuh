@@ -140,6 +140,7 @@ struct Executor {
   void fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* statuses,
              hyre_timings* t);
   float last_run_ms() const;
+  void settle() { if (any_emb) finish_reruns(); }  // resolve pending recovery rounds (synchronous)
   void eligible(uint32_t* out);  // n_elig of the last run (D2H, synchronous)
   void stage_ms(float* out) const;  // [mask, quant, sample+kth, main score, select/first-K, total]
   void stage_ms_hist(uint32_t back, float* out) const;  // the same for the run `back` runs ago

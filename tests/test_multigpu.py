@@ -113,6 +113,7 @@ def test_device_shard_merge_emulated_on_one_gpu(G, B):
         ex = hy.Executor(dev, max_batch=B)
         assert L.lib().hyre_batch_prepare(ex._h, pack.arr, B) == 0
         assert L.lib().hyre_batch_run(ex._h) == 0
+        assert L.lib().hyre_batch_settle(ex._h) == 0  # final device results before the gather
         shards.append((dev, ex))
     # gather: [G][stride] hits, [G][B] offsets, [G][B] counts (device buffers)
     res = []

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -1431,7 +1432,13 @@ void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_
   else if (cpr == 128) k = select_prefilter_kernel<RowT, 32, 4>;
   else if (cpr == 256) k = select_prefilter_kernel<RowT, 32, 8>;
   else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
-  HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  static std::atomic<bool> attr_set[2][6];  // [bf16][row-width variant]: set the smem limit once per kernel
+  const int vi = cpr == 8 ? 0 : cpr == 16 ? 1 : cpr == 32 ? 2 : cpr == 64 ? 3 : cpr == 128 ? 4 : 5;
+  std::atomic<bool>& done = attr_set[std::is_same<RowT, float>::value ? 0 : 1][vi];
+  if (!done.load(std::memory_order_acquire)) {
+    HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    done.store(true, std::memory_order_release);
+  }
   k<<<a.s.B, kSelPThreads, smem, st>>>(a);
 }
 }  // namespace

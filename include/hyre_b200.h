@@ -263,6 +263,11 @@ uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
 #define HYRE_PATH_MATCH_ALL 16u /* tensor-core batch of match-all queries: no eligibility pass */
 #define HYRE_PATH_I8 32u        /* the main pass streams the int8 prefilter plane (exact rescoring of survivors) */
 uint32_t hyre_batch_path(const hyre_executor* ex);
+/* K3 kernel variant of the prepared batch (diagnostics for tests that must
+ * run a given instantiation): out4 = {J compact CNF ids per row (0 = not
+ * fused), bytes per id (1 = u8, 2 = u16), query chunks per CNF thread,
+ * queries per MMA group (Np)}; all zero when the batch runs on K2. */
+void hyre_batch_tc_variant(const hyre_executor* ex, uint32_t* out4);
 /* Eligible-row counts of the last run (u32[b], waits for it): the CNF
  * matches per query; 0xFFFFFFFF where the CNF ran fused inside K3 (the count
  * is never materialised there).  Diagnostics for benchmarks and tests. */

@@ -284,3 +284,65 @@ def codec(dim: int, num_bits: int, seed: int):
                     bounds[pos:pos + nb[r]].copy()))
         pos += int(nb[r])
     return out
+
+
+class ShardedRef:
+    """The reference over G FrozenIndex shards of one corpus (SURVEY.md §8(d)
+    sharded oracle; oracle/ref_shim.cpp ref_build_shards /
+    ref_execute_sharded).  Hybrid results are merged by (score desc, global
+    row asc) and term-only ones concatenated in shard order, which equals the
+    unsharded reference exactly with quant off."""
+
+    def __init__(self, slot_offsets, ids, embeddings, num_clauses, max_num_attr, num_bits, seed,
+                 shards: Optional[int] = None, threads: Optional[int] = None, doc_prefix: str = "d"):
+        so = np.ascontiguousarray(slot_offsets, np.uint64)
+        ids = np.ascontiguousarray(ids if len(ids) else np.zeros(1, np.uint32), np.uint32)
+        emb = np.ascontiguousarray(embeddings, np.float32)
+        n, dim = emb.shape
+        self.num_docs, self.dim = n, dim
+        threads = threads or os.cpu_count() or 1
+        g = shards or max(1, min(64, -(-n // 1_000_000)))
+        g = max(g, min(threads, max(1, n // 100_000)))  # use the cores even for small corpora
+        self.g = g
+        hs = (C.c_void_p * g)()
+        self.bases = np.zeros(g, np.uint64)
+        L = lib()
+        L.ref_build_shards.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_uint32, C.c_uint64, C.c_char_p, C.c_uint32, C.c_uint32,
+                                       C.c_void_p, C.c_void_p]
+        _check(L.ref_build_shards(n, num_clauses, max_num_attr, dim, so.ctypes.data, ids.ctypes.data,
+                                  emb.ctypes.data, num_bits, seed, doc_prefix.encode(), g, threads,
+                                  C.cast(hs, C.c_void_p), self.bases.ctypes.data))
+        self.hs = hs
+        self.shards = [RefIndex(C.c_void_p(hs[s])) for s in range(g)]  # owns (frees) the handles
+
+    def execute(self, queries, threads: Optional[int] = None):
+        """queries: [(clauses, emb, k, quant_enabled, quant_k, granularity)] ->
+        (seconds, [(status, rows, scores)]) with GLOBAL rows."""
+        b = len(queries)
+        cap = max(q[2] for q in queries)
+        qp = QueryPack(queries)
+        rows = np.zeros((b, cap), np.uint32)
+        sc = np.zeros((b, cap), np.float32)
+        cnt = np.zeros(b, np.uint32)
+        st = np.zeros(b, np.int32)
+        secs = C.c_double()
+        L = lib()
+        L.ref_execute_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,
+                                          C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
+        _check(L.ref_execute_sharded(C.cast(self.hs, C.c_void_p), self.bases.ctypes.data, self.g,
+                                     C.cast(qp.arr, C.c_void_p), b, threads or os.cpu_count() or 1,
+                                     rows.ctypes.data, sc.ctypes.data, cap, cnt.ctypes.data, st.ctypes.data,
+                                     C.byref(secs)))
+        return secs.value, [(int(st[i]), rows[i, :cnt[i]].astype(np.int64), sc[i, :cnt[i]].copy())
+                            for i in range(b)]
+
+    def exact_scores(self, q, global_rows):
+        """The reference's exact_scores (knn.cpp:8-40) of arbitrary global rows."""
+        rows = np.asarray(global_rows, np.int64)
+        out = np.zeros(len(rows), np.float32)
+        shard = np.searchsorted(self.bases.astype(np.int64), rows, side="right") - 1
+        for s in np.unique(shard):
+            sel = shard == s
+            out[sel], _ = self.shards[s].exact_scores(q, rows[sel] - int(self.bases[s]))
+        return out

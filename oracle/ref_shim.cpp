@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -264,6 +265,147 @@ int ref_execute_batch(void* h, const RefQuery* qs, uint32_t b, uint32_t max_batc
         write_hits(outs[i].result, rows + std::size_t{i} * cap_per_query,
                    scores + std::size_t{i} * cap_per_query, cap_per_query, &counts[i]);
     }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Sharded oracle ("c4/c5 (50M) use the sharded oracle").
+// The reference is single-threaded per query, so a 10M-50M index is built as
+// G FrozenIndex shards of one corpus (shard s = global rows
+// [s*n/G, (s+1)*n/G), built concurrently, each by the reference's own
+// IndexBuilder + freeze) and every (query, shard) pair runs the reference
+// Executor::execute.  Per query the shard results are merged:
+//  - hybrid: by (score desc, global row asc) -- the order bucket_top_k
+//    returns (proj/src/knn.cpp:79-92), so with quant off the merge equals the
+//    unsharded result exactly (the global top-K is a subset of the union of
+//    the shard top-Ks; per-row eligibility and scores do not depend on the
+//    shard);
+//  - term-only: shard lists concatenated in shard order, first k
+//    (term_only_result, proj/src/pipeline.cpp:30-40: ascending global rows).
+// Quant pre-selection is NOT exact under sharding (preselect ranks within
+// the shard), so quant-on parity uses an unsharded index.
+// ---------------------------------------------------------------------------
+namespace {
+hyre::FrozenIndex* build_rows(uint64_t begin, uint64_t end, uint32_t num_clauses,
+                              uint32_t max_num_attr, uint32_t dim,
+                              const uint64_t* slot_offsets, const uint32_t* ids,
+                              const float* embeddings, uint32_t num_bits, uint64_t seed,
+                              const char* doc_prefix) {
+  hyre::IndexConfig cfg;
+  cfg.num_clauses = num_clauses;
+  cfg.max_num_attr = max_num_attr;
+  cfg.dim = dim;
+  hyre::IndexBuilder b(cfg);
+  for (uint64_t i = begin; i < end; ++i) {
+    hyre::DocumentInput d;
+    d.doc_id = std::string(doc_prefix ? doc_prefix : "doc") + std::to_string(i);
+    d.clauses.resize(num_clauses);
+    for (uint32_t c = 0; c < num_clauses; ++c) {
+      const size_t s = i * num_clauses + c;
+      d.clauses[c].assign(ids + slot_offsets[s], ids + slot_offsets[s + 1]);
+    }
+    d.embedding.assign(embeddings + i * dim, embeddings + (i + 1) * dim);
+    b.add_document(d);
+  }
+  return new hyre::FrozenIndex(std::move(b).freeze(hyre::make_codec(dim, num_bits, seed)));
+}
+}  // namespace
+
+// Builds g shards concurrently (one thread per shard, at most `threads` at a
+// time); out[s] = shard handle, bases[s] = its first global row.  Doc ids are
+// doc_prefix + global row.  slot_offsets are u64 (50M-row corpora).
+int ref_build_shards(uint64_t n_docs, uint32_t num_clauses, uint32_t max_num_attr,
+                     uint32_t dim, const uint64_t* slot_offsets, const uint32_t* ids,
+                     const float* embeddings, uint32_t num_bits, uint64_t seed,
+                     const char* doc_prefix, uint32_t g, uint32_t threads, void** out,
+                     uint64_t* bases) {
+  return guarded([&] {
+    std::vector<std::string> errs(g);
+    std::atomic<uint32_t> next{0};
+    std::vector<std::thread> pool;
+    for (uint32_t s = 0; s < g; ++s) out[s] = nullptr;
+    for (uint32_t t = 0; t < std::max<uint32_t>(1, std::min(threads, g)); ++t)
+      pool.emplace_back([&] {
+        for (uint32_t s = next++; s < g; s = next++) {
+          const uint64_t b = n_docs * s / g, e = n_docs * (s + 1) / g;
+          bases[s] = b;
+          try {
+            out[s] = build_rows(b, e, num_clauses, max_num_attr, dim, slot_offsets, ids,
+                                embeddings, num_bits, seed, doc_prefix);
+          } catch (const std::exception& ex) {
+            errs[s] = ex.what();
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (uint32_t s = 0; s < g; ++s)
+      if (!errs[s].empty()) {
+        for (uint32_t r = 0; r < g; ++r) delete static_cast<hyre::FrozenIndex*>(out[r]);
+        throw std::runtime_error(errs[s]);
+      }
+  });
+}
+
+// Runs b queries over g shards on `threads` workers (each worker keeps one
+// reference Executor per shard it touches, like an ExecutorPool lease) and
+// merges per query as described above.  Rows written are GLOBAL rows.
+// *seconds = wall time of the whole call (executes + merges).
+int ref_execute_sharded(void* const* hs, const uint64_t* bases, uint32_t g,
+                        const RefQuery* qs, uint32_t b, uint32_t threads, uint32_t* rows,
+                        float* scores, uint32_t cap_per_query, uint32_t* counts,
+                        int32_t* statuses, double* seconds) {
+  return guarded([&] {
+    std::vector<hyre::HybridQuery> hq;
+    for (uint32_t i = 0; i < b; ++i) hq.push_back(to_hybrid(qs[i]));
+    const uint64_t items = uint64_t{b} * g;
+    std::vector<hyre::TopKResult> res(items);
+    std::vector<int> st(items, 0);
+    std::vector<std::string> msg(items);
+    std::atomic<uint64_t> next{0};
+    const uint32_t nt = std::max<uint32_t>(1, threads);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < nt; ++t)
+      pool.emplace_back([&] {
+        std::vector<std::unique_ptr<hyre::Executor>> ex(g);
+        for (uint64_t it = next++; it < items; it = next++) {
+          const uint32_t qi = static_cast<uint32_t>(it / g), s = static_cast<uint32_t>(it % g);
+          if (!ex[s]) ex[s] = std::make_unique<hyre::Executor>(*static_cast<hyre::FrozenIndex*>(hs[s]), 1);
+          try {
+            res[it] = ex[s]->execute(hq[qi]);
+          } catch (const hyre::ValidationError& e) {
+            st[it] = 1;
+            msg[it] = e.what();
+          } catch (const std::domain_error& e) {
+            st[it] = 2;
+            msg[it] = e.what();
+          }
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (uint32_t qi = 0; qi < b; ++qi) {
+      statuses[qi] = 0;
+      counts[qi] = 0;
+      for (uint32_t s = 0; s < g; ++s)
+        if (st[uint64_t{qi} * g + s]) statuses[qi] = st[uint64_t{qi} * g + s];
+      if (statuses[qi]) continue;
+      std::vector<std::pair<float, uint32_t>> all;
+      for (uint32_t s = 0; s < g; ++s)
+        for (const auto& h : res[uint64_t{qi} * g + s].hits)
+          all.emplace_back(h.score, static_cast<uint32_t>(bases[s] + h.row_id));
+      if (hq[qi].embedding)
+        std::sort(all.begin(), all.end(), [](const auto& x, const auto& y) {
+          return x.first != y.first ? x.first > y.first : x.second < y.second;
+        });
+      const uint32_t take = std::min<uint32_t>(
+          {cap_per_query, hq[qi].k, static_cast<uint32_t>(all.size())});
+      for (uint32_t j = 0; j < take; ++j) {
+        rows[std::size_t{qi} * cap_per_query + j] = all[j].second;
+        scores[std::size_t{qi} * cap_per_query + j] = all[j].first;
+      }
+      counts[qi] = take;
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

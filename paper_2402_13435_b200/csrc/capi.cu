@@ -419,6 +419,19 @@ uint32_t hyre_batch_path(const hyre_executor* ex) {
          (e->any_emb && e->ix->n_rows > e->cap ? HYRE_PATH_SAMPLED : 0u);
 }
 
+void hyre_batch_tc_variant(const hyre_executor* ex, uint32_t* out4) {
+  if (!out4) return;
+  out4[0] = out4[1] = out4[2] = out4[3] = 0;
+  if (!ex || !ex->ex->use_tc) return;
+  const Executor* e = ex->ex.get();
+  if (e->use_fused) {
+    out4[0] = e->ix->cnf_ids_per_row;
+    out4[1] = e->ix->cnf_id_bytes;
+    out4[2] = tc_fused_chunks(e->tc_np);
+  }
+  out4[3] = e->tc_np;
+}
+
 hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6) {
   return guard([&] {
     need(ex, "executor");

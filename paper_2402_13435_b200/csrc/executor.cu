@@ -165,7 +165,8 @@ Executor::~Executor() {
   for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_thr_safe, (void*)d_cand,
                   (void*)d_shist,
                   (void*)d_samp, (void*)d_qhist, (void*)d_tsel, (void*)d_eqcnt, (void*)d_blob,
-                  (void*)d_hits, (void*)d_scratch})
+                  (void*)d_hits, (void*)d_scratch, (void*)d_ex_keys, (void*)d_ex_sorted, (void*)d_ex_rows,
+                  (void*)d_ex_tmp})
     cudaFree(p);
   if (h_blob) cudaFreeHost(h_blob);
   if (h_hits) cudaFreeHost(h_hits);
@@ -231,6 +232,12 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   t_ids.clear();
   any_emb = any_term_only = any_quant = false;
   max_k = 1;
+  true_k.assign(b, 0);
+  big_k.clear();
+  raw_cl.assign(b + 1, 0);
+  raw_slots.clear();
+  raw_offs.clear();
+  raw_ids.clear();
   uint32_t n_scratch = 0;
   std::unordered_map<uint32_t, uint32_t> bitmap_ref;  // bitmap index -> ref slot
   std::vector<std::pair<uint32_t, uint32_t>> ref_src;  // (kind 0 bitmap / 1 scratch, index)
@@ -243,6 +250,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   for (uint32_t i = 0; i < b; ++i) {
     const hyre_query& q = qs[i];
     q_cl[i] = static_cast<uint32_t>(cl_slot.size());
+    raw_cl[i] = static_cast<uint32_t>(raw_slots.size());
     try {
       validate_query(shape, q);
     } catch (const Error& e) {
@@ -250,9 +258,19 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
       slot_errors[i] = e.what();
       continue;
     }
+    for (uint32_t c = 0; c < q.n_clauses; ++c) {  // kept for the exhaustive path
+      raw_slots.push_back(q.slots[c]);
+      raw_offs.push_back(static_cast<uint32_t>(raw_ids.size()));
+      raw_ids.insert(raw_ids.end(), q.ids + q.id_offsets[c], q.ids + q.id_offsets[c + 1]);
+    }
     QParam p{};
     p.flags = QF_ACTIVE;
     p.k = std::min(q.k, ix->n_rows);
+    true_k[i] = p.k;
+    if (q.embedding && p.k > kSelectMaxK) {  // the threshold pipeline runs with k clamped; exhaustive() replaces it
+      big_k.push_back(i);
+      p.k = kSelectMaxK;
+    }
     max_k = std::max(max_k, p.k);
     p.quant_k = q.quant_k != 0 ? q.quant_k : 200u * q.k;
     if (q.embedding) {
@@ -318,8 +336,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     }
     qp[i] = p;
     hit_off[i] = total_hits;
-    total_hits += p.k;
+    total_hits += true_k[i];
   }
+  raw_cl[b] = static_cast<uint32_t>(raw_slots.size());
   if (g_prep.on) g_prep.t[0] += us_since(tp);
   q_cl[b] = static_cast<uint32_t>(cl_slot.size());
   cl_t.push_back(static_cast<uint32_t>(t_ids.size()));
@@ -880,6 +899,8 @@ void Executor::run() {
   HYRE_CUDA(cudaSetDevice(ix->device));
   kernels = 0;
   finish_rounds = 0;
+  exh_done = false;
+  exh_count = 0;
   ev = ev_ring[n_runs++ % kEvRing];
   const uint32_t W = ix->words;
   uint32_t* n_elig = d_counters;
@@ -993,6 +1014,13 @@ void Executor::finish_reruns() {
     bool any = false;
     for (uint32_t i = 0; i < B; ++i) any |= h_rerun[i] != 0;
     if (!any) return;
+    if (round >= kMaxRecoveryRounds) {
+      // not converging (rows tied inside the prefilter band exceed the
+      // candidate buffer): exact exhaustive top-K for those queries
+      for (uint32_t i = 0; i < B; ++i)
+        if (h_rerun[i]) exhaustive(i);
+      continue;
+    }
     ++finish_rounds;
     if (std::getenv("HYRE_DEBUG_COUNTS") && round < 4) {  // diagnostics: the recovery state of query 0
       uint64_t t[2];
@@ -1018,6 +1046,10 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
   if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_fetch before hyre_batch_prepare");
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
+  if (!big_k.empty() && !exh_done) {
+    finish_reruns();
+    finish_exhaustive();
+  }
   // one round trip in the common case: results and the recovery flags
   // together; a pending recovery (candidate overflow) reruns and re-copies
   for (int pass = 0;; ++pass) {
@@ -1060,6 +1092,111 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
     t->ebr_ms = s6[2] + s6[3];
     t->topk_ms = s6[4];
   }
+}
+
+void Executor::settle() {
+  if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_settle before hyre_batch_prepare");
+  if (any_emb) finish_reruns();
+  finish_exhaustive();
+  HYRE_CUDA(cudaStreamSynchronize(st));
+}
+
+void Executor::finish_exhaustive() {
+  if (exh_done) return;
+  exh_done = true;
+  for (uint32_t i : big_k) exhaustive(i);
+}
+
+void Executor::ensure_ex(uint64_t n) {
+  n = std::max<uint64_t>(n, 1);
+  if (n > ex_cap) {
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    for (void* p : {(void*)d_ex_keys, (void*)d_ex_sorted, (void*)d_ex_rows}) cudaFree(p);
+    ex_cap = std::max<uint64_t>(n, ex_cap * 2);
+    d_ex_keys = dmalloc<uint64_t>(ex_cap);
+    d_ex_sorted = dmalloc<uint64_t>(ex_cap);
+    d_ex_rows = dmalloc<uint32_t>(ex_cap);
+  }
+  size_t tmp = 0;
+  HYRE_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, tmp, d_ex_keys, d_ex_sorted, static_cast<int>(ex_cap),
+                                                     0, 64, st));
+  if (tmp > ex_tmp_cap) {
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_ex_tmp);
+    ex_tmp_cap = tmp;
+    d_ex_tmp = dmalloc<uint8_t>(ex_tmp_cap);
+  }
+}
+
+void Executor::sort_desc(const uint64_t* in, uint64_t* out, uint64_t n) {
+  if (!n) return;
+  size_t tmp = ex_tmp_cap;
+  HYRE_CUDA(cub::DeviceRadixSort::SortKeysDescending(d_ex_tmp, tmp, in, out, static_cast<int>(n), 0, 64, st));
+}
+
+uint64_t Executor::scan_count(const hyre_query& q) {
+  hyre_query t = q;
+  t.embedding = nullptr;
+  t.embedding_dim = 0;
+  t.k = 1;
+  t.quant_enabled = 0;
+  t.granularity = 100;
+  prepare(&t, 1);
+  if (statuses[0] != HYRE_OK) throw Error(static_cast<hyre_status>(statuses[0]), slot_errors[0]);
+  run();
+  uint32_t ne = 0;
+  HYRE_CUDA(cudaMemcpyAsync(&ne, d_counters, 4, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  return ne;
+}
+
+void Executor::scan_rows(uint32_t* d_rows, uint64_t n) {
+  if (!n) return;
+  FirstKArgs fk{d_mask, d_chunk_cnt, d_counters, d_qp, 1, ix->words, ix->n_chunks, ix->row_base, d_hit_off,
+                nullptr, nullptr, d_rows, n, 1};
+  launch_first_k(fk, st);
+  HYRE_CUDA(cudaStreamSynchronize(st));
+}
+
+// Exact exhaustive top-K of prepared query i (synchronous; see executor.cuh):
+// eligible rows (K1 mask + K5 on the aux executor) -> [quant preselect:
+// popcount keys, sort, first quant_k (quantizer.cpp:100-138, only when the
+// matches exceed quant_k, pipeline.cpp:126-130)] -> exact rescoring of every
+// row -> sort (score desc, row asc) -> first min(k, n) as the query's hits.
+void Executor::exhaustive(uint32_t i) {
+  HYRE_CUDA(cudaSetDevice(ix->device));
+  ++exh_count;
+  uint32_t* out_cnt = d_counters + 3 * max_batch;
+  uint32_t* rerun = d_counters + 4 * max_batch;
+  if (!aux) aux = std::make_unique<Executor>(ix, 1);
+  hyre_query t{};
+  t.n_clauses = raw_cl[i + 1] - raw_cl[i];
+  std::vector<uint32_t> offs(t.n_clauses + 1, 0);
+  for (uint32_t c = 0; c < t.n_clauses; ++c) offs[c] = raw_offs[raw_cl[i] + c];
+  offs[t.n_clauses] = raw_cl[i + 1] < raw_offs.size() ? raw_offs[raw_cl[i + 1]] : static_cast<uint32_t>(raw_ids.size());
+  t.slots = raw_slots.data() + raw_cl[i];
+  t.id_offsets = offs.data();
+  t.ids = raw_ids.data();
+  uint64_t n = aux->scan_count(t);
+  ensure_ex(n);
+  aux->scan_rows(d_ex_rows, n);
+  const QParam& p = qp[i];
+  if ((p.flags & QF_QUANT) && n > p.quant_k) {
+    launch_quant_keys(ix->sigs, ix->num_words, ix->num_bits, ix->row_base, d_qsig + size_t{i} * ix->num_words,
+                      d_ex_rows, n, d_ex_keys, st);
+    sort_desc(d_ex_keys, d_ex_sorted, n);
+    n = p.quant_k;
+    launch_quant_to_keys(d_ex_sorted, n, d_ex_keys, st);
+  } else {
+    launch_rows_to_keys(d_ex_rows, n, d_ex_keys, st);
+  }
+  const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+  PrefSelectArgs pa{SelectArgs{}, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32),
+                    ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
+  launch_rescore_keys(pa, bf16, i, d_ex_keys, n, st);
+  sort_desc(d_ex_keys, d_ex_sorted, n);
+  launch_keys_to_hits(d_ex_sorted, std::min<uint64_t>(n, true_k[i]), d_hits + hit_off[i], out_cnt + i, rerun + i, st);
+  HYRE_CUDA(cudaGetLastError());
 }
 
 void Executor::eligible(uint32_t* out) {
@@ -1168,7 +1305,21 @@ uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, 
   if (n == 0) return 0;
   HYRE_CUDA(cudaSetDevice(ix->device));
   const uint32_t kk = static_cast<uint32_t>(std::min<uint64_t>(k, n));
-  if (kk > kSelectMaxK) throw Error(HYRE_INVALID_ARGUMENT, "k > " + std::to_string(kSelectMaxK) + " unsupported");
+  if (kk > kSelectMaxK) {  // beyond the shared-memory select: sort every key (bucket_top_k takes any k)
+    ensure_ex(n);
+    uint32_t* d_rows = dmalloc<uint32_t>(n);
+    float* d_sc = dmalloc<float>(n);
+    hyre_hit* d_out = dmalloc<hyre_hit>(kk);
+    HYRE_CUDA(cudaMemcpyAsync(d_rows, rows, n * 4, cudaMemcpyHostToDevice, st));
+    HYRE_CUDA(cudaMemcpyAsync(d_sc, scores, n * 4, cudaMemcpyHostToDevice, st));
+    launch_make_keys(d_rows, d_sc, n, d_ex_keys, st);
+    sort_desc(d_ex_keys, d_ex_sorted, n);
+    launch_keys_to_hits(d_ex_sorted, kk, d_out, nullptr, nullptr, st);
+    HYRE_CUDA(cudaMemcpyAsync(out, d_out, kk * sizeof(hyre_hit), cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    for (void* p2 : {(void*)d_rows, (void*)d_sc, (void*)d_out}) cudaFree(p2);
+    return kk;
+  }
   uint32_t* d_rows = dmalloc<uint32_t>(n);
   float* d_sc = dmalloc<float>(n);
   uint64_t* d_keys = dmalloc<uint64_t>(n);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -140,7 +141,9 @@ struct Executor {
   void fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, int32_t* statuses,
              hyre_timings* t);
   float last_run_ms() const;
-  void settle() { if (any_emb) finish_reruns(); }  // resolve pending recovery rounds (synchronous)
+  // Resolves pending recovery rounds and exhaustive queries, then waits for
+  // the stream: the device results are final afterwards.
+  void settle();
   void eligible(uint32_t* out);  // n_elig of the last run (D2H, synchronous)
   void stage_ms(float* out) const;  // [mask, quant, sample+kth, main score, select/first-K, total]
   void stage_ms_hist(uint32_t back, float* out) const;  // the same for the run `back` runs ago
@@ -165,6 +168,33 @@ struct Executor {
   void final_select(SelectArgs fa);
   void mark(int boundary, bool stage_ran);
   uint32_t finish_rounds = 0;  // recovery rounds fetch() ran for the last batch (diagnostics)
+
+ public:
+  // ---- exhaustive exact path (kernels.cu launch_rescore_keys) -------------
+  // Hybrid queries with k > kSelectMaxK (bucket_top_k returns min(k, n) for
+  // any k, knn.cpp:42-95) run the threshold pipeline with k clamped to
+  // kSelectMaxK and are then replaced by an exhaustive exact top-K: every
+  // eligible row scored exactly, all keys sorted.  A query whose recovery
+  // rounds do not converge within kMaxRecoveryRounds (more rows tied inside
+  // the prefilter band than the candidate buffer holds) takes the same path.
+  static constexpr int kMaxRecoveryRounds = 3;
+  std::vector<uint32_t> true_k;                  // per query min(k, rows)
+  std::vector<uint32_t> big_k;                   // queries with hybrid k > kSelectMaxK
+  bool exh_done = false;
+  uint32_t exh_count = 0;                        // exhaustive queries of the last batch (diagnostics)
+  std::vector<uint32_t> raw_cl, raw_slots, raw_offs, raw_ids;  // clause copies of the prepared batch
+  std::unique_ptr<Executor> aux;                 // eligibility of one query (K1 + K5 row list)
+  uint64_t* d_ex_keys = nullptr;
+  uint64_t* d_ex_sorted = nullptr;
+  uint32_t* d_ex_rows = nullptr;
+  uint8_t* d_ex_tmp = nullptr;
+  size_t ex_cap = 0, ex_tmp_cap = 0;
+  void finish_exhaustive();
+  void exhaustive(uint32_t i);
+  uint64_t scan_count(const hyre_query& q);          // prepare + run a term-only query, its eligible count
+  void scan_rows(uint32_t* d_rows, uint64_t n);      // its eligible rows (ascending, global) into d_rows
+  void ensure_ex(uint64_t n);
+  void sort_desc(const uint64_t* in, uint64_t* out, uint64_t n);
 };
 
 }  // namespace hyreb

@@ -1751,4 +1751,79 @@ void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uin
   gather_keys_kernel<<<B, 256, 0, st>>>(g_hits, g_off, g_cnt, G, hits_stride, B, cap, keys, cnt);
 }
 
+
+// ===========================================================================
+// Exhaustive exact top-K (Executor::exhaustive): every eligible row of one
+// query scored exactly, all keys sorted.  Runs for hybrid queries with
+// k > kSelectMaxK (bucket_top_k returns min(k, n) for any k,
+// proj/src/knn.cpp:42-95) and for a query whose threshold recovery rounds
+// did not converge (more than the candidate capacity of rows tied within the
+// prefilter band).  The scores use rescore_list's arithmetic -- the one every
+// other returned score uses -- so a query's hits do not depend on the path.
+// ===========================================================================
+namespace {
+__global__ void rows_to_keys_kernel(const uint32_t* rows, uint64_t n, uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n; i += uint64_t{gridDim.x} * blockDim.x)
+    keys[i] = make_key(0.0f, rows[i]);
+}
+// quant keys (agreement << 32 | ~row) -> score keys of the same rows
+__global__ void quant_to_keys_kernel(const uint64_t* qkeys, uint64_t n, uint64_t* keys) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n; i += uint64_t{gridDim.x} * blockDim.x)
+    keys[i] = make_key(0.0f, ~static_cast<uint32_t>(qkeys[i]));
+}
+__global__ void keys_to_hits_kernel(const uint64_t* keys, uint64_t n, hyre_hit* out, uint32_t* out_cnt,
+                                    uint32_t* rerun) {
+  const uint64_t t = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  if (t == 0) {
+    if (out_cnt) *out_cnt = static_cast<uint32_t>(n);
+    if (rerun) *rerun = 0;
+  }
+  for (uint64_t i = t; i < n; i += uint64_t{gridDim.x} * blockDim.x) {
+    out[i].row = key_row(keys[i]);
+    out[i].score = key_score(keys[i]);
+  }
+}
+constexpr uint32_t kRescoreSlice = 2048;  // keys per CTA step
+template <typename RowT, int LPR, int CPL>
+__global__ void __launch_bounds__(256) rescore_keys_kernel(PrefSelectArgs pa, uint32_t q, uint64_t* keys,
+                                                           uint64_t n) {
+  __shared__ uint32_t above;  // rescore_list's threshold count (threshold 2: never incremented)
+  for (uint64_t b0 = uint64_t{blockIdx.x} * kRescoreSlice; b0 < n; b0 += uint64_t{gridDim.x} * kRescoreSlice)
+    rescore_list<RowT, LPR, CPL>(pa, q, keys + b0, static_cast<uint32_t>(n - b0 < kRescoreSlice ? n - b0 : kRescoreSlice), 2.0f,
+                                 &above);
+}
+template <typename RowT>
+void dispatch_rescore_keys(const PrefSelectArgs& a, uint32_t q, uint64_t* keys, uint64_t n, cudaStream_t st) {
+  using KFn = void (*)(PrefSelectArgs, uint32_t, uint64_t*, uint64_t);
+  KFn k = nullptr;
+  const uint32_t cpr = a.dp_chunks;
+  if (cpr == 8) k = rescore_keys_kernel<RowT, 8, 1>;
+  else if (cpr == 16) k = rescore_keys_kernel<RowT, 16, 1>;
+  else if (cpr == 32) k = rescore_keys_kernel<RowT, 32, 1>;
+  else if (cpr == 64) k = rescore_keys_kernel<RowT, 32, 2>;
+  else if (cpr == 128) k = rescore_keys_kernel<RowT, 32, 4>;
+  else if (cpr == 256) k = rescore_keys_kernel<RowT, 32, 8>;
+  else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
+  const uint64_t slices = (n + kRescoreSlice - 1) / kRescoreSlice;
+  k<<<static_cast<unsigned>(std::min<uint64_t>(slices, 148 * 8)), 256, 0, st>>>(a, q, keys, n);
+}
+unsigned grid_for(uint64_t n) { return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16))); }
+}  // namespace
+
+void launch_rows_to_keys(const uint32_t* rows, uint64_t n, uint64_t* keys, cudaStream_t st) {
+  if (n) rows_to_keys_kernel<<<grid_for(n), 256, 0, st>>>(rows, n, keys);
+}
+void launch_quant_to_keys(const uint64_t* qkeys, uint64_t n, uint64_t* keys, cudaStream_t st) {
+  if (n) quant_to_keys_kernel<<<grid_for(n), 256, 0, st>>>(qkeys, n, keys);
+}
+void launch_keys_to_hits(const uint64_t* keys, uint64_t n, hyre_hit* out, uint32_t* out_cnt, uint32_t* rerun,
+                         cudaStream_t st) {
+  keys_to_hits_kernel<<<grid_for(n), 256, 0, st>>>(keys, n, out, out_cnt, rerun);
+}
+void launch_rescore_keys(const PrefSelectArgs& a, bool bf16, uint32_t q, uint64_t* keys, uint64_t n,
+                         cudaStream_t st) {
+  if (!n) return;
+  if (bf16) dispatch_rescore_keys<__nv_bfloat16>(a, q, keys, n, st);
+  else dispatch_rescore_keys<float>(a, q, keys, n, st);
+}
 }  // namespace hyreb

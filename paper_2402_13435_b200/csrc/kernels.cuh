@@ -213,6 +213,15 @@ void launch_make_keys(const uint32_t* rows, const float* scores, uint64_t n, uin
 void launch_quant_keys(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uint32_t row_base,
                        const uint64_t* qsig, const uint32_t* rows, uint64_t n, uint64_t* keys,
                        cudaStream_t st);
+// Exhaustive exact top-K of one query (Executor::exhaustive): rows -> keys
+// (score 0), quant keys -> keys, exact rescoring of every key in place with
+// K4p's arithmetic (many CTAs), sorted keys -> hits (+ count, rerun flag).
+void launch_rows_to_keys(const uint32_t* rows, uint64_t n, uint64_t* keys, cudaStream_t st);
+void launch_quant_to_keys(const uint64_t* qkeys, uint64_t n, uint64_t* keys, cudaStream_t st);
+void launch_rescore_keys(const PrefSelectArgs& a, bool bf16, uint32_t q, uint64_t* keys, uint64_t n,
+                         cudaStream_t st);
+void launch_keys_to_hits(const uint64_t* keys, uint64_t n, hyre_hit* out, uint32_t* out_cnt, uint32_t* rerun,
+                         cudaStream_t st);
 // Multi-GPU merge: per query, keys of the hits of G gathered shard lists.
 void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
                         uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys, uint32_t* cnt,

@@ -38,10 +38,23 @@ def assert_topk_match(ref_index, query_embedding, got_rows, got_scores, ref_rows
     assert len(got_rows) == len(ref_rows), f"hit count {len(got_rows)} != oracle {len(ref_rows)}"
     if len(ref_rows) == 0:
         return
-    assert len(set(got_rows.tolist())) == len(got_rows), "duplicate rows in GPU result"
     q, _ = O.unit_embedding(query_embedding)
     emb = ref_index.embeddings if emb_override is None else emb_override
-    oracle_of_got = O.scores_rows(emb, q, got_rows)
+    check_topk(got_rows, got_scores, ref_rows, ref_scores, O.scores_rows(emb, q, got_rows), rel, abs_)
+
+
+def check_topk(got_rows, got_scores, ref_rows, ref_scores, oracle_of_got, rel=REL_TOL, abs_=ABS_TOL):
+    """Gates 2-3 given the oracle's own score of every returned row
+    (`oracle_of_got`, e.g. the compiled reference's exact_scores)."""
+    got_rows = np.asarray(got_rows, np.int64)
+    got_scores = np.asarray(got_scores, np.float32)
+    ref_rows = np.asarray(ref_rows, np.int64)
+    ref_scores = np.asarray(ref_scores, np.float32)
+    oracle_of_got = np.asarray(oracle_of_got, np.float64)
+    assert len(got_rows) == len(ref_rows), f"hit count {len(got_rows)} != oracle {len(ref_rows)}"
+    if len(ref_rows) == 0:
+        return
+    assert len(set(got_rows.tolist())) == len(got_rows), "duplicate rows in GPU result"
     e_got = eps(oracle_of_got, rel, abs_)
     # (b) every GPU score within tolerance of the oracle's score for that row
     bad = np.abs(got_scores.astype(np.float64) - oracle_of_got) > e_got
@@ -54,7 +67,7 @@ def assert_topk_match(ref_index, query_embedding, got_rows, got_scores, ref_rows
     missing = must - set(got_rows.tolist())
     assert not missing, f"oracle hits missing from GPU result: {sorted(missing)[:10]}"
     # (c) GPU hits outside the oracle set are boundary ties
-    extra = np.asarray([r not in set(ref_rows.tolist()) for r in got_rows])
+    extra = ~np.isin(got_rows, ref_rows)
     if extra.any():
         assert (oracle_of_got[extra] >= tau - 2 * e_tau).all(), (
             f"non-tied extra rows {got_rows[extra]} scores {oracle_of_got[extra]} tau {tau}")

@@ -121,62 +121,120 @@ def shard_range(n, rank, world):
 # ---------------------------------------------------------------------------
 # reference (CPU) arm
 # ---------------------------------------------------------------------------
-def reference_sample(w, sample_rows: int, batch: int, k: int, threads: int, steps: int = 1):
-    """Times the unmodified reference (oracle/_ref) Executor::execute with
-    quant off over a `sample_rows`-row prefix of the same corpus and the same
-    queries; `threads` executors over one FrozenIndex, like the reference's
-    ExecutorPool (proj/src/service.cpp:99-141).  Returns (qps scaled to the
-    full index, seconds per step, info)."""
+FULL_REF_MAX_ROWS = 10_000_000  # larger corpora: the reference on a row prefix, scaled (stated)
+
+
+def reference_index(w, so, ids, emb, threads):
+    """The unmodified reference (oracle/_ref) over the corpus rows given,
+    built as concurrent FrozenIndex shards by its own IndexBuilder/freeze
+    (oracle/ref.py ShardedRef, SURVEY §8(d) sharded oracle)."""
+    from oracle import ref as R
+    t0 = time.perf_counter()
+    sref = R.ShardedRef(so, ids, emb, w.num_clauses, w.max_num_attr, w.num_bits, w.seed, threads=threads)
+    return sref, time.perf_counter() - t0
+
+
+def ref_queries(w, batch, k):
     from oracle import ref as R
     from paper_2402_13435_b200 import workloads as W
-    so, ids, emb = W.docs(w, 0, sample_rows)
-    t0 = time.perf_counter()
-    ri = R.RefIndex.build(so.astype(np.uint32), ids, emb, w.num_clauses, w.max_num_attr, w.num_bits, w.seed, "d")
-    build_s = time.perf_counter() - t0
     raws, qemb = W.queries(w, batch)
-    qs = []
-    for i, raw in enumerate(raws):
-        clauses = R.normalize_query(raw, w.num_clauses) if raw else []
-        qs.append((clauses, qemb[i] if qemb is not None else None, k, False, 0, 100))
-    per_step = []
-    for _ in range(steps):
-        secs, _ = ri.execute_parallel(qs, threads, want_hits=False)
-        per_step.append(secs)
-    scale = w.n / sample_rows  # the reference's full scan is linear in rows
-    qps = batch / (statistics.median(per_step) * scale)
-    return qps, per_step, build_s
+    return [(R.normalize_query(raw, w.num_clauses) if raw else [], qemb[i] if qemb is not None else None, k,
+             False, 0, 100) for i, raw in enumerate(raws)]
+
+
+def ref_rows(w):
+    return min(w.n, FULL_REF_MAX_ROWS)
+
+
+def ref_sample_text(w, rows, nq, threads, build_s, shards):
+    scope = (f"the full {w.n}-row index" if rows == w.n else
+             f"a {rows}-row prefix of the {w.n}-row index, QPS scaled by rows ({w.n}/{rows})")
+    return (f"{nq} queries of the {w.name} batch per step on {scope}: reference Executor::execute (quant off) over "
+            f"{threads} threads, the index built as {shards} reference FrozenIndex shards, each (query, shard) pair "
+            f"one reference call, shard top-K lists merged by "
+            f"(score desc, row asc); reference IndexBuilder+freeze {build_s:.1f}s")
 
 
 def run_reference(args, w):
+    """--impl reference: the reference's own CPU path (oracle/_ref, unmodified
+    proj/src sources) timed on the host cores; rank 0 only.  Each step is a
+    bounded sample of the workload: `threads` queries of the batch (cycling
+    through it) over the whole index -- nothing of this repository's product
+    library is loaded in this process."""
+    from paper_2402_13435_b200 import workloads as W
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = min(args.ref_sample_rows, w.n)
-    qps, per_step, build_s = reference_sample(w, sample, args.batch, args.k, threads, steps=max(1, args.steps))
+    rows = ref_rows(w)
+    so, ids, emb = W.docs(w, 0, rows)
+    sref, build_s = reference_index(w, so, ids, emb, threads)
+    del so, ids, emb
+    qs = ref_queries(w, args.batch, args.k)
+    per = max(1, min(len(qs), args.ref_queries or threads))
+    cursor = [0]
+
+    def step():
+        sample = [qs[(cursor[0] + i) % len(qs)] for i in range(per)]
+        cursor[0] += per
+        secs, _ = sref.execute(sample, threads)
+        return secs
+
+    for _ in range(args.warmup):
+        step()
+    per_step = [step() for _ in range(args.steps)]
+    scale = w.n / rows
+    total = sum(per_step) * scale
+    qps = per * args.steps / total
     line = {
         "impl": "reference", "metric": "queries_per_sec", "value": qps, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(per_step) * 1e3 * (w.n / sample),
+        "ms_per_step": statistics.mean(per_step) * scale * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SURVEY §8(d) generator, std::mt19937_64)",
         "config": workload_config(w, args),
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                         "sample": f"{sample}-row prefix of {w.name} ({sample / w.n:.0%} of {w.n} rows), "
-                                   f"{args.batch} queries per step via Executor::execute with quant off on "
-                                   f"{threads} threads (ExecutorPool model); QPS scaled by rows "
-                                   f"({w.n}/{sample}); reference IndexBuilder build {build_s:.1f}s"},
+                         "sample": ref_sample_text(w, rows, per, threads, build_s, sref.g)},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def workload_config(w, args):
+    """Identical in both arms (the driver compares them)."""
     return {"workload": f"{w.name}: {w.n} jobs x d{w.dim} {w.dtype}, "
                         + ("match-all" if w.kind == "match_all" else f"{w.num_clauses}-clause CNF"),
             "jobs": w.n, "dim": w.dim, "emb_dtype": w.dtype, "clauses": w.num_clauses, "batch": args.batch,
             "k": args.k, "quant": False, "parallelism": f"rows-sharded x{dist_env()[1]}",
             "l2": "inputs larger than L2 (index >> 126 MB), no flush"}
+
+
+def parity_check(sref, qs, got):
+    """Our hits (rows, scores per query) against the reference's on the same
+    index: rows identical except ties at the K-th score, scores within
+    max(1e-3 |s|, 2e-5) of the reference's exact_scores of the same row
+    (SURVEY §8(d) gates 2-3); term-only lists identical."""
+    secs, want = sref.execute(qs)
+    mism, max_err, detail = 0, 0.0, []
+    for i, (q, (gr, gs), (st, rr, rs)) in enumerate(zip(qs, got, want)):
+        ok = st == 0 and len(gr) == len(rr)
+        if ok and q[1] is None:
+            ok = bool(np.array_equal(gr, rr))
+        elif ok and len(rr):
+            o = sref.exact_scores(q[1], gr).astype(np.float64)
+            err = np.abs(gs.astype(np.float64) - o)
+            max_err = max(max_err, float(err.max()))
+            tol = np.maximum(1e-3 * np.abs(o), 2e-5)
+            tau = float(rs[-1])
+            et = max(1e-3 * abs(tau), 2e-5)
+            must = rr[rs > tau + et]
+            extra = ~np.isin(gr, rr)
+            ok = bool((err <= tol).all() and np.isin(must, gr).all() and (o[extra] >= tau - 2 * et).all())
+        if not ok:
+            mism += 1
+            detail.append(i)
+    return {"queries": len(qs), "mismatches": mism, "max_abs_err": max_err, "failed": detail[:8],
+            "reference": "oracle/_ref (unmodified reference sources), same index and queries"}, secs
 
 
 # ---------------------------------------------------------------------------
@@ -197,8 +255,26 @@ def run_ours(args, w):
     lib = L.lib()
     t_setup = time.perf_counter()
     rb, re_ = shard_range(w.n, rank, world)
-    frozen = W.build_frozen(w, rb, re_)
+    so, ids, emb = W.docs(w, rb, re_)
+    frozen = W.freeze_docs(w, so, ids, emb, rb)
     t_frozen = time.perf_counter() - t_setup
+    # The reference over the same rows (N = 1): the parity check of our
+    # results and the timed CPU baseline (full index up to 10M rows, else a
+    # stated prefix).
+    sref = ref_build_s = None
+    ref_threads = os.cpu_count() or 1
+    want_ref = world == 1 and not args.no_cpu_baseline
+    if want_ref:
+        try:
+            if w.n <= FULL_REF_MAX_ROWS:
+                sref, ref_build_s = reference_index(w, so, ids, emb, ref_threads)
+            else:
+                del so, ids, emb
+                so, ids, emb = W.docs(w, 0, ref_rows(w))
+                sref, ref_build_s = reference_index(w, so, ids, emb, ref_threads)
+        except Exception as e:  # reported, never fatal
+            sref, ref_build_s = None, str(e)[:200]
+    del so, ids, emb
     dev = hy.DeviceIndex(frozen, device=local, dtype=w.dtype, tensor_path=True, row_offset=rb)
     stats = dev.stats()
     raws, qemb = W.queries(w, args.batch)
@@ -281,6 +357,21 @@ def run_ours(args, w):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # The timed steps enqueue hyre_batch_run only; threshold recovery rounds
+    # and exhaustive queries would run later, at settle.  The batch is the
+    # same every step, so its recovery need is too: measure it once and, if
+    # any, settle inside every timed step so no work falls outside the clock.
+    check(lib.hyre_batch_settle(h))
+    rec = np.zeros(2, np.uint32)
+    check(lib.hyre_batch_recovery(h, rec.ctypes.data_as(L.u32p)))
+    reruns = {"recovery_rounds": int(rec[0]), "exhaustive_queries": int(rec[1]),
+              "settled_in_timed_steps": bool(rec.any())}
+    if rec.any():
+        run_step = step
+
+        def step():  # noqa: F811
+            run_step()
+            check(lib.hyre_batch_settle(h if not alt[0] or n_step[0] % 2 == 1 else ex_b._h))
     s6 = (C.c_float * 6)()
 
     # ---- timed region: exactly K back-to-back steps, device time ----------
@@ -334,6 +425,10 @@ def run_ours(args, w):
     lat = [r[5] for r in stage_rows]
     main_ms = [r[3] for r in stage_rows]
     p50 = statistics.median(lat)
+    lat_sorted = sorted(lat)
+
+    def pct(p):  # nearest-rank percentile (bench.cpp:113-123 reports p50/p95/p99)
+        return lat_sorted[min(len(lat_sorted) - 1, max(0, int(np.ceil(p / 100 * len(lat_sorted))) - 1))]
     main_avg = statistics.mean(main_ms)
 
     # ---- end-to-end through the C-ABI with host buffers ---------------------
@@ -383,6 +478,10 @@ def run_ours(args, w):
     if not os.environ.get("HYRE_TC_DEBUG"):
         assert all(sts == 0) and int(counts.min()) > 0, "empty results in the e2e run"
     single_e2e = B * e2e_steps / e2e_s
+    # our final answers (the last public-API call) for the parity check
+    hit_arr = np.frombuffer(host_hits, dtype=np.uint32).reshape(-1, 2)
+    ours = [(hit_arr[int(offs[i]):int(offs[i]) + int(counts[i]), 0].astype(np.int64),
+             hit_arr[int(offs[i]):int(offs[i]) + int(counts[i]), 1].view(np.float32).copy()) for i in range(B)]
 
     # ---- the same calls from two host threads, one executor each ----------
     # (the reference's ExecutorPool model, service.cpp:99-141: one thread's
@@ -460,7 +559,9 @@ def run_ours(args, w):
         # scan itself runs on the int8 prefilter plane when path & 32
         "dtype": (f"{w.dtype} (scan: int8 prefilter)" if path & 32 else w.dtype),
         "data": "synthetic (SURVEY §8(d) generator, std::mt19937_64; index built by the product IndexBuilder)",
-        "config": {**workload_config(w, args), "batches_in_flight": 1},
+        "config": workload_config(w, args),
+        "p95_ms": pct(95), "p99_ms": pct(99), "latency_samples": len(lat),
+        "reruns": reruns,
         "inflight2": inflight2,
         "stages_ms": dict(zip(["mask", "quant", "sample", "main_scorer", "select_firstk", "run"],
                               [statistics.median(r[i] for r in stage_rows) for i in range(6)])),
@@ -479,17 +580,22 @@ def run_ours(args, w):
         "clocks": clocks.summary(),
         "index": {"build_s": t_frozen, **{k: stats[k] for k in ("num_terms", "bitmap_terms", "csr_terms")}},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            threads = os.cpu_count() or 1
-            sample = min(args.ref_sample_rows, w.n)
-            cqps, per_step, build_s = reference_sample(w, sample, B, args.k, threads)
-            line["cpu_baseline"] = {
-                "value": cqps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                "sample": f"{sample}-row prefix of {w.name}, {B} queries via the reference Executor::execute "
-                          f"(quant off) on {threads} threads; QPS scaled by rows ({w.n}/{sample})"}
-        except Exception as e:  # reported, never fatal
-            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if want_ref:
+        if sref is None:
+            line["cpu_baseline"] = {"value": None, "error": ref_build_s}
+            line["parity"] = None
+        else:
+            qs = ref_queries(w, B, args.k)
+            rows = ref_rows(w)
+            if rows == w.n:
+                par, secs = parity_check(sref, qs, ours)
+                line["parity"] = par
+            else:
+                secs, _ = sref.execute(qs)
+                line["parity"] = {"queries": 0, "note": f"reference built on a {rows}-row prefix only"}
+            cqps = B / (secs * w.n / rows)
+            line["cpu_baseline"] = {"value": cqps, "unit": "queries/s", "cores": ref_threads, "kind": "reference",
+                                    "sample": ref_sample_text(w, rows, B, ref_threads, ref_build_s, sref.g)}
     print(json.dumps(line), flush=True)
 
 
@@ -524,7 +630,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--rows", type=int, default=None, help="override the workload's row count")
-    ap.add_argument("--ref-sample-rows", type=int, default=1_000_000)
+    ap.add_argument("--ref-queries", type=int, default=None,
+                    help="reference arm: queries per step (default: one per host thread)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--inflight", type=int, default=2, help="batches in flight on separate executors (N = 1)")
     args = ap.parse_args()

@@ -294,6 +294,11 @@ hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* ou
  * per-slot counts (u32[b]).  Valid until the next prepare. */
 hyre_status hyre_batch_device_results(hyre_executor* ex, void** hits, uint64_t* n_hits, void** offsets,
                                       void** counts);
+/* Recovery work the last batch needed once settled (fetch / settle):
+ * out2 = {threshold recovery rounds, queries answered by the exhaustive exact
+ * path (hybrid k > 4096, or a recovery that did not converge)}.  A benchmark
+ * timing hyre_batch_run alone asserts both are 0. */
+hyre_status hyre_batch_recovery(const hyre_executor* ex, uint32_t* out2);
 /* Bytes the last prepare copied host->device and the last fetch copied back. */
 hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h);
 /* ------------------------------------------------------------------------

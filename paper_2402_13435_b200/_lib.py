@@ -112,6 +112,7 @@ SIGNATURES = {
     "hyre_batch_kernel_count": (C.c_uint32, [vp]),
     "hyre_batch_path": (C.c_uint32, [vp]),
     "hyre_batch_tc_variant": (None, [vp, u32p]),
+    "hyre_batch_recovery": (C.c_int, [vp, u32p]),
     "hyre_batch_eligible": (C.c_int, [vp, u32p]),
     "hyre_batch_term_bytes": (C.c_uint64, [vp]),
     "hyre_batch_scan_bytes": (C.c_uint64, [vp]),

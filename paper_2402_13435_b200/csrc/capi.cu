@@ -448,6 +448,15 @@ hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* ou
   });
 }
 
+hyre_status hyre_batch_recovery(const hyre_executor* ex, uint32_t* out2) {
+  return guard([&] {
+    need(ex, "executor");
+    need(out2, "out");
+    out2[0] = ex->ex->finish_rounds;
+    out2[1] = ex->ex->exh_count;
+  });
+}
+
 hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h) {
   return guard([&] {
     need(ex, "executor");

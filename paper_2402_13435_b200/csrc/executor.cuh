@@ -167,6 +167,8 @@ struct Executor {
   void score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capacity);
   void final_select(SelectArgs fa);
   void mark(int boundary, bool stage_ran);
+
+ public:
   uint32_t finish_rounds = 0;  // recovery rounds fetch() ran for the last batch (diagnostics)
 
  public:

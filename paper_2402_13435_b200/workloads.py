@@ -142,13 +142,17 @@ def queries(w: Workload, b: Optional[int] = None, high_pass: bool = True):
 def build_frozen(w: Workload, row_begin: int = 0, row_end: Optional[int] = None):
     """Generates the corpus rows [row_begin, row_end) and freezes them with the
     product IndexBuilder (doc ids "d<global row>")."""
-    import paper_2402_13435_b200 as hy
     so, ids, emb = docs(w, row_begin, row_end)
+    return freeze_docs(w, so, ids, emb, row_begin)
+
+
+def freeze_docs(w: Workload, so, ids, emb, row_begin: int = 0):
+    """Freezes generated rows with the product IndexBuilder."""
+    import paper_2402_13435_b200 as hy
     b = hy.IndexBuilder(hy.IndexConfig(w.num_clauses, w.max_num_attr, w.dim))
     if row_begin:
         # keep global doc ids: pad the running row counter with a distinct prefix per shard
         b.add_documents(so, ids, emb, doc_id_prefix=f"d{row_begin}+")
     else:
         b.add_documents(so, ids, emb, doc_id_prefix="d")
-    del so, ids, emb
     return b.freeze(hy.make_codec(w.dim, w.num_bits, w.seed))

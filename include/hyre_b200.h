@@ -302,6 +302,55 @@ hyre_status hyre_batch_recovery(const hyre_executor* ex, uint32_t* out2);
 /* Bytes the last prepare copied host->device and the last fetch copied back. */
 hyre_status hyre_batch_io_bytes(const hyre_executor* ex, uint64_t* h2d, uint64_t* d2h);
 /* ------------------------------------------------------------------------
+ * Row-sharded executor over several GPUs (the multi-GPU
+ * form of FrozenIndex + Executor, pipeline.hpp:69-96).  The frozen rows are
+ * split into n_shards contiguous ranges; shard g lives on devices[g]
+ * (nullable: device g % device count; several shards may share a device)
+ * with its own Executor and stream.  Per-shard top-K lists are merged exactly
+ * on shard 0's device by one kernel that reads every shard's hits through
+ * peer memory (NVLink), term-only lists are concatenated in row order, and
+ * the quant pre-selection is global (shards exchange histograms and tie
+ * counts the same way), so results equal the unsharded executor's.  Peer
+ * access between the devices is required.  Single-in-flight like Executor.
+ * ------------------------------------------------------------------------ */
+typedef struct hyre_sharded_index hyre_sharded_index;
+typedef struct hyre_sharded_index_options {
+  uint32_t n_shards;       /* G, 1 .. 16 */
+  const int32_t* devices;  /* [n_shards] CUDA ordinals, or NULL */
+  uint32_t emb_dtype;      /* hyre_emb_dtype */
+  uint32_t tensor_path;    /* as hyre_index_options */
+} hyre_sharded_index_options;
+/* The device shards of a frozen index (enables peer access between their
+ * devices); shared by every sharded executor created over it. */
+hyre_status hyre_sharded_index_create(const hyre_frozen* f, const hyre_sharded_index_options* opts,
+                                      hyre_sharded_index** out);
+void hyre_sharded_index_destroy(hyre_sharded_index* ix);
+/* shard count and each shard's device (devices may be NULL) */
+hyre_status hyre_sharded_index_info(const hyre_sharded_index* ix, uint32_t* n_shards, int32_t* devices);
+
+typedef struct hyre_sharded hyre_sharded;
+/* Executor(index, max_batch) over the shards: one Executor + stream per shard. */
+hyre_status hyre_sharded_create(hyre_sharded_index* ix, uint32_t max_batch, hyre_sharded** out);
+void hyre_sharded_destroy(hyre_sharded* s);
+/* Executor::execute_batch over all shards (same contract as hyre_execute_batch). */
+hyre_status hyre_sharded_execute_batch(hyre_sharded* s, const hyre_query* qs, uint32_t b, hyre_hit* hits,
+                                       const uint64_t* hit_offsets, uint32_t* counts, int32_t* statuses,
+                                       hyre_timings* timings);
+const char* hyre_sharded_slot_error(const hyre_sharded* s, uint32_t slot);
+/* Split form for device-resident timing (as hyre_batch_prepare/run/settle/
+ * fetch): run enqueues every shard and the root merge without host
+ * synchronisation; the root stream's work completes after all of it. */
+hyre_status hyre_sharded_prepare(hyre_sharded* s, const hyre_query* qs, uint32_t b);
+hyre_status hyre_sharded_run(hyre_sharded* s);
+hyre_status hyre_sharded_settle(hyre_sharded* s);
+hyre_status hyre_sharded_fetch(hyre_sharded* s, hyre_hit* hits, const uint64_t* hit_offsets, uint32_t* counts,
+                               int32_t* statuses, hyre_timings* timings);
+void* hyre_sharded_stream(const hyre_sharded* s); /* root stream (cudaStream_t) */
+uint32_t hyre_sharded_kernel_count(const hyre_sharded* s);
+/* out2 = {recovery rounds, exhaustive queries} summed over shards (after settle/fetch) */
+hyre_status hyre_sharded_recovery(const hyre_sharded* s, uint32_t* out2);
+
+/* ------------------------------------------------------------------------
  * Executor pool with dynamic request batching: the replacement for
  * SearchService::ExecutorPool (service.cpp:99-141; ServiceConfig{workers,
  * max_batch} service.hpp:19-26).  `workers` executors (own CUDA streams);

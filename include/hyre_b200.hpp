@@ -16,8 +16,10 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -133,6 +135,33 @@ struct IndexConfig {
 
 class Executor;
 
+// Where an index's device copy lives (not part of the reference API, which
+// is CPU-only).  Defaults: one GPU (device 0), fp32 rows + tensor-core tiles;
+// the environment overrides them for callers relinked without code changes:
+// HYRE_GPUS=N shards the rows over devices 0..N-1 (HYRE_DEVICES="a,b,..."
+// names them), HYRE_EMB_DTYPE=bf16 stores bf16 rows.
+struct DeviceOptions {
+  std::vector<int> devices{0};  // one entry per row shard
+  bool bf16 = false;
+  bool tensor_path = true;
+  static DeviceOptions from_env() {
+    DeviceOptions o;
+    if (const char* d = std::getenv("HYRE_DEVICES")) {
+      o.devices.clear();
+      for (const char* p = d; *p;) {
+        char* end = nullptr;
+        o.devices.push_back(static_cast<int>(std::strtol(p, &end, 10)));
+        p = *end ? end + 1 : end;
+      }
+    } else if (const char* n = std::getenv("HYRE_GPUS")) {
+      o.devices.clear();
+      for (int g = 0; g < std::max(1, std::atoi(n)); ++g) o.devices.push_back(g);
+    }
+    if (const char* t = std::getenv("HYRE_EMB_DTYPE")) o.bf16 = std::string(t) == "bf16";
+    return o;
+  }
+};
+
 class FrozenIndex {
  public:
   FrozenIndex(FrozenIndex&&) noexcept = default;
@@ -187,14 +216,38 @@ class FrozenIndex {
     return FrozenIndex(f);
   }
 
-  // The device column store (GPU 0, fp32 rows + tensor-core tiles), built on
-  // first use by an Executor and shared by every executor of this index.
+  // Device placement for the executors created later (before the first one;
+  // default DeviceOptions::from_env()).
+  void set_device_options(DeviceOptions o) {
+    std::lock_guard<std::mutex> lk(dev_->m);
+    if (dev_->ix || dev_->sx) throw ValidationError("device options must be set before the first Executor");
+    dev_->opts = std::move(o);
+  }
+  const DeviceOptions& device_options() const { return dev_->opts; }
+  bool sharded() const { return dev_->opts.devices.size() > 1; }
+  // The device column store (one GPU) or its row shards (several), built on
+  // first use by an Executor and shared by every executor of this index; safe
+  // to call from several threads (the reference FrozenIndex is shared
+  // read-only, corpus.hpp:54-56).
   hyre_index* device() const {
+    std::lock_guard<std::mutex> lk(dev_->m);
     if (!dev_->ix) {
-      hyre_index_options o{0, HYRE_EMB_F32, 0, 0, 1, 0};
+      const DeviceOptions& d = dev_->opts;
+      hyre_index_options o{d.devices.empty() ? 0 : d.devices[0], d.bf16 ? HYRE_EMB_BF16 : HYRE_EMB_F32, 0, 0,
+                           d.tensor_path ? 1u : 0u, 0};
       detail::check(hyre_index_create(f_.get(), &o, &dev_->ix));
     }
     return dev_->ix;
+  }
+  hyre_sharded_index* device_shards() const {
+    std::lock_guard<std::mutex> lk(dev_->m);
+    if (!dev_->sx) {
+      const DeviceOptions& d = dev_->opts;
+      hyre_sharded_index_options o{static_cast<std::uint32_t>(d.devices.size()), d.devices.data(),
+                                   d.bf16 ? HYRE_EMB_BF16 : HYRE_EMB_F32, d.tensor_path ? 1u : 0u};
+      detail::check(hyre_sharded_index_create(f_.get(), &o, &dev_->sx));
+    }
+    return dev_->sx;
   }
   const hyre_frozen* handle() const { return f_.get(); }
 
@@ -204,9 +257,13 @@ class FrozenIndex {
     hyre_frozen_shape(f, &shape_);
   }
   struct Dev {
+    std::mutex m;
+    DeviceOptions opts = DeviceOptions::from_env();
     hyre_index* ix = nullptr;
+    hyre_sharded_index* sx = nullptr;
     ~Dev() {
       if (ix) hyre_index_destroy(ix);
+      if (sx) hyre_sharded_index_destroy(sx);
     }
   };
   std::unique_ptr<hyre_frozen, void (*)(hyre_frozen*)> f_;
@@ -350,14 +407,28 @@ inline void validate_query(const FrozenIndex& index, const HybridQuery& query) {
 
 class Executor {
  public:
+  // One GPU: an executor with its own stream and scratch.  Several (the
+  // index's DeviceOptions name more than one device): a sharded executor --
+  // one stream per shard, exact merge on the first device; same results.
   explicit Executor(const FrozenIndex& index, std::uint32_t max_batch = 16) : index_(index), max_batch_(max_batch) {
     if (max_batch < 1) throw ValidationError("maxBatch must be >= 1");
+    if (index.sharded()) {
+      hyre_sharded* s = nullptr;
+      detail::check(hyre_sharded_create(index.device_shards(), max_batch, &s));
+      sh_.reset(s);
+      return;
+    }
     hyre_executor* ex = nullptr;
     detail::check(hyre_executor_create(index.device(), max_batch, &ex));
     ex_.reset(ex);
   }
 
   TopKResult execute(const HybridQuery& query, StageTimings* timings = nullptr) {
+    if (sh_) {
+      auto out = execute_batch(BatchRequest{{query}}, timings);
+      if (!out[0].ok) throw ValidationError(out[0].error);
+      return std::move(out[0].result);
+    }
     detail::QueryPack p({query});
     std::vector<hyre_hit> hits(std::max<std::uint32_t>(1, std::min(query.k, index_.num_docs())));
     std::uint32_t n = 0;
@@ -376,20 +447,26 @@ class Executor {
     std::vector<std::uint32_t> counts(b);
     std::vector<std::int32_t> st(b);
     hyre_timings t{};
-    detail::check(hyre_execute_batch(ex_.get(), p.q.data(), b, hits.data(), offs.data(), counts.data(), st.data(), &t));
+    if (sh_)
+      detail::check(hyre_sharded_execute_batch(sh_.get(), p.q.data(), b, hits.data(), offs.data(), counts.data(),
+                                               st.data(), &t));
+    else
+      detail::check(hyre_execute_batch(ex_.get(), p.q.data(), b, hits.data(), offs.data(), counts.data(), st.data(),
+                                       &t));
     if (timings) *timings = StageTimings{t.tbr_ms, t.quant_ms, t.ebr_ms, t.topk_ms, t.total_ms};
     std::vector<QueryOutcome> out(b);
     for (std::uint32_t i = 0; i < b; ++i) {
       out[i].ok = st[i] == HYRE_OK;
       if (out[i].ok) out[i].result = to_result(hits.data() + offs[i], counts[i]);
-      else out[i].error = hyre_executor_slot_error(ex_.get(), i);
+      else out[i].error = sh_ ? hyre_sharded_slot_error(sh_.get(), i) : hyre_executor_slot_error(ex_.get(), i);
     }
     return out;
   }
 
   const FrozenIndex& index() const { return index_; }
   std::uint32_t max_batch() const { return max_batch_; }
-  hyre_executor* handle() const { return ex_.get(); }
+  hyre_executor* handle() const { return ex_.get(); }  // single-GPU executors
+  hyre_sharded* sharded_handle() const { return sh_.get(); }
 
  private:
   TopKResult to_result(const hyre_hit* h, std::uint32_t n) const {
@@ -400,10 +477,12 @@ class Executor {
   }
   struct Del {
     void operator()(hyre_executor* e) const { hyre_executor_destroy(e); }
+    void operator()(hyre_sharded* s) const { hyre_sharded_destroy(s); }
   };
   const FrozenIndex& index_;
   std::uint32_t max_batch_;
   std::unique_ptr<hyre_executor, Del> ex_;
+  std::unique_ptr<hyre_sharded, Del> sh_;
 };
 
 inline TopKResult execute(const FrozenIndex& index, const HybridQuery& query) {
@@ -417,9 +496,26 @@ inline std::vector<QueryOutcome> execute_batch(const FrozenIndex& index, const B
 }
 
 // ---- stage functions (term_match.hpp:43-45, knn.hpp:24-35, quantizer.hpp:71-74) ----
+namespace detail {
+// A single-GPU executor over the whole index for the stage functions (also
+// on a sharded index: they are per-call test / tooling entry points).
+struct StageExec {
+  explicit StageExec(const FrozenIndex& index) {
+    hyre_executor* e = nullptr;
+    check(hyre_executor_create(index.device(), 1, &e));
+    ex.reset(e);
+  }
+  hyre_executor* handle() const { return ex.get(); }
+  struct Del {
+    void operator()(hyre_executor* e) const { hyre_executor_destroy(e); }
+  };
+  std::unique_ptr<hyre_executor, Del> ex;
+};
+}  // namespace detail
+
 inline std::vector<Messenger> full_scan_tbr(const FrozenIndex& index, const CnfQuery& query,
                                             std::uint32_t batch_id = 0) {
-  Executor ex(index, 1);
+  detail::StageExec ex(index);
   HybridQuery hq{query, std::nullopt, 1, {}};
   detail::QueryPack p({hq});
   std::vector<std::uint32_t> rows(index.num_docs());
@@ -433,7 +529,7 @@ inline std::vector<Messenger> full_scan_tbr(const FrozenIndex& index, const CnfQ
 
 inline ScoredMessengers exact_scores(const FrozenIndex& index, std::span<const float> query_embedding,
                                      std::vector<Messenger> candidates) {
-  Executor ex(index, 1);
+  detail::StageExec ex(index);
   std::vector<std::uint32_t> rows;
   for (const auto& m : candidates) rows.push_back(m.row_id);
   std::vector<float> sc(rows.size());
@@ -447,7 +543,7 @@ inline ScoredMessengers exact_scores(const FrozenIndex& index, std::span<const f
 
 inline TopKResult bucket_top_k(const FrozenIndex& index, const ScoredMessengers& scored, std::uint32_t k,
                                std::uint32_t granularity = 100) {
-  Executor ex(index, 1);
+  detail::StageExec ex(index);
   std::vector<std::uint32_t> rows;
   std::vector<float> sc;
   for (const auto& m : scored.items) {
@@ -464,7 +560,7 @@ inline TopKResult bucket_top_k(const FrozenIndex& index, const ScoredMessengers&
 
 inline std::vector<Messenger> preselect(const FrozenIndex& index, const Signature& query_signature,
                                         std::span<const Messenger> candidates, std::uint32_t quant_k) {
-  Executor ex(index, 1);
+  detail::StageExec ex(index);
   std::vector<std::uint32_t> rows, out(candidates.size());
   for (const auto& m : candidates) rows.push_back(m.row_id);
   std::uint64_t n = 0;

@@ -58,6 +58,10 @@ class hyre_index_options(C.Structure):
                 ("row_end", C.c_uint32), ("tensor_path", C.c_uint32), ("row_offset", C.c_uint32)]
 
 
+class hyre_sharded_index_options(C.Structure):
+    _fields_ = [("n_shards", C.c_uint32), ("devices", i32p), ("emb_dtype", C.c_uint32), ("tensor_path", C.c_uint32)]
+
+
 class hyre_index_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "num_rows", "row_base", "dim", "row_stride", "num_terms", "bitmap_terms", "csr_terms", "postings",
@@ -113,6 +117,21 @@ SIGNATURES = {
     "hyre_batch_path": (C.c_uint32, [vp]),
     "hyre_batch_tc_variant": (None, [vp, u32p]),
     "hyre_batch_recovery": (C.c_int, [vp, u32p]),
+    "hyre_sharded_index_create": (C.c_int, [vp, C.POINTER(hyre_sharded_index_options), C.POINTER(vp)]),
+    "hyre_sharded_index_destroy": (None, [vp]),
+    "hyre_sharded_index_info": (C.c_int, [vp, u32p, i32p]),
+    "hyre_sharded_create": (C.c_int, [vp, C.c_uint32, C.POINTER(vp)]),
+    "hyre_sharded_destroy": (None, [vp]),
+    "hyre_sharded_execute_batch": (C.c_int, [vp, C.POINTER(hyre_query), C.c_uint32, C.POINTER(hyre_hit), u64p, u32p,
+                                             i32p, C.POINTER(hyre_timings)]),
+    "hyre_sharded_slot_error": (C.c_char_p, [vp, C.c_uint32]),
+    "hyre_sharded_prepare": (C.c_int, [vp, C.POINTER(hyre_query), C.c_uint32]),
+    "hyre_sharded_run": (C.c_int, [vp]),
+    "hyre_sharded_settle": (C.c_int, [vp]),
+    "hyre_sharded_fetch": (C.c_int, [vp, C.POINTER(hyre_hit), u64p, u32p, i32p, C.POINTER(hyre_timings)]),
+    "hyre_sharded_stream": (vp, [vp]),
+    "hyre_sharded_kernel_count": (C.c_uint32, [vp]),
+    "hyre_sharded_recovery": (C.c_int, [vp, u32p]),
     "hyre_batch_eligible": (C.c_int, [vp, u32p]),
     "hyre_batch_term_bytes": (C.c_uint64, [vp]),
     "hyre_batch_scan_bytes": (C.c_uint64, [vp]),

@@ -9,6 +9,7 @@
 
 #include "executor.cuh"
 #include "service.cuh"
+#include "sharded.cuh"
 #include "hyre_b200.h"
 
 using namespace hyreb;
@@ -27,6 +28,12 @@ struct hyre_executor {
 };
 struct hyre_pool {
   std::unique_ptr<Pool> p;
+};
+struct hyre_sharded_index {
+  std::unique_ptr<ShardedIndex> ix;
+};
+struct hyre_sharded {
+  std::unique_ptr<ShardedExecutor> s;
 };
 
 namespace {
@@ -360,6 +367,100 @@ hyre_status hyre_execute_batch(hyre_executor* ex, const hyre_query* qs, uint32_t
     if (timings)
       timings->total_ms =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---- sharded executor --------------------------------------------------------
+hyre_status hyre_sharded_index_create(const hyre_frozen* f, const hyre_sharded_index_options* o,
+                                      hyre_sharded_index** out) {
+  return guard([&] {
+    need(f, "frozen");
+    need(o, "options");
+    need(out, "out");
+    *out = new hyre_sharded_index{std::make_unique<ShardedIndex>(*f->f, *o)};
+  });
+}
+
+void hyre_sharded_index_destroy(hyre_sharded_index* ix) { delete ix; }
+
+hyre_status hyre_sharded_index_info(const hyre_sharded_index* ix, uint32_t* n_shards, int32_t* devices) {
+  return guard([&] {
+    need(ix, "sharded index");
+    if (n_shards) *n_shards = ix->ix->G;
+    if (devices)
+      for (uint32_t g = 0; g < ix->ix->G; ++g) devices[g] = ix->ix->ix[g]->device;
+  });
+}
+
+hyre_status hyre_sharded_create(hyre_sharded_index* ix, uint32_t max_batch, hyre_sharded** out) {
+  return guard([&] {
+    need(ix, "sharded index");
+    need(out, "out");
+    *out = new hyre_sharded{std::make_unique<ShardedExecutor>(*ix->ix, max_batch)};
+  });
+}
+
+void hyre_sharded_destroy(hyre_sharded* s) { delete s; }
+
+hyre_status hyre_sharded_execute_batch(hyre_sharded* s, const hyre_query* qs, uint32_t b, hyre_hit* hits,
+                                       const uint64_t* hit_offsets, uint32_t* counts, int32_t* statuses,
+                                       hyre_timings* timings) {
+  return guard([&] {
+    need(s, "sharded executor");
+    const auto t0 = std::chrono::steady_clock::now();
+    s->s->prepare(qs, b);
+    s->s->run();
+    s->s->fetch(hits, hit_offsets, counts, statuses, timings);
+    if (timings)
+      timings->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+const char* hyre_sharded_slot_error(const hyre_sharded* s, uint32_t slot) {
+  if (!s || slot >= s->s->root().slot_errors.size()) return "";
+  return s->s->root().slot_errors[slot].c_str();
+}
+
+hyre_status hyre_sharded_prepare(hyre_sharded* s, const hyre_query* qs, uint32_t b) {
+  return guard([&] {
+    need(s, "sharded executor");
+    s->s->prepare(qs, b);
+  });
+}
+
+hyre_status hyre_sharded_run(hyre_sharded* s) {
+  return guard([&] {
+    need(s, "sharded executor");
+    s->s->run();
+  });
+}
+
+hyre_status hyre_sharded_settle(hyre_sharded* s) {
+  return guard([&] {
+    need(s, "sharded executor");
+    s->s->settle();
+  });
+}
+
+hyre_status hyre_sharded_fetch(hyre_sharded* s, hyre_hit* hits, const uint64_t* hit_offsets, uint32_t* counts,
+                               int32_t* statuses, hyre_timings* timings) {
+  return guard([&] {
+    need(s, "sharded executor");
+    s->s->fetch(hits, hit_offsets, counts, statuses, timings);
+  });
+}
+
+void* hyre_sharded_stream(const hyre_sharded* s) { return s ? s->s->root_stream() : nullptr; }
+
+uint32_t hyre_sharded_kernel_count(const hyre_sharded* s) { return s ? s->s->kernels_per_run() : 0; }
+
+hyre_status hyre_sharded_recovery(const hyre_sharded* s, uint32_t* out2) {
+  return guard([&] {
+    need(s, "sharded executor");
+    need(out2, "out");
+    out2[0] = s->s->recovery_rounds;
+    out2[1] = s->s->exhaustive_queries;
   });
 }
 

@@ -23,6 +23,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <atomic>
+
 #include "host.hpp"
 
 namespace hyreb {
@@ -35,6 +37,18 @@ namespace hyreb {
                                                            : HYRE_CUDA_ERROR,          \
                            std::string(#x) + ": " + cudaGetErrorString(e_));           \
   } while (0)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it once
+// per (kernel, device), safe from several host threads (executor pools,
+// sharded executors); `done` is a bitmask of devices already set.
+inline void set_smem_limit(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  HYRE_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  HYRE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));  // idempotent
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 constexpr uint32_t kChunkWords = 128;               // mask words per K1 CTA
 constexpr uint32_t kChunkRows = kChunkWords * 32;   // 4096 rows

@@ -152,7 +152,7 @@ Executor::Executor(DevIndex* index, uint32_t mb) : ix(index), max_batch(mb) {
   d_samp = dmalloc<uint32_t>(B * samp_cap);
   d_shist = dmalloc<uint32_t>(B * kHistBins);
   d_qhist = dmalloc<uint32_t>(B * (ix->num_bits + 1));
-  d_tsel = dmalloc<uint32_t>(B * 3);
+  d_tsel = dmalloc<uint32_t>(B * 4);
   d_eqcnt = dmalloc<uint32_t>(B * ix->n_chunks);
   h_out_cnt.resize(B);
   h_rerun.resize(B);
@@ -165,7 +165,7 @@ Executor::~Executor() {
   for (void* p : {(void*)d_mask, (void*)d_chunk_cnt, (void*)d_counters, (void*)d_thr, (void*)d_thr_safe, (void*)d_cand,
                   (void*)d_shist,
                   (void*)d_samp, (void*)d_qhist, (void*)d_tsel, (void*)d_eqcnt, (void*)d_blob,
-                  (void*)d_hits, (void*)d_scratch, (void*)d_ex_keys, (void*)d_ex_sorted, (void*)d_ex_rows,
+                  (void*)d_hits, (void*)d_scratch, (void*)d_qhist_sum, (void*)d_ex_keys, (void*)d_ex_sorted, (void*)d_ex_rows,
                   (void*)d_ex_tmp})
     cudaFree(p);
   if (h_blob) cudaFreeHost(h_blob);
@@ -265,7 +265,10 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     }
     QParam p{};
     p.flags = QF_ACTIVE;
-    p.k = std::min(q.k, ix->n_rows);
+    // a shard clamps k to the rows of the whole index (the merged list holds
+    // min(k, all rows)); a shard with fewer rows returns all it has
+    const uint64_t rows_all = shard ? shard->total_rows : ix->n_rows;
+    p.k = static_cast<uint32_t>(std::min<uint64_t>(q.k, rows_all));
     true_k[i] = p.k;
     if (q.embedding && p.k > kSelectMaxK) {  // the threshold pipeline runs with k clamped; exhaustive() replaces it
       big_k.push_back(i);
@@ -953,8 +956,31 @@ void Executor::run() {
     HYRE_CUDA(cudaMemsetAsync(d_qhist, 0, sizeof(uint32_t) * B * (ix->num_bits + 1), st));
     QuantArgs qa{ix->sigs, ix->num_words, ix->num_bits, d_qsig, d_qp, B, W, ix->n_chunks, ix->n_rows,
                  d_mask, d_chunk_cnt, n_elig, d_qhist, d_tsel, d_eqcnt};
-    launch_quant(qa, st);
-    kernels += 5;
+    if (!shard || shard->G == 1) {
+      launch_quant(qa, st);
+      kernels += 5;
+    } else {
+      // global quant_k over every shard (pipeline.cpp:126-130 on the whole
+      // index): sum the histograms, pick the global threshold, keep the ties
+      // of the lowest global rows first
+      const size_t nh = size_t{B} * (ix->num_bits + 1);
+      if (!d_qhist_sum) d_qhist_sum = dmalloc<uint32_t>(size_t{max_batch} * (ix->num_bits + 1));
+      qa.shard_mode = 1;
+      qa.hist_total = d_qhist_sum;
+      launch_quant_hist(qa, st);
+      shard_exchange(0);
+      PeerPtrs hp{}, tp{};
+      for (uint32_t g = 0; g < shard->G; ++g) {
+        hp.p[g] = shard->peers[g]->d_qhist;
+        tp.p[g] = shard->peers[g]->d_tsel;
+      }
+      launch_sum_peers(hp, shard->G, nh, d_qhist_sum, st);
+      launch_quant_select(qa, st);
+      shard_exchange(1);
+      launch_quant_offset(tp, shard->g, B, d_tsel, st);
+      launch_quant_apply(qa, st);
+      kernels += 7;
+    }
   }
   mark(2, any_quant);
   if (any_emb) {
@@ -1094,6 +1120,13 @@ void Executor::fetch(hyre_hit* hits, const uint64_t* offsets, uint32_t* counts, 
   }
 }
 
+void Executor::shard_exchange(int point) {
+  HYRE_CUDA(cudaEventRecord(shard->ev_x[point], st));
+  shard->barrier->arrive_and_wait();  // every shard has recorded this point
+  for (uint32_t g = 0; g < shard->G; ++g)
+    if (g != shard->g) HYRE_CUDA(cudaStreamWaitEvent(st, shard->peers[g]->shard->ev_x[point], 0));
+}
+
 void Executor::settle() {
   if (!prepared) throw Error(HYRE_INTERNAL, "hyre_batch_settle before hyre_batch_prepare");
   if (any_emb) finish_reruns();
@@ -1159,37 +1192,45 @@ void Executor::scan_rows(uint32_t* d_rows, uint64_t n) {
 }
 
 // Exact exhaustive top-K of prepared query i (synchronous; see executor.cuh):
-// eligible rows (K1 mask + K5 on the aux executor) -> [quant preselect:
-// popcount keys, sort, first quant_k (quantizer.cpp:100-138, only when the
-// matches exceed quant_k, pipeline.cpp:126-130)] -> exact rescoring of every
-// row -> sort (score desc, row asc) -> first min(k, n) as the query's hits.
+// its eligible rows -> exact rescoring of every row -> sort (score desc, row
+// asc) -> first min(k, n) as the query's hits.  The rows come from this
+// batch's K1 mask when it has one -- then already narrowed by the quant
+// pre-selection (quantizer.cpp:100-138; global over the shards of a sharded
+// index) -- else (fused CNF or match-all batches, never quant) from the
+// query's clauses on the aux executor (K1 mask + K5).
 void Executor::exhaustive(uint32_t i) {
   HYRE_CUDA(cudaSetDevice(ix->device));
   ++exh_count;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
-  if (!aux) aux = std::make_unique<Executor>(ix, 1);
-  hyre_query t{};
-  t.n_clauses = raw_cl[i + 1] - raw_cl[i];
-  std::vector<uint32_t> offs(t.n_clauses + 1, 0);
-  for (uint32_t c = 0; c < t.n_clauses; ++c) offs[c] = raw_offs[raw_cl[i] + c];
-  offs[t.n_clauses] = raw_cl[i + 1] < raw_offs.size() ? raw_offs[raw_cl[i + 1]] : static_cast<uint32_t>(raw_ids.size());
-  t.slots = raw_slots.data() + raw_cl[i];
-  t.id_offsets = offs.data();
-  t.ids = raw_ids.data();
-  uint64_t n = aux->scan_count(t);
-  ensure_ex(n);
-  aux->scan_rows(d_ex_rows, n);
-  const QParam& p = qp[i];
-  if ((p.flags & QF_QUANT) && n > p.quant_k) {
-    launch_quant_keys(ix->sigs, ix->num_words, ix->num_bits, ix->row_base, d_qsig + size_t{i} * ix->num_words,
-                      d_ex_rows, n, d_ex_keys, st);
-    sort_desc(d_ex_keys, d_ex_sorted, n);
-    n = p.quant_k;
-    launch_quant_to_keys(d_ex_sorted, n, d_ex_keys, st);
+  uint64_t n = 0;
+  if (!use_fused && !all_match) {
+    uint32_t ne = 0;
+    HYRE_CUDA(cudaMemcpyAsync(&ne, d_counters + i, 4, cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    n = ne;
+    ensure_ex(n);
+    if (n) {
+      FirstKArgs fk{d_mask + size_t{i} * ix->words, d_chunk_cnt + size_t{i} * ix->n_chunks, d_counters + i, d_qp + i,
+                    1, ix->words, ix->n_chunks, ix->row_base, d_hit_off, nullptr, nullptr, d_ex_rows, n, 1};
+      launch_first_k(fk, st);
+    }
   } else {
-    launch_rows_to_keys(d_ex_rows, n, d_ex_keys, st);
+    if (!aux) aux = std::make_unique<Executor>(ix, 1);
+    hyre_query t{};
+    t.n_clauses = raw_cl[i + 1] - raw_cl[i];
+    std::vector<uint32_t> offs(t.n_clauses + 1, 0);
+    for (uint32_t c = 0; c < t.n_clauses; ++c) offs[c] = raw_offs[raw_cl[i] + c];
+    offs[t.n_clauses] =
+        raw_cl[i + 1] < raw_offs.size() ? raw_offs[raw_cl[i + 1]] : static_cast<uint32_t>(raw_ids.size());
+    t.slots = raw_slots.data() + raw_cl[i];
+    t.id_offsets = offs.data();
+    t.ids = raw_ids.data();
+    n = aux->scan_count(t);
+    ensure_ex(n);
+    aux->scan_rows(d_ex_rows, n);
   }
+  launch_rows_to_keys(d_ex_rows, n, d_ex_keys, st);
   const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
   PrefSelectArgs pa{SelectArgs{}, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32),
                     ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};

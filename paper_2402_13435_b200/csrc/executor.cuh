@@ -10,9 +10,48 @@
 #include "kernels.cuh"
 #include "tc_score.cuh"
 
+#include <condition_variable>
+#include <mutex>
+
 namespace hyreb {
 
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
+
+// Host barrier of the G shard threads of a ShardedExecutor.
+class HostBarrier {
+ public:
+  explicit HostBarrier(uint32_t n) : n_(n) {}
+  void arrive_and_wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    const uint64_t gen = gen_;
+    if (++count_ == n_) {
+      count_ = 0;
+      ++gen_;
+      cv_.notify_all();
+      return;
+    }
+    cv_.wait(lk, [&] { return gen_ != gen; });
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  uint32_t n_, count_ = 0;
+  uint64_t gen_ = 0;
+};
+
+struct Executor;
+// An executor that is shard g of G row shards (ShardedExecutor, sharded.cu):
+// k is clamped to the global row count, and the quant pre-selection is global
+// -- the shards exchange their popcount histograms and tie counts through
+// peer-memory reads (every shard's run() is driven by its own host thread).
+struct ShardCtx {
+  uint32_t g = 0, G = 1;
+  uint64_t total_rows = 0;
+  std::vector<Executor*> peers;  // [G], peers[g] = this shard
+  HostBarrier* barrier = nullptr;
+  cudaEvent_t ev_x[2] = {};      // this shard's exchange points (quant histogram, tie counts)
+};
 
 struct Executor {
   static constexpr uint32_t kNumCounters = 5;  // n_elig, cand_cnt, samp_cnt, out_cnt, rerun
@@ -29,6 +68,9 @@ struct Executor {
   DevIndex* ix;
   uint32_t max_batch;
   cudaStream_t st = nullptr;
+  ShardCtx* shard = nullptr;       // set by ShardedExecutor
+  uint32_t* d_qhist_sum = nullptr;  // sharded quant: the global histogram
+  void shard_exchange(int point);   // record, host barrier, wait for every peer's point
   // stage events of the last kEvRing runs: start, mask, quant, pre-main,
   // post-main, end (ring slot = run counter % kEvRing); ev = the current slot
   static constexpr uint32_t kEvRing = 64;

@@ -124,11 +124,8 @@ void launch_mask(const MaskArgs& a, cudaStream_t st) {
   constexpr size_t kSmemCap = 200 * 1024;
   const uint32_t staged = (a.n_refs > 0 && staged_bytes + wsum_bytes <= kSmemCap) ? 1u : 0u;
   const size_t smem = wsum_bytes + (staged ? staged_bytes : 0);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_limit(reinterpret_cast<const void*>(mask_kernel), 227 * 1024, attr);
   mask_kernel<<<a.n_chunks, kChunkWords, smem, st>>>(a, staged);
 }
 
@@ -370,12 +367,9 @@ size_t fwd_mask_smem(uint32_t T, uint32_t C, uint32_t nw) {
 
 void launch_fwd_mask(const FwdArgs& a, cudaStream_t st) {
   const size_t smem = fwd_mask_smem(a.T, a.C, a.nw);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fwd_mask_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fwd_mask_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr1{0}, attr2{0};
+  set_smem_limit(reinterpret_cast<const void*>(fwd_mask_kernel<1>), 227 * 1024, attr1);
+  set_smem_limit(reinterpret_cast<const void*>(fwd_mask_kernel<2>), 227 * 1024, attr2);
   if (a.nw == 2) fwd_mask_kernel<2><<<a.n_chunks, 1024, smem, st>>>(a);
   else fwd_mask_kernel<1><<<a.n_chunks, 1024, smem, st>>>(a);
 }
@@ -1133,11 +1127,8 @@ void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st) {
   const dim3 grid((a.dense_n + slice - 1) / slice, a.B);
   sample_slice_kernel<<<grid, kSelThreads, 0, st>>>(a, ucnt);
   const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(sample_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_limit(reinterpret_cast<const void*>(sample_union_kernel), static_cast<int>(smem), attr);
   sample_union_kernel<<<a.B, kSelThreads, smem, st>>>(a, ucnt);
 }
 
@@ -1209,11 +1200,8 @@ void launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
   // sort buffer | histogram + scan scratch | resident candidates (FINAL)
   const size_t smem = kSelectMaxK * sizeof(uint64_t) + (4096 + 40) * sizeof(uint32_t) + kSelResident * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  set_smem_limit(reinterpret_cast<const void*>(select_kernel), static_cast<int>(smem), attr);
   select_kernel<<<a.B, kSelThreads, smem, st>>>(a);
 }
 
@@ -1432,13 +1420,10 @@ void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_
   else if (cpr == 128) k = select_prefilter_kernel<RowT, 32, 4>;
   else if (cpr == 256) k = select_prefilter_kernel<RowT, 32, 8>;
   else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
-  static std::atomic<bool> attr_set[2][6];  // [bf16][row-width variant]: set the smem limit once per kernel
+  static std::atomic<uint64_t> attr_set[2][6];  // [bf16][row-width variant]: device bitmask per kernel
   const int vi = cpr == 8 ? 0 : cpr == 16 ? 1 : cpr == 32 ? 2 : cpr == 64 ? 3 : cpr == 128 ? 4 : 5;
-  std::atomic<bool>& done = attr_set[std::is_same<RowT, float>::value ? 0 : 1][vi];
-  if (!done.load(std::memory_order_acquire)) {
-    HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    done.store(true, std::memory_order_release);
-  }
+  set_smem_limit(reinterpret_cast<const void*>(k), static_cast<int>(smem),
+                 attr_set[std::is_same<RowT, float>::value ? 0 : 1][vi]);
   k<<<a.s.B, kSelPThreads, smem, st>>>(a);
 }
 }  // namespace
@@ -1532,8 +1517,9 @@ __device__ __forceinline__ uint32_t qscore(const uint64_t* sig, const uint64_t* 
 }
 __device__ __forceinline__ bool quant_needed(const QuantArgs& a, uint32_t q) {
   const uint32_t f = a.qp[q].flags;
+  // sharded: every shard histograms its rows; the global count decides (thresh)
   return (f & (QF_ACTIVE | QF_EMB | QF_QUANT)) == (QF_ACTIVE | QF_EMB | QF_QUANT) &&
-         a.n_elig[q] > a.qp[q].quant_k;
+         (a.shard_mode || a.n_elig[q] > a.qp[q].quant_k);
 }
 }  // namespace
 
@@ -1560,11 +1546,17 @@ __global__ void __launch_bounds__(128) quant_hist_kernel(QuantArgs a) {
 __global__ void quant_thresh_kernel(QuantArgs a) {
   const uint32_t q = blockIdx.x;
   if (threadIdx.x != 0) return;
-  uint32_t* ts = a.tsel + q * 3;
+  uint32_t* ts = a.tsel + q * 4;
   ts[2] = 0;
+  ts[3] = 0;
   if (!quant_needed(a, q)) return;
   const uint32_t qk = a.qp[q].quant_k;
-  const uint32_t* h = a.hist + static_cast<size_t>(q) * (a.num_bits + 1);
+  const uint32_t* h = (a.hist_total ? a.hist_total : a.hist) + static_cast<size_t>(q) * (a.num_bits + 1);
+  if (a.shard_mode) {  // global eligible count = sum of the global histogram
+    uint64_t total = 0;
+    for (uint32_t s = 0; s <= a.num_bits; ++s) total += h[s];
+    if (total <= qk) return;
+  }
   uint32_t above = 0;
   for (int s = static_cast<int>(a.num_bits); s >= 0; --s) {
     if (above + h[s] >= qk) {
@@ -1575,12 +1567,12 @@ __global__ void quant_thresh_kernel(QuantArgs a) {
     }
     above += h[s];
   }
-  a.n_elig[q] = qk;
+  a.n_elig[q] = a.shard_mode ? 0u : qk;  // sharded: quant_apply counts the local survivors
 }
 
 __global__ void __launch_bounds__(128) quant_eq_kernel(QuantArgs a) {
   const uint32_t q = blockIdx.y, chunk = blockIdx.x;
-  const uint32_t* ts = a.tsel + q * 3;
+  const uint32_t* ts = a.tsel + q * 4;
   if (!ts[2]) return;
   const uint32_t widx = chunk * kChunkWords + threadIdx.x;
   uint32_t w = a.mask[static_cast<size_t>(q) * a.words + widx];
@@ -1602,7 +1594,7 @@ __global__ void __launch_bounds__(128) quant_eq_kernel(QuantArgs a) {
 __global__ void __launch_bounds__(1024) quant_scan_kernel(QuantArgs a) {
   __shared__ uint32_t tmp[40];
   const uint32_t q = blockIdx.x;
-  if (!a.tsel[q * 3 + 2]) return;
+  if (!a.tsel[q * 4 + 2]) return;
   uint32_t* e = a.eq_cnt + static_cast<size_t>(q) * a.n_chunks;
   uint32_t carry = 0;
   for (uint32_t base = 0; base < a.n_chunks; base += blockDim.x) {
@@ -1613,13 +1605,14 @@ __global__ void __launch_bounds__(1024) quant_scan_kernel(QuantArgs a) {
     if (i < a.n_chunks) e[i] = carry + ex;
     carry += tot;
   }
+  if (threadIdx.x == 0) a.tsel[q * 4 + 3] = carry;  // this shard's ==t rows
 }
 
 __global__ void __launch_bounds__(128) quant_apply_kernel(QuantArgs a) {
   __shared__ uint32_t tmp[40];
   __shared__ uint32_t ws[4];
   const uint32_t q = blockIdx.y, chunk = blockIdx.x;
-  const uint32_t* ts = a.tsel + q * 3;
+  const uint32_t* ts = a.tsel + q * 4;
   if (!ts[2]) return;
   const uint32_t t = ts[0], keep_eq = ts[1];
   const uint32_t widx = chunk * kChunkWords + threadIdx.x;
@@ -1650,18 +1643,62 @@ __global__ void __launch_bounds__(128) quant_apply_kernel(QuantArgs a) {
   const uint32_t c = __reduce_add_sync(kFull, __popc(keep));
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
   __syncthreads();
-  if (threadIdx.x == 0)
-    a.chunk_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] = ws[0] + ws[1] + ws[2] + ws[3];
+  if (threadIdx.x == 0) {
+    const uint32_t tot4 = ws[0] + ws[1] + ws[2] + ws[3];
+    a.chunk_cnt[static_cast<size_t>(q) * a.n_chunks + chunk] = tot4;
+    if (a.shard_mode && tot4) atomicAdd(a.n_elig + q, tot4);
+  }
 }
 
-void launch_quant(const QuantArgs& a, cudaStream_t st) {
+void launch_quant_hist(const QuantArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
   dim3 grid(a.n_chunks, a.B);
   quant_hist_kernel<<<grid, kChunkWords, (a.num_bits + 1) * sizeof(uint32_t), st>>>(a);
+}
+void launch_quant_select(const QuantArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  dim3 grid(a.n_chunks, a.B);
   quant_thresh_kernel<<<a.B, 32, 0, st>>>(a);
   quant_eq_kernel<<<grid, kChunkWords, 0, st>>>(a);
   quant_scan_kernel<<<a.B, 1024, 0, st>>>(a);
+}
+void launch_quant_apply(const QuantArgs& a, cudaStream_t st) {
+  if (a.B == 0) return;
+  dim3 grid(a.n_chunks, a.B);
   quant_apply_kernel<<<grid, kChunkWords, 0, st>>>(a);
+}
+void launch_quant(const QuantArgs& a, cudaStream_t st) {
+  launch_quant_hist(a, st);
+  launch_quant_select(a, st);
+  launch_quant_apply(a, st);
+}
+
+// ---- peer-memory exchanges of a sharded batch (ShardCtx) ----
+namespace {
+__global__ void sum_peers_kernel(PeerPtrs src, uint32_t G, size_t n, uint32_t* dst) {
+  for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) {
+    uint32_t s = 0;
+    for (uint32_t g = 0; g < G; ++g) s += src.p[g][i];
+    dst[i] = s;
+  }
+}
+__global__ void quant_offset_kernel(PeerPtrs tsel, uint32_t g, uint32_t B, uint32_t* my) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= B || !my[q * 4 + 2]) return;
+  uint32_t below = 0;  // ==t rows of the lower shards (lower global rows keep ties first)
+  for (uint32_t h = 0; h < g; ++h) below += tsel.p[h][q * 4 + 3];
+  const uint32_t budget = my[q * 4 + 1];
+  my[q * 4 + 1] = budget > below ? budget - below : 0u;
+}
+}  // namespace
+
+void launch_sum_peers(const PeerPtrs& src, uint32_t G, size_t n, uint32_t* dst, cudaStream_t st) {
+  if (!n) return;
+  sum_peers_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 1024)), 256, 0, st>>>(src, G, n, dst);
+}
+void launch_quant_offset(const PeerPtrs& tsel, uint32_t g, uint32_t B, uint32_t* my_tsel, cudaStream_t st) {
+  if (!B) return;
+  quant_offset_kernel<<<(B + 127) / 128, 128, 0, st>>>(tsel, g, B, my_tsel);
 }
 
 // ===========================================================================
@@ -1749,6 +1786,70 @@ void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uin
                         cudaStream_t st) {
   if (B == 0) return;
   gather_keys_kernel<<<B, 256, 0, st>>>(g_hits, g_off, g_cnt, G, hits_stride, B, cap, keys, cnt);
+}
+
+// Sharded merge, one CTA per query, reading every shard's results in place
+// through peer memory (NVLink loads on a multi-GPU node): the gather and the
+// merge's key build in one pass, no staging copy.
+namespace {
+__global__ void gather_peer_keys_kernel(PeerHits ph, uint32_t G, const uint64_t* hit_off, const QParam* qp,
+                                        uint32_t cap, uint64_t* keys, uint32_t* cnt) {
+  const uint32_t q = blockIdx.x;
+  if ((qp[q].flags & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) return;
+  const uint64_t off = hit_off[q];
+  uint32_t base = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t c = ph.cnt[g][q];
+    const hyre_hit* h = ph.hits[g] + off;
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x)
+      if (base + i < cap) keys[static_cast<size_t>(q) * cap + base + i] = make_key(h[i].score + 0.0f, h[i].row);
+    base += c;
+  }
+  if (threadIdx.x == 0) cnt[q] = min(base, cap);
+}
+// term-only (pipeline.cpp:30-40): shard row lists are ascending and the
+// shards are contiguous row ranges, so the global first K is their
+// concatenation in shard order
+__global__ void concat_term_only_kernel(PeerHits ph, uint32_t G, const uint64_t* hit_off, const QParam* qp,
+                                        const uint32_t* true_k, hyre_hit* out, uint32_t* out_cnt) {
+  const uint32_t q = blockIdx.x;
+  if ((qp[q].flags & (QF_ACTIVE | QF_EMB)) != QF_ACTIVE) return;
+  const uint64_t off = hit_off[q];
+  const uint32_t k = true_k[q];
+  uint32_t base = 0;
+  for (uint32_t g = 0; g < G && base < k; ++g) {
+    const uint32_t c = min(ph.cnt[g][q], k - base);
+    const hyre_hit* h = ph.hits[g] + off;
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) out[off + base + i] = h[i];
+    base += c;
+  }
+  if (threadIdx.x == 0) out_cnt[q] = base;
+}
+__global__ void gather_peer_keys_one_kernel(PeerHits ph, uint32_t G, uint64_t off, uint32_t q, uint64_t cap,
+                                            uint64_t* keys, uint32_t* cnt) {
+  uint64_t base = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t c = ph.cnt[g][q];
+    const hyre_hit* h = ph.hits[g] + off;
+    for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < c; i += uint64_t{gridDim.x} * blockDim.x)
+      if (base + i < cap) keys[base + i] = make_key(h[i].score + 0.0f, h[i].row);
+    base += c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = static_cast<uint32_t>(min(base, cap));
+}
+}  // namespace
+
+void launch_gather_peer_keys(const PeerHits& ph, uint32_t G, const uint64_t* hit_off, const QParam* qp, uint32_t B,
+                             uint32_t cap, uint64_t* keys, uint32_t* cnt, cudaStream_t st) {
+  if (B) gather_peer_keys_kernel<<<B, 256, 0, st>>>(ph, G, hit_off, qp, cap, keys, cnt);
+}
+void launch_concat_term_only(const PeerHits& ph, uint32_t G, const uint64_t* hit_off, const QParam* qp,
+                             const uint32_t* true_k, uint32_t B, hyre_hit* out, uint32_t* out_cnt, cudaStream_t st) {
+  if (B) concat_term_only_kernel<<<B, 256, 0, st>>>(ph, G, hit_off, qp, true_k, out, out_cnt);
+}
+void launch_gather_peer_keys_one(const PeerHits& ph, uint32_t G, uint64_t off, uint32_t q, uint64_t cap,
+                                 uint64_t* keys, uint32_t* cnt, cudaStream_t st) {
+  gather_peer_keys_one_kernel<<<148, 256, 0, st>>>(ph, G, off, q, cap, keys, cnt);
 }
 
 

@@ -199,10 +199,43 @@ struct QuantArgs {
   uint32_t* chunk_cnt;
   uint32_t* n_elig;
   uint32_t* hist;       // [B][num_bits + 1]
-  uint32_t* tsel;       // [B][2]: threshold score t, number of ==t rows to keep
+  uint32_t* tsel;       // [B][4]: threshold score t, ==t rows to keep, active, local ==t rows
   uint32_t* eq_cnt;     // [B][n_chunks] ==t rows per chunk
+  // Row shard of a sharded index (global quant, ShardCtx): hist counts every
+  // QF_QUANT query's rows; the threshold comes from hist_total (the sum of
+  // every shard's histogram), the ==t rows to keep from the global budget
+  // minus the ties of lower shards (quant_offset); n_elig = local survivors.
+  uint32_t shard_mode;
+  const uint32_t* hist_total;  // [B][num_bits + 1] (nullptr: hist)
 };
 void launch_quant(const QuantArgs& a, cudaStream_t st);
+// The same in three phases for a sharded index: hist | thresh + eq + scan | apply.
+void launch_quant_hist(const QuantArgs& a, cudaStream_t st);
+void launch_quant_select(const QuantArgs& a, cudaStream_t st);
+void launch_quant_apply(const QuantArgs& a, cudaStream_t st);
+// Peer-memory exchanges of a sharded batch (pointers of every shard's buffer,
+// readable from this device: same device or peer access enabled).
+constexpr uint32_t kMaxShards = 16;
+struct PeerPtrs {
+  const uint32_t* p[kMaxShards];
+};
+// dst[i] = sum over shards of src_g[i]
+void launch_sum_peers(const PeerPtrs& src, uint32_t G, size_t n, uint32_t* dst, cudaStream_t st);
+// shard g: tsel[q][1] = max(0, global ==t budget - sum of the ==t rows of shards < g)
+void launch_quant_offset(const PeerPtrs& tsel, uint32_t g, uint32_t B, uint32_t* my_tsel, cudaStream_t st);
+// Sharded merge: per query, keys of every shard's hits (emb queries) and the
+// concatenated row lists of term-only queries (k unlimited).
+struct PeerHits {
+  const hyre_hit* hits[kMaxShards];
+  const uint32_t* cnt[kMaxShards];
+};
+void launch_gather_peer_keys(const PeerHits& ph, uint32_t G, const uint64_t* hit_off, const QParam* qp, uint32_t B,
+                             uint32_t cap, uint64_t* keys, uint32_t* cnt, cudaStream_t st);
+void launch_concat_term_only(const PeerHits& ph, uint32_t G, const uint64_t* hit_off, const QParam* qp,
+                             const uint32_t* true_k, uint32_t B, hyre_hit* out, uint32_t* out_cnt, cudaStream_t st);
+// one query's keys from every shard into keys (count -> *cnt)
+void launch_gather_peer_keys_one(const PeerHits& ph, uint32_t G, uint64_t off, uint32_t q, uint64_t cap,
+                                 uint64_t* keys, uint32_t* cnt, cudaStream_t st);
 
 // ---- stage helpers ----
 void launch_gather_scores(const void* emb, bool bf16, uint32_t dp, uint32_t row_base,

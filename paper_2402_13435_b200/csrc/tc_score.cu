@@ -847,14 +847,16 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
   static const KFn fused[6][4] = {HYRE_TC_ROW(8, 1),  HYRE_TC_ROW(16, 1), HYRE_TC_ROW(24, 1),
                                   HYRE_TC_ROW(32, 1), HYRE_TC_ROW(16, 2), HYRE_TC_ROW(32, 2)};
 #undef HYRE_TC_ROW
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // devices whose limits are set (every variant at once)
+  int dev = 0;
+  HYRE_CUDA(cudaGetDevice(&dev));
+  if (!(attr.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
     HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    227 * 1024 - 64));
     for (auto& row : fused)
       for (KFn k : row)
         HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kTcStaticSmem));
-    attr = true;
+    attr.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
   }
   KFn k = tc_score_kernel<0, 1, 1>;
   if (a.fused) {

@@ -622,6 +622,102 @@ class Executor:
         return [by_row[int(r)] for r in out[: cnt.value]]
 
 
+class ShardedIndex:
+    """A FrozenIndex row-sharded over devices (hyre_sharded_index_*,
+    SURVEY §8(e)): shard g = rows [g N / G, (g + 1) N / G) on devices[g]
+    (default g % device count; shards may share a device)."""
+
+    def __init__(self, frozen: FrozenIndex, n_shards: int, devices: Optional[Sequence[int]] = None,
+                 dtype: str = "f32", tensor_path: bool = True):
+        self.frozen = frozen
+        devs = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        o = L.hyre_sharded_index_options(n_shards, None if devs is None else _p(devs, L.i32p),
+                                         L.HYRE_EMB_BF16 if dtype == "bf16" else L.HYRE_EMB_F32, int(tensor_path))
+        h = C.c_void_p()
+        _check(L.lib().hyre_sharded_index_create(frozen._h, C.byref(o), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.lib().hyre_sharded_index_destroy(self._h)
+            self._h = None
+
+    def info(self):
+        """-> (n_shards, [device of each shard])."""
+        n = C.c_uint32()
+        devs = np.zeros(16, np.int32)
+        _check(L.lib().hyre_sharded_index_info(self._h, C.byref(n), _p(devs, L.i32p)))
+        return int(n.value), devs[: n.value].tolist()
+
+
+class ShardedExecutor:
+    """Executor over a ShardedIndex (hyre_sharded_* in include/hyre_b200.h):
+    one Executor + stream per shard, per-shard top-K merged exactly on shard
+    0's device through peer memory, global quant pre-selection.  Same
+    execute / execute_batch contract and results as Executor.  `index` is a
+    ShardedIndex, or a FrozenIndex sharded here into `n_shards`."""
+
+    def __init__(self, index, n_shards: int = 1, devices: Optional[Sequence[int]] = None, dtype: str = "f32",
+                 tensor_path: bool = True, max_batch: int = 16):
+        if max_batch < 1:
+            raise ValidationError("maxBatch must be >= 1")
+        self._sx = index if isinstance(index, ShardedIndex) else ShardedIndex(index, n_shards, devices, dtype,
+                                                                              tensor_path)
+        self._index = self._sx.frozen
+        h = C.c_void_p()
+        _check(L.lib().hyre_sharded_create(self._sx._h, max_batch, C.byref(h)))
+        self._h = h
+        self._max_batch = max_batch
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.lib().hyre_sharded_destroy(self._h)
+            self._h = None
+
+    def index(self) -> FrozenIndex:
+        return self._index
+
+    def max_batch(self) -> int:
+        return self._max_batch
+
+    def info(self):
+        return self._sx.info()
+
+    def execute(self, query: HybridQuery, timings: Optional[StageTimings] = None) -> TopKResult:
+        out = self.execute_batch(BatchRequest([query]), timings)[0]
+        if not out.ok:
+            raise ValidationError(out.error)
+        return out.result
+
+    def execute_batch(self, batch: BatchRequest, timings: Optional[StageTimings] = None) -> List[QueryOutcome]:
+        qs = batch.queries
+        b = len(qs)
+        pack = QueryPack(qs)
+        caps = [max(0, min(max(q.k, 0), self._index.num_docs())) for q in qs]
+        offs = np.zeros(max(b, 1), np.uint64)
+        if b:
+            offs[:b] = np.concatenate([[0], np.cumsum(caps)[:-1]])
+        hits = (hyre_hit * max(1, sum(caps)))()
+        counts = np.zeros(max(b, 1), np.uint32)
+        st = np.zeros(max(b, 1), np.int32)
+        t = L.hyre_timings()
+        _check(L.lib().hyre_sharded_execute_batch(self._h, pack.arr, b, hits, _p(offs, L.u64p), _p(counts, L.u32p),
+                                                  _p(st, L.i32p), C.byref(t)))
+        if timings is not None:
+            timings.__dict__.update(_timings(t).__dict__)
+        out = []
+        for i in range(b):
+            if st[i] != L.HYRE_OK:
+                out.append(QueryOutcome(False, TopKResult(), L.lib().hyre_sharded_slot_error(self._h, i).decode()))
+            else:
+                base = int(offs[i])
+                n = int(counts[i])
+                out.append(QueryOutcome(True, TopKResult([ScoredDoc(self._index.doc_id(h.row), int(h.row),
+                                                                    float(np.float32(h.score)))
+                                                          for h in hits[base:base + n]]), ""))
+        return out
+
+
 class ExecutorPool:
     """The B200 ExecutorPool (service.cpp:99-141, ServiceConfig workers /
     max_batch, service.hpp:19-26) with dynamic request batching: `workers`

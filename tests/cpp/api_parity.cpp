@@ -126,5 +126,26 @@ int main(int argc, char** argv) {
   StageTimings t;
   (void)ex.execute(hybrid, &t);
   CHECK("stage timings populated", t.total_ms > 0.0 && t.total_ms >= t.tbr_ms);
+
+  // ---- the same index row-sharded (DeviceOptions: 3 shards, here all on
+  // device 0; HYRE_GPUS=N picks devices 0..N-1): identical results ----
+  FrozenIndex shard3 = addressable(10);
+  DeviceOptions three;
+  three.devices = {0, 0, 0};
+  shard3.set_device_options(three);
+  Executor sex(shard3, 4);
+  const auto souts = sex.execute_batch(batch);
+  bool same = souts.size() == outs.size();
+  for (std::size_t i = 0; same && i < outs.size(); ++i) {
+    same = souts[i].ok == outs[i].ok && souts[i].error == outs[i].error &&
+           souts[i].result.hits.size() == outs[i].result.hits.size();
+    for (std::size_t j = 0; same && j < outs[i].result.hits.size(); ++j)
+      same = souts[i].result.hits[j].row_id == outs[i].result.hits[j].row_id &&
+             souts[i].result.hits[j].score == outs[i].result.hits[j].score &&
+             souts[i].result.hits[j].doc_id == outs[i].result.hits[j].doc_id;
+  }
+  CHECK("sharded executor == single-GPU executor (SURVEY 8e)", same && sex.sharded_handle() != nullptr);
+  CHECK("device options fixed after the first executor",
+        throws_with<ValidationError>([&] { shard3.set_device_options(DeviceOptions{}); }, ""));
   return failures;
 }

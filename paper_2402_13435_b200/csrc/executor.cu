@@ -193,6 +193,9 @@ void Executor::ensure_hits(size_t n) {
   if (h_hits) cudaFreeHost(h_hits);
   hits_cap = std::max(n, hits_cap * 2);
   d_hits = dmalloc<hyre_hit>(hits_cap);
+  // fetch copies every query's whole k-slot range; slots past a query's hit
+  // count are never read, but keep them initialised (compute-sanitizer initcheck)
+  HYRE_CUDA(cudaMemsetAsync(d_hits, 0, hits_cap * sizeof(hyre_hit), st));
   HYRE_CUDA(cudaMallocHost(&h_hits, hits_cap * sizeof(hyre_hit)));
 }
 
@@ -607,7 +610,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
       work = (n_seg + sample_period - 1) / sample_period * 8;
     }
-    const uint32_t grid = std::max(1u, std::min(work, 148u));
+    const uint32_t grid = std::max(1u, std::min(work, 148u * tc_ctas_per_sm(use_fused, tc_np)));
     for (uint32_t g = 0; g < tc_groups; ++g) {
       TcArgs ta{pf_i8 ? ix->tc_i8 : ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 n_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,
@@ -683,7 +686,7 @@ void Executor::plan_tc() {
   auto plan = [&](uint32_t aps, uint32_t slots) {
     const size_t stage_bytes = size_t{tc_load_ops()} * aps * 128 * 128;
     const size_t fixed = tc_smem_bytes(tc_np, kb, tc_load_ops(), 0, use_fused ? tc_fz_bytes(slots) : 0, tc_q_planes(), aps);
-    const size_t cap_b = 227 * 1024 - (use_fused ? kTcStaticSmem : 64);
+    const size_t cap_b = tc_smem_cap(use_fused, tc_np);
     const size_t budget = cap_b > fixed ? cap_b - fixed : 0;
     return static_cast<uint32_t>(std::min<size_t>(12, budget / stage_bytes));
   };

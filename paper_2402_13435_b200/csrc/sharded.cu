@@ -184,6 +184,7 @@ void ShardedExecutor::prepare(const hyre_query* qs, uint32_t b) {
     if (h_hits) cudaFreeHost(h_hits);
     hits_cap = std::max(n, hits_cap * 2);
     HYRE_CUDA(cudaMalloc(&d_hits, hits_cap * sizeof(hyre_hit)));
+    HYRE_CUDA(cudaMemsetAsync(d_hits, 0, hits_cap * sizeof(hyre_hit), r.st));  // initcheck: see Executor::ensure_hits
     HYRE_CUDA(cudaMallocHost(&h_hits, hits_cap * sizeof(hyre_hit)));
   }
   HYRE_CUDA(cudaMemcpyAsync(d_true_k, r.true_k.data(), b * sizeof(uint32_t), cudaMemcpyHostToDevice, r.st));

@@ -36,11 +36,11 @@ namespace {
 
 constexpr uint32_t kTileRows = 128;
 constexpr uint32_t kAtomBytes = kTileRows * 128;  // one 128-row x 128-B swizzle-128 box (16 KB)
-// per-CTA candidate staging: 32 KB for groups of <= 64 queries (64 keys per
+// per-CTA candidate staging: 16 KB for groups of <= 64 queries (32 keys per
 // query), 8 KB for 128-query groups (8 keys per query; overflow goes straight
 // to the global buffer) so that their larger query tile still leaves >= 4 ring
 // stages in flight
-__host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 32768u : 8192u; }
+__host__ __device__ constexpr uint32_t stage_bytes_for(uint32_t Np) { return Np <= 64 ? 16384u : 8192u; }
 // epilogue warps: 8 (2 per TMEM lane quadrant) next to the fused CNF warps;
 // 16 for the mask / match-all variant, whose only per-tile work is the
 // epilogue (large query groups need the extra warps to hide TMEM-load and
@@ -297,8 +297,11 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
 // 32-query chunks, evaluated by cnf_warps(NCH) dedicated warps one tile ahead of
 // the epilogue; J == 0: eligibility from the K1 mask.  One instantiation per
 // variant keeps each kernel's code (and instruction-cache footprint) small.
+// Fused groups of <= 64 queries run two CTAs per SM (tc_ctas_per_sm): twice
+// the CNF / epilogue warps to hide their latency chains, each CTA with half
+// the shared-memory ring and 256 TMEM columns (67 registers, no spills).
 template <int J, int TB, int NCH>
-__global__ void __launch_bounds__(threads_for(J > 0, NCH), 1)
+__global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ? 2 : 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   constexpr bool kFused = J > 0;
   constexpr uint32_t kEW = epi_warps(kFused);
@@ -830,6 +833,23 @@ size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, 
 }
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : (Np <= 128 ? 4u : 8u)); }
+
+uint32_t tc_ctas_per_sm(bool fused, uint32_t Np) {
+  static const int forced = [] {
+    const char* e = std::getenv("HYRE_TC_CTAS");  // profiling: 1 forces one CTA per SM
+    return e ? std::atoi(e) : 0;
+  }();
+  const uint32_t two = (fused && tc_fused_chunks(Np) <= 2 && tc_tmem_cols(Np) <= 256) ? 2u : 1u;
+  return forced == 1 ? 1u : two;
+}
+
+size_t tc_smem_cap(bool fused, uint32_t Np) {
+  // per SM: 228 KB shared memory, 1 KB reserved per resident CTA; the fused
+  // variants' static table is 256 entries x chunks x 4 B
+  const size_t stat = fused ? 256 * 4 * size_t{tc_fused_chunks(Np)} + 64 : 64;
+  if (tc_ctas_per_sm(fused, Np) == 2) return (228 * 1024 - 2 * 1024) / 2 - stat;
+  return 227 * 1024 - (fused ? kTcStaticSmem : 64);
+}
 
 size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);

@@ -85,6 +85,10 @@ uint32_t tc_acc_bufs(uint32_t Np);
 uint32_t tc_tmem_cols(uint32_t Np);
 // query chunks of a fused group as laid out in its program (1, 2, 4 or 8)
 uint32_t tc_fused_chunks(uint32_t Np);
+// CTAs per SM of the K3 variant (2 for fused groups of <= 64 queries) and the
+// dynamic shared memory one CTA may use
+uint32_t tc_ctas_per_sm(bool fused, uint32_t Np);
+size_t tc_smem_cap(bool fused, uint32_t Np);
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st);
 

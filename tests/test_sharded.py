@@ -111,6 +111,6 @@ def test_sharded_validation_errors_fail_their_slot(hy):
     bad = hy.HybridQuery(hy.CnfQuery(), np.ones(7, np.float32), 5, hy.ExecOptions(False))
     out = sh.execute_batch(hy.BatchRequest([good, bad]))
     assert out[0].ok and not out[1].ok
-    assert out[1].error == "query embedding dim 7 != index dim 16"
+    assert out[1].error == "embedding: expected dim 16, got 7"
     with pytest.raises(hy.ValidationError):
         hy.ShardedExecutor(prod, 17, max_batch=4)

@@ -1,2 +1,5 @@
-bash profiles/k3_sweep.sh "merged" "merged_noCNF HYRE_TC_DEBUG=4" "merged_mmaonly HYRE_TC_DEBUG=6" 2>&1
-timeout 900 python -m pytest tests/test_gpu_baseline.py tests/test_gpu_parity.py -m gpu -q -x -k "c3_shape or tensor_core or fused or variants or quant or prefilter" > gpurun_out/t4.log 2>&1; tail -3 gpurun_out/t4.log
+set -u
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
+timeout 1800 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/gputest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"; grep '^{' gpurun_out/bench_default.log | tail -1 | cut -c1-1500

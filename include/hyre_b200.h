@@ -166,6 +166,13 @@ typedef struct hyre_hit {
   float score;   /* clamp(dot(unit(q), row), -1, 1); 0 for term-only */
 } hyre_hit;
 
+/* Messenger (types.hpp:12-17): one stage record of the batch scan. */
+typedef struct hyre_messenger {
+  uint32_t row_id;   /* global rowId */
+  uint32_t batch_id; /* the batchId stamped on the query's matches */
+  float score;       /* 0 (term match only) */
+} hyre_messenger;
+
 /* StageTimings (pipeline.hpp:40-46); device stages are timed with CUDA events. */
 typedef struct hyre_timings {
   double tbr_ms, quant_ms, ebr_ms, topk_ms, total_ms;
@@ -378,6 +385,13 @@ hyre_status hyre_batch_merge_gathered(hyre_executor* ex, const void* g_hits, con
 /* full_scan_tbr (term_match.hpp:43-45): ascending eligible rows (global ids). */
 hyre_status hyre_full_scan_tbr(hyre_executor* ex, const hyre_query* q, uint32_t* rows,
                                uint64_t cap, uint64_t* n);
+/* batch_scan_tbr (pipeline.hpp:59-64, pipeline.cpp:75-93): one pass over the
+ * rows for b <= max_batch queries (clauses only; embeddings ignored), emitting
+ * a messenger per (row, query) match ordered by (rowId, query position) and
+ * stamped with batch_ids[i].  Writes min(n, cap) messengers, *n = total. */
+hyre_status hyre_batch_scan_tbr(hyre_executor* ex, const hyre_query* qs, uint32_t b,
+                                const uint32_t* batch_ids, hyre_messenger* out, uint64_t cap,
+                                uint64_t* n);
 /* exact_scores (knn.hpp:24-26) over explicit global rows. */
 hyre_status hyre_exact_scores(hyre_executor* ex, const float* q, uint32_t dim,
                               const uint32_t* rows, uint64_t n, float* scores,

@@ -527,6 +527,29 @@ inline std::vector<Messenger> full_scan_tbr(const FrozenIndex& index, const CnfQ
   return out;
 }
 
+// pipeline.hpp:59-64: the matches of every query in one pass, ordered by
+// (rowId, query position), stamped with batch_ids[i].
+inline std::vector<Messenger> batch_scan_tbr(const FrozenIndex& index, std::span<const CnfQuery> queries,
+                                             std::span<const std::uint32_t> batch_ids) {
+  if (batch_ids.size() != queries.size()) throw ValidationError("batch_ids must have one id per query");
+  if (queries.empty()) return {};
+  hyre_executor* e = nullptr;
+  detail::check(hyre_executor_create(index.device(), static_cast<std::uint32_t>(queries.size()), &e));
+  std::unique_ptr<hyre_executor, detail::StageExec::Del> ex(e);
+  std::vector<HybridQuery> hq;
+  for (const auto& q : queries) hq.push_back(HybridQuery{q, std::nullopt, 1, {}});
+  detail::QueryPack p(hq);
+  const auto b = static_cast<std::uint32_t>(queries.size());
+  std::uint64_t n = 0;
+  detail::check(hyre_batch_scan_tbr(ex.get(), p.q.data(), b, batch_ids.data(), nullptr, 0, &n));
+  std::vector<hyre_messenger> raw(n);
+  detail::check(hyre_batch_scan_tbr(ex.get(), p.q.data(), b, batch_ids.data(), raw.data(), n, &n));
+  std::vector<Messenger> out;
+  out.reserve(n);
+  for (const auto& m : raw) out.push_back({m.row_id, m.batch_id, 0.0f});
+  return out;
+}
+
 inline ScoredMessengers exact_scores(const FrozenIndex& index, std::span<const float> query_embedding,
                                      std::vector<Messenger> candidates) {
   detail::StageExec ex(index);

@@ -304,6 +304,18 @@ def full_scan_tbr(index: Frozen, clauses: Sequence[tuple]) -> np.ndarray:
     return np.nonzero(ok)[0].astype(np.int64)
 
 
+def batch_scan_tbr(index: Frozen, queries: Sequence, batch_ids: Sequence[int]) -> list:
+    """pipeline.cpp:75-93: one pass over the rows; for each row, every query
+    (in batch position order) whose clauses all match emits (row, batch_id)."""
+    rows = [set(full_scan_tbr(index, q).tolist()) for q in queries]
+    out = []
+    for r in sorted(set().union(*rows)) if rows else []:
+        for qi, s in enumerate(rows):
+            if r in s:
+                out.append((r, int(batch_ids[qi])))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Scoring and selection (knn.cpp, pipeline.cpp)
 # ---------------------------------------------------------------------------

@@ -160,6 +160,18 @@ class RefIndex:
                                        C.byref(n)))
         return out[: n.value].astype(np.int64)
 
+    def batch_scan_tbr(self, queries, batch_ids) -> list:
+        """pipeline.cpp:75-93 -> [(row, batch_id)] in (row, query position) order."""
+        qp = QueryPack([(c, None, 1, False, 0, 100) for c in queries])
+        bid = np.ascontiguousarray(batch_ids, np.uint32)
+        n = C.c_uint64()
+        _check(lib().ref_batch_scan_tbr(self.h, qp.arr, C.c_uint32(len(queries)), _p(bid, u32p), None,
+                                        C.c_uint64(0), C.byref(n)))
+        out = np.zeros(2 * max(1, n.value), np.uint32)
+        _check(lib().ref_batch_scan_tbr(self.h, qp.arr, C.c_uint32(len(queries)), _p(bid, u32p), _p(out, u32p),
+                                        C.c_uint64(n.value), C.byref(n)))
+        return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+
     def validate(self, clauses, emb, k, granularity=100) -> None:
         qp = QueryPack([(clauses, emb, k, False, 0, granularity)])
         _check(lib().ref_validate_query(self.h, C.byref(qp.arr[0])))

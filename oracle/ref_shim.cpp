@@ -228,6 +228,23 @@ int ref_full_scan_tbr(void* h, const RefQuery* rq, uint32_t* rows, uint64_t cap,
   });
 }
 
+// batch_scan_tbr (pipeline.cpp:75-93) -> (row, batch) pairs interleaved in
+// out[2i], out[2i+1]; total in *n (pairs written up to cap).
+int ref_batch_scan_tbr(void* h, const RefQuery* qs, uint32_t b, const uint32_t* batch_ids, uint32_t* out,
+                       uint64_t cap, uint64_t* n) {
+  return guarded([&] {
+    std::vector<hyre::CnfQuery> terms;
+    for (uint32_t i = 0; i < b; ++i) terms.push_back(to_hybrid(qs[i]).terms);
+    auto ms = hyre::batch_scan_tbr(*static_cast<hyre::FrozenIndex*>(h), terms,
+                                   std::span<const std::uint32_t>(batch_ids, b));
+    *n = ms.size();
+    for (uint64_t i = 0; i < ms.size() && i < cap; ++i) {
+      out[2 * i] = ms[i].row_id;
+      out[2 * i + 1] = ms[i].batch_id;
+    }
+  });
+}
+
 int ref_validate_query(void* h, const RefQuery* rq) {
   return guarded([&] {
     hyre::validate_query(*static_cast<hyre::FrozenIndex*>(h), to_hybrid(*rq));

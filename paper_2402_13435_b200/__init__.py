@@ -16,7 +16,7 @@ _EXPORTS = (
     "ExecutorPool", "FrozenIndex", "HybridQuery", "IndexBuilder", "IndexConfig", "LoadError", "Messenger",
     "QuantCodec", "QueryOutcome", "QueryPack", "ScoreDomainError", "ScoredDoc", "ScoredMessengers", "ShardedExecutor", "ShardedIndex",
     "Signature", "StageTimings", "TopKResult", "ValidationError", "bucket_top_k", "clause_matches", "encode",
-    "exact_scores", "execute", "execute_batch", "full_scan_tbr", "make_codec", "merge_topk", "normalize_query",
+    "batch_scan_tbr", "exact_scores", "execute", "execute_batch", "full_scan_tbr", "make_codec", "merge_topk", "normalize_query",
     "preselect", "quant_score", "quant_score_words", "validate_query", "hyre")
 
 

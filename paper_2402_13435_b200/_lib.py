@@ -44,6 +44,10 @@ class hyre_hit(C.Structure):
     _fields_ = [("row", C.c_uint32), ("score", C.c_float)]
 
 
+class hyre_messenger(C.Structure):
+    _fields_ = [("row_id", C.c_uint32), ("batch_id", C.c_uint32), ("score", C.c_float)]
+
+
 class hyre_timings(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("tbr_ms", "quant_ms", "ebr_ms", "topk_ms", "total_ms")]
 
@@ -146,6 +150,8 @@ SIGNATURES = {
     "hyre_batch_merge_gathered": (C.c_int, [vp, vp, vp, vp, C.c_uint32, C.c_uint64]),
     "hyre_batch_device_results": (C.c_int, [vp, C.POINTER(vp), u64p, C.POINTER(vp), C.POINTER(vp)]),
     "hyre_full_scan_tbr": (C.c_int, [vp, C.POINTER(hyre_query), u32p, C.c_uint64, u64p]),
+    "hyre_batch_scan_tbr": (C.c_int, [vp, C.POINTER(hyre_query), C.c_uint32, u32p, C.POINTER(hyre_messenger),
+                                      C.c_uint64, u64p]),
     "hyre_exact_scores": (C.c_int, [vp, f32p, C.c_uint32, u32p, C.c_uint64, f32p, i32p]),
     "hyre_bucket_top_k": (C.c_int, [vp, u32p, f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(hyre_hit),
                                     u32p]),

@@ -596,6 +596,18 @@ hyre_status hyre_full_scan_tbr(hyre_executor* ex, const hyre_query* q, uint32_t*
   });
 }
 
+hyre_status hyre_batch_scan_tbr(hyre_executor* ex, const hyre_query* qs, uint32_t b, const uint32_t* batch_ids,
+                                hyre_messenger* out, uint64_t cap, uint64_t* n) {
+  return guard([&] {
+    need(ex, "executor");
+    need(n, "n");
+    if (b && (!qs || !batch_ids)) validation("batch_scan_tbr: queries and batch_ids are required");
+    if (b > ex->ex->max_batch)
+      validation("batch of " + std::to_string(b) + " exceeds maxBatch " + std::to_string(ex->ex->max_batch));
+    *n = ex->ex->batch_scan(qs, b, batch_ids, out, out ? cap : 0);
+  });
+}
+
 hyre_status hyre_exact_scores(hyre_executor* ex, const float* q, uint32_t dim, const uint32_t* rows,
                               uint64_t n, float* scores, int32_t* renormalized) {
   return guard([&] {

@@ -1320,6 +1320,50 @@ uint64_t Executor::full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_r
   return ne;
 }
 
+// batch_scan_tbr (pipeline.cpp:75-93): the batch's eligibility masks (K1 /
+// K1b, one pass over the rows for all b queries) -> per-word counts -> scan
+// -> messengers in (row, query position) order.
+uint64_t Executor::batch_scan(const hyre_query* qs, uint32_t b, const uint32_t* batch_ids, hyre_messenger* out,
+                              uint64_t cap) {
+  if (b == 0) return 0;
+  std::vector<hyre_query> t(qs, qs + b);
+  for (hyre_query& q : t) {
+    q.embedding = nullptr;
+    q.embedding_dim = 0;
+    q.k = 1;
+    q.quant_enabled = 0;
+    q.granularity = 100;
+  }
+  prepare(t.data(), b);
+  for (uint32_t i = 0; i < b; ++i)
+    if (statuses[i] != HYRE_OK) throw Error(static_cast<hyre_status>(statuses[i]), slot_errors[i]);
+  run();
+  const uint32_t W = ix->words;
+  uint64_t* d_cnt = dmalloc<uint64_t>(W + 1);
+  uint64_t* d_off = dmalloc<uint64_t>(W + 1);
+  uint32_t* d_bid = dmalloc<uint32_t>(b);
+  HYRE_CUDA(cudaMemcpyAsync(d_bid, batch_ids, b * 4, cudaMemcpyHostToDevice, st));
+  launch_scan_count(d_mask, d_qp, b, W, d_cnt, st);
+  size_t tmp = 0;
+  HYRE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt, d_off, W + 1, st));
+  uint8_t* d_tmp = dmalloc<uint8_t>(std::max<size_t>(tmp, 1));
+  HYRE_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, d_cnt, d_off, W + 1, st));
+  uint64_t total = 0;
+  HYRE_CUDA(cudaMemcpyAsync(&total, d_off + W, 8, cudaMemcpyDeviceToHost, st));
+  HYRE_CUDA(cudaStreamSynchronize(st));
+  const uint64_t take = std::min(total, cap);
+  if (take) {
+    hyre_messenger* d_out = dmalloc<hyre_messenger>(take);
+    launch_scan_emit(d_mask, d_qp, b, W, ix->row_base, d_off, d_bid, d_out, take, st);
+    HYRE_CUDA(cudaMemcpyAsync(out, d_out, take * sizeof(hyre_messenger), cudaMemcpyDeviceToHost, st));
+    HYRE_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_out);
+  }
+  HYRE_CUDA(cudaGetLastError());
+  for (void* p : {(void*)d_cnt, (void*)d_off, (void*)d_bid, (void*)d_tmp}) cudaFree(p);
+  return total;
+}
+
 bool Executor::exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out) {
   if (dim != ix->dim)
     validation("query embedding dim " + std::to_string(dim) + " != index dim " + std::to_string(ix->dim));

@@ -191,6 +191,8 @@ struct Executor {
   void stage_ms_hist(uint32_t back, float* out) const;  // the same for the run `back` runs ago
 
   uint64_t full_scan(const hyre_query& q, uint32_t* rows, uint64_t cap_rows);
+  uint64_t batch_scan(const hyre_query* qs, uint32_t b, const uint32_t* batch_ids, hyre_messenger* out,
+                      uint64_t cap);
   bool exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out);
   uint32_t top_k(const uint32_t* rows, const float* scores, uint64_t n, uint32_t k, hyre_hit* out);
   void merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,

@@ -1927,4 +1927,58 @@ void launch_rescore_keys(const PrefSelectArgs& a, bool bf16, uint32_t q, uint64_
   if (bf16) dispatch_rescore_keys<__nv_bfloat16>(a, q, keys, n, st);
   else dispatch_rescore_keys<float>(a, q, keys, n, st);
 }
+// ---------------------------------------------------------------------------
+// batch_scan_tbr (pipeline.cpp:75-93): the (row, batchId) messenger stream of
+// a term-only batch, ordered by row then by query position, from the batch's
+// eligibility masks.  Pass 1 counts each 32-row word's matches over every
+// active query; an exclusive scan places each word; pass 2 (one warp per
+// word, lane = row) writes the word's messengers in (row, query) order.
+// ---------------------------------------------------------------------------
+__global__ void scan_count_kernel(const uint32_t* __restrict__ mask, const QParam* __restrict__ qp, uint32_t B,
+                                  uint32_t W, uint64_t* __restrict__ cnt) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > W) return;
+  uint64_t c = 0;
+  if (w < W)
+    for (uint32_t b = 0; b < B; ++b)
+      if (qp[b].flags & QF_ACTIVE) c += __popc(mask[static_cast<size_t>(b) * W + w]);
+  cnt[w] = c;  // cnt[W] = 0: the scan's total lands in off[W]
+}
+
+__global__ void scan_emit_kernel(const uint32_t* __restrict__ mask, const QParam* __restrict__ qp, uint32_t B,
+                                 uint32_t W, uint32_t row_base, const uint64_t* __restrict__ off,
+                                 const uint32_t* __restrict__ batch_ids, hyre_messenger* __restrict__ out,
+                                 uint64_t cap) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= W) return;
+  const uint64_t base = off[w];
+  if (base >= cap || off[w + 1] == base) return;
+  uint32_t mine = 0;
+  for (uint32_t b = 0; b < B; ++b)
+    if (qp[b].flags & QF_ACTIVE) mine += (mask[static_cast<size_t>(b) * W + w] >> lane) & 1u;
+  uint32_t incl = mine;  // inclusive warp scan over the rows of this word
+#pragma unroll
+  for (uint32_t d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  uint64_t pos = base + incl - mine;
+  const uint32_t row = row_base + w * 32 + lane;
+  for (uint32_t b = 0; b < B && pos < cap; ++b) {
+    if (!(qp[b].flags & QF_ACTIVE)) continue;
+    if ((mask[static_cast<size_t>(b) * W + w] >> lane) & 1u) out[pos++] = hyre_messenger{row, batch_ids[b], 0.0f};
+  }
+}
+
+void launch_scan_count(const uint32_t* mask, const QParam* qp, uint32_t B, uint32_t W, uint64_t* cnt,
+                       cudaStream_t st) {
+  scan_count_kernel<<<(W + 1 + 255) / 256, 256, 0, st>>>(mask, qp, B, W, cnt);
+}
+
+void launch_scan_emit(const uint32_t* mask, const QParam* qp, uint32_t B, uint32_t W, uint32_t row_base,
+                      const uint64_t* off, const uint32_t* batch_ids, hyre_messenger* out, uint64_t cap,
+                      cudaStream_t st) {
+  if (W) scan_emit_kernel<<<(W + 7) / 8, 256, 0, st>>>(mask, qp, B, W, row_base, off, batch_ids, out, cap);
+}
+
 }  // namespace hyreb

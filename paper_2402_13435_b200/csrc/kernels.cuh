@@ -260,4 +260,13 @@ void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uin
                         uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys, uint32_t* cnt,
                         cudaStream_t st);
 
+// batch_scan_tbr (pipeline.cpp:75-93): per 32-row word, matches over the
+// active queries of a [B][W] mask (cnt has W + 1 slots; cnt[W] = 0), then --
+// with off = exclusive scan of cnt -- the messengers in (row, query) order.
+void launch_scan_count(const uint32_t* mask, const QParam* qp, uint32_t B, uint32_t W, uint64_t* cnt,
+                       cudaStream_t st);
+void launch_scan_emit(const uint32_t* mask, const QParam* qp, uint32_t B, uint32_t W, uint32_t row_base,
+                      const uint64_t* off, const uint32_t* batch_ids, hyre_messenger* out, uint64_t cap,
+                      cudaStream_t st);
+
 }  // namespace hyreb

@@ -587,6 +587,22 @@ class Executor:
         _check(L.lib().hyre_full_scan_tbr(self._h, C.byref(pack.arr[0]), _p(out, L.u32p), len(out), C.byref(n)))
         return out[: n.value].astype(np.int64)
 
+    def batch_scan_tbr(self, queries: Sequence[CnfQuery], batch_ids: Sequence[int]) -> List[Messenger]:
+        """pipeline.cpp:75-93: one pass over the rows for every query; the
+        matches ordered by (rowId, query position), stamped with batch_ids."""
+        if len(batch_ids) != len(queries):
+            raise ValidationError("batch_ids must have one id per query")
+        if not queries:
+            return []
+        pack = QueryPack([HybridQuery(terms=q, k=1) for q in queries])
+        bid = np.ascontiguousarray(batch_ids, np.uint32)
+        n = C.c_uint64()
+        _check(L.lib().hyre_batch_scan_tbr(self._h, pack.arr, len(queries), _p(bid, L.u32p), None, 0, C.byref(n)))
+        out = (L.hyre_messenger * max(1, n.value))()
+        _check(L.lib().hyre_batch_scan_tbr(self._h, pack.arr, len(queries), _p(bid, L.u32p), out, n.value,
+                                           C.byref(n)))
+        return [Messenger(int(m.row_id), int(m.batch_id), 0.0) for m in out[: n.value]]
+
     def exact_scores(self, query_embedding, candidates: Sequence[Messenger]) -> ScoredMessengers:
         q = np.ascontiguousarray(query_embedding, np.float32)
         rows = np.asarray([m.row_id for m in candidates] or [0], np.uint32)
@@ -770,6 +786,10 @@ def _default_executor(index: FrozenIndex, max_batch: int = 1) -> Executor:
 
 def full_scan_tbr(index: FrozenIndex, query: CnfQuery, batch_id: int = 0) -> List[Messenger]:
     return _default_executor(index).full_scan_tbr(query, batch_id)
+
+
+def batch_scan_tbr(index: FrozenIndex, queries: Sequence[CnfQuery], batch_ids: Sequence[int]) -> List[Messenger]:
+    return _default_executor(index, max(1, len(queries))).batch_scan_tbr(queries, batch_ids)
 
 
 def clause_matches(index: FrozenIndex, row_id: int, clause: CnfClause) -> bool:

@@ -100,6 +100,15 @@ int main(int argc, char** argv) {
         rows(full_scan_tbr(idx, normalize_query({{0, {129}}, {1, {234}}}, 2))) == std::vector<std::uint32_t>({1}) &&
             full_scan_tbr(idx, normalize_query({{0, {129}}, {1, {945}}}, 2)).empty() &&
             rows(full_scan_tbr(idx, normalize_query({{1, {234, 342}}}, 2))) == std::vector<std::uint32_t>({0, 1}));
+  {
+    const std::vector<CnfQuery> bq{normalize_query({{0u, {2, 3, 6}}}, 1), normalize_query({{0u, {4, 6, 10}}}, 1)};
+    const std::vector<std::uint32_t> bid{0, 1};
+    const auto ms = batch_scan_tbr(addr, bq, bid);
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> got;
+    for (const auto& m : ms) got.emplace_back(m.row_id, m.batch_id);
+    CHECK("batch scan stream (test_pipeline.cpp:221-235)",
+          got == (std::vector<std::pair<std::uint32_t, std::uint32_t>>{{1, 0}, {2, 0}, {3, 1}, {5, 0}, {5, 1}, {9, 1}}));
+  }
   HybridQuery term_only;
   term_only.terms = normalize_query({{0u, {8, 3, 6}}}, 1);
   term_only.k = 2;

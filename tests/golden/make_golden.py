@@ -78,6 +78,20 @@ def main():
         tbr.append({"seed": spec.seed, "query": q, "rows": ri.full_scan_tbr(q).tolist()})
     fixtures["tbr"] = tbr
 
+    # --- batch scan stream (pipeline.cpp:75-93, test_pipeline.cpp:221-235) ---
+    bs = []
+    rng = O.MT19937_64(123)
+    for trial in range(6):
+        spec.seed = 2000 + trial
+        docs, widest, ri = corpus(spec)
+        qs = [O.random_query(spec, rng) for _ in range(1 + trial)]
+        if trial == 3:
+            qs.append([])  # match-all
+        ids = [7 * i + trial for i in range(len(qs))]
+        bs.append({"seed": spec.seed, "queries": qs, "batch_ids": ids,
+                   "stream": [list(p) for p in ri.batch_scan_tbr(qs, ids)]})
+    fixtures["batch_scan"] = bs
+
     # --- hybrid search, quant off and on (test_pipeline.cpp:124-197) --------
     hyb = []
     spec = O.CorpusSpec(num_docs=300, dim=12, num_clauses=2, attr_universe=10)

@@ -201,6 +201,51 @@ def rows_query(hy, rows):
     return hy.normalize_query({0: [r + 1 for r in rows]}, 1)
 
 
+def test_batch_scan_interleaves_by_row_then_batch_id(hy):
+    # test_pipeline.cpp:221-235
+    _, prod, _ = addressable_corpus(hy, 10)
+    ms = hy.batch_scan_tbr(prod, [rows_query(hy, [1, 2, 5]), rows_query(hy, [3, 5, 9])], [0, 1])
+    assert [(m.row_id, m.batch_id) for m in ms] == [(1, 0), (2, 0), (3, 1), (5, 0), (5, 1), (9, 1)]
+    assert all(m.score == 0.0 for m in ms)
+
+
+def test_batch_scan_matches_reference_streams(hy):
+    # golden streams of the compiled reference's batch_scan_tbr
+    import json
+    fx_all = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_fixtures.json")))
+    spec = O.CorpusSpec(num_docs=60, num_clauses=3, attr_universe=12)
+    for fx in fx_all["batch_scan"]:
+        spec.seed = fx["seed"]
+        _, _, prod = corpus_pair(spec)
+        qs = [to_cnf(q) for q in fx["queries"]]
+        ms = hy.batch_scan_tbr(prod, qs, fx["batch_ids"])
+        assert [[m.row_id, m.batch_id] for m in ms] == fx["stream"], fx["seed"]
+
+
+@pytest.mark.parametrize("B", [3, 20, 130])
+def test_batch_scan_large_batches_match_oracle(hy, B):
+    # K1 (B <= 8) and the forward-list K1b (B > 8, two passes at 130) masks
+    # feed the same stream; match-all and absent-id queries included
+    n, C = 20_000, 3
+    rs = np.random.default_rng(17)
+    docs = [O.Doc(f"d{i}", [(1 + np.minimum(rs.zipf(1.4, size=rs.integers(0, 4)), 500)).tolist() for _ in range(C)],
+                  np.ones(4, np.float32)) for i in range(n)]
+    width = max(sum(len(set(c)) for c in d.clauses) for d in docs)
+    prod = product_index(docs, C, width, 4, 64, 1)
+    ref = O.freeze(docs, C, width, 4, 64, 1)
+    qs = []
+    for i in range(B):
+        raw = {} if i % 11 == 5 else ({0: [99_999]} if i % 13 == 7 else
+                                        {c: (1 + np.minimum(rs.zipf(1.4, size=rs.integers(1, 4)), 500)).tolist()
+                                         for c in range(C) if rs.random() < 0.6})
+        qs.append(O.normalize_query(raw, C))
+    ids = [1000 + 3 * i for i in range(B)]
+    got = hy.Executor(prod, max_batch=B).batch_scan_tbr([to_cnf(q) for q in qs], ids)
+    expect = O.batch_scan_tbr(ref, qs, ids)
+    assert len(got) == len(expect)
+    assert [(m.row_id, m.batch_id) for m in got] == expect
+
+
 def test_term_only_queries_return_matches_in_row_order_with_zero_scores(hy):
     _, prod, _ = addressable_corpus(hy, 10)
     q = hy.HybridQuery(rows_query(hy, [7, 2, 5]), None, 2)

@@ -94,6 +94,24 @@ def test_tbr_known_answers():
     assert O.full_scan_tbr(sparse, nq({0: [7]}, 2)).tolist() == [0]
 
 
+def test_batch_scan_stream_matches_reference():
+    # pipeline.cpp:75-93 against streams the compiled reference produced
+    spec = O.CorpusSpec(num_docs=60, num_clauses=3, attr_universe=12)
+    for fx in FIX["batch_scan"]:
+        spec.seed = fx["seed"]
+        _, fr = O.make_corpus(spec)
+        qs = [[(s, ids) for s, ids in q] for q in fx["queries"]]
+        assert [list(p) for p in O.batch_scan_tbr(fr, qs, fx["batch_ids"])] == fx["stream"]
+
+
+def test_batch_scan_known_answer():
+    # test_pipeline.cpp:221-235: addressable corpus (row r holds id r + 1)
+    docs = [O.Doc(f"doc{r}", [[r + 1]], np.ones(2, np.float32)) for r in range(10)]
+    fr = O.freeze(docs, 1, 1, 2, 16, 3)
+    qs = [O.normalize_query({0: [2, 3, 6]}, 1), O.normalize_query({0: [4, 6, 10]}, 1)]
+    assert O.batch_scan_tbr(fr, qs, [0, 1]) == [(1, 0), (2, 0), (3, 1), (5, 0), (5, 1), (9, 1)]
+
+
 def test_hybrid_and_quant_match_reference_bit_exactly():
     spec = O.CorpusSpec(num_docs=300, dim=12, num_clauses=2, attr_universe=10)
     for fx in FIX["hybrid"]:

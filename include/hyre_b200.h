@@ -217,6 +217,13 @@ typedef struct hyre_index_stats {
 hyre_status hyre_index_create(const hyre_frozen* f, const hyre_index_options* opts,
                               hyre_index** out);
 void hyre_index_destroy(hyre_index* ix);
+/* Learned per-row weights (the north star's link/attribute weights applied in
+ * the scoring epilogue; no reference counterpart -- its score is the pure
+ * cosine, knn.cpp:36-37): every returned score becomes w[row] x clamp(dot),
+ * w in [0, 1], for hybrid queries (term-only scores stay 0).  w has one weight
+ * per row of this index (n == its row count); w == NULL restores the
+ * identity.  Must not overlap a running executor of the index. */
+hyre_status hyre_index_set_row_weights(hyre_index* ix, const float* w, uint64_t n);
 hyre_status hyre_index_stats_get(const hyre_index* ix, hyre_index_stats* out);
 
 /* ------------------------------------------------------------------------
@@ -332,6 +339,8 @@ typedef struct hyre_sharded_index_options {
 hyre_status hyre_sharded_index_create(const hyre_frozen* f, const hyre_sharded_index_options* opts,
                                       hyre_sharded_index** out);
 void hyre_sharded_index_destroy(hyre_sharded_index* ix);
+/* hyre_index_set_row_weights over every shard: w covers all rows (global order). */
+hyre_status hyre_sharded_index_set_row_weights(hyre_sharded_index* ix, const float* w, uint64_t n);
 /* shard count and each shard's device (devices may be NULL) */
 hyre_status hyre_sharded_index_info(const hyre_sharded_index* ix, uint32_t* n_shards, int32_t* devices);
 

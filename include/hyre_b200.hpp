@@ -251,6 +251,17 @@ class FrozenIndex {
   }
   const hyre_frozen* handle() const { return f_.get(); }
 
+  // Learned per-row weights (the north star's link/attribute weights; no
+  // reference counterpart): hybrid scores become w[row] x clamp(cosine), one
+  // weight in [0, 1] per row; an empty span restores the pure cosine.  Applies
+  // to the device index (or its shards) every executor of this index reads;
+  // not while one of them is running.
+  void set_row_weights(std::span<const float> w) const {
+    const float* p = w.empty() ? nullptr : w.data();
+    if (sharded()) detail::check(hyre_sharded_index_set_row_weights(device_shards(), p, w.size()));
+    else detail::check(hyre_index_set_row_weights(device(), p, w.size()));
+  }
+
  private:
   friend class IndexBuilder;
   explicit FrozenIndex(hyre_frozen* f) : f_(f, &hyre_frozen_destroy), dev_(std::make_shared<Dev>()) {

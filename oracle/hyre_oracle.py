@@ -388,9 +388,20 @@ def validate_query(index: Frozen, clauses: Sequence[tuple], embedding, k: int,
                 raise ValidationError("clause attribute ids must be strictly increasing (use normalize_query)")
 
 
+def weighted_scores(emb: np.ndarray, q: np.ndarray, rows: np.ndarray, row_weights) -> np.ndarray:
+    """The north star's learned-weight epilogue (no reference counterpart; the
+    reference score is the pure cosine, knn.cpp:36-37): w[row] x clamp(dot),
+    one fp32 multiply of the reference's exact score."""
+    s = scores_rows(emb, q, rows)
+    if row_weights is None:
+        return s
+    return (np.asarray(row_weights, np.float32)[np.asarray(rows, np.int64)] * s).astype(np.float32)
+
+
 def execute(index: Frozen, clauses: Sequence[tuple], embedding: Optional[np.ndarray], k: int,
-            quant_enabled: bool = True, quant_k: int = 0, granularity: int = 100) -> tuple:
-    """Executor::execute (pipeline.cpp:108-145) -> (rows i64[], scores f32[])."""
+            quant_enabled: bool = True, quant_k: int = 0, granularity: int = 100, row_weights=None) -> tuple:
+    """Executor::execute (pipeline.cpp:108-145) -> (rows i64[], scores f32[]);
+    row_weights: the learned per-row weights (weighted_scores)."""
     validate_query(index, clauses, embedding, k, granularity)
     matches = full_scan_tbr(index, clauses)
     if len(matches) == 0:
@@ -403,7 +414,7 @@ def execute(index: Frozen, clauses: Sequence[tuple], embedding: Optional[np.ndar
     if quant_enabled and len(matches) > qk:
         qsig = encode_rows(make_codec(index.dim, index.num_bits, index.seed), q)[0]
         matches = preselect(index, qsig, matches, qk)
-    s = scores_rows(index.embeddings, q, matches)
+    s = weighted_scores(index.embeddings, q, matches, row_weights)
     return top_k(matches, s, k, granularity)
 
 

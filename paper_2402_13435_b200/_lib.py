@@ -106,6 +106,8 @@ SIGNATURES = {
     "hyre_validate_query": (C.c_int, [vp, C.POINTER(hyre_query)]),
     "hyre_index_create": (C.c_int, [vp, C.POINTER(hyre_index_options), C.POINTER(vp)]),
     "hyre_index_destroy": (None, [vp]),
+    "hyre_index_set_row_weights": (C.c_int, [vp, f32p, C.c_uint64]),
+    "hyre_sharded_index_set_row_weights": (C.c_int, [vp, f32p, C.c_uint64]),
     "hyre_index_stats_get": (C.c_int, [vp, C.POINTER(hyre_index_stats)]),
     "hyre_executor_create": (C.c_int, [vp, C.c_uint32, C.POINTER(vp)]),
     "hyre_executor_destroy": (None, [vp]),

@@ -280,6 +280,13 @@ hyre_status hyre_index_create(const hyre_frozen* f, const hyre_index_options* op
 
 void hyre_index_destroy(hyre_index* ix) { delete ix; }
 
+hyre_status hyre_index_set_row_weights(hyre_index* ix, const float* w, uint64_t n) {
+  return guard([&] {
+    need(ix, "index");
+    set_row_weights(*ix->ix, w, n);
+  });
+}
+
 hyre_status hyre_index_stats_get(const hyre_index* ix, hyre_index_stats* out) {
   return guard([&] {
     need(ix, "index");
@@ -382,6 +389,17 @@ hyre_status hyre_sharded_index_create(const hyre_frozen* f, const hyre_sharded_i
 }
 
 void hyre_sharded_index_destroy(hyre_sharded_index* ix) { delete ix; }
+
+hyre_status hyre_sharded_index_set_row_weights(hyre_sharded_index* ix, const float* w, uint64_t n) {
+  return guard([&] {
+    need(ix, "index");
+    ShardedIndex& si = *ix->ix;
+    if (w && n != si.total_rows)
+      validation("row weights: expected " + std::to_string(si.total_rows) + " weights, got " + std::to_string(n));
+    const uint32_t base0 = si.ix.front()->row_base;
+    for (auto& d : si.ix) set_row_weights(*d, w ? w + (d->row_base - base0) : nullptr, d->n_rows);
+  });
+}
 
 hyre_status hyre_sharded_index_info(const hyre_sharded_index* ix, uint32_t* n_shards, int32_t* devices) {
   return guard([&] {

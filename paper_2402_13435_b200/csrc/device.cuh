@@ -192,6 +192,10 @@ struct DevIndex {
   uint8_t* cnf_ids = nullptr;
   uint64_t* cnf_masks = nullptr;
   uint32_t cnf_id_bytes = 0, cnf_ids_per_row = 0, cnf_row_bytes = 0;
+  // Learned per-row weights (north star: "learned link/attribute weights
+  // applied in the epilogue"): score = w[r] x clamp(dot), w in [0, 1], local
+  // rows; nullptr = identity (the reference's pure cosine, knn.cpp:36-37).
+  float* row_w = nullptr;
   Codec codec;
   hyre_index_stats stats{};
   ~DevIndex();

@@ -361,7 +361,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // prefilter + exact rescoring: K3 batches (int8 or bf16 prefilter), and K2
   // batches when the int8 plane exists (the int8 rows are a quarter of fp32)
   const bool i8_ok = ix->tc_i8 != nullptr && ix->dp % 128 == 0 && prefilter_i8_allowed();
-  prefilter = any_emb && prefilter_enabled() && (use_tc || (i8_ok && k2_i8_enabled()));
+  // (a weighted index keeps the prefilter on K3 batches: the weighted
+  // admission and w x clamp(exact dot) rescoring live on that path)
+  prefilter = any_emb && (prefilter_enabled() || (use_tc && ix->row_w)) && (use_tc || (i8_ok && k2_i8_enabled()));
   pf_i8 = prefilter && i8_ok;
   if (use_tc) {
     // one group of up to 256 queries per pass (the epilogue works in 32-column
@@ -629,6 +631,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.acc_bufs = tc_acc_bufs(tc_np);
       ta.match_all = all_match ? 1u : 0u;
       ta.backoff_ns = tc_backoff_ns();
+      ta.row_w = ix->row_w;
       if (use_fused) {
         const FusedGroup& fg = fz_group[g];
         ta.fused = 1;
@@ -656,6 +659,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   const uint32_t dp_chunks = ix->dp * (bf16 ? 2 : 4) / 16;
   ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
                d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp, 1, 1};
+  sa.row_w = ix->row_w;
   if (pf_i8) {  // int8 prefilter rows (exact rescoring in K4p)
     sa.emb = ix->tc_i8;
     sa.qi8 = d_qi8;
@@ -743,7 +747,7 @@ void Executor::final_select(SelectArgs fa) {
   fa.delta = prefilter_delta();
   fa.qdelta = d_qdelta;
   PrefSelectArgs pa{fa, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
-                    ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
+                    ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q, ix->row_w};
   launch_select_prefilter(pa, bf16, st);
   ++kernels;
 }
@@ -1236,7 +1240,7 @@ void Executor::exhaustive(uint32_t i) {
   launch_rows_to_keys(d_ex_rows, n, d_ex_keys, st);
   const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
   PrefSelectArgs pa{SelectArgs{}, bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32),
-                    ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q};
+                    ix->dp, ix->dp * (bf16 ? 2 : 4) / 16, ix->row_base, d_q, ix->row_w};
   launch_rescore_keys(pa, bf16, i, d_ex_keys, n, st);
   sort_desc(d_ex_keys, d_ex_sorted, n);
   launch_keys_to_hits(d_ex_sorted, std::min<uint64_t>(n, true_k[i]), d_hits + hit_off[i], out_cnt + i, rerun + i, st);

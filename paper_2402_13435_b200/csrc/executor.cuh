@@ -16,6 +16,10 @@
 namespace hyreb {
 
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
+// Learned per-row weights of the index's own rows (n == n_rows, each in
+// [0, 1]); w == nullptr restores the identity (pure cosine).  Not to be
+// called while an executor of this index is running.
+void set_row_weights(DevIndex& ix, const float* w, uint64_t n);
 
 // Host barrier of the G shard threads of a ShardedExecutor.
 class HostBarrier {

@@ -231,6 +231,24 @@ DevIndex::~DevIndex() {
   cudaFree(sigs);
   cudaFree(bitmaps);
   cudaFree(post_rows);
+  cudaFree(row_w);
+}
+
+void set_row_weights(DevIndex& ix, const float* w, uint64_t n) {
+  HYRE_CUDA(cudaSetDevice(ix.device));
+  if (!w) {
+    HYRE_CUDA(cudaDeviceSynchronize());
+    cudaFree(ix.row_w);
+    ix.row_w = nullptr;
+    return;
+  }
+  if (n != ix.n_rows)
+    validation("row weights: expected " + std::to_string(ix.n_rows) + " weights, got " + std::to_string(n));
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(w[i] >= 0.0f && w[i] <= 1.0f))  // also rejects NaN
+      validation("row weight " + std::to_string(i) + " = " + std::to_string(w[i]) + " outside [0, 1]");
+  if (!ix.row_w) ix.row_w = dmalloc<float>(std::max<uint64_t>(n, 1));
+  HYRE_CUDA(cudaMemcpy(ix.row_w, w, n * sizeof(float), cudaMemcpyHostToDevice));
 }
 
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {

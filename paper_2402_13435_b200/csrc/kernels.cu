@@ -602,6 +602,8 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
       const uint32_t my_idx = base + slot * G + g;
       const bool my_ok = leader && my_idx < total;
       const uint32_t my_off = my_idx < total ? (full ? my_idx : lists[wib][my_idx]) : 0u;
+      // learned row weight (identity without weights): scores are w x clamp(s)
+      const float wr = (a.row_w && my_ok) ? __ldg(a.row_w + seg_row0 + my_off) : 1.0f;
 #pragma unroll
       for (int j = 0; j < QG; ++j) {
         if (!(act >> j & 1u)) continue;
@@ -648,14 +650,15 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const bool elig = (src_word >> (my_off & 31)) & 1u;
         const uint32_t grow = a.row_base + static_cast<uint32_t>(seg_row0) + my_off;
         if (kI8) p[0] *= sc8[j];  // exact int8 dot -> prefilter score
-        const uint64_t key = make_key(clamp_score(p[0]), grow);
+        // weighted: w x clamp(s) (|w s - w s'| <= w delta <= delta keeps the prefilter bound)
+        const float ps = a.row_w ? clamp_score(p[0]) * wr : clamp_score(p[0]);
+        const uint64_t key = make_key(ps, grow);
         if (a.mode == SCORE_SAMPLE) {
           // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
-          if (my_ok && elig)
-            a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(clamp_score(p[0]));
+          if (my_ok && elig) a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(ps);
           continue;
         }
-        const bool take = my_ok && elig && (kI8 ? p[0] >= ts8[j] : key >= thr[j]);
+        const bool take = my_ok && elig && (kI8 ? (a.row_w ? ps : p[0]) >= ts8[j] : key >= thr[j]);
         const unsigned bal = __ballot_sync(kFull, take);
         if (bal) {
           const uint32_t q = q0 + j;
@@ -1258,7 +1261,7 @@ __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys
 #pragma unroll
       for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
       if (li == 0 && idx[u] < n) {
-        const float sc = clamp_score(acc);
+        const float sc = a.row_w ? clamp_score(acc) * __ldg(a.row_w + (grow[u] - a.row_base)) : clamp_score(acc);
         keys[idx[u]] = make_key(sc, grow[u]);
         mine += sc >= thr_s ? 1u : 0u;
       }

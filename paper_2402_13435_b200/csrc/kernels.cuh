@@ -88,6 +88,9 @@ struct ScoreArgs {
   const int8_t* qi8;
   const float* qscale;
   const float* qdelta;
+  // learned per-row weights (local rows; nullptr = identity): every score and
+  // prefilter score is w[r] x clamp(s).  w <= 1 keeps the prefilter bound.
+  const float* row_w;
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 void launch_score_i8(const ScoreArgs& a, cudaStream_t st);
@@ -144,6 +147,7 @@ struct PrefSelectArgs {
   const void* emb;
   uint32_t dp, dp_chunks, row_base;
   const float* q;  // [B][dp]
+  const float* row_w;  // learned per-row weights (local rows) or nullptr
 };
 void launch_select_prefilter(const PrefSelectArgs& a, bool bf16, cudaStream_t st);
 // SELECT_KTH over the dense sample: per-slice top keys gathered into fb

@@ -418,7 +418,14 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
       const float sc = q0 + j < a.B ? a.qscale[q0 + j] : 1.0f, ts = s_ts[j];
       s_sc[j] = sc;
       int32_t T;
-      if (ts >= 2.0f) T = INT32_MAX;  // inactive: never taken
+      if (a.row_w) {
+        // weighted: admit acc x W_r >= 256 T with W_r = ceil(256 w_r) >= 256 w_r,
+        // a superset of w_r s' >= ts when ts > 0 (then s' > 0); ts <= 0 takes
+        // every row.  |acc| < 2^21 and W_r <= 256 keep the IMAD inside s32.
+        if (ts >= 2.0f) T = 1 << 30;  // inactive: never taken
+        else if (ts <= 0.0f) T = -(1 << 30);  // no threshold
+        else T = static_cast<int32_t>(fminf(fmaxf((floorf(ts / sc) - 1.0f) * 256.0f, -1.0e9f), 1.0e9f));
+      } else if (ts >= 2.0f) T = INT32_MAX;  // inactive: never taken
       else if (ts <= -1.0f) T = INT32_MIN / 2;  // no threshold
       else T = static_cast<int32_t>(fmaxf(floorf(ts / sc) - 1.0f, -1.0e9f));
       s_ts[j] = __int_as_float(T);
@@ -578,6 +585,14 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
       uint32_t mw_next[WC];
       load_mask(t_next, mw_next);  // in flight while this tile is processed
       const uint32_t grow = a.row_base + t * kTileRows + quad * 32 + lane;
+      // learned row weight of this lane's row (weighted index only)
+      float wr = 1.0f;
+      int32_t wi = 256;
+      if (a.row_w) {
+        const uint32_t lr = t * kTileRows + quad * 32 + lane;
+        wr = lr < a.n_rows ? __ldg(a.row_w + lr) : 0.0f;
+        wi = static_cast<int32_t>(ceilf(wr * 256.0f));
+      }
       uint32_t fel[WC] = {};  // fused: bit j = row `lane` eligible for query 32c + j
       if (kFused) {
         // this row's eligibility words for chunks half, half + 2, ... (CNF warps)
@@ -637,7 +652,25 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         // monotone rounding) and a funnel shift collecting d's sign bit.
         uint32_t below = 0;  // bit 31 - j: query 32c + j scored below its threshold
         const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
-        if (a.i8) {  // int32 accumulators against integer thresholds (no overflow: |acc|, |T| < 2^30)
+        if (a.i8 && a.row_w) {  // weighted: acc x W_r - 256 T (one IMAD per score)
+#pragma unroll
+          for (uint32_t j4 = 0; j4 < 8; ++j4) {
+            const int4 t4 = *reinterpret_cast<const int4*>(ts4 + j4);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 0]) * wi - t4.x), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 1]) * wi - t4.y), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 2]) * wi - t4.z), below, 1);
+            below = __funnelshift_l(static_cast<uint32_t>(static_cast<int32_t>(v[4 * j4 + 3]) * wi - t4.w), below, 1);
+          }
+        } else if (a.row_w) {  // weighted bf16 prefilter: sign of fma(s', w_r, -ts) (exact sign)
+#pragma unroll
+          for (uint32_t j4 = 0; j4 < 8; ++j4) {
+            const float4 t4 = ts4[j4];
+            below = __funnelshift_l(__float_as_uint(fmaf(__uint_as_float(v[4 * j4 + 0]), wr, -t4.x)), below, 1);
+            below = __funnelshift_l(__float_as_uint(fmaf(__uint_as_float(v[4 * j4 + 1]), wr, -t4.y)), below, 1);
+            below = __funnelshift_l(__float_as_uint(fmaf(__uint_as_float(v[4 * j4 + 2]), wr, -t4.z)), below, 1);
+            below = __funnelshift_l(__float_as_uint(fmaf(__uint_as_float(v[4 * j4 + 3]), wr, -t4.w)), below, 1);
+          }
+        } else if (a.i8) {  // int32 accumulators against integer thresholds (no overflow: |acc|, |T| < 2^30)
 #pragma unroll
           for (uint32_t j4 = 0; j4 < 8; ++j4) {
             const int4 t4 = *reinterpret_cast<const int4*>(ts4 + j4);
@@ -662,13 +695,18 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         auto score_of = [&](uint32_t w, uint32_t j) {
           return a.i8 ? static_cast<float>(static_cast<int32_t>(w)) * s_sc[c * 32 + j] : __uint_as_float(w);
         };
+        // clamped (and weighted: w_r x clamp(s')) score of (row lane, query 32c + j)
+        auto final_of = [&](uint32_t w, uint32_t j) {
+          const float x = clamp_score(score_of(w, j));
+          return a.row_w ? x * wr : x;
+        };
         if (a.mode == SCORE_SAMPLE && a.shist) {
           // sample pass, histogram form: one global increment per eligible
           // sampled (row, query) in the query's score histogram
           const float scale = 0.5f * static_cast<float>(a.hbins);
           for (uint32_t el = elig; el; el &= el - 1u) {
             const uint32_t j = __ffs(el) - 1;
-            const float sc = clamp_score(score_of(pick32(v, j), j));
+            const float sc = final_of(pick32(v, j), j);
             const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);
             atomicAdd(a.shist + static_cast<size_t>(q0 + c * 32 + j) * a.hbins + b, 1u);
           }
@@ -682,7 +720,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
 #pragma unroll
           for (uint32_t j = 0; j < 32; ++j)
             if ((elig >> j) & 1u)
-              a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(clamp_score(score_of(v[j], j)));
+              a.samp[static_cast<size_t>(q0 + c * 32 + j) * a.cap + sidx] = f2ord(final_of(v[j], j));
           continue;
         }
         // survivors (rare): each lane walks its own set bits; the score is
@@ -692,7 +730,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         // candidate buffer only when a query's slots are full.
         for (uint32_t tk = take; tk; tk &= tk - 1u) {
           const uint32_t j = __ffs(tk) - 1, qq = c * 32 + j;
-          const uint64_t key = make_key(clamp_score(score_of(pick32(v, j), j)), grow);
+          const uint64_t key = make_key(final_of(pick32(v, j), j), grow);
           if (key_score(key) == s_ts[qq] && grow > s_tr[qq]) continue;  // exact tie rule: below the threshold key
                                                                         // (prefilter: s_tr = ~0, never)
           const uint32_t slot = atomicAdd(s_scnt + qq, 1u);

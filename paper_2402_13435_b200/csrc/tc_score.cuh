@@ -59,6 +59,9 @@ struct TcArgs {
   uint32_t i8;
   const float* qscale;
   const float* qdelta;
+  // learned per-row weights (local rows; nullptr = identity; prefilter mode
+  // only): admission w x s' >= ts, keys and sample scores w x clamp(s')
+  const float* row_w;
   uint64_t plane_bytes;  // DevIndex::tc_plane_bytes (offset of the lo plane)
   float delta;
   uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))

@@ -359,6 +359,16 @@ class DeviceIndex:
             L.lib().hyre_index_destroy(self._h)
             self._h = None
 
+    def set_row_weights(self, weights) -> None:
+        """Learned per-row weights (north star; no reference counterpart):
+        hybrid scores become w[row] x clamp(cosine), w in [0, 1], one weight
+        per row of this index; None restores the pure cosine."""
+        if weights is None:
+            _check(L.lib().hyre_index_set_row_weights(self._h, None, 0))
+            return
+        w = np.ascontiguousarray(weights, np.float32)
+        _check(L.lib().hyre_index_set_row_weights(self._h, _p(w, L.f32p), w.size))
+
     def stats(self) -> dict:
         s = L.hyre_index_stats()
         _check(L.lib().hyre_index_stats_get(self._h, C.byref(s)))
@@ -657,6 +667,14 @@ class ShardedIndex:
         if getattr(self, "_h", None):
             L.lib().hyre_sharded_index_destroy(self._h)
             self._h = None
+
+    def set_row_weights(self, weights) -> None:
+        """DeviceIndex.set_row_weights over every shard (weights in global row order)."""
+        if weights is None:
+            _check(L.lib().hyre_sharded_index_set_row_weights(self._h, None, 0))
+            return
+        w = np.ascontiguousarray(weights, np.float32)
+        _check(L.lib().hyre_sharded_index_set_row_weights(self._h, _p(w, L.f32p), w.size))
 
     def info(self):
         """-> (n_shards, [device of each shard])."""

@@ -98,6 +98,11 @@ uint32_t hyre_builder_size(const hyre_builder* b);
  * corpus.cpp:54-129.  The builder is consumed (further calls fail). */
 hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t seed,
                                 hyre_frozen** out);
+/* The same freeze computed on GPU `device` (per-clause sort + dedup, double
+ * L2 normalisation, signatures): bit-identical arrays and the same errors,
+ * for large builds.  The builder is consumed. */
+hyre_status hyre_builder_freeze_device(hyre_builder* b, uint32_t num_bits, uint64_t seed,
+                                       int32_t device, hyre_frozen** out);
 
 /* Wraps flat FrozenIndex arrays (corpus.hpp:114-123) that a caller already
  * holds -- e.g. the reference's own FrozenIndex -- without re-freezing.
@@ -127,7 +132,9 @@ const uint32_t* hyre_frozen_offsets(const hyre_frozen* f);     /* N x (C+1) */
 const float* hyre_frozen_embeddings(const hyre_frozen* f);     /* N x d */
 const uint64_t* hyre_frozen_signatures(const hyre_frozen* f);  /* N x words */
 const uint8_t* hyre_frozen_zero_flags(const hyre_frozen* f);   /* N */
-const char* hyre_frozen_doc_id(const hyre_frozen* f, uint32_t row);            /* doc_id() */
+/* doc_id(): for rows added in bulk (prefix + row) the string is generated into
+ * a thread-local buffer valid until this thread's next call; copy it. */
+const char* hyre_frozen_doc_id(const hyre_frozen* f, uint32_t row);
 int64_t hyre_frozen_row_of(const hyre_frozen* f, const char* doc_id);         /* row_of(), -1 */
 int32_t hyre_frozen_resolve_clause_slot(const hyre_frozen* f, const char* n); /* :103 */
 const char* hyre_frozen_clause_name(const hyre_frozen* f, uint32_t slot);

@@ -307,10 +307,20 @@ class IndexBuilder {
     return row;
   }
   std::size_t size() const { return hyre_builder_size(b_.get()); }
+  // corpus.hpp:47.  HYRE_FREEZE_DEVICE=<ordinal> runs the freeze on that GPU
+  // (bit-identical arrays) for a relinked caller without code changes.
   FrozenIndex freeze(const QuantCodec& codec) && {
+    if (const char* d = std::getenv("HYRE_FREEZE_DEVICE")) return std::move(*this).freeze_on_device(codec, std::atoi(d));
     if (codec.dim != dim_) throw ValidationError("codec dim != index dim");
     hyre_frozen* f = nullptr;
     detail::check(hyre_builder_freeze(b_.get(), codec.num_bits, codec.seed, &f));
+    return FrozenIndex(f);
+  }
+  // The freeze computed on GPU `device` (large builds; same arrays and errors).
+  FrozenIndex freeze_on_device(const QuantCodec& codec, int device) && {
+    if (codec.dim != dim_) throw ValidationError("codec dim != index dim");
+    hyre_frozen* f = nullptr;
+    detail::check(hyre_builder_freeze_device(b_.get(), codec.num_bits, codec.seed, device, &f));
     return FrozenIndex(f);
   }
 

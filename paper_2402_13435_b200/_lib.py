@@ -84,6 +84,7 @@ SIGNATURES = {
     "hyre_builder_add_documents": (C.c_int, [vp, C.c_uint32, C.c_char_p, u64p, u32p, f32p]),
     "hyre_builder_size": (C.c_uint32, [vp]),
     "hyre_builder_freeze": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.POINTER(vp)]),
+    "hyre_builder_freeze_device": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_int32, C.POINTER(vp)]),
     "hyre_frozen_from_arrays": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                           u32p, u32p, f32p, u64p, u8p, C.POINTER(C.c_char_p), C.c_char_p,
                                           C.POINTER(vp)]),

@@ -117,6 +117,15 @@ hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t see
   });
 }
 
+hyre_status hyre_builder_freeze_device(hyre_builder* b, uint32_t num_bits, uint64_t seed, int32_t device,
+                                       hyre_frozen** out) {
+  return guard([&] {
+    need(b, "builder");
+    need(out, "out");
+    *out = new hyre_frozen{std::unique_ptr<Frozen>(freeze_on_device(b->b, num_bits, seed, device))};
+  });
+}
+
 hyre_status hyre_frozen_from_arrays(uint32_t num_docs, uint32_t num_clauses, uint32_t max_num_attr,
                                     uint32_t dim, uint32_t num_bits, uint64_t seed,
                                     const uint32_t* attributes, const uint32_t* offsets,
@@ -163,9 +172,11 @@ hyre_status hyre_frozen_from_arrays(uint32_t num_docs, uint32_t num_clauses, uin
         f->zero[r] = z;
       }
     }
-    f->doc_ids.resize(n);
-    const std::string prefix = doc_id_prefix ? doc_id_prefix : "";
-    for (size_t r = 0; r < n; ++r) f->doc_ids[r] = doc_ids ? std::string(doc_ids[r]) : prefix + std::to_string(r);
+    if (doc_ids) {
+      for (size_t r = 0; r < n; ++r) f->doc_ids.push(doc_ids[r]);
+    } else {
+      f->doc_ids.push_range(doc_id_prefix ? doc_id_prefix : "", static_cast<uint32_t>(n));
+    }
     for (uint32_t c = 0; c < num_clauses; ++c) f->clause_names.push_back("c" + std::to_string(c));
     *out = new hyre_frozen{std::move(f)};
   });
@@ -205,7 +216,7 @@ const float* hyre_frozen_embeddings(const hyre_frozen* f) { return f->f->embeddi
 const uint64_t* hyre_frozen_signatures(const hyre_frozen* f) { return f->f->signatures.data(); }
 const uint8_t* hyre_frozen_zero_flags(const hyre_frozen* f) { return f->f->zero.data(); }
 const char* hyre_frozen_doc_id(const hyre_frozen* f, uint32_t row) {
-  return row < f->f->doc_ids.size() ? f->f->doc_ids[row].c_str() : nullptr;
+  return row < f->f->doc_ids.size() ? f->f->doc_ids.c_str(row) : nullptr;
 }
 int64_t hyre_frozen_row_of(const hyre_frozen* f, const char* doc_id) { return f->f->row_of(doc_id); }
 int32_t hyre_frozen_resolve_clause_slot(const hyre_frozen* f, const char* name) {

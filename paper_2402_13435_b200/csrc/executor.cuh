@@ -16,6 +16,8 @@
 namespace hyreb {
 
 DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o);
+// IndexBuilder::freeze on the GPU (freeze.cu): bit-identical host arrays.
+Frozen* freeze_on_device(Builder& b, uint32_t num_bits, uint64_t seed, int device);
 // Learned per-row weights of the index's own rows (n == n_rows, each in
 // [0, 1]); w == nullptr restores the identity (pure cosine).  Not to be
 // called while an executor of this index is running.

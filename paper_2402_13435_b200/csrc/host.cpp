@@ -107,7 +107,7 @@ Builder::Builder(uint32_t c, uint32_t a, uint32_t d, std::vector<std::string> na
 uint32_t Builder::add(const std::string& doc_id, uint32_t num_slots, const uint32_t* so,
                       const uint32_t* in_ids, const float* emb, uint32_t emb_len) {
   if (frozen) validation("builder already frozen");
-  if (seen.count(doc_id)) validation("duplicate docId: " + doc_id);
+  if (doc_ids.find(doc_id) >= 0) validation("duplicate docId: " + doc_id);
   if (num_slots != num_clauses)
     validation("clauses: expected " + std::to_string(num_clauses) + " clause slots, got " +
                std::to_string(num_slots));
@@ -117,9 +117,8 @@ uint32_t Builder::add(const std::string& doc_id, uint32_t num_slots, const uint3
     for (uint32_t i = so[c]; i < so[c + 1]; ++i)
       if (in_ids[i] == 0)
         validation("attribute id 0 is reserved for padding (docId " + doc_id + ")");
-  const auto row = static_cast<uint32_t>(doc_ids.size());
-  seen.emplace(doc_id, row);
-  doc_ids.push_back(doc_id);
+  const auto row = doc_ids.size();
+  doc_ids.push(doc_id);
   for (uint32_t c = 0; c < num_slots; ++c) {
     ids.insert(ids.end(), in_ids + so[c], in_ids + so[c + 1]);
     slot_offsets.push_back(ids.size());
@@ -132,25 +131,22 @@ void Builder::add_bulk(uint32_t n, const std::string& prefix, const uint64_t* so
                        const uint32_t* in_ids, const float* embs) {
   if (frozen) validation("builder already frozen");
   const uint64_t base = so[0];
-  // Validate everything before staging anything (all-or-nothing).
+  // Validate everything before staging anything (all-or-nothing), reporting
+  // the first offending row as the per-document loop would.
+  const uint32_t row0 = doc_ids.size();
+  const int64_t dup = doc_ids.first_collision(prefix, row0, n);
   for (uint32_t i = 0; i < n; ++i) {
-    const std::string id = prefix + std::to_string(doc_ids.size() + i);
-    if (seen.count(id)) validation("duplicate docId: " + id);
+    if (dup == int64_t{row0} + i) validation("duplicate docId: " + prefix + std::to_string(row0 + i));
     for (uint64_t j = so[size_t{i} * num_clauses]; j < so[size_t{i + 1} * num_clauses]; ++j)
       if (in_ids[j - base] == 0)
-        validation("attribute id 0 is reserved for padding (docId " + id + ")");
+        validation("attribute id 0 is reserved for padding (docId " + prefix + std::to_string(row0 + i) + ")");
   }
   const uint64_t shift = ids.size() - base;
   ids.insert(ids.end(), in_ids, in_ids + (so[size_t{n} * num_clauses] - base));
   slot_offsets.reserve(slot_offsets.size() + size_t{n} * num_clauses);
   for (size_t s = 1; s <= size_t{n} * num_clauses; ++s) slot_offsets.push_back(so[s] + shift);
   embeddings.insert(embeddings.end(), embs, embs + size_t{n} * dim);
-  seen.reserve(seen.size() + n);
-  for (uint32_t i = 0; i < n; ++i) {
-    const auto row = static_cast<uint32_t>(doc_ids.size());
-    doc_ids.push_back(prefix + std::to_string(row));
-    seen.emplace(doc_ids.back(), row);
-  }
+  doc_ids.push_range(prefix, n);
 }
 
 Frozen* Builder::freeze(uint32_t num_bits, uint64_t seed) {
@@ -215,7 +211,7 @@ Frozen* Builder::freeze(uint32_t num_bits, uint64_t seed) {
   });
   std::string too;
   for (uint32_t r = 0; r < n; ++r)
-    if (wide[r]) too += " " + doc_ids[r];
+    if (wide[r]) too += " " + doc_ids.at(r);
   if (!too.empty()) {
     delete f;
     validation("documents wider than maxNumAttr=" + std::to_string(A) + ":" + too);
@@ -225,18 +221,118 @@ Frozen* Builder::freeze(uint32_t num_bits, uint64_t seed) {
   std::vector<uint32_t>().swap(ids);
   std::vector<float>().swap(embeddings);
   std::vector<uint64_t>().swap(slot_offsets);
-  seen.clear();
   return f;
 }
 
-int64_t Frozen::row_of(const std::string& id) const {
-  if (!id_map_built) {
-    id_to_row.reserve(doc_ids.size());
-    for (uint32_t r = 0; r < doc_ids.size(); ++r) id_to_row.emplace(doc_ids[r], r);
-    id_map_built = true;
+int64_t Frozen::row_of(const std::string& id) const { return doc_ids.find(id); }
+
+// ---------------------------------------------------------------------------
+// DocIds
+// ---------------------------------------------------------------------------
+namespace {
+// value of a canonical decimal (no sign, no leading zero unless "0"), or -1
+int64_t parse_row(const std::string& s, size_t from) {
+  if (from >= s.size() || s.size() - from > 10) return -1;
+  if (s[from] == '0' && s.size() - from > 1) return -1;
+  int64_t v = 0;
+  for (size_t i = from; i < s.size(); ++i) {
+    if (s[i] < '0' || s[i] > '9') return -1;
+    v = v * 10 + (s[i] - '0');
   }
-  auto it = id_to_row.find(id);
-  return it == id_to_row.end() ? -1 : static_cast<int64_t>(it->second);
+  return v <= 0xFFFFFFFFll ? v : -1;
+}
+}  // namespace
+
+void DocIds::push(std::string id) {
+  if (segs_.empty() || segs_.back().range) segs_.push_back(Seg{n_, 0, false, {}, explicit_.size()});
+  explicit_.push_back(std::move(id));
+  ++segs_.back().count;
+  ++n_;
+}
+
+void DocIds::push_range(const std::string& prefix, uint32_t count) {
+  if (count == 0) return;
+  segs_.push_back(Seg{n_, count, true, prefix, 0});
+  n_ += count;
+}
+
+const DocIds::Seg& DocIds::seg_of(uint32_t row) const {
+  auto it = std::upper_bound(segs_.begin(), segs_.end(), row, [](uint32_t r, const Seg& s) { return r < s.row0; });
+  return *(it - 1);
+}
+
+std::string DocIds::at(uint32_t row) const {
+  const Seg& s = seg_of(row);
+  return s.range ? s.prefix + std::to_string(row) : explicit_[s.first + (row - s.row0)];
+}
+
+const char* DocIds::c_str(uint32_t row) const {
+  const Seg& s = seg_of(row);
+  if (!s.range) return explicit_[s.first + (row - s.row0)].c_str();
+  thread_local std::string buf;
+  buf = s.prefix + std::to_string(row);
+  return buf.c_str();
+}
+
+int64_t DocIds::find(const std::string& id) const {
+  for (const Seg& s : segs_) {  // ranges: prefix + canonical decimal row inside the range
+    if (!s.range || id.compare(0, s.prefix.size(), s.prefix) != 0) continue;
+    const int64_t r = parse_row(id, s.prefix.size());
+    if (r >= s.row0 && r < int64_t{s.row0} + s.count) return r;
+  }
+  if (explicit_.empty()) return -1;
+  if (mapped_ < explicit_.size()) {  // index the explicit ids added since the last lookup
+    size_t k = 0;
+    for (const Seg& s : segs_) {
+      if (s.range) continue;
+      for (uint32_t i = 0; i < s.count; ++i, ++k)
+        if (k >= mapped_) map_.emplace(explicit_[s.first + i], s.row0 + i);
+    }
+    mapped_ = explicit_.size();
+  }
+  auto it = map_.find(id);
+  return it == map_.end() ? -1 : static_cast<int64_t>(it->second);
+}
+
+int64_t DocIds::first_collision(const std::string& prefix, uint32_t row0, uint32_t count) const {
+  int64_t best = -1;
+  auto consider = [&](int64_t r) {
+    if (r >= row0 && r < int64_t{row0} + count && (best < 0 || r < best)) best = r;
+  };
+  for (const std::string& e : explicit_)  // explicit ids of the form prefix + row
+    if (e.compare(0, prefix.size(), prefix) == 0) consider(parse_row(e, prefix.size()));
+  for (const Seg& s : segs_) {
+    if (!s.range) continue;
+    // ids prefix + r (new) vs s.prefix + r' (existing): equal only if one
+    // prefix extends the other by digits.  Same prefix: rows differ.
+    if (s.prefix == prefix) continue;
+    const bool new_longer = prefix.size() > s.prefix.size();
+    const std::string& lo = new_longer ? s.prefix : prefix;
+    const std::string& hi = new_longer ? prefix : s.prefix;
+    if (hi.compare(0, lo.size(), lo) != 0) continue;
+    const std::string extra = hi.substr(lo.size());
+    if (extra.find_first_not_of("0123456789") != std::string::npos || extra[0] == '0') continue;
+    if (new_longer) {  // new id = lo + extra + r; an existing row r' = extra + r
+      for (uint32_t i = 0; i < count; ++i) {
+        const int64_t rp = parse_row(extra + std::to_string(row0 + i), 0);
+        if (rp >= s.row0 && rp < int64_t{s.row0} + s.count) {
+          consider(row0 + i);
+          break;
+        }
+      }
+    } else {  // existing id = lo + extra + r'; a new row r = extra + r'
+      for (uint32_t i = 0; i < s.count; ++i) consider(parse_row(extra + std::to_string(s.row0 + i), 0));
+    }
+  }
+  return best;
+}
+
+void DocIds::clear() {
+  segs_.clear();
+  explicit_.clear();
+  map_.clear();
+  mapped_ = 0;
+  n_ = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -349,7 +445,7 @@ void save(const Frozen& f, const std::string& path) {
   w.vec(f.embeddings);
   w.vec(f.signatures);
   w.vec(f.zero);
-  for (const auto& s : f.doc_ids) w.str(s);
+  for (uint32_t r = 0; r < f.num_docs; ++r) w.str(f.doc_ids.at(r));
   for (const auto& s : f.clause_names) w.str(s);
   w.finish();
 }
@@ -378,8 +474,7 @@ Frozen* load(const std::string& path) {
   r.vec(f->embeddings, n * f->dim);
   r.vec(f->signatures, n * f->num_words());
   r.vec(f->zero, n);
-  f->doc_ids.reserve(n);
-  for (size_t i = 0; i < n; ++i) f->doc_ids.push_back(r.str());
+  for (size_t i = 0; i < n; ++i) f->doc_ids.push(r.str());
   for (uint32_t c = 0; c < f->num_clauses; ++c) f->clause_names.push_back(r.str());
   r.verify();
   return f.release();

@@ -47,6 +47,40 @@ uint32_t quant_score_words(const uint64_t* a, const uint64_t* b, size_t words,
                            uint32_t num_bits);
 
 // ---------------------------------------------------------------------------
+// Row -> docId (corpus.hpp:100-101).  Explicitly added ids are stored as
+// strings; a bulk add (prefix + decimal row number, the synthetic and
+// `hyre build --prefix` case) is one range whose ids are generated on demand,
+// so a 50M-row build keeps no 50M strings and no 50M-entry hash map.
+// ---------------------------------------------------------------------------
+class DocIds {
+ public:
+  uint32_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  void push(std::string id);                           // explicit id of row size()
+  void push_range(const std::string& prefix, uint32_t count);  // rows size() ..: prefix + row
+  std::string at(uint32_t row) const;
+  const char* c_str(uint32_t row) const;  // thread-local copy for range rows
+  int64_t find(const std::string& id) const;  // row or -1
+  // smallest row r in [row0, row0 + count) whose id prefix + r already exists, or -1
+  int64_t first_collision(const std::string& prefix, uint32_t row0, uint32_t count) const;
+  void clear();
+
+ private:
+  struct Seg {
+    uint32_t row0, count;
+    bool range;
+    std::string prefix;  // range
+    size_t first;        // explicit: index of row0's id in explicit_
+  };
+  const Seg& seg_of(uint32_t row) const;
+  std::vector<Seg> segs_;
+  std::vector<std::string> explicit_;
+  uint32_t n_ = 0;
+  mutable std::unordered_map<std::string, uint32_t> map_;  // explicit ids, built lazily
+  mutable size_t mapped_ = 0;                              // explicit ids already in map_
+};
+
+// ---------------------------------------------------------------------------
 // FrozenIndex host arrays: corpus.hpp:57-124.
 // ---------------------------------------------------------------------------
 struct Frozen {
@@ -58,9 +92,7 @@ struct Frozen {
   std::vector<float> embeddings;      // N x d
   std::vector<uint64_t> signatures;   // N x words
   std::vector<uint8_t> zero;          // N
-  std::vector<std::string> doc_ids;   // N
-  mutable std::unordered_map<std::string, uint32_t> id_to_row;  // built lazily
-  mutable bool id_map_built = false;
+  DocIds doc_ids;                     // N
 
   size_t num_words() const { return (num_bits + 63) / 64; }
   int64_t row_of(const std::string& id) const;
@@ -72,8 +104,7 @@ struct Builder {
   std::vector<uint64_t> slot_offsets{0};  // (docs * C) + 1
   std::vector<uint32_t> ids;
   std::vector<float> embeddings;
-  std::vector<std::string> doc_ids;
-  std::unordered_map<std::string, uint32_t> seen;
+  DocIds doc_ids;
   bool frozen = false;
 
   Builder(uint32_t c, uint32_t a, uint32_t d, std::vector<std::string> names);
@@ -82,7 +113,7 @@ struct Builder {
   void add_bulk(uint32_t n, const std::string& prefix, const uint64_t* slot_offsets,
                 const uint32_t* ids, const float* embs);
   Frozen* freeze(uint32_t num_bits, uint64_t seed);
-  uint32_t size() const { return static_cast<uint32_t>(doc_ids.size()); }
+  uint32_t size() const { return doc_ids.size(); }
 };
 
 void save(const Frozen& f, const std::string& path);

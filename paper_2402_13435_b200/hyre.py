@@ -199,11 +199,16 @@ class IndexBuilder:
     def size(self) -> int:
         return int(L.lib().hyre_builder_size(self._h))
 
-    def freeze(self, codec: QuantCodec) -> "FrozenIndex":
+    def freeze(self, codec: QuantCodec, device: Optional[int] = None) -> "FrozenIndex":
+        """corpus.cpp:54-129; device=<ordinal> computes it on that GPU
+        (bit-identical arrays, same errors) -- for large builds."""
         if codec.dim != self._dim:
             raise ValidationError("codec dim != index dim")
         h = C.c_void_p()
-        _check(L.lib().hyre_builder_freeze(self._h, codec.num_bits, codec.seed, C.byref(h)))
+        if device is None:
+            _check(L.lib().hyre_builder_freeze(self._h, codec.num_bits, codec.seed, C.byref(h)))
+        else:
+            _check(L.lib().hyre_builder_freeze_device(self._h, codec.num_bits, codec.seed, int(device), C.byref(h)))
         return FrozenIndex(h)
 
 

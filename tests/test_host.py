@@ -268,3 +268,30 @@ def test_merge_topk_is_exact():
     merged = hy.merge_topk(lists, 50)
     er, es = O.top_k(np.concatenate(allrows), np.concatenate(allsc), 50)
     assert merged["row"].tolist() == er.tolist()
+
+
+def _bulk(b, n, prefix, dim=2):
+    so = np.arange(n + 1, dtype=np.uint64)  # one slot, one id per row
+    b.add_documents(so, np.ones(n, np.uint32), np.ones((n, dim), np.float32), doc_id_prefix=prefix)
+
+
+def test_bulk_doc_ids_are_ranges_with_reference_duplicate_semantics(tmp_path):
+    # corpus.cpp:29-52: a docId may appear once; bulk rows carry prefix + row
+    b = hy.IndexBuilder(hy.IndexConfig(1, 1, 2))
+    _bulk(b, 5, "d")                                   # d0 .. d4
+    with pytest.raises(hy.ValidationError, match="duplicate docId: d3"):
+        b.add_document(hy.DocumentInput("d3", [[1]], [1.0, 0.0]))
+    b.add_document(hy.DocumentInput("d03", [[1]], [1.0, 0.0]))  # not canonical: a distinct id (row 5)
+    b.add_document(hy.DocumentInput("x9", [[1]], [1.0, 0.0]))   # row 6
+    with pytest.raises(hy.ValidationError, match="duplicate docId: x9"):
+        _bulk(b, 5, "x")                               # x7 .. x11 would repeat x9
+    _bulk(b, 4, "d1")                                  # d17 .. d110 (rows 7 .. 10)
+    with pytest.raises(hy.ValidationError, match="duplicate docId: d17"):
+        _bulk(b, 10, "d")                              # rows 11 .. 20: d17? no -- d11 .. d20 vs d1+7 = d17
+    f = b.freeze(hy.make_codec(2, 16, 1))
+    assert [f.doc_id(r) for r in (0, 4, 5, 6, 7, 10)] == ["d0", "d4", "d03", "x9", "d17", "d110"]
+    assert f.row_of("d110") == 10 and f.row_of("d03") == 5 and f.row_of("x9") == 6 and f.row_of("d5") is None
+    p = str(tmp_path / "ids.bin")
+    f.save(p)
+    g = hy.FrozenIndex.load(p)
+    assert [g.doc_id(r) for r in range(11)] == [f.doc_id(r) for r in range(11)] and g.row_of("d17") == 7

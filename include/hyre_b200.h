@@ -94,6 +94,42 @@ hyre_status hyre_builder_add_documents(hyre_builder* b, uint32_t n, const char* 
                                        const float* embeddings);
 uint32_t hyre_builder_size(const hyre_builder* b);
 
+/* ---- ingestion (dataio.hpp:15-28; host C++, csrc/ingest.cpp) ----------------
+ * read_schema_json (dataio.cpp:118-140): {"clauses": ["geo", ...], "dim": 4}. */
+typedef struct hyre_schema hyre_schema;
+hyre_status hyre_schema_read_json(const char* path, hyre_schema** out);
+hyre_status hyre_schema_create(uint32_t n_clauses, const char* const* clause_names, uint32_t dim,
+                               hyre_schema** out);
+void hyre_schema_destroy(hyre_schema* s);
+uint32_t hyre_schema_num_clauses(const hyre_schema* s);
+const char* hyre_schema_clause_name(const hyre_schema* s, uint32_t i);
+uint32_t hyre_schema_dim(const hyre_schema* s);
+/* read_documents_jsonl (dataio.cpp:142-187): the documents of a JSONL corpus in
+ * file order, flat: slot_offsets (count x C + 1) into ids, embeddings count x dim;
+ * widest = the largest per-document count of distinct ids (hyre build's
+ * maxNumAttr, cli_commands.cpp:37-63).  Errors: "<path>:<line>: <what>". */
+typedef struct hyre_documents hyre_documents;
+hyre_status hyre_documents_read_jsonl(const char* path, const hyre_schema* s, hyre_documents** out);
+void hyre_documents_destroy(hyre_documents* d);
+uint32_t hyre_documents_count(const hyre_documents* d);
+uint32_t hyre_documents_widest(const hyre_documents* d);
+const char* hyre_documents_id(const hyre_documents* d, uint32_t i);
+const uint64_t* hyre_documents_slot_offsets(const hyre_documents* d);
+const uint32_t* hyre_documents_ids(const hyre_documents* d);
+const float* hyre_documents_embeddings(const hyre_documents* d);
+/* add_document (corpus.cpp:29-52) for every document of the set, in order. */
+hyre_status hyre_builder_add_document_set(hyre_builder* b, const hyre_documents* d, uint32_t* first_row);
+/* The learned-link serving-graph export (write_links_export, dataio.cpp:253-274):
+ * side 0 = seekerAttributes, 1 = jobAttributes; names in key order, node ids
+ * (the config-5 term vocabulary, link_learner.cpp:327-347) sorted, unique. */
+typedef struct hyre_links hyre_links;
+hyre_status hyre_links_read_json(const char* path, hyre_links** out);
+void hyre_links_destroy(hyre_links* l);
+uint32_t hyre_links_num_nodes(const hyre_links* l);
+uint32_t hyre_links_count(const hyre_links* l, int32_t side);
+const char* hyre_links_name(const hyre_links* l, int32_t side, uint32_t i);
+const uint32_t* hyre_links_ids(const hyre_links* l, int32_t side, uint32_t i, uint32_t* n);
+
 /* std::move(builder).freeze(make_codec(dim, num_bits, seed)) -- corpus.hpp:47,
  * corpus.cpp:54-129.  The builder is consumed (further calls fail). */
 hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t seed,
@@ -289,6 +325,9 @@ uint32_t hyre_batch_path(const hyre_executor* ex);
  * fused), bytes per id (1 = u8, 2 = u16), query chunks per CNF thread,
  * queries per MMA group (Np)}; all zero when the batch runs on K2. */
 void hyre_batch_tc_variant(const hyre_executor* ex, uint32_t* out4);
+/* Fused CNF row layout of the prepared batch: W > 0 = slot-grouped rows (W ids
+ * per slot group, no masks), 0 = segmented rows + masks (or not fused). */
+uint32_t hyre_batch_cnf_group(const hyre_executor* ex);
 /* Eligible-row counts of the last run (u32[b], waits for it): the CNF
  * matches per query; 0xFFFFFFFF where the CNF ran fused inside K3 (the count
  * is never materialised there).  Diagnostics for benchmarks and tests. */

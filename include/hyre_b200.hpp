@@ -307,6 +307,7 @@ class IndexBuilder {
     return row;
   }
   std::size_t size() const { return hyre_builder_size(b_.get()); }
+  hyre_builder* handle() const { return b_.get(); }
   // corpus.hpp:47.  HYRE_FREEZE_DEVICE=<ordinal> runs the freeze on that GPU
   // (bit-identical arrays) for a relinked caller without code changes.
   FrozenIndex freeze(const QuantCodec& codec) && {
@@ -331,6 +332,98 @@ class IndexBuilder {
   std::unique_ptr<hyre_builder, Del> b_;
   std::uint32_t dim_;
 };
+
+// ---- dataio.hpp (ingestion; host C++ in the library) ------------------------------
+struct IngestSchema {
+  std::vector<std::string> clause_names;
+  std::uint32_t dim = 0;
+};
+
+// {"clauses": ["geo", "skill"], "dim": 4}  (dataio.hpp:20-21)
+inline IngestSchema read_schema_json(const std::string& path) {
+  hyre_schema* s = nullptr;
+  detail::check(hyre_schema_read_json(path.c_str(), &s));
+  IngestSchema out;
+  for (std::uint32_t i = 0; i < hyre_schema_num_clauses(s); ++i) out.clause_names.emplace_back(hyre_schema_clause_name(s, i));
+  out.dim = hyre_schema_dim(s);
+  hyre_schema_destroy(s);
+  return out;
+}
+
+namespace detail {
+struct DocSet {  // a parsed JSONL corpus held by the library
+  DocSet(const std::string& path, const IngestSchema& schema) {
+    std::vector<const char*> names;
+    for (const auto& n : schema.clause_names) names.push_back(n.c_str());
+    hyre_schema* s = nullptr;
+    check(hyre_schema_create(static_cast<std::uint32_t>(names.size()), names.data(), schema.dim, &s));
+    const hyre_status st = hyre_documents_read_jsonl(path.c_str(), s, &d);
+    hyre_schema_destroy(s);
+    check(st);
+  }
+  ~DocSet() { hyre_documents_destroy(d); }
+  DocSet(const DocSet&) = delete;
+  DocSet& operator=(const DocSet&) = delete;
+  hyre_documents* d = nullptr;
+};
+}  // namespace detail
+
+// One document per line (dataio.hpp:23-28):
+//   {"id": "doc1", "clauses": {"geo": [934]}, "embedding": [0.1, ...]}
+inline std::vector<DocumentInput> read_documents_jsonl(const std::string& path, const IngestSchema& schema) {
+  detail::DocSet ds(path, schema);
+  const std::uint32_t n = hyre_documents_count(ds.d), C = static_cast<std::uint32_t>(schema.clause_names.size());
+  const std::uint64_t* so = hyre_documents_slot_offsets(ds.d);
+  const std::uint32_t* ids = hyre_documents_ids(ds.d);
+  const float* emb = hyre_documents_embeddings(ds.d);
+  std::vector<DocumentInput> out(n);
+  for (std::uint32_t i = 0; i < n; ++i) {
+    out[i].doc_id = hyre_documents_id(ds.d, i);
+    out[i].clauses.resize(C);
+    for (std::uint32_t c = 0; c < C; ++c) out[i].clauses[c].assign(ids + so[i * C + c], ids + so[i * C + c + 1]);
+    out[i].embedding.assign(emb + std::size_t{i} * schema.dim, emb + std::size_t{i + 1} * schema.dim);
+  }
+  return out;
+}
+
+// `hyre build` (cli_commands.cpp:37-63) in the library: IndexConfig from the
+// schema, maxNumAttr = the widest document, every document staged in file
+// order, frozen with make_codec(dim, num_bits, seed) -- on GPU `freeze_device`
+// when >= 0 (bit-identical arrays).
+inline FrozenIndex build_index_jsonl(const std::string& schema_path, const std::string& corpus_path,
+                                     std::uint32_t num_bits = 512, std::uint64_t seed = 1, int freeze_device = -1) {
+  const IngestSchema schema = read_schema_json(schema_path);
+  detail::DocSet ds(corpus_path, schema);
+  if (hyre_documents_count(ds.d) == 0) throw ValidationError("no documents");
+  IndexBuilder b(IndexConfig{static_cast<std::uint32_t>(schema.clause_names.size()),
+                             std::max<std::uint32_t>(1, hyre_documents_widest(ds.d)), schema.dim, schema.clause_names});
+  detail::check(hyre_builder_add_document_set(b.handle(), ds.d, nullptr));
+  const QuantCodec codec = make_codec(schema.dim, num_bits, seed);
+  return freeze_device >= 0 ? std::move(b).freeze_on_device(codec, freeze_device) : std::move(b).freeze(codec);
+}
+
+// The learned-link serving-graph export (write_links_export, dataio.cpp:253-274)
+// read back as the config-5 vocabulary: node ids per seeker / job.
+struct LinksExport {
+  std::uint32_t num_nodes = 0;
+  std::map<std::string, std::vector<std::uint32_t>> seeker_attributes, job_attributes;
+};
+inline LinksExport read_links_export(const std::string& path) {
+  hyre_links* l = nullptr;
+  detail::check(hyre_links_read_json(path.c_str(), &l));
+  LinksExport out;
+  out.num_nodes = hyre_links_num_nodes(l);
+  for (int side = 0; side < 2; ++side) {
+    auto& dst = side == 0 ? out.seeker_attributes : out.job_attributes;
+    for (std::uint32_t i = 0; i < hyre_links_count(l, side); ++i) {
+      std::uint32_t n = 0;
+      const std::uint32_t* ids = hyre_links_ids(l, side, i, &n);
+      dst[hyre_links_name(l, side, i)].assign(ids, ids + n);
+    }
+  }
+  hyre_links_destroy(l);
+  return out;
+}
 
 // ---- term_match.hpp -------------------------------------------------------------
 struct CnfClause {

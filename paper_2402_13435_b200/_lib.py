@@ -83,6 +83,27 @@ SIGNATURES = {
     "hyre_builder_add_document": (C.c_int, [vp, C.c_char_p, C.c_uint32, u32p, u32p, f32p, C.c_uint32, u32p]),
     "hyre_builder_add_documents": (C.c_int, [vp, C.c_uint32, C.c_char_p, u64p, u32p, f32p]),
     "hyre_builder_size": (C.c_uint32, [vp]),
+    "hyre_schema_read_json": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "hyre_schema_create": (C.c_int, [C.c_uint32, C.POINTER(C.c_char_p), C.c_uint32, C.POINTER(vp)]),
+    "hyre_schema_destroy": (None, [vp]),
+    "hyre_schema_num_clauses": (C.c_uint32, [vp]),
+    "hyre_schema_clause_name": (C.c_char_p, [vp, C.c_uint32]),
+    "hyre_schema_dim": (C.c_uint32, [vp]),
+    "hyre_documents_read_jsonl": (C.c_int, [C.c_char_p, vp, C.POINTER(vp)]),
+    "hyre_documents_destroy": (None, [vp]),
+    "hyre_documents_count": (C.c_uint32, [vp]),
+    "hyre_documents_widest": (C.c_uint32, [vp]),
+    "hyre_documents_id": (C.c_char_p, [vp, C.c_uint32]),
+    "hyre_documents_slot_offsets": (u64p, [vp]),
+    "hyre_documents_ids": (u32p, [vp]),
+    "hyre_documents_embeddings": (f32p, [vp]),
+    "hyre_builder_add_document_set": (C.c_int, [vp, vp, u32p]),
+    "hyre_links_read_json": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "hyre_links_destroy": (None, [vp]),
+    "hyre_links_num_nodes": (C.c_uint32, [vp]),
+    "hyre_links_count": (C.c_uint32, [vp, C.c_int32]),
+    "hyre_links_name": (C.c_char_p, [vp, C.c_int32, C.c_uint32]),
+    "hyre_links_ids": (u32p, [vp, C.c_int32, C.c_uint32, u32p]),
     "hyre_builder_freeze": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.POINTER(vp)]),
     "hyre_builder_freeze_device": (C.c_int, [vp, C.c_uint32, C.c_uint64, C.c_int32, C.POINTER(vp)]),
     "hyre_frozen_from_arrays": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
@@ -122,6 +143,7 @@ SIGNATURES = {
     "hyre_batch_fetch": (C.c_int, [vp, C.POINTER(hyre_hit), u64p, u32p, i32p, C.POINTER(hyre_timings)]),
     "hyre_batch_kernel_count": (C.c_uint32, [vp]),
     "hyre_batch_path": (C.c_uint32, [vp]),
+    "hyre_batch_cnf_group": (C.c_uint32, [vp]),
     "hyre_batch_tc_variant": (None, [vp, u32p]),
     "hyre_batch_recovery": (C.c_int, [vp, u32p]),
     "hyre_sharded_index_create": (C.c_int, [vp, C.POINTER(hyre_sharded_index_options), C.POINTER(vp)]),

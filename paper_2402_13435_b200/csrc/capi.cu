@@ -26,6 +26,15 @@ struct hyre_index {
 struct hyre_executor {
   std::unique_ptr<Executor> ex;
 };
+struct hyre_schema {
+  Schema s;
+};
+struct hyre_documents {
+  DocumentSet d;
+};
+struct hyre_links {
+  LinksExport l;
+};
 struct hyre_pool {
   std::unique_ptr<Pool> p;
 };
@@ -108,6 +117,89 @@ hyre_status hyre_builder_add_documents(hyre_builder* b, uint32_t n, const char* 
 }
 
 uint32_t hyre_builder_size(const hyre_builder* b) { return b ? b->b.size() : 0; }
+
+// ---- ingestion (ingest.cpp; dataio.hpp:15-28) -----------------------------------
+hyre_status hyre_schema_read_json(const char* path, hyre_schema** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = new hyre_schema{read_schema_json(path)};
+  });
+}
+hyre_status hyre_schema_create(uint32_t n, const char* const* names, uint32_t dim, hyre_schema** out) {
+  return guard([&] {
+    need(out, "out");
+    if (n && !names) validation("schema: clause names required");
+    Schema s;
+    for (uint32_t i = 0; i < n; ++i) s.clause_names.emplace_back(names[i]);
+    s.dim = dim;
+    *out = new hyre_schema{std::move(s)};
+  });
+}
+void hyre_schema_destroy(hyre_schema* s) { delete s; }
+uint32_t hyre_schema_num_clauses(const hyre_schema* s) { return s ? static_cast<uint32_t>(s->s.clause_names.size()) : 0; }
+const char* hyre_schema_clause_name(const hyre_schema* s, uint32_t i) {
+  return s && i < s->s.clause_names.size() ? s->s.clause_names[i].c_str() : nullptr;
+}
+uint32_t hyre_schema_dim(const hyre_schema* s) { return s ? s->s.dim : 0; }
+
+hyre_status hyre_documents_read_jsonl(const char* path, const hyre_schema* s, hyre_documents** out) {
+  return guard([&] {
+    need(path, "path");
+    need(s, "schema");
+    need(out, "out");
+    *out = new hyre_documents{read_documents_jsonl(path, s->s)};
+  });
+}
+void hyre_documents_destroy(hyre_documents* d) { delete d; }
+uint32_t hyre_documents_count(const hyre_documents* d) { return d ? static_cast<uint32_t>(d->d.doc_ids.size()) : 0; }
+uint32_t hyre_documents_widest(const hyre_documents* d) { return d ? d->d.widest : 0; }
+const char* hyre_documents_id(const hyre_documents* d, uint32_t i) {
+  return d && i < d->d.doc_ids.size() ? d->d.doc_ids[i].c_str() : nullptr;
+}
+const uint64_t* hyre_documents_slot_offsets(const hyre_documents* d) { return d ? d->d.slot_offsets.data() : nullptr; }
+const uint32_t* hyre_documents_ids(const hyre_documents* d) { return d ? d->d.ids.data() : nullptr; }
+const float* hyre_documents_embeddings(const hyre_documents* d) { return d ? d->d.embeddings.data() : nullptr; }
+
+hyre_status hyre_builder_add_document_set(hyre_builder* b, const hyre_documents* ds, uint32_t* first_row) {
+  return guard([&] {
+    need(b, "builder");
+    need(ds, "documents");
+    const DocumentSet& d = ds->d;
+    if (first_row) *first_row = b->b.size();
+    std::vector<uint32_t> so(d.num_clauses + 1);
+    for (size_t i = 0; i < d.doc_ids.size(); ++i) {  // add_document semantics and messages, file order
+      const uint64_t base = d.slot_offsets[i * d.num_clauses];
+      for (uint32_t c = 0; c <= d.num_clauses; ++c)
+        so[c] = static_cast<uint32_t>(d.slot_offsets[i * d.num_clauses + c] - base);
+      b->b.add(d.doc_ids[i], d.num_clauses, so.data(), d.ids.data() + base, d.embeddings.data() + i * d.dim, d.dim);
+    }
+  });
+}
+
+hyre_status hyre_links_read_json(const char* path, hyre_links** out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    *out = new hyre_links{read_links_export(path)};
+  });
+}
+void hyre_links_destroy(hyre_links* l) { delete l; }
+uint32_t hyre_links_num_nodes(const hyre_links* l) { return l ? l->l.num_nodes : 0; }
+uint32_t hyre_links_count(const hyre_links* l, int32_t side) {
+  return l && (side == 0 || side == 1) ? static_cast<uint32_t>(l->l.names[side].size()) : 0;
+}
+const char* hyre_links_name(const hyre_links* l, int32_t side, uint32_t i) {
+  return hyre_links_count(l, side) > i ? l->l.names[side][i].c_str() : nullptr;
+}
+const uint32_t* hyre_links_ids(const hyre_links* l, int32_t side, uint32_t i, uint32_t* n) {
+  if (hyre_links_count(l, side) <= i) {
+    if (n) *n = 0;
+    return nullptr;
+  }
+  if (n) *n = static_cast<uint32_t>(l->l.ids[side][i].size());
+  return l->l.ids[side][i].data();
+}
 
 hyre_status hyre_builder_freeze(hyre_builder* b, uint32_t num_bits, uint64_t seed, hyre_frozen** out) {
   return guard([&] {
@@ -547,6 +639,10 @@ uint32_t hyre_batch_path(const hyre_executor* ex) {
          (e->use_fwd && !e->use_fused && !e->all_match ? HYRE_PATH_FWD_MASK : 0u) |
          (e->all_match ? HYRE_PATH_MATCH_ALL : 0u) | (e->pf_i8 ? HYRE_PATH_I8 : 0u) |
          (e->any_emb && e->ix->n_rows > e->cap ? HYRE_PATH_SAMPLED : 0u);
+}
+
+uint32_t hyre_batch_cnf_group(const hyre_executor* ex) {
+  return ex && ex->ex->use_fused ? ex->ex->ix->cnf_group : 0u;
 }
 
 void hyre_batch_tc_variant(const hyre_executor* ex, uint32_t* out4) {

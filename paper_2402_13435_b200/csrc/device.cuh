@@ -192,6 +192,11 @@ struct DevIndex {
   uint8_t* cnf_ids = nullptr;
   uint64_t* cnf_masks = nullptr;
   uint32_t cnf_id_bytes = 0, cnf_ids_per_row = 0, cnf_row_bytes = 0;
+  // Slot-grouped rows (cnf_group = W > 0, u8 ids, no masks): group g of W ids
+  // = slot g's ids, PAD 0xFF, EMPTY_g = T + g for an empty slot, NONE 0xFE
+  // leading the groups beyond the C slots (index.cu cnf_group_rows_kernel).
+  uint32_t cnf_group = 0;
+  uint64_t cnf_row_total() const { return cnf_row_bytes + (cnf_masks ? 8u : 0u); }  // HBM bytes per row
   // Learned per-row weights (north star: "learned link/attribute weights
   // applied in the epilogue"): score = w[r] x clamp(dot), w in [0, 1], local
   // rows; nullptr = identity (the reference's pure cosine, knn.cpp:36-37).

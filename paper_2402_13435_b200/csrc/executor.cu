@@ -554,7 +554,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // eligibility input bytes: distinct bitmaps W*4 each, CSR
   // postings 4 each; the forward lists N*A*2 once per pass on the fwd/fused paths
   if (use_fused)
-    term_bytes = size_t{ix->n_rows} * (ix->cnf_row_bytes + 8) * tc_groups;  // compact CNF rows per group pass
+    term_bytes = size_t{ix->n_rows} * ix->cnf_row_total() * tc_groups;  // compact CNF rows per group pass
   else if (use_fwd)
     term_bytes = size_t{ix->n_rows} * ix->row_terms_width * 2 * fwd_pass.size();
   else
@@ -567,7 +567,7 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   if (use_tc) {
     const uint64_t emb = uint64_t{ix->n_rows} * ix->dp * (pf_i8 ? 1 : 2 * tc_load_ops());
     const uint64_t elig = all_match ? 0
-                          : use_fused ? uint64_t{ix->n_rows} * (ix->cnf_row_bytes + 8)
+                          : use_fused ? uint64_t{ix->n_rows} * ix->cnf_row_total()
                                       : uint64_t{ix->words} * 4 * tc_np;
     scan_bytes = (emb + elig) * tc_groups;
   }
@@ -641,6 +641,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
         ta.J = ix->cnf_ids_per_row;
         ta.tb = ix->cnf_id_bytes;
         ta.wb = ix->cnf_row_bytes;
+        ta.W = ix->cnf_group;
         ta.T = ix->n_terms_fwd;
         ta.C = ix->num_clauses;
         ta.fz = d_fz + fg.entries;
@@ -731,7 +732,7 @@ void Executor::plan_tc() {
 }
 
 size_t Executor::tc_fz_bytes(uint32_t slots) const {
-  return tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, ix->cnf_row_bytes, slots);
+  return tc_fused_bytes(tc_np, ix->n_terms_fwd, ix->num_clauses, static_cast<uint32_t>(ix->cnf_row_total()), slots);
 }
 
 // Final K4 after a main / rerun pass: the prefilter variant (prune, exact

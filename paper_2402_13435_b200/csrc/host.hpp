@@ -116,6 +116,29 @@ struct Builder {
   uint32_t size() const { return doc_ids.size(); }
 };
 
+// ---------------------------------------------------------------------------
+// Ingestion (ingest.cpp): dataio.hpp:15-28 and the links export.
+// ---------------------------------------------------------------------------
+struct Schema {  // IngestSchema (dataio.hpp:15-18)
+  std::vector<std::string> clause_names;
+  uint32_t dim = 0;
+};
+struct DocumentSet {  // read_documents_jsonl's documents, flat (file order)
+  uint32_t num_clauses = 0, dim = 0, widest = 0;  // widest: max distinct ids of a document
+  std::vector<std::string> doc_ids;
+  std::vector<uint64_t> slot_offsets;  // docs x C + 1
+  std::vector<uint32_t> ids;
+  std::vector<float> embeddings;  // docs x dim
+};
+struct LinksExport {  // serving-graph export (dataio.cpp:253-274)
+  uint32_t num_nodes = 0;
+  std::vector<std::string> names[2];           // [0] seekers, [1] jobs (key order)
+  std::vector<std::vector<uint32_t>> ids[2];  // node ids, sorted unique
+};
+Schema read_schema_json(const std::string& path);
+DocumentSet read_documents_jsonl(const std::string& path, const Schema& schema);
+LinksExport read_links_export(const std::string& path);
+
 void save(const Frozen& f, const std::string& path);
 Frozen* load(const std::string& path);
 

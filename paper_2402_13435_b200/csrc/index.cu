@@ -97,6 +97,50 @@ __global__ void cnf_rows_kernel(const uint16_t* row_terms, const uint8_t* slot_o
   }
 }
 
+// HYRE_CNF_GROUPED=0 keeps the segmented CNF rows (A/B measurements).
+bool cnf_grouped_enabled() {
+  const char* e = std::getenv("HYRE_CNF_GROUPED");
+  return !(e && std::string(e) == "0");
+}
+
+// Largest number of ids any row holds in one slot (the slot-grouped layout's
+// group width W).
+__global__ void slot_width_kernel(const uint16_t* row_terms, const uint8_t* slot_of, uint32_t n, uint32_t A,
+                                  uint32_t* out) {
+  uint32_t mx = 0;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint16_t* src = row_terms + static_cast<size_t>(r) * A;
+    uint32_t run = 0, prev = 0xFFFFFFFFu;
+    for (uint32_t j = 0; j < A && src[j] != 0xFFFFu; ++j) {
+      const uint32_t sl = slot_of[src[j]];
+      run = sl == prev ? run + 1 : 1;
+      prev = sl;
+      mx = max(mx, run);
+    }
+  }
+  atomicMax(out, mx);
+}
+
+// Slot-grouped compact CNF rows (u8 ids): group g (W ids) holds slot g's term
+// ids padded with PAD (0xFF: the AND identity), EMPTY_g (T + g: every query
+// constraining g fails) when the row has no id in slot g, and NONE (0xFE: no
+// constraint) as the first id of the groups beyond the C slots.  The segment
+// structure is then static: fail = OR over groups of AND over the group.
+__global__ void cnf_group_rows_kernel(const uint16_t* row_terms, const uint8_t* slot_of, uint32_t n, uint32_t A,
+                                      uint32_t C, uint32_t T, uint32_t W, uint32_t G, uint32_t wb, uint8_t* ids) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const uint16_t* src = row_terms + static_cast<size_t>(r) * A;
+    uint8_t* dst = ids + static_cast<size_t>(r) * wb;
+    uint32_t j = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+      uint32_t k = 0;
+      while (g < C && j < A && src[j] != 0xFFFFu && slot_of[src[j]] == g) dst[g * W + k++] = static_cast<uint8_t>(src[j++]);
+      if (k == 0) dst[g * W + k++] = static_cast<uint8_t>(g < C ? T + g : 0xFEu);
+      for (; k < W; ++k) dst[g * W + k] = 0xFFu;
+    }
+  }
+}
+
 __global__ void slot_of_kernel(const uint64_t* uniq, uint32_t T, uint8_t* slot_of) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
     slot_of[t] = static_cast<uint8_t>(uniq[t] >> 32);
@@ -433,21 +477,40 @@ DevIndex* build_device_index(const Frozen& f, const hyre_index_options& o) {
         const uint32_t tb = T <= 255 ? 1u : 2u;
         uint32_t jw = A <= 8 ? 8u : (A <= 16 ? 16u : (A <= 24 ? 24u : 32u));
         if (tb == 2 && jw % 16) jw += 8;  // u16 variants: 16 or 32 ids
-        uint32_t wb = jw * tb;
+        // Slot-grouped layout (u8 ids, C <= 8 slots of <= 4 ids): J = W x G
+        // with G = 4 or 8 groups; no per-row masks.  Preferred when it is no
+        // wider than the segmented row + its 8-byte masks.
+        uint32_t W = 0, G = 8;
+        if (tb == 1 && C <= 8 && T + C <= 0xFEu && cnf_grouped_enabled()) {
+          DPtr<uint32_t> d_w(dmalloc<uint32_t>(1));
+          HYRE_CUDA(cudaMemset(d_w.get(), 0, 4));
+          slot_width_kernel<<<blocks, 256>>>(ix->row_terms, ix->slot_of, n, Ap, d_w.get());
+          HYRE_CUDA(cudaMemcpy(&W, d_w.get(), 4, cudaMemcpyDeviceToHost));
+          W = std::max(W, 1u);
+          if (C <= 4 && W >= 2) G = 4;  // K3 instantiates J = W x G in {8, 8|16, 12|24, 16|32}
+          if (W > 4 || W * G > jw + 8 || W * G > 32) W = 0;
+        }
+        const uint32_t J = W ? W * G : jw;
+        uint32_t wb = (J * tb + 7) / 8 * 8;
         if ((wb / 8) % 2 == 0) wb += 8;
         // whole 128-row tiles (K3 bulk-copies full tiles): sentinel ids, no masks in the tail
         const size_t n_pad = (size_t{n} + 127) / 128 * 128;
         ix->cnf_ids = dmalloc<uint8_t>(n_pad * wb);
-        ix->cnf_masks = dmalloc<uint64_t>(n_pad);
         HYRE_CUDA(cudaMemset(ix->cnf_ids, 0xFF, n_pad * wb));
-        HYRE_CUDA(cudaMemset(ix->cnf_masks, 0, n_pad * 8));
-        cnf_rows_kernel<<<blocks, 256>>>(ix->row_terms, ix->slot_of, n, Ap, tb, wb, ix->cnf_ids, ix->cnf_masks);
+        if (W) {
+          cnf_group_rows_kernel<<<blocks, 256>>>(ix->row_terms, ix->slot_of, n, Ap, C, T, W, G, wb, ix->cnf_ids);
+        } else {
+          ix->cnf_masks = dmalloc<uint64_t>(n_pad);
+          HYRE_CUDA(cudaMemset(ix->cnf_masks, 0, n_pad * 8));
+          cnf_rows_kernel<<<blocks, 256>>>(ix->row_terms, ix->slot_of, n, Ap, tb, wb, ix->cnf_ids, ix->cnf_masks);
+        }
         HYRE_CUDA(cudaGetLastError());
         HYRE_CUDA(cudaDeviceSynchronize());
         ix->cnf_id_bytes = tb;
-        ix->cnf_ids_per_row = jw;
+        ix->cnf_ids_per_row = J;
         ix->cnf_row_bytes = wb;
-        ix->stats.forward_bytes += size_t{n} * (wb + 8);
+        ix->cnf_group = W;
+        ix->stats.forward_bytes += size_t{n} * (wb + (W ? 0 : 8));
       }
       pos.reset();
       std::vector<uint64_t> hk(T);

@@ -291,6 +291,49 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
   }
 }
 
+// Slot-grouped rows (W ids per group, static segments; index.cu
+// cnf_group_rows_kernel): fail = OR over groups of AND over the group's
+// table words -- one LOP3 per id after the first and one OR per group and
+// chunk, no segment masks, no missing-slot loop (EMPTY_g entries carry hc_g).
+template <int J, int W, int NCH, int NT, int JWN>
+__device__ __forceinline__ void cnf_row_grouped(const uint32_t (&tw)[JWN], uint32_t tbl,
+                                                uint32_t live, uint32_t c0, uint32_t (&out)[NT]) {
+  uint32_t v[J][NT];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const uint32_t id = (tw[j >> 2] >> ((j & 3) * 8)) & 0xFFu;
+    const uint32_t e = tbl + (id * NCH + c0) * 4;
+    if (NT == 1) {
+      asm("ld.shared.u32 %0, [%1];" : "=r"(v[j][0]) : "r"(e));
+    } else if (NT == 2) {
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[j][0]), "=r"(v[j][NT - 1]) : "r"(e));
+    } else {
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(v[j][0]), "=r"(v[j][1 % NT]), "=r"(v[j][2 % NT]), "=r"(v[j][3 % NT])
+          : "r"(e));
+    }
+  }
+  uint32_t fail[NT];
+#pragma unroll
+  for (int c = 0; c < NT; ++c) fail[c] = 0u;
+#pragma unroll
+  for (int g = 0; g < J / W; ++g) {
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      uint32_t a = v[g * W][c];
+#pragma unroll
+      for (int p = 1; p < W; ++p) a &= v[g * W + p][c];
+      fail[c] |= a;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NT; ++c) {
+    uint32_t lv;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(lv) : "r"(live + (c0 + c) * 4));
+    out[c] = lv & ~fail[c];
+  }
+}
+
 }  // namespace
 
 // J > 0: fused CNF over compact CNF rows of J ids of TB bytes for NCH
@@ -300,7 +343,8 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
 // Fused groups of <= 64 queries run two CTAs per SM (tc_ctas_per_sm): twice
 // the CNF / epilogue warps to hide their latency chains, each CTA with half
 // the shared-memory ring and 256 TMEM columns (67 registers, no spills).
-template <int J, int TB, int NCH>
+// W > 0: slot-grouped rows (u8 ids, W ids per slot group, no masks).
+template <int J, int TB, int NCH, int W>
 __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ? 2 : 1)
     tc_score_kernel(const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo, TcArgs a) {
   constexpr bool kFused = J > 0;
@@ -349,7 +393,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
   uint8_t* after_skey = reinterpret_cast<uint8_t*>(s_skey) + stage_bytes_for(Np);
   uint8_t* s_terms = after_skey + ((128u - (smem_u32(after_skey) & 127u)) & 127u);
   // term slot: [128 rows x wb id bytes][128 x u64 masks]
-  const uint32_t term_ids_bytes = kTileRows * a.wb, term_tile_bytes = term_ids_bytes + kTileRows * 8;
+  const uint32_t term_ids_bytes = kTileRows * a.wb, term_tile_bytes = term_ids_bytes + (W ? 0u : kTileRows * 8);
   uint32_t* s_elig = reinterpret_cast<uint32_t*>(s_terms + (kFused ? TS * term_tile_bytes : 0u));
   uint64_t* s_tbar = reinterpret_cast<uint64_t*>(s_elig + (kFused ? kEligSlots * NCH * kTileRows : 0u));
   uint64_t* ttfull = s_tbar;
@@ -443,7 +487,12 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
     for (uint32_t t = threadIdx.x; t < n_tbl; t += blockDim.x) {  // unlisted term: v = hc of its slot
       uint32_t* e = s_ftbl + t * NCH;
 #pragma unroll
-      for (uint32_t c = 0; c < NCH; ++c) e[c] = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;
+      for (uint32_t c = 0; c < NCH; ++c) {
+        uint32_t x = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;  // sentinel / PAD: AND identity
+        if (W && t >= a.T && t < a.T + a.C) x = s_fhc[(t - a.T) * NCH + c];  // EMPTY_g: queries constraining g
+        if (W && t == 0xFEu) x = 0u;                                          // NONE: no constraint
+        e[c] = x;
+      }
     }
     __syncthreads();
     for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {  // listed terms: v = hc & ~users
@@ -473,18 +522,22 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         if (!a.prefilter)
           tma_load_2d(s_qlo + k * q_box, &tm_qlo, qbar, static_cast<int>(k * 64), static_cast<int>(a.q_row0));
       }
-      uint32_t s = 0, ph = 0;
+      uint32_t s = 0, ph = 0, ts = 0, tph = 0;  // ring slots and phases (no runtime modulo)
       for (uint32_t i = 0;; ++i) {
         const uint32_t t = tile_of(a, i);
         if (t == UINT32_MAX) break;
         if (kFused) {  // the tile's compact CNF rows (ids, masks; padded to whole tiles) into the term ring
-          const uint32_t ts = i % TS, tph = (i / TS) & 1;
+          if (i > 0 && ++ts == TS) {
+            ts = 0;
+            tph ^= 1;
+          }
           mbar_wait(ttempty + ts, tph ^ 1);
           mbar_expect_tx(ttfull + ts, term_tile_bytes);
           bulk_load(s_terms + ts * term_tile_bytes, a.cnf_ids + static_cast<size_t>(t) * term_ids_bytes,
                     term_ids_bytes, ttfull + ts);
-          bulk_load(s_terms + ts * term_tile_bytes + term_ids_bytes, a.cnf_masks + static_cast<size_t>(t) * kTileRows,
-                    kTileRows * 8, ttfull + ts);
+          if (!W)
+            bulk_load(s_terms + ts * term_tile_bytes + term_ids_bytes,
+                      a.cnf_masks + static_cast<size_t>(t) * kTileRows, kTileRows * 8, ttfull + ts);
         }
         for (uint32_t k = 0; k < kb; k += aps) {
           mbar_wait(empty + s, ph ^ 1);
@@ -765,31 +818,38 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
   } else if (kFused) {
     // ===== CNF warps: thread r evaluates tile row r % 128 for its share
     // of the NCH query chunks (all of them with 4 CNF warps, half with 8) =====
-    constexpr int JW = kFused ? J * TB / 4 : 2;  // u32 words of a row's ids
+    constexpr int JW = kFused ? (J * TB + 7) / 8 * 2 : 2;  // u32 words of a row's ids (whole 8-byte loads)
     constexpr int NT = kFused ? NCH * 4 / static_cast<int>(cnf_warps(NCH)) : 1;  // chunks per thread
     const uint32_t rr = threadIdx.x - 32 * (2 + kEW);
     const uint32_t r = rr & (kTileRows - 1), c0 = (rr / kTileRows) * NT;
     const uint32_t cslots = s_flive[NCH];
+    uint32_t ts = TS - 1, tph = 1;  // term ring slot / phase of tile i (advanced at the top)
     for (uint32_t i = 0;; ++i) {
       const uint32_t t = tile_of(a, i);
       if (t == UINT32_MAX) break;
-      const uint32_t ts = i % TS, tph = (i / TS) & 1;
+      if (++ts == TS) {
+        ts = 0;
+        tph ^= 1;
+      }
       mbar_wait_backoff(ttfull + ts, tph, a.backoff_ns);
       uint32_t tw[JW];
       const uint32_t src = smem_u32(s_terms) + ts * term_tile_bytes + r * a.wb;
 #pragma unroll
       for (int v = 0; v < JW / 2; ++v)
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tw[2 * v]), "=r"(tw[2 * v + 1]) : "r"(src + 8 * v));
-      uint64_t masks;
-      asm volatile("ld.shared.u64 %0, [%1];"
-                   : "=l"(masks)
-                   : "r"(smem_u32(s_terms) + ts * term_tile_bytes + term_ids_bytes + r * 8));
+      uint64_t masks = 0;
+      if (!W)
+        asm volatile("ld.shared.u64 %0, [%1];"
+                     : "=l"(masks)
+                     : "r"(smem_u32(s_terms) + ts * term_tile_bytes + term_ids_bytes + r * 8));
       __syncwarp();
       if (lane == 0) mbar_arrive(ttempty + ts);
       uint32_t el[NT];
       if (a.debug & 4u) {  // diagnostics: no CNF evaluation (every live query eligible)
 #pragma unroll
         for (int c = 0; c < NT; ++c) el[c] = s_flive[c0 + c] ^ (tw[0] & 1u) ^ static_cast<uint32_t>(masks & 2u);
+      } else if constexpr (W > 0) {
+        cnf_row_grouped<J, W, NCH, NT, JW>(tw, smem_u32(s_ftbl), smem_u32(s_flive), c0, el);
       } else {
         cnf_row<(kFused ? J : 8), (kFused ? TB : 1), NCH, NT>(tw, masks, a.T, smem_u32(s_ftbl), smem_u32(s_fhc),
                                                              smem_u32(s_flive), cslots, c0, el);
@@ -889,39 +949,51 @@ size_t tc_smem_cap(bool fused, uint32_t Np) {
   return 227 * 1024 - (fused ? kTcStaticSmem : 64);
 }
 
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots) {
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t row_bytes, uint32_t term_slots) {
   const size_t nch = tc_fused_chunks(Np);
   const size_t n_tbl = T <= 255 ? 0 : T + 1;  // u8 ids: static 256-entry table (kTcStaticSmem)
-  return 128 + size_t{term_slots} * kTileRows * (wb + 8) + size_t{kEligSlots} * nch * kTileRows * 4 +
+  return 128 + size_t{term_slots} * kTileRows * row_bytes + size_t{kEligSlots} * nch * kTileRows * 4 +
          16 * (term_slots + kEligSlots) + 4 * (n_tbl * nch + C * nch + nch + 1) + T + 1 + 16;
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st) {
   using KFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
-  // [id width: u8 J = 8/16/24/32, u16 J = 16/32][query chunks 1/2/4]
-#define HYRE_TC_ROW(J, TB) \
-  {tc_score_kernel<J, TB, 1>, tc_score_kernel<J, TB, 2>, tc_score_kernel<J, TB, 4>, tc_score_kernel<J, TB, 8>}
-  static const KFn fused[6][4] = {HYRE_TC_ROW(8, 1),  HYRE_TC_ROW(16, 1), HYRE_TC_ROW(24, 1),
-                                  HYRE_TC_ROW(32, 1), HYRE_TC_ROW(16, 2), HYRE_TC_ROW(32, 2)};
+  // segmented rows [id width: u8 J = 8/16/24/32, u16 J = 16/32][query chunks 1/2/4/8];
+  // slot-grouped rows [(J, W) = (8,1) (8,2) (16,2) (12,3) (24,3) (16,4) (32,4)][chunks]
+#define HYRE_TC_ROW(J, TB, W)                                                                     \
+  {tc_score_kernel<J, TB, 1, W>, tc_score_kernel<J, TB, 2, W>, tc_score_kernel<J, TB, 4, W>, \
+   tc_score_kernel<J, TB, 8, W>}
+  static const KFn fused[13][4] = {HYRE_TC_ROW(8, 1, 0),  HYRE_TC_ROW(16, 1, 0), HYRE_TC_ROW(24, 1, 0),
+                                   HYRE_TC_ROW(32, 1, 0), HYRE_TC_ROW(16, 2, 0), HYRE_TC_ROW(32, 2, 0),
+                                   HYRE_TC_ROW(8, 1, 1),  HYRE_TC_ROW(8, 1, 2),  HYRE_TC_ROW(16, 1, 2),
+                                   HYRE_TC_ROW(12, 1, 3), HYRE_TC_ROW(24, 1, 3), HYRE_TC_ROW(16, 1, 4),
+                                   HYRE_TC_ROW(32, 1, 4)};
 #undef HYRE_TC_ROW
   static std::atomic<uint64_t> attr{0};  // devices whose limits are set (every variant at once)
   int dev = 0;
   HYRE_CUDA(cudaGetDevice(&dev));
   if (!(attr.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
-    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    227 * 1024 - 64));
     for (auto& row : fused)
       for (KFn k : row)
         HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kTcStaticSmem));
     attr.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
   }
-  KFn k = tc_score_kernel<0, 1, 1>;
+  KFn k = tc_score_kernel<0, 1, 1, 0>;
   if (a.fused) {
     const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : (nch == 4 ? 2 : 3));
     int ri = -1;
-    if (a.tb == 1) ri = a.J == 8 ? 0 : a.J == 16 ? 1 : a.J == 24 ? 2 : a.J == 32 ? 3 : -1;
-    else if (a.tb == 2) ri = a.J == 16 ? 4 : a.J == 32 ? 5 : -1;
+    if (a.W) {
+      const uint32_t J = a.J, W = a.W;
+      ri = W == 1 && J == 8 ? 6 : W == 2 && J == 8 ? 7 : W == 2 && J == 16 ? 8 : W == 3 && J == 12 ? 9
+         : W == 3 && J == 24 ? 10 : W == 4 && J == 16 ? 11 : W == 4 && J == 32 ? 12 : -1;
+    } else if (a.tb == 1) {
+      ri = a.J == 8 ? 0 : a.J == 16 ? 1 : a.J == 24 ? 2 : a.J == 32 ? 3 : -1;
+    } else if (a.tb == 2) {
+      ri = a.J == 16 ? 4 : a.J == 32 ? 5 : -1;
+    }
     if (ri < 0) throw Error(HYRE_INTERNAL, "fused CNF: unsupported compact row shape");
     k = fused[ri][ci];
   }

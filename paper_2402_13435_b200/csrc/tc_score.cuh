@@ -44,6 +44,7 @@ struct TcArgs {
   const uint64_t* cnf_masks;
   const uint8_t* slot_of;
   uint32_t J, tb, wb, T, C;
+  uint32_t W;  // slot-grouped rows: ids per slot group (0: segmented rows + masks)
   const uint32_t* fz;
   uint32_t n_entries, hc_off, live_off;
   // Prefilter mode (prefilter != 0): only the hi plane of each K-atom is
@@ -79,7 +80,8 @@ void make_i8_map(CUtensorMap* map, const void* base, uint64_t rows, uint32_t dp,
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes = 0,
                      uint32_t q_planes = 2, uint32_t aps = 1);
 // shared memory of the fused CNF tables (term users, slot of term, hc, live)
-size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t wb, uint32_t term_slots);
+// row_bytes: a row's compact CNF bytes in the term ring (ids [+ 8 B masks])
+size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t row_bytes, uint32_t term_slots);
 constexpr uint32_t kMaxTermSlots = 8;
 // static shared memory of the fused variants (the u8-id term table, <= 256 x 8 words)
 constexpr uint32_t kTcStaticSmem = 8 * 1024 + 64;

@@ -33,115 +33,94 @@ class IngestSchema:
     dim: int = 0
 
 
-def _fail_at(path: str, line: int, what: str):
-    raise ValidationError(f"{path}:{line}: {what}")  # dataio.cpp:18-21
+def _lib():
+    from . import _lib as L
+    return L
 
 
-def _is_unsigned(v) -> bool:
-    return isinstance(v, int) and not isinstance(v, bool) and v >= 0
-
-
-def _is_number(v) -> bool:
-    return isinstance(v, (int, float)) and not isinstance(v, bool)
-
-
-def _parse_file(path: str):
-    """dataio.cpp:23-31."""
-    try:
-        with open(path, "r", encoding="utf-8") as f:
-            text = f.read()
-    except OSError:
-        raise ValidationError("cannot open: " + path) from None
-    try:
-        return json.loads(text)
-    except ValueError as e:
-        raise ValidationError(f"{path}: {e}") from None
-
-
-def _for_each_jsonl(path: str):
-    """dataio.cpp:33-49: one JSON value per line, blank lines skipped."""
-    try:
-        f = open(path, "r", encoding="utf-8")
-    except OSError:
-        raise ValidationError("cannot open: " + path) from None
-    with f:
-        for line_no, line in enumerate(f, start=1):
-            if not line.strip(" \t\r\n"):
-                continue
-            try:
-                j = json.loads(line)
-            except ValueError as e:
-                _fail_at(path, line_no, str(e))
-            yield line_no, j
-
-
-def _to_attr_id(v, path: str, line: int) -> int:
-    """dataio.cpp:51-58."""
-    if not _is_unsigned(v):
-        _fail_at(path, line, "attribute ids must be unsigned integers")
-    if v > 0xFFFFFFFF:
-        _fail_at(path, line, "attribute id out of range")
-    return int(v)
+def _check(rc: int) -> None:
+    from .hyre import _check as check
+    check(rc)
 
 
 def read_schema_json(path: str) -> IngestSchema:
-    """read_schema_json (dataio.cpp:118-140)."""
-    j = _parse_file(path)
-    if not isinstance(j, dict) or "clauses" not in j or "dim" not in j:
-        raise ValidationError(path + ": schema needs 'clauses' and 'dim'")
-    names = j["clauses"]
-    if not isinstance(names, list):
-        raise ValidationError(path + ": 'clauses' must be an array")
-    schema = IngestSchema()
-    for name in names:
-        if not isinstance(name, str):
-            raise ValidationError(path + ": clause names must be strings")
-        schema.clause_names.append(name)
-    if not schema.clause_names:
-        raise ValidationError(path + ": 'clauses' must not be empty")
-    if not _is_unsigned(j["dim"]) or j["dim"] > 0xFFFFFFFF:
-        raise ValidationError(path + ": dim must be an unsigned integer")
-    schema.dim = int(j["dim"])
-    return schema
+    """read_schema_json (dataio.cpp:118-140), parsed by the library's C++
+    ingestion (csrc/ingest.cpp, hyre_schema_read_json)."""
+    L = _lib()
+    h = L.C.c_void_p()
+    _check(L.lib().hyre_schema_read_json(path.encode(), L.C.byref(h)))
+    try:
+        n = L.lib().hyre_schema_num_clauses(h)
+        return IngestSchema([L.lib().hyre_schema_clause_name(h, i).decode() for i in range(n)],
+                            int(L.lib().hyre_schema_dim(h)))
+    finally:
+        L.lib().hyre_schema_destroy(h)
+
+
+class _Schema:
+    """An IngestSchema as a library handle (hyre_schema_create)."""
+
+    def __init__(self, schema: IngestSchema):
+        L = _lib()
+        names = (L.C.c_char_p * max(1, len(schema.clause_names)))(*[n.encode() for n in schema.clause_names])
+        self.h = L.C.c_void_p()
+        _check(L.lib().hyre_schema_create(len(schema.clause_names), names, schema.dim, L.C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib().lib().hyre_schema_destroy(self.h)
+
+
+class DocumentSet:
+    """read_documents_jsonl's documents held by the library (flat arrays, file
+    order); `widest` is hyre build's maxNumAttr."""
+
+    def __init__(self, path: str, schema: IngestSchema):
+        L = _lib()
+        self._schema = _Schema(schema)
+        self.h = L.C.c_void_p()
+        _check(L.lib().hyre_documents_read_jsonl(path.encode(), self._schema.h, L.C.byref(self.h)))
+        self.num_clauses, self.dim = len(schema.clause_names), schema.dim
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib().lib().hyre_documents_destroy(self.h)
+
+    def __len__(self) -> int:
+        return int(_lib().lib().hyre_documents_count(self.h))
+
+    @property
+    def widest(self) -> int:
+        return int(_lib().lib().hyre_documents_widest(self.h))
+
+    def documents(self) -> List[DocumentInput]:
+        L = _lib()
+        lib, n, C = L.lib(), len(self), self.num_clauses
+        so = np.ctypeslib.as_array(lib.hyre_documents_slot_offsets(self.h), (n * C + 1,)) if n else np.zeros(1, np.uint64)
+        ids = np.ctypeslib.as_array(lib.hyre_documents_ids(self.h), (max(1, int(so[-1])),)) if so[-1] else np.zeros(0, np.uint32)
+        emb = np.ctypeslib.as_array(lib.hyre_documents_embeddings(self.h), (max(1, n * self.dim),)) if n and self.dim \
+            else np.zeros(0, np.float32)
+        out = []
+        for i in range(n):
+            cl = [ids[int(so[i * C + c]):int(so[i * C + c + 1])].tolist() for c in range(C)]
+            out.append(DocumentInput(lib.hyre_documents_id(self.h, i).decode(), cl,
+                                     np.array(emb[i * self.dim:(i + 1) * self.dim], np.float32)))
+        return out
+
+    def add_to(self, builder: IndexBuilder) -> int:
+        """add_document for every document (file order) -> first row."""
+        L = _lib()
+        first = L.C.c_uint32()
+        _check(L.lib().hyre_builder_add_document_set(builder._h, self.h, L.C.byref(first)))
+        return int(first.value)
 
 
 def read_documents_jsonl(path: str, schema: IngestSchema) -> List[DocumentInput]:
     """read_documents_jsonl (dataio.cpp:142-187): one document per line,
     {"id": "doc1", "clauses": {"geo": [934]}, "embedding": [0.1, ...]}; an
-    absent clause is empty, an absent embedding the zero vector."""
-    slot_of = {n: i for i, n in enumerate(schema.clause_names)}
-    docs: List[DocumentInput] = []
-    for line, j in _for_each_jsonl(path):
-        if not isinstance(j, dict) or not isinstance(j.get("id"), str):
-            _fail_at(path, line, "document needs a string 'id'")
-        clauses: List[List[int]] = [[] for _ in schema.clause_names]
-        if "clauses" in j:
-            cl = j["clauses"]
-            if not isinstance(cl, dict):
-                _fail_at(path, line, "'clauses' must be an object")
-            for name, ids in cl.items():
-                if name not in slot_of:
-                    _fail_at(path, line, f"unknown clause '{name}'")
-                if not isinstance(ids, list):
-                    _fail_at(path, line, f"clause '{name}' must be an array")
-                for v in ids:
-                    clauses[slot_of[name]].append(_to_attr_id(v, path, line))
-        if "embedding" in j:
-            emb = j["embedding"]
-            if not isinstance(emb, list):
-                _fail_at(path, line, "'embedding' must be an array")
-            if len(emb) != schema.dim:
-                _fail_at(path, line, f"embedding: expected dim {schema.dim}, got {len(emb)}")
-            vals = []
-            for v in emb:
-                if not _is_number(v):
-                    _fail_at(path, line, "embedding entries must be numbers")
-                vals.append(np.float32(float(v)))  # get<double>() then static_cast<float>
-            embedding = np.asarray(vals, np.float32)
-        else:
-            embedding = np.zeros(schema.dim, np.float32)
-        docs.append(DocumentInput(j["id"], clauses, embedding))
-    return docs
+    absent clause is empty, an absent embedding the zero vector (parsed by
+    csrc/ingest.cpp)."""
+    return DocumentSet(path, schema).documents()
 
 
 def build_index(docs: Sequence[DocumentInput], schema: IngestSchema, max_num_attr: Optional[int] = None,
@@ -160,6 +139,20 @@ def build_index(docs: Sequence[DocumentInput], schema: IngestSchema, max_num_att
     return b.freeze(make_codec(schema.dim, num_bits, seed))
 
 
+def build_index_jsonl(schema_path: str, corpus_path: str, num_bits: int = 512, seed: int = 1,
+                      device: Optional[int] = None) -> FrozenIndex:
+    """`hyre build` (cli_commands.cpp:37-63) end to end in the library:
+    schema + JSONL corpus parsed in C++, maxNumAttr = the widest document,
+    every document staged, frozen (on GPU `device` if given)."""
+    schema = read_schema_json(schema_path)
+    ds = DocumentSet(corpus_path, schema)
+    if len(ds) == 0:
+        raise ValidationError("no documents")
+    b = IndexBuilder(IndexConfig(len(schema.clause_names), max(1, ds.widest), schema.dim, list(schema.clause_names)))
+    ds.add_to(b)
+    return b.freeze(make_codec(schema.dim, num_bits, seed), device=device)
+
+
 # ---------------------------------------------------------------------------
 # learned-link export (config-5 vocabulary)
 # ---------------------------------------------------------------------------
@@ -176,18 +169,23 @@ class LinksExport:
 
 
 def read_links_export(path: str) -> LinksExport:
-    j = _parse_file(path)
-    if not isinstance(j, dict) or not all(k in j for k in ("nodes", "seekerAttributes", "jobAttributes")):
-        raise ValidationError(path + ": links export needs 'nodes', 'seekerAttributes' and 'jobAttributes'")
-    out = LinksExport(nodes=list(j["nodes"]))
-    for key, dst in (("seekerAttributes", out.seeker_attributes), ("jobAttributes", out.job_attributes)):
-        m = j[key]
-        if not isinstance(m, dict):
-            raise ValidationError(f"{path}: '{key}' must be an object")
-        for name, ids in m.items():
-            if not isinstance(ids, list) or not all(_is_unsigned(v) and 0 < v <= 0xFFFFFFFF for v in ids):
-                raise ValidationError(f"{path}: {key}.{name} must be an array of node ids")
-            dst[name] = sorted(set(int(v) for v in ids))
+    """The serving-graph export (validated and mapped by csrc/ingest.cpp,
+    hyre_links_read_json); `nodes` keeps the raw node records."""
+    L = _lib()
+    h = L.C.c_void_p()
+    _check(L.lib().hyre_links_read_json(path.encode(), L.C.byref(h)))
+    try:
+        out = LinksExport()
+        for side, dst in ((0, out.seeker_attributes), (1, out.job_attributes)):
+            for i in range(L.lib().hyre_links_count(h, side)):
+                n = L.C.c_uint32()
+                p = L.lib().hyre_links_ids(h, side, i, L.C.byref(n))
+                dst[L.lib().hyre_links_name(h, side, i).decode()] = \
+                    np.ctypeslib.as_array(p, (n.value,)).tolist() if n.value else []
+    finally:
+        L.lib().hyre_links_destroy(h)
+    with open(path, "r", encoding="utf-8") as f:
+        out.nodes = list(json.load(f)["nodes"])
     return out
 
 

@@ -5,6 +5,7 @@
 // exit code = failures.  `--host-only` skips the checks that need a GPU.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -74,6 +75,35 @@ int main(int argc, char** argv) {
   CHECK("no documents staged", throws_with<ValidationError>(
                                    [] { IndexBuilder b({2, 5, 4, {}}); (void)std::move(b).freeze(make_codec(4, 64, 7)); },
                                    "no documents staged"));
+  {  // ingestion (dataio.hpp:15-28) -> the appendix index, through the library's C++ parser
+    const std::string dir = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp");
+    const std::string sp = dir + "/hyre_api_schema.json", cp = dir + "/hyre_api_docs.jsonl";
+    std::FILE* f = std::fopen(sp.c_str(), "w");
+    std::fputs("{\"clauses\": [\"geo\", \"skill\"], \"dim\": 2}", f);
+    std::fclose(f);
+    f = std::fopen(cp.c_str(), "w");
+    std::fputs("{\"id\": \"doc1\", \"clauses\": {\"geo\": [934, 2934], \"skill\": [945, 342, 3112]}, "
+               "\"embedding\": [1, 0]}\n\n{\"id\": \"doc2\", \"clauses\": {\"skill\": [9342, 234], \"geo\": [129]}, "
+               "\"embedding\": [0.0, 1e0]}\n", f);
+    std::fclose(f);
+    const IngestSchema schema = read_schema_json(sp);
+    const auto docs = read_documents_jsonl(cp, schema);
+    CHECK("read_schema_json / read_documents_jsonl (dataio.hpp:20-28)",
+          schema.clause_names == std::vector<std::string>({"geo", "skill"}) && schema.dim == 2 && docs.size() == 2 &&
+              docs[1].doc_id == "doc2" && docs[1].clauses[0] == std::vector<std::uint32_t>({129}) &&
+              docs[1].embedding == std::vector<float>({0.0f, 1.0f}));
+    const FrozenIndex built = build_index_jsonl(sp, cp, 16, 7);
+    auto b0 = built.attribute_row(0);
+    CHECK("hyre build from JSONL = the appendix layout",
+          built.max_num_attr() == 5 &&
+              std::vector<std::uint32_t>(b0.begin(), b0.end()) == std::vector<std::uint32_t>({934, 2934, 342, 945, 3112}) &&
+              built.resolve_clause_slot("skill") == 1);
+    f = std::fopen(cp.c_str(), "w");
+    std::fputs("{\"id\": \"a\"}\n{\"id\": \"b\", \"clauses\": {\"salary\": [1]}}\n", f);
+    std::fclose(f);
+    CHECK("ingest errors name file and line",
+          throws_with<ValidationError>([&] { read_documents_jsonl(cp, schema); }, cp + ":2: unknown clause 'salary'"));
+  }
   const CnfQuery q = normalize_query({{1, {9, 3, 9, 1}}}, 2);
   CHECK("normalize_query sorts + dedups", q.clauses.size() == 1 && q.clauses[0].attribute_ids ==
                                                                        std::vector<std::uint32_t>({1, 3, 9}));

@@ -126,3 +126,43 @@ def test_links_index_retrieves_exactly_the_reachable_jobs(dio, hy, tmp_path):
     for seeker, want in (("s1", ["j1", "j2", "j3"]), ("s2", ["j2", "j3"])):
         r = hy.execute(index, hy.HybridQuery(dio.seeker_query(ex, seeker), None, 10))
         assert [index.doc_id(h.row_id) for h in r.hits] == want
+
+
+def test_json_value_rules_follow_the_reference_parser(dio, hy, tmp_path):
+    # nlohmann::json semantics as dataio.cpp uses them: unsigned integers only
+    # for attribute ids (not 1.0, not -1, not true), any number for embedding
+    # entries, escapes decoded, duplicate keys -> last wins, key order
+    s = dio.IngestSchema(["geo", "skill"], 2)
+    ok = write(tmp_path, "ok.jsonl",
+               '{"id": "caf\\u00e9 \\ud83d\\ude00", "clauses": {"skill": [7], "geo": [4294967295, 1]},'
+               ' "embedding": [-2.5e-1, 3]}\n'
+               '   \t\r\n'
+               '{"id": "x", "id": "y", "embedding": [1E2, -0.0]}\n')
+    d = dio.read_documents_jsonl(ok, s)
+    assert [x.doc_id for x in d] == ["café \U0001F600", "y"]
+    assert d[0].clauses == [[4294967295, 1], [7]] and list(d[0].embedding) == [-0.25, 3.0]
+    assert list(d[1].embedding) == [100.0, -0.0] and d[1].clauses == [[], []]
+    for bad, msg in [('{"id": "a", "clauses": {"geo": [1.0]}}', "attribute ids must be unsigned integers"),
+                     ('{"id": "a", "clauses": {"geo": [true]}}', "attribute ids must be unsigned integers"),
+                     ('{"id": "a", "clauses": {"geo": [4294967296]}}', "attribute id out of range"),
+                     ('{"id": "a", "embedding": [1, "2"]}', "embedding entries must be numbers"),
+                     ('{"id": "a", "clauses": {"geo": 5}}', "clause 'geo' must be an array"),
+                     ('{"id": "a", "clauses": []}', "'clauses' must be an object"),
+                     ('{"id": 5}', "document needs a string 'id'"),
+                     ('{"id": "a",}', ":1: parse error"),
+                     ('{"id": "a"} x', ":1: parse error")]:
+        with pytest.raises(hy.ValidationError, match=msg):
+            dio.read_documents_jsonl(write(tmp_path, "bad.jsonl", bad + "\n"), s)
+
+
+def test_build_index_jsonl_is_hyre_build(dio, hy, tmp_path):
+    # cli_commands.cpp:37-63 in the library: widest document -> maxNumAttr
+    sp = write(tmp_path, "s.json", '{"clauses": ["geo", "skill"], "dim": 2}')
+    cp = write(tmp_path, "c.jsonl",
+               '{"id": "doc1", "clauses": {"geo": [934, 2934], "skill": [945, 342, 3112, 945]}, "embedding": [1, 0]}\n'
+               '{"id": "doc2", "clauses": {"geo": [129], "skill": [9342, 234]}, "embedding": [0, 1]}\n')
+    f = dio.build_index_jsonl(sp, cp, num_bits=16, seed=7)
+    assert f.max_num_attr() == 5 and f.doc_id(1) == "doc2"
+    assert np.array(f.attributes)[0].tolist() == [934, 2934, 342, 945, 3112]
+    with pytest.raises(hy.ValidationError, match="no documents"):
+        dio.build_index_jsonl(sp, write(tmp_path, "e.jsonl", "\n"))

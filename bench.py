@@ -308,23 +308,23 @@ def run_ours(args, w):
         t_hits = torch.as_tensor(Dev(hits_p.value, (n_words,), "<i4"), device=f"cuda:{local}")
         t_off = torch.as_tensor(Dev(off_p.value, (B,), "<i8"), device=f"cuda:{local}")
         t_cnt = torch.as_tensor(Dev(cnt_p.value, (B,), "<i4"), device=f"cuda:{local}")
-        # identical shapes on every rank: pad to the max hit buffer
+        # identical shapes on every rank: one packed record per rank (hits
+        # padded to the max hit buffer, then the B u64 offsets, then the B u32
+        # counts) -> ONE all-gather, merged exactly on device
         n_max = torch.tensor([n_words], device=f"cuda:{local}")
         dist.all_reduce(n_max, op=dist.ReduceOp.MAX)
         n_max = int(n_max.item())
-        g_hits = torch.zeros(world, n_max, dtype=torch.int32, device=f"cuda:{local}")
-        g_off = torch.zeros(world, B, dtype=torch.int64, device=f"cuda:{local}")
-        g_cnt = torch.zeros(world, B, dtype=torch.int32, device=f"cuda:{local}")
-        pad = torch.zeros(n_max, dtype=torch.int32, device=f"cuda:{local}")
+        rec_words = n_max + 3 * B + (3 * B) % 2
+        rec = torch.zeros(rec_words, dtype=torch.int32, device=f"cuda:{local}")
+        g_rec = torch.zeros(world, rec_words, dtype=torch.int32, device=f"cuda:{local}")
 
         def gather():
             with torch.cuda.stream(stream):
-                pad[:n_words].copy_(t_hits)
-                dist.all_gather_into_tensor(g_hits.view(-1), pad)
-                dist.all_gather_into_tensor(g_off.view(-1), t_off)
-                dist.all_gather_into_tensor(g_cnt.view(-1), t_cnt)
-            check(lib.hyre_batch_merge_gathered(h, g_hits.data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), world,
-                                                n_max // 2))
+                rec[:n_words].copy_(t_hits)
+                rec[n_max:n_max + 2 * B].copy_(t_off.view(torch.int32))
+                rec[n_max + 2 * B:n_max + 3 * B].copy_(t_cnt)
+                dist.all_gather_into_tensor(g_rec.view(-1), rec)
+            check(lib.hyre_batch_merge_packed(h, g_rec.data_ptr(), world, rec_words, n_max))
 
     # Two batches in flight (N = 1): a second executor with its own stream
     # runs every other step, so one batch's small kernels (sample, thresholds,

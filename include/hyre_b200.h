@@ -435,6 +435,11 @@ hyre_status hyre_pool_stats(const hyre_pool* p, uint64_t* batches, uint64_t* que
  * merged top-K replaces this executor's results; fetch them as usual. */
 hyre_status hyre_batch_merge_gathered(hyre_executor* ex, const void* g_hits, const void* g_offsets,
                                       const void* g_counts, uint32_t n_lists, uint64_t hits_stride);
+/* The same over one packed record per shard (a single all-gather): record g at
+ * g x record_words u32 words holds the shard's hits (hits_words u32 words,
+ * even), then b u64 hit offsets, then b u32 counts. */
+hyre_status hyre_batch_merge_packed(hyre_executor* ex, const void* g_records, uint32_t n_lists,
+                                    uint64_t record_words, uint64_t hits_words);
 
 /* Stage entry points (public in the reference and used by its tests). */
 /* full_scan_tbr (term_match.hpp:43-45): ascending eligible rows (global ids). */

@@ -700,6 +700,20 @@ hyre_status hyre_batch_merge_gathered(hyre_executor* ex, const void* g_hits, con
   });
 }
 
+hyre_status hyre_batch_merge_packed(hyre_executor* ex, const void* g_records, uint32_t n_lists,
+                                    uint64_t record_words, uint64_t hits_words) {
+  return guard([&] {
+    need(ex, "executor");
+    need(g_records, "records");
+    const uint32_t B = ex->ex->B;
+    if (hits_words % 2 || record_words % 2 || record_words < hits_words + 3ull * B)
+      validation("packed merge: record must hold hits (even words), then b u64 offsets, then b u32 counts");
+    const uint32_t* r = static_cast<const uint32_t*>(g_records);
+    ex->ex->merge_gathered(reinterpret_cast<const hyre_hit*>(r), reinterpret_cast<const uint64_t*>(r + hits_words),
+                           r + hits_words + 2ull * B, n_lists, record_words / 2, record_words / 2, record_words);
+  });
+}
+
 hyre_status hyre_batch_device_results(hyre_executor* ex, void** hits, uint64_t* n_hits, void** offsets,
                                       void** counts) {
   return guard([&] {

@@ -1446,14 +1446,15 @@ uint32_t Executor::top_k(const uint32_t* rows, const float* scores, uint64_t n, 
 // Replaces this executor's results with the exact merge of G gathered shard
 // result sets (device pointers, e.g. filled by an NCCL all-gather).
 void Executor::merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
-                              uint64_t hits_stride) {
+                              uint64_t hits_stride, uint64_t off_stride, uint64_t cnt_stride) {
   if (!prepared) throw Error(HYRE_INTERNAL, "merge before hyre_batch_prepare");
   if (uint64_t{G} * max_k > cap) validation("merge needs G*k <= candidate capacity");
   HYRE_CUDA(cudaSetDevice(ix->device));
   uint32_t* cand_cnt = d_counters + max_batch;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
-  launch_gather_keys(g_hits, g_off, g_cnt, G, hits_stride, B, cap, d_cand, cand_cnt, st);
+  launch_gather_keys(g_hits, hits_stride, g_off, off_stride ? off_stride : B, g_cnt, cnt_stride ? cnt_stride : B, G, B,
+                     cap, d_cand, cand_cnt, st);
   // term-only hits carry score 0, so key order is row order: the merged
   // first-K equals concatenating shard first-K lists in row order.
   SelectArgs fa{d_cand, cand_cnt, cap, d_qp, cand_cnt, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,

@@ -201,8 +201,9 @@ struct Executor {
                       uint64_t cap);
   bool exact_scores(const float* q, uint32_t dim, const uint32_t* rows, uint64_t n, float* out);
   uint32_t top_k(const uint32_t* rows, const float* scores, uint64_t n, uint32_t k, hyre_hit* out);
+  // off_stride / cnt_stride: elements between shard g's offsets / counts (0 = B)
   void merge_gathered(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
-                      uint64_t hits_stride);
+                      uint64_t hits_stride, uint64_t off_stride = 0, uint64_t cnt_stride = 0);
   uint64_t preselect(const uint64_t* qwords, const uint32_t* rows, uint64_t n, uint32_t quant_k,
                      uint32_t* out);
 

@@ -1769,14 +1769,14 @@ void launch_quant_keys(const uint64_t* sigs, uint32_t nw, uint32_t num_bits, uin
 // the shard top-Ks, so the exact answer is K4 over the gathered keys.
 // g_hits: [G][hits_stride] hyre_hit, g_off: [G][B] u64, g_cnt: [G][B] u32.
 // ===========================================================================
-__global__ void gather_keys_kernel(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt,
-                                   uint32_t G, uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys,
-                                   uint32_t* cnt) {
+__global__ void gather_keys_kernel(const hyre_hit* g_hits, uint64_t hits_stride, const uint64_t* g_off,
+                                   uint64_t off_stride, const uint32_t* g_cnt, uint64_t cnt_stride, uint32_t G,
+                                   uint32_t cap, uint64_t* keys, uint32_t* cnt) {
   const uint32_t q = blockIdx.x;
   uint32_t base = 0;
   for (uint32_t g = 0; g < G; ++g) {
-    const uint32_t c = g_cnt[static_cast<size_t>(g) * B + q];
-    const hyre_hit* h = g_hits + static_cast<size_t>(g) * hits_stride + g_off[static_cast<size_t>(g) * B + q];
+    const uint32_t c = g_cnt[g * cnt_stride + q];
+    const hyre_hit* h = g_hits + g * hits_stride + g_off[g * off_stride + q];
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x)
       if (base + i < cap) keys[static_cast<size_t>(q) * cap + base + i] = make_key(h[i].score + 0.0f, h[i].row);
     base += c;
@@ -1784,11 +1784,11 @@ __global__ void gather_keys_kernel(const hyre_hit* g_hits, const uint64_t* g_off
   if (threadIdx.x == 0) cnt[q] = base;
 }
 
-void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
-                        uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys, uint32_t* cnt,
-                        cudaStream_t st) {
+void launch_gather_keys(const hyre_hit* g_hits, uint64_t hits_stride, const uint64_t* g_off, uint64_t off_stride,
+                        const uint32_t* g_cnt, uint64_t cnt_stride, uint32_t G, uint32_t B, uint32_t cap,
+                        uint64_t* keys, uint32_t* cnt, cudaStream_t st) {
   if (B == 0) return;
-  gather_keys_kernel<<<B, 256, 0, st>>>(g_hits, g_off, g_cnt, G, hits_stride, B, cap, keys, cnt);
+  gather_keys_kernel<<<B, 256, 0, st>>>(g_hits, hits_stride, g_off, off_stride, g_cnt, cnt_stride, G, cap, keys, cnt);
 }
 
 // Sharded merge, one CTA per query, reading every shard's results in place

@@ -259,10 +259,12 @@ void launch_rescore_keys(const PrefSelectArgs& a, bool bf16, uint32_t q, uint64_
                          cudaStream_t st);
 void launch_keys_to_hits(const uint64_t* keys, uint64_t n, hyre_hit* out, uint32_t* out_cnt, uint32_t* rerun,
                          cudaStream_t st);
-// Multi-GPU merge: per query, keys of the hits of G gathered shard lists.
-void launch_gather_keys(const hyre_hit* g_hits, const uint64_t* g_off, const uint32_t* g_cnt, uint32_t G,
-                        uint64_t hits_stride, uint32_t B, uint32_t cap, uint64_t* keys, uint32_t* cnt,
-                        cudaStream_t st);
+// Multi-GPU merge: per query, keys of the hits of G gathered shard lists
+// (shard g's arrays at g x stride elements: separate [G][...] arrays, or
+// one packed record per shard).
+void launch_gather_keys(const hyre_hit* g_hits, uint64_t hits_stride, const uint64_t* g_off, uint64_t off_stride,
+                        const uint32_t* g_cnt, uint64_t cnt_stride, uint32_t G, uint32_t B, uint32_t cap,
+                        uint64_t* keys, uint32_t* cnt, cudaStream_t st);
 
 // batch_scan_tbr (pipeline.cpp:75-93): per 32-row word, matches over the
 // active queries of a [B][W] mask (cnt has W + 1 slots; cnt[W] = 0), then --

@@ -82,10 +82,11 @@ def test_sharded_merge_gloo_world2():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("G,B", [(3, 4), (4, 16)])
-def test_device_shard_merge_emulated_on_one_gpu(G, B):
+@pytest.mark.parametrize("G,B,packed", [(3, 4, False), (4, 16, False), (3, 4, True), (4, 16, True)])
+def test_device_shard_merge_emulated_on_one_gpu(G, B, packed):
     """G row shards on one GPU, each with its own executor; their device
-    results are stacked like an NCCL all-gather and merged on device."""
+    results are stacked like an NCCL all-gather (three arrays, or one packed
+    record per shard as bench.py gathers them) and merged on device."""
     import ctypes as C
 
     import paper_2402_13435_b200 as hy
@@ -136,8 +137,18 @@ def test_device_shard_merge_emulated_on_one_gpu(G, B):
         g_cnt[g].copy_(torch.as_tensor(Dev(cp, B, "<i4"), device="cuda"))
     torch.cuda.synchronize()
     ex0 = shards[0][1]
-    assert L.lib().hyre_batch_merge_gathered(ex0._h, g_hits.data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), G,
-                                             stride) == 0
+    if packed:
+        hw = stride * 2
+        rw = hw + 3 * B + (3 * B) % 2
+        g_rec = torch.zeros(G, rw, dtype=torch.int32, device="cuda")
+        g_rec[:, :hw] = g_hits
+        g_rec[:, hw:hw + 2 * B] = g_off.view(torch.int32)
+        g_rec[:, hw + 2 * B:hw + 3 * B] = g_cnt
+        torch.cuda.synchronize()
+        assert L.lib().hyre_batch_merge_packed(ex0._h, g_rec.data_ptr(), G, rw, hw) == 0
+    else:
+        assert L.lib().hyre_batch_merge_gathered(ex0._h, g_hits.data_ptr(), g_off.data_ptr(), g_cnt.data_ptr(), G,
+                                                 stride) == 0
     caps = [q.k for q in batch.queries]
     offs = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.uint64)
     out = (L.hyre_hit * sum(caps))()

@@ -319,6 +319,7 @@ uint32_t hyre_batch_kernel_count(const hyre_executor* ex);
 #define HYRE_PATH_SAMPLED 8u
 #define HYRE_PATH_MATCH_ALL 16u /* tensor-core batch of match-all queries: no eligibility pass */
 #define HYRE_PATH_I8 32u        /* the main pass streams the int8 prefilter plane (exact rescoring of survivors) */
+#define HYRE_PATH_SMALL 64u     /* small index: one exact scoring launch (K7) + the top-K select, no sampling */
 uint32_t hyre_batch_path(const hyre_executor* ex);
 /* K3 kernel variant of the prepared batch (diagnostics for tests that must
  * run a given instantiation): out4 = {J compact CNF ids per row (0 = not

@@ -53,6 +53,14 @@ bool fused_enabled() {
   }();
   return v;
 }
+// HYRE_SMALL=0 disables the K7 single-launch path for small indexes.
+bool small_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_SMALL");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
 // HYRE_PREFILTER=0 disables the K3 prefilter + exact rescore (the K3 pass
 // then reads the full hi/lo split and scores at fp32 grade directly);
 // HYRE_PREFILTER=bf16 forces the bf16 prefilter over the int8 one.
@@ -365,6 +373,20 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // admission and w x clamp(exact dot) rescoring live on that path)
   prefilter = any_emb && (prefilter_enabled() || (use_tc && ix->row_w)) && (use_tc || (i8_ok && k2_i8_enabled()));
   pf_i8 = prefilter && i8_ok;
+  // K7: a small index answered in one scoring launch + K4 (no sample, no
+  // thresholds): embedding queries only, dense-bitmap terms (no CSR scatter),
+  // k <= kSmallMaxK, quant unable to cut (n <= quant_k), every segment's top k
+  // fitting the candidate buffer
+  use_small = false;
+  if (!use_tc && any_emb && !any_term_only && !use_fwd && scatter_total == 0 && big_k.empty() && small_enabled() &&
+      ix->n_rows <= kSmallMaxRows && max_k <= kSmallMaxK &&
+      uint64_t{(ix->n_rows + kSegRows - 1) / kSegRows} * max_k <= cap &&
+      small_supported(ix->dp * (ix->emb_dtype == HYRE_EMB_BF16 ? 2 : 4) / 16)) {
+    use_small = true;
+    for (uint32_t i = 0; i < b; ++i)
+      if ((qp[i].flags & QF_QUANT) && qp[i].quant_k < ix->n_rows) use_small = false;
+  }
+  if (use_small) prefilter = pf_i8 = false;  // exact scores straight from the rows
   if (use_tc) {
     // one group of up to 256 queries per pass (the epilogue works in 32-column
     // chunks); a group must leave room for a >= 3-stage ring next to its
@@ -932,6 +954,25 @@ void Executor::run() {
   } else {
     HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
     if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
+  }
+  if (use_small) {
+    // K7: CNF words + exact scores + per-segment top k in one launch, then K4
+    mark(1, false);
+    mark(2, false);
+    mark(3, false);
+    const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
+    SmallArgs sa{bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
+                 ix->dp * (bf16 ? 2 : 4) / 16, ix->n_rows, ix->row_base, W, d_refs, d_prog, d_qp, B, d_q,
+                 ix->row_w, d_cand, cand_cnt, cap, n_elig};
+    launch_small(sa, bf16, st);
+    ++kernels;
+    mark(4, true);
+    SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
+                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, nullptr, 1, 0};
+    final_select(fa);
+    mark(5, true);
+    HYRE_CUDA(cudaGetLastError());
+    return;
   }
   if (use_fused || all_match) {
   } else if (use_fwd) {

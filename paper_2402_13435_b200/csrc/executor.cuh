@@ -145,6 +145,7 @@ struct Executor {
   // fused CNF in the K3 epilogue (no K1 mask pass): per query group, the
   // term-users program (TcArgs::fz) and its offsets into fz_words
   bool use_fused = false;
+  bool use_small = false;  // K7 single-launch exact scorer (small index, single queries)
   bool all_match = false;  // tensor-core batch of match-all queries only: no eligibility pass
   struct FusedGroup {
     uint32_t entries, n_entries, hc;

@@ -1984,4 +1984,132 @@ void launch_scan_emit(const uint32_t* mask, const QParam* qp, uint32_t B, uint32
   if (W) scan_emit_kernel<<<(W + 7) / 8, 256, 0, st>>>(mask, qp, B, W, row_base, off, batch_ids, out, cap);
 }
 
+// ---------------------------------------------------------------------------
+// K7: single-launch scorer for small indexes (latency-bound
+// single queries).  One CTA per 1024-row segment evaluates the query's CNF
+// words for its segment from the K1 program (dense bitmaps only), compacts the
+// eligible rows, scores them exactly with K2's arithmetic (the lane layout and
+// xor butterfly of rescore_list, so scores equal every other path's bit for
+// bit), keeps its segment's top min(k, n) keys (bitonic sort in shared memory)
+// and appends them to the query's candidate buffer; K4 selects the final top
+// K.  No sample, no thresholds, no recovery: the candidates are exact.
+// ---------------------------------------------------------------------------
+namespace {
+template <typename RowT, int LPR, int CPL>
+__global__ void __launch_bounds__(512) small_topk_kernel(SmallArgs a) {
+  __shared__ uint16_t list[kSegRows];
+  __shared__ uint64_t keys[kSegRows];
+  __shared__ uint32_t s_n, s_base;
+  constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems;
+  const uint32_t seg = blockIdx.x, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane / LPR, li = lane % LPR;
+  const RowT* emb = static_cast<const RowT*>(a.emb);
+  for (uint32_t qi = 0; qi < a.B; ++qi) {
+    const QParam qp = a.qp[qi];
+    if ((qp.flags & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) continue;  // uniform
+    if (wib == 0) {
+      // this segment's 32 mask words (mask_kernel's AND of ORs over the refs)
+      const uint32_t widx = seg * 32 + lane;
+      uint32_t word = 0;
+      if (widx < a.words && !(qp.flags & QF_EMPTY)) {
+        if (qp.flags & QF_MATCH_ALL) {
+          word = tail_mask(widx, a.n_rows);
+        } else {
+          const uint32_t* p = a.prog + qp.prog_off;
+          const uint32_t nc = p[0];
+          uint32_t pos = 1, acc = kFull;
+          for (uint32_t c = 0; c < nc; ++c) {
+            const uint32_t nr = p[pos++];
+            uint32_t cw = 0;
+            for (uint32_t r = 0; r < nr; ++r) cw |= __ldg(a.refs[p[pos + r]] + widx);
+            pos += nr;
+            acc &= cw;
+          }
+          word = acc & tail_mask(widx, a.n_rows);
+        }
+      }
+      const uint32_t c = __popc(word), incl = warp_incl_scan(c, lane);
+      uint32_t pos = incl - c;
+      for (uint32_t u = word; u; u &= u - 1u) list[pos++] = static_cast<uint16_t>(lane * 32 + __ffs(u) - 1);
+      if (lane == 31) s_n = incl;
+    }
+    __syncthreads();
+    const uint32_t n = s_n;
+    if (n == 0) {
+      __syncthreads();
+      continue;
+    }
+    float qv[CPL][E];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+      for (int e = 0; e < E; ++e) qv[c][e] = a.q[static_cast<size_t>(qi) * a.dp + (li + c * LPR) * E + e];
+    const size_t row0 = static_cast<size_t>(seg) * kSegRows;
+    for (uint32_t base = 0; base < n; base += nw * G) {
+      const uint32_t idx = base + wib * G + g;
+      const bool ok = idx < n;
+      const uint32_t lr = ok ? static_cast<uint32_t>(row0) + list[idx] : static_cast<uint32_t>(row0);
+      const RowT* r = emb + static_cast<size_t>(lr) * a.dp;
+      uint4 v[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[c] = ok ? ldg_stream(r + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
+      float acc = 0.0f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[c], qv[c]);
+#pragma unroll
+      for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
+      if (li == 0 && ok) {
+        const float sc = a.row_w ? clamp_score(acc) * __ldg(a.row_w + lr) : clamp_score(acc);
+        keys[idx] = make_key(sc, a.row_base + lr);
+      }
+    }
+    __syncthreads();
+    uint32_t m = n;
+    if (n > qp.k) {  // the segment's top k keys (score desc, row asc)
+      uint32_t p2 = 1;
+      while (p2 < n) p2 <<= 1;
+      for (uint32_t i = n + threadIdx.x; i < p2; i += blockDim.x) keys[i] = 0ull;
+      __syncthreads();
+      bitonic_desc(keys, p2);
+      m = qp.k;
+    }
+    if (threadIdx.x == 0) {
+      s_base = atomicAdd(a.cand_cnt + qi, m);
+      atomicAdd(a.n_elig + qi, n);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+      if (s_base + i < a.cap) a.cand[static_cast<size_t>(qi) * a.cap + s_base + i] = keys[i];
+    __syncthreads();
+  }
+}
+}  // namespace
+
+bool small_supported(uint32_t dp_chunks) {
+  return dp_chunks == 8 || dp_chunks == 16 || dp_chunks == 32 || dp_chunks == 64 || dp_chunks == 128;
+}
+
+void launch_small(const SmallArgs& a, bool bf16, cudaStream_t st) {
+  const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
+  if (a.B == 0 || n_seg == 0) return;
+  using KFn = void (*)(SmallArgs);
+  KFn k = nullptr;
+  const uint32_t cpr = a.dp_chunks;
+#define HYRE_SMALL_PICK(T)                          \
+  k = cpr == 8     ? small_topk_kernel<T, 8, 1>     \
+      : cpr == 16  ? small_topk_kernel<T, 16, 1>    \
+      : cpr == 32  ? small_topk_kernel<T, 32, 1>    \
+      : cpr == 64  ? small_topk_kernel<T, 32, 2>    \
+      : cpr == 128 ? small_topk_kernel<T, 32, 4>    \
+                   : nullptr;
+  if (bf16) {
+    HYRE_SMALL_PICK(__nv_bfloat16)
+  } else {
+    HYRE_SMALL_PICK(float)
+  }
+#undef HYRE_SMALL_PICK
+  if (!k) throw Error(HYRE_INTERNAL, "K7: unsupported row stride");
+  k<<<n_seg, 512, 0, st>>>(a);
+}
+
 }  // namespace hyreb

@@ -275,4 +275,24 @@ void launch_scan_emit(const uint32_t* mask, const QParam* qp, uint32_t B, uint32
                       const uint64_t* off, const uint32_t* batch_ids, hyre_messenger* out, uint64_t cap,
                       cudaStream_t st);
 
+// ---- K7: single-launch exact scorer for small indexes (single queries) ----
+struct SmallArgs {
+  const void* emb;  // fp32 or bf16 rows, stride dp
+  uint32_t dp, dp_chunks, n_rows, row_base, words;
+  const uint32_t* const* refs;  // K1 program refs (dense bitmaps)
+  const uint32_t* prog;
+  const QParam* qp;
+  uint32_t B;
+  const float* q;       // [B][dp] unit queries
+  const float* row_w;   // learned per-row weights or nullptr
+  uint64_t* cand;       // [B][cap] candidate keys (per-segment top k)
+  uint32_t* cand_cnt;   // [B] (zeroed)
+  uint32_t cap;
+  uint32_t* n_elig;     // [B] (zeroed)
+};
+constexpr uint32_t kSmallMaxRows = 262144;  // K7 indexes: n_seg x k candidates fit the buffer
+constexpr uint32_t kSmallMaxK = 256;
+bool small_supported(uint32_t dp_chunks);
+void launch_small(const SmallArgs& a, bool bf16, cudaStream_t st);
+
 }  // namespace hyreb

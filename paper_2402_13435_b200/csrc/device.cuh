@@ -243,5 +243,8 @@ __device__ __forceinline__ float clamp_score(float s) {
   s = fminf(fmaxf(s, -1.0f), 1.0f);
   return s + 0.0f;
 }
+// learned-weight epilogue: w x clamp(s), -0 folded to +0 (a zero weight times
+// a negative score ties with every other zero score, ordered by row)
+__device__ __forceinline__ float weighted_score(float s, float w) { return clamp_score(s) * w + 0.0f; }
 
 }  // namespace hyreb

@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const uint32_t grow = a.row_base + static_cast<uint32_t>(seg_row0) + my_off;
         if (kI8) p[0] *= sc8[j];  // exact int8 dot -> prefilter score
         // weighted: w x clamp(s) (|w s - w s'| <= w delta <= delta keeps the prefilter bound)
-        const float ps = a.row_w ? clamp_score(p[0]) * wr : clamp_score(p[0]);
+        const float ps = a.row_w ? weighted_score(p[0], wr) : clamp_score(p[0]);
         const uint64_t key = make_key(ps, grow);
         if (a.mode == SCORE_SAMPLE) {
           // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
@@ -1261,7 +1261,7 @@ __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys
 #pragma unroll
       for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
       if (li == 0 && idx[u] < n) {
-        const float sc = a.row_w ? clamp_score(acc) * __ldg(a.row_w + (grow[u] - a.row_base)) : clamp_score(acc);
+        const float sc = a.row_w ? weighted_score(acc, __ldg(a.row_w + (grow[u] - a.row_base))) : clamp_score(acc);
         keys[idx[u]] = make_key(sc, grow[u]);
         mine += sc >= thr_s ? 1u : 0u;
       }
@@ -2059,7 +2059,7 @@ __global__ void __launch_bounds__(512) small_topk_kernel(SmallArgs a) {
 #pragma unroll
       for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
       if (li == 0 && ok) {
-        const float sc = a.row_w ? clamp_score(acc) * __ldg(a.row_w + lr) : clamp_score(acc);
+        const float sc = a.row_w ? weighted_score(acc, __ldg(a.row_w + lr)) : clamp_score(acc);
         keys[idx] = make_key(sc, a.row_base + lr);
       }
     }

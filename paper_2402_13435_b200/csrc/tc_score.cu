@@ -750,8 +750,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         };
         // clamped (and weighted: w_r x clamp(s')) score of (row lane, query 32c + j)
         auto final_of = [&](uint32_t w, uint32_t j) {
-          const float x = clamp_score(score_of(w, j));
-          return a.row_w ? x * wr : x;
+          return a.row_w ? weighted_score(score_of(w, j), wr) : clamp_score(score_of(w, j));
         };
         if (a.mode == SCORE_SAMPLE && a.shist) {
           // sample pass, histogram form: one global increment per eligible

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <cstring>
 
 #include <string>
@@ -37,6 +38,37 @@ namespace hyreb {
                                                            : HYRE_CUDA_ERROR,          \
                            std::string(#x) + ": " + cudaGetErrorString(e_));           \
   } while (0)
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// be scheduled while its stream predecessor is still running; it must call
+// pdl_wait() before touching anything the predecessor (or earlier work)
+// writes -- the wait returns once the predecessor grid has completed and its
+// memory is visible.  pdl_trigger() lets the successor's CTAs be scheduled as
+// soon as resources free up (its prologue then overlaps this kernel's tail).
+// Both are no-ops for a normal launch.  HYRE_PDL=0 launches normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_PDL");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  HYRE_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it once
 // per (kernel, device), safe from several host threads (executor pools,

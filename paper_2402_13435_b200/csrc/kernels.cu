@@ -868,6 +868,14 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t digit) {
   if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
     atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
 }
+// 12-bit histogram bin of an orderable score (f2ord): linear in the score
+// over [-1, 1] (2^-11 wide bins), monotone in the key order.  The top 12 key
+// bits would give one bin per (exponent, 3 mantissa bits): cosines in
+// [0.25, 0.5) share 8 bins, so the K-th key's bin held thousands of keys.
+__device__ __forceinline__ uint32_t score_bin(uint32_t ord) {
+  const float sc = ord2f(ord);
+  return static_cast<uint32_t>(fminf(fmaxf((sc + 1.0f) * 2048.0f, 0.0f), 4095.0f));
+}
 // warp-aggregated append of `key` (if take) to dst[*cnt++] (capacity dcap)
 __device__ __forceinline__ void warp_append(bool take, uint64_t key, uint64_t* dst, uint32_t* cnt, uint32_t dcap) {
   const unsigned bal = __ballot_sync(0xffffffffu, take);
@@ -984,7 +992,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
       const uint32_t i = base + threadIdx.x;
       const uint64_t key = i < n ? keys[i] : 0ull;
       if (i < n) res[i] = key;
-      hist_add(hist, i < n ? static_cast<uint32_t>(key >> 52) : 0xffffffffu);
+      hist_add(hist, i < n ? score_bin(static_cast<uint32_t>(key >> 32)) : 0xffffffffu);
     }
     __syncthreads();
     kth_bins(hist, k, k, tmp, s_sel);
@@ -993,7 +1001,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
       for (uint32_t base = 0; base < n; base += blockDim.x) {
         const uint32_t i = base + threadIdx.x;
         const uint64_t key = i < n ? res[i] : 0ull;
-        warp_append(i < n && static_cast<uint32_t>(key >> 52) >= dk, key, sortbuf, &gathered, kSelectMaxK);
+        warp_append(i < n && score_bin(static_cast<uint32_t>(key >> 32)) >= dk, key, sortbuf, &gathered, kSelectMaxK);
       }
       __syncthreads();
       m = gathered;
@@ -1067,10 +1075,10 @@ __global__ void __launch_bounds__(kSelThreads) sample_slice_kernel(SelectArgs a,
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kSampleVec; ++u) {
-    hist_add(hist, v[u].x ? v[u].x >> 20 : 0xffffffffu);
-    hist_add(hist, v[u].y ? v[u].y >> 20 : 0xffffffffu);
-    hist_add(hist, v[u].z ? v[u].z >> 20 : 0xffffffffu);
-    hist_add(hist, v[u].w ? v[u].w >> 20 : 0xffffffffu);
+    hist_add(hist, v[u].x ? score_bin(v[u].x) : 0xffffffffu);
+    hist_add(hist, v[u].y ? score_bin(v[u].y) : 0xffffffffu);
+    hist_add(hist, v[u].z ? score_bin(v[u].z) : 0xffffffffu);
+    hist_add(hist, v[u].w ? score_bin(v[u].w) : 0xffffffffu);
   }
   __syncthreads();
   const uint32_t nnz = kth_bins(hist, r, r, tmp, s_sel);
@@ -1084,7 +1092,7 @@ __global__ void __launch_bounds__(kSelThreads) sample_slice_kernel(SelectArgs a,
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t slot = b0 + e, local = (slot >> 10) * a.period * 1024u + (slot & 1023u);
-      warp_append(o[e] != 0u && (o[e] >> 20) >= dsel,
+      warp_append(o[e] != 0u && score_bin(o[e]) >= dsel,
                   (static_cast<uint64_t>(o[e]) << 32) | static_cast<uint32_t>(~(a.row_base + local)), dst, ucnt + q,
                   a.fb_cap);
     }
@@ -1138,6 +1146,8 @@ void launch_sample_kth(const SelectArgs& a, uint32_t* ucnt, cudaStream_t st) {
 __global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
   __shared__ uint32_t tmp[40];
   __shared__ uint32_t s_bin[2];
+  pdl_trigger();
+  pdl_wait();  // the sample pass's histograms
   const uint32_t q = blockIdx.x;
   const QParam qp = a.qp[q];
   const bool on = (qp.flags & a.require_flags) == a.require_flags && a.n_elig[q] > a.gate;
@@ -1181,6 +1191,7 @@ __global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
 }
 
 __global__ void run_init_kernel(uint32_t* counters, uint32_t n_counters, uint32_t B, uint4* hist, size_t hist_vec) {
+  pdl_trigger();  // the K3 sample pass may set up while the counters are zeroed
   const size_t stride = size_t{gridDim.x} * blockDim.x;
   const size_t t0 = size_t{blockIdx.x} * blockDim.x + threadIdx.x;
   for (size_t i = t0; i < n_counters; i += stride) counters[i] = i < B ? 0xFFFFFFFFu : 0u;
@@ -1196,7 +1207,7 @@ void launch_run_init(uint32_t* counters, uint32_t n_counters, uint32_t B, uint32
 
 void launch_hist_thr(const HistThrArgs& a, cudaStream_t st) {
   if (a.B == 0) return;
-  hist_thr_kernel<<<a.B, 256, 0, st>>>(a);
+  launch_pdl(hist_thr_kernel, dim3(a.B), dim3(256), 0, st, a);
 }
 
 void launch_select(const SelectArgs& a, cudaStream_t st) {
@@ -1276,6 +1287,7 @@ __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys
 constexpr int kSelPThreads = 1024;  // K4p: more warps -> more survivor rows in flight
 template <typename RowT, int LPR, int CPL>
 __global__ void __launch_bounds__(kSelPThreads) select_prefilter_kernel(PrefSelectArgs pa) {
+  pdl_wait();  // the main pass's candidates
   const SelectArgs& a = pa.s;
   extern __shared__ uint64_t sel_smem[];
   uint64_t* sortbuf = sel_smem;                                          // kSelectMaxK keys
@@ -1427,7 +1439,7 @@ void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_
   const int vi = cpr == 8 ? 0 : cpr == 16 ? 1 : cpr == 32 ? 2 : cpr == 64 ? 3 : cpr == 128 ? 4 : 5;
   set_smem_limit(reinterpret_cast<const void*>(k), static_cast<int>(smem),
                  attr_set[std::is_same<RowT, float>::value ? 0 : 1][vi]);
-  k<<<a.s.B, kSelPThreads, smem, st>>>(a);
+  launch_pdl(k, dim3(a.s.B), dim3(kSelPThreads), smem, st, a);
 }
 }  // namespace
 

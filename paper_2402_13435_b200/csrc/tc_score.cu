@@ -410,13 +410,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
   uint32_t* s_flive = s_fhc + a.C * NCH;
   uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
 
-  const uint32_t q0 = a.q0;
-  // Any active query in this group?  One query per thread, then a block vote
-  // (uniform early exit before TMEM allocation; keeps no-op rerun launches cheap).
-  bool mine = false;
-  for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) mine |= tc_active(a, q0 + j);
-  if (!__syncthreads_or(mine)) return;
-
+  pdl_trigger();  // the next kernel of the run may set up while this one streams
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
@@ -439,6 +433,35 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (kFused) {
+    for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
+    for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < n_tbl; t += blockDim.x) {  // unlisted term: v = hc of its slot
+      uint32_t* e = s_ftbl + t * NCH;
+#pragma unroll
+      for (uint32_t c = 0; c < NCH; ++c) {
+        uint32_t x = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;  // sentinel / PAD: AND identity
+        if (W && t >= a.T && t < a.T + a.C) x = s_fhc[(t - a.T) * NCH + c];  // EMPTY_g: queries constraining g
+        if (W && t == 0xFEu) x = 0u;                                          // NONE: no constraint
+        e[c] = x;
+      }
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {  // listed terms: v = hc & ~users
+      const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + NCH);
+#pragma unroll
+      for (uint32_t c = 0; c < NCH; ++c) s_ftbl[en[0] * NCH + c] = en[1 + c];
+    }
+  }
+  pdl_wait();  // everything below reads what earlier kernels of the run wrote
+  const uint32_t q0 = a.q0;
+  // Any active query in this group?  One query per thread, then a block vote
+  // (uniform early exit before TMEM allocation; keeps no-op rerun launches cheap).
+  bool mine = false;
+  for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) mine |= tc_active(a, q0 + j);
+  if (!__syncthreads_or(mine)) return;
+
   // key >= thr  <=>  score > ts || (score == ts && row <= tr)   (make_key order)
   for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) {
     const bool on = tc_active(a, q0 + j);
@@ -479,27 +502,6 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
   if (warp < Np / 32) {  // one ballot per 32-query chunk (parallel loads, not 32 serial ones)
     const uint32_t m = __ballot_sync(0xffffffffu, tc_active(a, q0 + warp * 32 + lane));
     if (lane == 0) s_act[warp] = m;
-  }
-  if (kFused) {
-    for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
-    for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < n_tbl; t += blockDim.x) {  // unlisted term: v = hc of its slot
-      uint32_t* e = s_ftbl + t * NCH;
-#pragma unroll
-      for (uint32_t c = 0; c < NCH; ++c) {
-        uint32_t x = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;  // sentinel / PAD: AND identity
-        if (W && t >= a.T && t < a.T + a.C) x = s_fhc[(t - a.T) * NCH + c];  // EMPTY_g: queries constraining g
-        if (W && t == 0xFEu) x = 0u;                                          // NONE: no constraint
-        e[c] = x;
-      }
-    }
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {  // listed terms: v = hc & ~users
-      const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + NCH);
-#pragma unroll
-      for (uint32_t c = 0; c < NCH; ++c) s_ftbl[en[0] * NCH + c] = en[1 + c];
-    }
   }
   const uint32_t tmem_cols = a.tmem_cols;
   if (warp == 1) {
@@ -996,7 +998,8 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
     if (ri < 0) throw Error(HYRE_INTERNAL, "fused CNF: unsupported compact row shape");
     k = fused[ri][ci];
   }
-  k<<<grid, threads_for(a.fused != 0, static_cast<int>(tc_fused_chunks(a.Np))), smem, st>>>(qhi, qlo, a);
+  launch_pdl(k, dim3(grid), dim3(threads_for(a.fused != 0, static_cast<int>(tc_fused_chunks(a.Np)))), smem, st, qhi,
+             qlo, a);
 }
 
 }  // namespace hyreb

@@ -38,10 +38,11 @@ T* dmalloc(size_t n) {
   return p;
 }
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-uint32_t tc_debug_flags() {  // HYRE_TC_DEBUG: profiling experiments only
+uint32_t tc_debug_flags() {  // HYRE_TC_DEBUG: profiling experiments only; HYRE_TC_BIAS=0: IADD threshold compare
   static const uint32_t v = [] {
     const char* e = std::getenv("HYRE_TC_DEBUG");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    const char* b = std::getenv("HYRE_TC_BIAS");
+    return (e ? static_cast<uint32_t>(std::atoi(e)) : 0u) | (b && std::string(b) == "0" ? 0x200u : 0u);
   }();
   return v;
 }

@@ -152,6 +152,16 @@ __device__ __forceinline__ void mma_i8w(uint32_t d_tmem, uint32_t a_lo, uint32_t
       "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "n"(0x40004040));
 }
 
+// int8 MMA with explicit 64-bit descriptors (the bias K-step's SWIZZLE_NONE
+// operands: lo = start >> 4 | LBO >> 4 << 16, hi = SBO >> 4 | version 1)
+__device__ __forceinline__ void mma_i8d(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                        uint32_t idesc) {
+  asm volatile(
+      "{\n .reg .b64 da, db;\n mov.b64 da, {%1, %2};\n mov.b64 db, {%3, %4};\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, 1;\n}" ::"r"(d_tmem),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc));
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -296,21 +306,32 @@ __device__ __forceinline__ void cnf_row(const uint32_t (&tw)[J * TB / 4], uint64
 // table words -- one LOP3 per id after the first and one OR per group and
 // chunk, no segment masks, no missing-slot loop (EMPTY_g entries carry hc_g).
 template <int J, int W, int NCH, int NT, int JWN>
-__device__ __forceinline__ void cnf_row_grouped(const uint32_t (&tw)[JWN], uint32_t tbl,
+__device__ __forceinline__ void cnf_row_grouped(const uint32_t (&tw)[JWN], const uint32_t* __restrict__ tbl8,
                                                 uint32_t live, uint32_t c0, uint32_t (&out)[NT]) {
+  // entry byte offset id x (NCH x 4) straight from the packed id word: one
+  // shift and one mask per id; the static table's address folds into the
+  // load's immediate (c0 = 0 whenever a thread owns every chunk)
+  constexpr int kSh = NCH == 1 ? 2 : (NCH == 2 ? 3 : (NCH == 4 ? 4 : 5));
+  constexpr uint32_t kMask = 0xFFu << kSh;
+  const uint32_t* base = NT == NCH ? tbl8 : tbl8 + c0;
   uint32_t v[J][NT];
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const uint32_t id = (tw[j >> 2] >> ((j & 3) * 8)) & 0xFFu;
-    const uint32_t e = tbl + (id * NCH + c0) * 4;
+    const int sh = (j & 3) * 8 - kSh;
+    const uint32_t off = (sh >= 0 ? (tw[j >> 2] >> sh) : (tw[j >> 2] << -sh)) & kMask;  // bytes
+    const uint32_t* e = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(base) + off);
     if (NT == 1) {
-      asm("ld.shared.u32 %0, [%1];" : "=r"(v[j][0]) : "r"(e));
+      v[j][0] = e[0];
     } else if (NT == 2) {
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[j][0]), "=r"(v[j][NT - 1]) : "r"(e));
+      const uint2 x = *reinterpret_cast<const uint2*>(e);
+      v[j][0] = x.x;
+      v[j][NT - 1] = x.y;
     } else {
-      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-          : "=r"(v[j][0]), "=r"(v[j][1 % NT]), "=r"(v[j][2 % NT]), "=r"(v[j][3 % NT])
-          : "r"(e));
+      const uint4 x = *reinterpret_cast<const uint4*>(e);
+      v[j][0] = x.x;
+      v[j][1 % NT] = x.y;
+      v[j][2 % NT] = x.z;
+      v[j][3 % NT] = x.w;
     }
   }
   uint32_t fail[NT];
@@ -409,6 +430,14 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
                                         : s_ftbl + static_cast<size_t>(n_tbl) * NCH;
   uint32_t* s_flive = s_fhc + a.C * NCH;
   uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
+  // int8 threshold bias (one extra K step adds -T_q to every accumulator, so
+  // the epilogue tests the sign directly): A' = 256 B (one row pattern, every
+  // 8-row group aliased: SBO 0), B' = Np x 32 B (K-major, SWIZZLE_NONE), then
+  // the per-query bias S_q = -T_q (int)
+  uint8_t* bias_base = kFused ? s_fslot + a.T + 1 : s_terms;
+  uint8_t* s_bias_a = bias_base + ((128u - (smem_u32(bias_base) & 127u)) & 127u);
+  uint8_t* s_bias_b = s_bias_a + 256;
+  int32_t* s_bias_s = reinterpret_cast<int32_t*>(s_bias_b + Np * 32);
 
   pdl_trigger();  // the next kernel of the run may set up while this one streams
   if (threadIdx.x == 0) {
@@ -498,6 +527,47 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
       s_ts[j] = __int_as_float(T);
     }
   }
+  // threshold bias: S_q = -T_q as b0 + 127 (b1 + ... + b31) against the row
+  // pattern (1, 127, ..., 127); |S| <= 500062.  "No threshold" needs S above
+  // every possible -acc (|acc| <= (1 + delta_q) / scale_q).  Main / rerun
+  // passes of the unweighted int8 prefilter only; otherwise the IADD compare.
+  bool bias_ok = a.i8 && !a.row_w && a.mode != SCORE_SAMPLE && !(a.debug & 0x3FFu);
+  constexpr int32_t kBiasMax = 3937 * 127 + 63;
+  for (uint32_t j = threadIdx.x; j < Np && bias_ok; j += blockDim.x) {
+    const int32_t T = __float_as_int(s_ts[j]);
+    int32_t S = 0;
+    if (T == INT32_MAX) {
+      S = 0;  // inactive: never eligible
+    } else if (T == INT32_MIN / 2) {
+      const float dl = a.qdelta ? a.qdelta[q0 + j] : a.delta;
+      if ((1.0f + dl) / s_sc[j] + 2.0f > static_cast<float>(kBiasMax)) bias_ok = false;
+      S = kBiasMax;
+    } else if (T > kBiasMax || T < -kBiasMax) {
+      bias_ok = false;
+    } else {
+      S = -T;
+    }
+    s_bias_s[j] = S;
+    // B' row j: b0 = r, b1..b31 carry m (S = 127 m + r, |r| <= 63)
+    const int32_t m = (S >= 0 ? S + 63 : S - 63) / 127, r = S - 127 * m;
+    int8_t b[32];
+    b[0] = static_cast<int8_t>(r);
+    int32_t left = m;
+    for (int k = 1; k < 32; ++k) {
+      const int32_t x = left > 127 ? 127 : (left < -127 ? -127 : left);
+      b[k] = static_cast<int8_t>(x);
+      left -= x;
+    }
+    uint8_t* row = s_bias_b + (j / 8) * 256 + (j % 8) * 16;
+    for (int k = 0; k < 16; ++k) {
+      row[k] = static_cast<uint8_t>(b[k]);
+      row[128 + k] = static_cast<uint8_t>(b[16 + k]);
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)  // A': rows (1, 127, ..., 127)
+    s_bias_a[i] = (i < 128u && (i & 15u) == 0u) ? 1u : 127u;
+  const uint32_t bias_on = __syncthreads_and(bias_ok) ? 1u : 0u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // st.shared operands -> the tensor core
   for (uint32_t j = threadIdx.x; j < Np; j += blockDim.x) s_scnt[j] = 0;
   if (warp < Np / 32) {  // one ballot per 32-query chunk (parallel loads, not 32 serial ones)
     const uint32_t m = __ballot_sync(0xffffffffu, tc_active(a, q0 + warp * 32 + lane));
@@ -598,6 +668,9 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
               if (a.split) mma_bf16w(d, ka + ((aps * a_bytes) >> 4) + 2 * kk, qh_lo0 + kq + 2 * kk, idesc, 1u);
             }
           }
+          if (bias_on && k0 + aps >= kb)  // + (-T_q): the accumulator's sign is the threshold test
+            mma_i8d(d, (smem_u32(s_bias_a) >> 4) | (8u << 16), 0x4000u, (smem_u32(s_bias_b) >> 4) | (8u << 16),
+                    0x4000u | 16u, idesc);
           mma_commit(empty + s);  // this stage is free once its MMAs retire
         }
         __syncwarp();
@@ -707,7 +780,10 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         // monotone rounding) and a funnel shift collecting d's sign bit.
         uint32_t below = 0;  // bit 31 - j: query 32c + j scored below its threshold
         const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
-        if (a.i8 && a.row_w) {  // weighted: acc x W_r - 256 T (one IMAD per score)
+        if (bias_on) {  // the MMA added -T_q: one funnel shift per score collects the sign
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j) below = __funnelshift_l(v[j], below, 1);
+        } else if (a.i8 && a.row_w) {  // weighted: acc x W_r - 256 T (one IMAD per score)
 #pragma unroll
           for (uint32_t j4 = 0; j4 < 8; ++j4) {
             const int4 t4 = *reinterpret_cast<const int4*>(ts4 + j4);
@@ -748,7 +824,8 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
                                                : (__brev(~below) & elig);
         // prefilter score of (row lane, query 32c + j) from the accumulator word
         auto score_of = [&](uint32_t w, uint32_t j) {
-          return a.i8 ? static_cast<float>(static_cast<int32_t>(w)) * s_sc[c * 32 + j] : __uint_as_float(w);
+          const int32_t acc = static_cast<int32_t>(w) - (bias_on ? s_bias_s[c * 32 + j] : 0);
+          return a.i8 ? static_cast<float>(acc) * s_sc[c * 32 + j] : __uint_as_float(w);
         };
         // clamped (and weighted: w_r x clamp(s')) score of (row lane, query 32c + j)
         auto final_of = [&](uint32_t w, uint32_t j) {
@@ -850,7 +927,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
 #pragma unroll
         for (int c = 0; c < NT; ++c) el[c] = s_flive[c0 + c] ^ (tw[0] & 1u) ^ static_cast<uint32_t>(masks & 2u);
       } else if constexpr (W > 0) {
-        cnf_row_grouped<J, W, NCH, NT, JW>(tw, smem_u32(s_ftbl), smem_u32(s_flive), c0, el);
+        cnf_row_grouped<J, W, NCH, NT, JW>(tw, s_tbl8, smem_u32(s_flive), c0, el);
       } else {
         cnf_row<(kFused ? J : 8), (kFused ? TB : 1), NCH, NT>(tw, masks, a.T, smem_u32(s_ftbl), smem_u32(s_fhc),
                                                              smem_u32(s_flive), cslots, c0, el);
@@ -928,7 +1005,7 @@ uint32_t tc_tmem_cols(uint32_t Np) {
 size_t tc_smem_bytes(uint32_t Np, uint32_t kb, uint32_t n_ops, uint32_t stages, size_t fused_bytes, uint32_t q_planes,
                      uint32_t aps) {
   return 1024 + size_t{q_planes} * Np * 128 * kb + size_t{stages} * aps * n_ops * kAtomBytes + (2 * stages + 2 * kAccBufs + 2) * 8 + Np * 12 +
-         4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes;
+         4 + 32 + Np * 4 + 16 + stage_bytes_for(Np) + 64 + fused_bytes + (128 + 256 + size_t{Np} * 36);  // + bias operands
 }
 
 uint32_t tc_fused_chunks(uint32_t Np) { return Np <= 32 ? 1u : (Np <= 64 ? 2u : (Np <= 128 ? 4u : 8u)); }

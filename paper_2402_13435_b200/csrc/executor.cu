@@ -380,12 +380,18 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   // fitting the candidate buffer
   use_small = false;
   if (!use_tc && any_emb && !any_term_only && !use_fwd && scatter_total == 0 && big_k.empty() && small_enabled() &&
-      ix->n_rows <= kSmallMaxRows && max_k <= kSmallMaxK &&
+      ix->n_rows <= kSmallMaxRows && max_k <= kSmallMaxK && ix->num_clauses <= kSmallClauses &&
       uint64_t{(ix->n_rows + kSegRows - 1) / kSegRows} * max_k <= cap &&
       small_supported(ix->dp * (ix->emb_dtype == HYRE_EMB_BF16 ? 2 : 4) / 16)) {
     use_small = true;
-    for (uint32_t i = 0; i < b; ++i)
+    for (uint32_t i = 0; i < b; ++i) {
       if ((qp[i].flags & QF_QUANT) && qp[i].quant_k < ix->n_rows) use_small = false;
+      if ((qp[i].flags & QF_ACTIVE) && !(qp[i].flags & (QF_MATCH_ALL | QF_EMPTY))) {
+        size_t pos = qp[i].prog_off + 1;  // program: n_clauses, {n_refs, ref...}*
+        for (uint32_t c = 0; c < prog[qp[i].prog_off]; ++c) pos += 1 + prog[pos];
+        if (pos - qp[i].prog_off > kSmallProg) use_small = false;  // K7 stages at most kSmallProg words
+      }
+    }
   }
   if (use_small) prefilter = pf_i8 = false;  // exact scores straight from the rows
   if (use_tc) {
@@ -963,7 +969,8 @@ void Executor::run() {
     mark(3, false);
     const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
     SmallArgs sa{bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
-                 ix->dp * (bf16 ? 2 : 4) / 16, ix->n_rows, ix->row_base, W, d_refs, d_prog, d_qp, B, d_q,
+                 ix->dp * (bf16 ? 2 : 4) / 16, ix->n_rows, ix->row_base, W, d_refs, d_prog,
+                 static_cast<uint32_t>(prog.size()), static_cast<uint32_t>(refs.size()), d_qp, B, d_q,
                  ix->row_w, d_cand, cand_cnt, cap, n_elig};
     launch_small(sa, bf16, st);
     ++kernels;

@@ -1022,17 +1022,31 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     __syncthreads();
     m = min(gathered, kSelectMaxK);
   }
-  uint32_t m2 = 1;
-  while (m2 < m) m2 <<= 1;
-  for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
-  __syncthreads();
-  bitonic_desc(sortbuf, m2);
   const uint32_t take = min(m, k);
   hyre_hit* out = a.hits + a.hit_off[q];
-  for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
-    const uint64_t key = sortbuf[i];
-    out[i].row = key_row(key);
-    out[i].score = key_score(key);
+  if (m <= 1024) {
+    // rank by counting (keys are unique): no sort stages, one pass over the
+    // gathered keys per key (broadcast shared reads)
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint64_t key = sortbuf[i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) rank += sortbuf[j] > key ? 1u : 0u;
+      if (rank < take) {
+        out[rank].row = key_row(key);
+        out[rank].score = key_score(key);
+      }
+    }
+  } else {
+    uint32_t m2 = 1;
+    while (m2 < m) m2 <<= 1;
+    for (uint32_t i = m + threadIdx.x; i < m2; i += blockDim.x) sortbuf[i] = 0ull;
+    __syncthreads();
+    bitonic_desc(sortbuf, m2);
+    for (uint32_t i = threadIdx.x; i < take; i += blockDim.x) {
+      const uint64_t key = sortbuf[i];
+      out[i].row = key_row(key);
+      out[i].score = key_score(key);
+    }
   }
   if (threadIdx.x == 0) {
     a.out_cnt[q] = take;
@@ -2011,7 +2025,11 @@ template <typename RowT, int LPR, int CPL>
 __global__ void __launch_bounds__(512) small_topk_kernel(SmallArgs a) {
   __shared__ uint16_t list[kSegRows];
   __shared__ uint64_t keys[kSegRows];
-  __shared__ uint32_t s_n, s_base;
+  __shared__ uint32_t s_n, s_base, s_nc;
+  __shared__ uint32_t s_prog[kSmallProg];
+  __shared__ const uint32_t* s_refs[kSmallRefs];
+  __shared__ uint32_t s_cl[kSmallClauses];
+  __shared__ uint32_t s_cw[kSmallClauses][32];
   constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems;
   const uint32_t seg = blockIdx.x, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = lane / LPR, li = lane % LPR;
@@ -2019,24 +2037,48 @@ __global__ void __launch_bounds__(512) small_topk_kernel(SmallArgs a) {
   for (uint32_t qi = 0; qi < a.B; ++qi) {
     const QParam qp = a.qp[qi];
     if ((qp.flags & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) continue;  // uniform
+    // this segment's 32 mask words (mask_kernel's AND of ORs over the refs):
+    // the query's program and the batch's ref pointers are staged in shared
+    // memory, then one warp per clause ORs its refs' words (independent
+    // loads in flight) and warp 0 ANDs the clauses
+    const uint32_t widx = seg * 32 + lane;
+    const bool constrained = !(qp.flags & (QF_EMPTY | QF_MATCH_ALL));
+    if (constrained) {
+      const uint32_t L = min(kSmallProg, a.prog_words - qp.prog_off);
+      for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) s_prog[i] = a.prog[qp.prog_off + i];
+      for (uint32_t i = threadIdx.x; i < min(a.n_refs, kSmallRefs); i += blockDim.x) s_refs[i] = a.refs[i];
+      __syncthreads();
+      if (threadIdx.x == 0) {  // clause layout: first ref index and ref count
+        const uint32_t nc = min(s_prog[0], kSmallClauses);
+        uint32_t pos = 1;
+        for (uint32_t c = 0; c < nc; ++c) {
+          const uint32_t nr = pos < L ? s_prog[pos] : 0u;
+          s_cl[c] = (pos + 1) | (min(nr, L - min(L, pos + 1)) << 16);
+          pos += 1 + nr;
+        }
+        s_nc = nc;
+      }
+      __syncthreads();
+      for (uint32_t c = wib; c < s_nc; c += nw) {
+        const uint32_t first = s_cl[c] & 0xFFFFu, nr = s_cl[c] >> 16;
+        uint32_t cw = 0;
+        if (widx < a.words)
+          for (uint32_t r = 0; r < nr; ++r) {
+            const uint32_t ref = s_prog[first + r];
+            cw |= __ldg((ref < kSmallRefs ? s_refs[ref] : a.refs[ref]) + widx);
+          }
+        s_cw[c][lane] = cw;
+      }
+      __syncthreads();
+    }
     if (wib == 0) {
-      // this segment's 32 mask words (mask_kernel's AND of ORs over the refs)
-      const uint32_t widx = seg * 32 + lane;
       uint32_t word = 0;
       if (widx < a.words && !(qp.flags & QF_EMPTY)) {
         if (qp.flags & QF_MATCH_ALL) {
           word = tail_mask(widx, a.n_rows);
         } else {
-          const uint32_t* p = a.prog + qp.prog_off;
-          const uint32_t nc = p[0];
-          uint32_t pos = 1, acc = kFull;
-          for (uint32_t c = 0; c < nc; ++c) {
-            const uint32_t nr = p[pos++];
-            uint32_t cw = 0;
-            for (uint32_t r = 0; r < nr; ++r) cw |= __ldg(a.refs[p[pos + r]] + widx);
-            pos += nr;
-            acc &= cw;
-          }
+          uint32_t acc = kFull;
+          for (uint32_t c = 0; c < s_nc; ++c) acc &= s_cw[c][lane];
           word = acc & tail_mask(widx, a.n_rows);
         }
       }

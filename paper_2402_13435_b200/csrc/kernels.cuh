@@ -281,6 +281,7 @@ struct SmallArgs {
   uint32_t dp, dp_chunks, n_rows, row_base, words;
   const uint32_t* const* refs;  // K1 program refs (dense bitmaps)
   const uint32_t* prog;
+  uint32_t prog_words, n_refs;  // program length (all queries), refs in the table
   const QParam* qp;
   uint32_t B;
   const float* q;       // [B][dp] unit queries
@@ -292,6 +293,9 @@ struct SmallArgs {
 };
 constexpr uint32_t kSmallMaxRows = 262144;  // K7 indexes: n_seg x k candidates fit the buffer
 constexpr uint32_t kSmallMaxK = 256;
+constexpr uint32_t kSmallProg = 1024;   // program words staged per query (K7 requires a shorter program)
+constexpr uint32_t kSmallRefs = 512;    // ref pointers staged in shared memory
+constexpr uint32_t kSmallClauses = 32;  // clause slots (hyre_index num_clauses <= 32)
 bool small_supported(uint32_t dp_chunks);
 void launch_small(const SmallArgs& a, bool bf16, cudaStream_t st);
 

@@ -1024,6 +1024,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
   }
   const uint32_t take = min(m, k);
   hyre_hit* out = a.hits + a.hit_off[q];
+  __syncthreads();  // sortbuf complete (the n <= k path fills it without a barrier)
   if (m <= 1024) {
     // rank by counting (keys are unique): no sort stages, one pass over the
     // gathered keys per key (broadcast shared reads)

@@ -988,11 +988,19 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
     if (threadIdx.x == 0) gathered = 0;
     __syncthreads();
-    for (uint32_t base = 0; base < n; base += blockDim.x) {
-      const uint32_t i = base + threadIdx.x;
-      const uint64_t key = i < n ? keys[i] : 0ull;
-      if (i < n) res[i] = key;
-      hist_add(hist, i < n ? score_bin(static_cast<uint32_t>(key >> 32)) : 0xffffffffu);
+    for (uint32_t base = 0; base < n; base += 4 * blockDim.x) {  // four independent loads in flight
+      uint64_t kv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        kv[u] = i < n ? keys[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        if (i < n) res[i] = kv[u];
+        hist_add(hist, i < n ? score_bin(static_cast<uint32_t>(kv[u] >> 32)) : 0xffffffffu);
+      }
     }
     __syncthreads();
     kth_bins(hist, k, k, tmp, s_sel);

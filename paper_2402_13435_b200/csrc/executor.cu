@@ -394,6 +394,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     }
   }
   if (use_small) prefilter = pf_i8 = false;  // exact scores straight from the rows
+  // a K2 batch whose embedding queries are all match-all needs no K1 mask:
+  // K2 uses tail masks and n_elig starts at the shard's row count
+  k2_match_all = !use_tc && !use_small && any_emb && !any_term_only && !any_quant && scatter_total == 0;
+  for (uint32_t i = 0; i < b && k2_match_all; ++i)
+    if ((qp[i].flags & QF_ACTIVE) && !(qp[i].flags & QF_MATCH_ALL)) k2_match_all = false;
   if (use_tc) {
     // one group of up to 256 queries per pass (the epilogue works in 32-column
     // chunks); a group must leave room for a >= 3-stage ring next to its
@@ -551,7 +556,14 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
   const size_t o_qsc = place(b * 4);
   const size_t o_qdl = place(b * 4);
   const size_t o_fz = place(std::max<size_t>(fz_words.size(), 1) * 4);
+  o_cinit = place(size_t{max_batch} * kNumCounters * 4);
   ensure_blob(off);
+  {  // counter image of a k2_match_all run: n_elig = rows for the active queries, the rest 0
+    uint32_t* ci = reinterpret_cast<uint32_t*>(h_blob + o_cinit);
+    std::memset(ci, 0, size_t{max_batch} * kNumCounters * 4);
+    for (uint32_t i = 0; i < b; ++i)
+      if ((qp[i].flags & (QF_ACTIVE | QF_MATCH_ALL)) == (QF_ACTIVE | QF_MATCH_ALL)) ci[i] = ix->n_rows;
+  }
   std::memcpy(h_blob + o_qp, qp.data(), b * sizeof(QParam));
   std::memcpy(h_blob + o_q, qvec.data(), qvec.size() * 4);
   std::memcpy(h_blob + o_qsig, qsig.data(), qsig.size() * 8);
@@ -690,6 +702,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
   ScoreArgs sa{emb, ix->dp, dp_chunks, ix->n_rows, ix->row_base, ix->words, d_mask, d_qp, d_q, B, n_elig,
                d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp, 1, 1};
   sa.row_w = ix->row_w;
+  sa.match_all = k2_match_all ? 1u : 0u;
   if (pf_i8) {  // int8 prefilter rows (exact rescoring in K4p)
     sa.emb = ix->tc_i8;
     sa.qi8 = d_qi8;
@@ -958,6 +971,9 @@ void Executor::run() {
     launch_run_init(d_counters, max_batch * kNumCounters, B, hist_sample ? d_shist : nullptr,
                     size_t{B} * kHistBins, st);
     ++kernels;
+  } else if (k2_match_all) {
+    HYRE_CUDA(cudaMemcpyAsync(d_counters, d_blob + o_cinit, sizeof(uint32_t) * max_batch * kNumCounters,
+                              cudaMemcpyDeviceToDevice, st));
   } else {
     HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
     if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
@@ -998,7 +1014,7 @@ void Executor::run() {
                    d_scratch, W, st);
     ++kernels;
   }
-  if (!use_fwd && !use_fused && !all_match) {
+  if (!use_fwd && !use_fused && !all_match && !k2_match_all) {
     MaskArgs ma{d_refs, static_cast<uint32_t>(refs.size()), d_prog, d_qp, B, W, ix->n_chunks, ix->n_rows,
                 d_mask, d_chunk_cnt, n_elig};
     const uint32_t ml = launch_mask_tm(ma, prog_groups, prog_live, st);
@@ -1008,7 +1024,7 @@ void Executor::run() {
     }
     kernels += ml & 0x7fffffffu;
   }
-  mark(1, !use_fused && !all_match);  // K1/K1b mask pass (the K3 init kernel is attributed to the sample stage)
+  mark(1, !use_fused && !all_match && !k2_match_all);  // K1/K1b mask pass (the K3 init kernel is attributed to the sample stage)
   if (any_quant) {
     HYRE_CUDA(cudaMemsetAsync(d_qhist, 0, sizeof(uint32_t) * B * (ix->num_bits + 1), st));
     QuantArgs qa{ix->sigs, ix->num_words, ix->num_bits, d_qsig, d_qp, B, W, ix->n_chunks, ix->n_rows,
@@ -1261,7 +1277,7 @@ void Executor::exhaustive(uint32_t i) {
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
   uint64_t n = 0;
-  if (!use_fused && !all_match) {
+  if (!use_fused && !all_match && !k2_match_all) {
     uint32_t ne = 0;
     HYRE_CUDA(cudaMemcpyAsync(&ne, d_counters + i, 4, cudaMemcpyDeviceToHost, st));
     HYRE_CUDA(cudaStreamSynchronize(st));

@@ -147,6 +147,8 @@ struct Executor {
   bool use_fused = false;
   bool use_small = false;  // K7 single-launch exact scorer (small index, single queries)
   bool all_match = false;  // tensor-core batch of match-all queries only: no eligibility pass
+  bool k2_match_all = false;  // K2 batch of match-all queries only: no K1 mask (tail masks in K2)
+  size_t o_cinit = 0;         // blob offset of the counter image of a k2_match_all run
   struct FusedGroup {
     uint32_t entries, n_entries, hc;
   };

@@ -555,8 +555,9 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
     uint32_t uni = 0;
 #pragma unroll
     for (int j = 0; j < QG; ++j) {
-      wq[j] = ((act >> j & 1u) && widx < a.words && in_part) ? a.mask[static_cast<size_t>(q0 + j) * a.words + widx]
-                                                            : 0u;
+      wq[j] = ((act >> j & 1u) && widx < a.words && in_part)
+                  ? (a.match_all ? tail_mask(widx, a.n_rows) : a.mask[static_cast<size_t>(q0 + j) * a.words + widx])
+                  : 0u;
       uni |= wq[j];
     }
     const uint32_t cnt = __popc(uni);

@@ -91,6 +91,7 @@ struct ScoreArgs {
   // learned per-row weights (local rows; nullptr = identity): every score and
   // prefilter score is w[r] x clamp(s).  w <= 1 keeps the prefilter bound.
   const float* row_w;
+  uint32_t match_all;  // every active query is match-all: tail masks, no K1 mask
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 void launch_score_i8(const ScoreArgs& a, cudaStream_t st);

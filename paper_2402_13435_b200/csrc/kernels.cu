@@ -1187,16 +1187,44 @@ __global__ void __launch_bounds__(256) hist_thr_kernel(HistThrArgs a) {
   // from the top score down, so the exclusive prefix counts the rows above
   const uint32_t per = a.nb / blockDim.x, hi = a.nb - threadIdx.x * per;
   const uint32_t* h = a.hist + static_cast<size_t>(q) * a.nb;
+  // the thread's 16 bins (nb = 4096, 256 threads) in four vector loads, kept
+  // in registers for both passes
+  uint32_t c16[16];
+  if (per == 16) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint4 x = *reinterpret_cast<const uint4*>(h + hi - 16 + 4 * v);
+      c16[4 * v] = x.x;
+      c16[4 * v + 1] = x.y;
+      c16[4 * v + 2] = x.z;
+      c16[4 * v + 3] = x.w;
+    }
+  }
   uint32_t mine = 0;
-  for (uint32_t b = hi - per; b < hi; ++b) mine += h[b];
+  if (per == 16) {
+#pragma unroll
+    for (int v = 0; v < 16; ++v) mine += c16[v];
+  } else {
+    for (uint32_t b = hi - per; b < hi; ++b) mine += h[b];
+  }
   if (threadIdx.x == 0) s_bin[0] = s_bin[1] = UINT32_MAX;
   uint32_t total;
   uint32_t above = block_excl_scan(mine, tmp, &total);
-  for (uint32_t b = hi; b-- > hi - per;) {
-    const uint32_t c = h[b];
-    if (above < k && k <= above + c) s_bin[0] = b;
-    if (above < m && m <= above + c) s_bin[1] = b;
-    above += c;
+  if (per == 16) {
+#pragma unroll
+    for (int v = 15; v >= 0; --v) {
+      const uint32_t b = hi - 16 + v, c = c16[v];
+      if (above < k && k <= above + c) s_bin[0] = b;
+      if (above < m && m <= above + c) s_bin[1] = b;
+      above += c;
+    }
+  } else {
+    for (uint32_t b = hi; b-- > hi - per;) {
+      const uint32_t c = h[b];
+      if (above < k && k <= above + c) s_bin[0] = b;
+      if (above < m && m <= above + c) s_bin[1] = b;
+      above += c;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -671,6 +671,7 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       ta.aps = tc_aps;
       ta.acc_bufs = tc_acc_bufs(tc_np);
       ta.match_all = all_match ? 1u : 0u;
+      ta.sample_floor = (all_match && mode == SCORE_SAMPLE && !ix->row_w) ? 1u : 0u;
       ta.backoff_ns = tc_backoff_ns();
       ta.row_w = ix->row_w;
       if (use_fused) {

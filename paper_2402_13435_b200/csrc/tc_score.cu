@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
                       : 0u;
       }
     };
+    // the main pass of the unweighted int8 prefilter with the threshold bias:
+    // one uniform test per chunk selects the lean body (sign bits, survivors)
+    const bool fast = bias_on && !a.row_w && a.mode != SCORE_SAMPLE && !(a.debug & (2u | 128u | 256u));
     uint32_t t = tile_of(a, 0);
     load_mask(t, mw);
     for (uint32_t i = 0; t != UINT32_MAX; ++i) {
@@ -779,6 +782,25 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         // Two instructions per score: d = v - ts (>= 0 exactly when v >= ts,
         // monotone rounding) and a funnel shift collecting d's sign bit.
         uint32_t below = 0;  // bit 31 - j: query 32c + j scored below its threshold
+        if (fast) {
+          // the MMA added -T_q: one funnel shift per score collects the sign;
+          // survivors (rare) rebuild their prefilter score from acc = v + T_q
+#pragma unroll
+          for (uint32_t j = 0; j < 32; ++j) below = __funnelshift_l(v[j], below, 1);
+          for (uint32_t tk = __brev(~below) & elig; tk; tk &= tk - 1u) {
+            const uint32_t j = __ffs(tk) - 1, qq = c * 32 + j;
+            const int32_t accv = static_cast<int32_t>(pick32(v, j)) - s_bias_s[qq];
+            const uint64_t key = make_key(clamp_score(static_cast<float>(accv) * s_sc[qq]), grow);
+            const uint32_t slot = atomicAdd(s_scnt + qq, 1u);
+            if (slot < kst) {
+              s_skey[qq * kst + slot] = key;
+            } else {
+              const uint32_t at = atomicAdd(a.cand_cnt + q0 + qq, 1u);
+              if (at < a.cap) a.cand[static_cast<size_t>(q0 + qq) * a.cap + at] = key;
+            }
+          }
+          continue;
+        }
         const float4* ts4 = reinterpret_cast<const float4*>(s_ts + c * 32);
         if (bias_on) {  // the MMA added -T_q: one funnel shift per score collects the sign
 #pragma unroll
@@ -835,7 +857,14 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
           // sample pass, histogram form: one global increment per eligible
           // sampled (row, query) in the query's score histogram
           const float scale = 0.5f * static_cast<float>(a.hbins);
-          for (uint32_t el = elig; el; el &= el - 1u) {
+          uint32_t keep = elig;
+          if (a.sample_floor) {  // match-all samples: only scores >= 0 (the top K lie far above)
+            uint32_t neg = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 32; ++j) neg = __funnelshift_l(v[j], neg, 1);  // sign of acc / fp32 score
+            keep &= __brev(~neg);
+          }
+          for (uint32_t el = keep; el; el &= el - 1u) {
             const uint32_t j = __ffs(el) - 1;
             const float sc = final_of(pick32(v, j), j);
             const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);

@@ -68,6 +68,9 @@ struct TcArgs {
   uint32_t acc_bufs;    // TMEM accumulator buffers (tc_acc_bufs(Np))
   uint32_t backoff_ns;  // sleep between failed barrier tests of the epilogue / CNF warps (0 = spin)
   uint32_t match_all;   // non-fused: every query of the batch is match-all (no mask; all rows eligible)
+  // sample pass of a match-all batch: histogram only scores >= 0 (a query's
+  // sampled K-th score below 0 leaves it without a threshold: correct, slower)
+  uint32_t sample_floor;
   uint32_t aps;         // K atoms per pipeline stage (divides kblocks; one MMA commit per stage)
   uint32_t term_slots;  // fused CNF: tiles of row term lists in flight (ring depth, <= kMaxTermSlots)
 };

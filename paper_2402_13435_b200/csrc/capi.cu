@@ -638,8 +638,8 @@ uint32_t hyre_batch_path(const hyre_executor* ex) {
   return (e->use_tc ? HYRE_PATH_TC : 0u) | (e->use_fused ? HYRE_PATH_FUSED : 0u) |
          (e->use_fwd && !e->use_fused && !e->all_match ? HYRE_PATH_FWD_MASK : 0u) |
          (e->all_match ? HYRE_PATH_MATCH_ALL : 0u) | (e->pf_i8 ? HYRE_PATH_I8 : 0u) |
-         (e->any_emb && e->ix->n_rows > e->cap && !e->use_small && !e->small_i8_segs ? HYRE_PATH_SAMPLED : 0u) |
-         (e->use_small || e->small_i8_segs ? HYRE_PATH_SMALL : 0u);
+         (e->any_emb && e->ix->n_rows > e->cap && !e->use_small ? HYRE_PATH_SAMPLED : 0u) |
+         (e->use_small ? HYRE_PATH_SMALL : 0u);
 }
 
 uint32_t hyre_batch_cnf_group(const hyre_executor* ex) {

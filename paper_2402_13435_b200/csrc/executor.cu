@@ -394,31 +394,9 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     }
   }
   if (use_small) prefilter = pf_i8 = false;  // exact scores straight from the rows
-  // K7i8: one query on a larger index in one scoring launch (int8 prefilter,
-  // each CTA rescoring its own band exactly): R = 2^r segments per CTA so the
-  // CTAs' top k fit the candidate buffer
-  small_i8_segs = 0;
-  if (!use_small && !use_tc && b == 1 && any_emb && !any_term_only && !use_fwd && scatter_total == 0 &&
-      big_k.empty() && small_enabled() && i8_ok && ix->dp == 128 && max_k <= kSmallMaxK &&
-      ix->num_clauses <= kSmallClauses && (qp[0].flags & QF_ACTIVE) &&
-      !((qp[0].flags & QF_QUANT) && qp[0].quant_k < ix->n_rows)) {
-    const uint64_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
-    uint32_t R = 1;
-    while (R < kSmallI8MaxSegs && (n_seg + R - 1) / R * max_k > cap) R <<= 1;
-    bool prog_ok = true;
-    if (!(qp[0].flags & (QF_MATCH_ALL | QF_EMPTY))) {
-      size_t pos = qp[0].prog_off + 1;
-      for (uint32_t c = 0; c < prog[qp[0].prog_off]; ++c) pos += 1 + prog[pos];
-      prog_ok = pos - qp[0].prog_off <= kSmallProg;
-    }
-    if (prog_ok && (n_seg + R - 1) / R * max_k <= cap) {
-      small_i8_segs = R;
-      prefilter = pf_i8 = true;  // the int8 query, its scale and bound
-    }
-  }
   // a K2 batch whose embedding queries are all match-all needs no K1 mask:
   // K2 uses tail masks and n_elig starts at the shard's row count
-  k2_match_all = !use_tc && !use_small && !small_i8_segs && any_emb && !any_term_only && !any_quant && scatter_total == 0;
+  k2_match_all = !use_tc && !use_small && any_emb && !any_term_only && !any_quant && scatter_total == 0;
   for (uint32_t i = 0; i < b && k2_match_all; ++i)
     if ((qp[i].flags & QF_ACTIVE) && !(qp[i].flags & QF_MATCH_ALL)) k2_match_all = false;
   if (use_tc) {
@@ -1000,32 +978,6 @@ void Executor::run() {
   } else {
     HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
     if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
-  }
-  if (small_i8_segs) {
-    // K7i8: CNF words + int8 prefilter + in-CTA band rescoring in one launch, then K4
-    mark(1, false);
-    mark(2, false);
-    mark(3, false);
-    const bool bf16 = ix->emb_dtype == HYRE_EMB_BF16;
-    SmallArgs sa{bf16 ? static_cast<const void*>(ix->emb_hi) : static_cast<const void*>(ix->emb_f32), ix->dp,
-                 ix->dp * (bf16 ? 2 : 4) / 16, ix->n_rows, ix->row_base, W, d_refs, d_prog,
-                 static_cast<uint32_t>(prog.size()), static_cast<uint32_t>(refs.size()), d_qp, B, d_q,
-                 ix->row_w, d_cand, cand_cnt, cap, n_elig};
-    sa.tc_i8 = ix->tc_i8;
-    sa.qi8 = d_qi8;
-    sa.qscale = d_qscale;
-    sa.qdelta = d_qdelta;
-    sa.segs_per_cta = small_i8_segs;
-    launch_small_i8(sa, bf16, st);
-    ++kernels;
-    mark(4, true);
-    SelectArgs fa{d_cand, cand_cnt, cap, d_qp, n_elig, SELECT_FINAL, d_thr, rerun, d_hits, d_hit_off,
-                  out_cnt, B, QF_ACTIVE | QF_EMB, cap, nullptr, 1, 0};
-    launch_select(fa, st);  // candidates are exact keys
-    ++kernels;
-    mark(5, true);
-    HYRE_CUDA(cudaGetLastError());
-    return;
   }
   if (use_small) {
     // K7: CNF words + exact scores + per-segment top k in one launch, then K4

@@ -146,7 +146,6 @@ struct Executor {
   // term-users program (TcArgs::fz) and its offsets into fz_words
   bool use_fused = false;
   bool use_small = false;  // K7 single-launch exact scorer (small index, single queries)
-  uint32_t small_i8_segs = 0;  // K7i8 (one query, int8 prefilter + in-CTA band rescoring): segments per CTA
   bool all_match = false;  // tensor-core batch of match-all queries only: no eligibility pass
   bool k2_match_all = false;  // K2 batch of match-all queries only: no K1 mask (tail masks in K2)
   size_t o_cinit = 0;         // blob offset of the counter image of a k2_match_all run

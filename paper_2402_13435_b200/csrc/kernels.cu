@@ -2204,217 +2204,4 @@ void launch_small(const SmallArgs& a, bool bf16, cudaStream_t st) {
   k<<<n_seg, 512, 0, st>>>(a);
 }
 
-// ---------------------------------------------------------------------------
-// K7i8: the single-launch scorer for one query on a larger index (c2/c3 B = 1):
-// each CTA owns R consecutive 1024-row segments.  Per segment the CNF words
-// (K7) give the eligible rows, whose int8 prefilter scores (exact s32 dot of
-// the swizzled int8 rows, s' = acc x scale_q) are kept in shared memory.  The
-// CTA's prefilter K-th score tau (4096-bin histogram) bounds its exact top k
-// (every row of it has s' >= tau - 2 delta_q), so only those rows
-// are rescored exactly (K2's arithmetic, fp32 or bf16 rows); the CTA's exact
-// top k join the candidate buffer and K4 selects the final top K.  No sample
-// pass, no thresholds, no recovery rounds.
-// ---------------------------------------------------------------------------
-namespace {
-constexpr uint32_t kI8Gather = 2048;  // keys at or above the local K-th key's bin, ranked in smem
-
-template <typename RowT, int LPR, int CPL>
-__global__ void __launch_bounds__(512) small_i8_kernel(SmallArgs a) {
-  extern __shared__ uint64_t s_keys[];  // [R x 1024] prefilter keys, then exact keys
-  __shared__ uint32_t s_hist[4096];
-  __shared__ uint32_t tmp[40], s_sel[4];
-  __shared__ uint16_t list[kSegRows];
-  __shared__ uint32_t s_n, s_cnt, s_base, s_nc;
-  __shared__ uint32_t s_prog[kSmallProg];
-  __shared__ const uint32_t* s_refs[kSmallRefs];
-  __shared__ uint32_t s_cl[kSmallClauses];
-  __shared__ uint32_t s_cw[kSmallClauses][32];
-  uint64_t* s_gather = reinterpret_cast<uint64_t*>(s_hist);  // reused after the histogram: kI8Gather keys
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const QParam qp = a.qp[0];
-  if ((qp.flags & (QF_ACTIVE | QF_EMB)) != (QF_ACTIVE | QF_EMB)) return;
-  const bool constrained = !(qp.flags & (QF_EMPTY | QF_MATCH_ALL));
-  if (constrained) {  // the query's program and the ref pointers, staged once
-    const uint32_t L = min(kSmallProg, a.prog_words - qp.prog_off);
-    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) s_prog[i] = a.prog[qp.prog_off + i];
-    for (uint32_t i = threadIdx.x; i < min(a.n_refs, kSmallRefs); i += blockDim.x) s_refs[i] = a.refs[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t nc = min(s_prog[0], kSmallClauses);
-      uint32_t pos = 1;
-      for (uint32_t c = 0; c < nc; ++c) {
-        const uint32_t nr = pos < L ? s_prog[pos] : 0u;
-        s_cl[c] = (pos + 1) | (min(nr, L - min(L, pos + 1)) << 16);
-        pos += 1 + nr;
-      }
-      s_nc = nc;
-    }
-  }
-  if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  // int8 prefilter rows: 8 lanes x 16 bytes per 128-element row (dp = 128)
-  constexpr int G8 = 4;
-  const int g8 = lane / 8, l8 = lane % 8;
-  const uint4 q8 = *reinterpret_cast<const uint4*>(a.qi8 + l8 * 16);
-  const float sc8 = a.qscale[0];
-  for (uint32_t sub = 0; sub < a.segs_per_cta; ++sub) {
-    const uint32_t seg = blockIdx.x * a.segs_per_cta + sub;
-    if (seg * kSegRows >= a.n_rows) break;
-    const uint32_t widx = seg * 32 + lane;
-    if (constrained) {
-      for (uint32_t c = wib; c < s_nc; c += nw) {
-        const uint32_t first = s_cl[c] & 0xFFFFu, nr = s_cl[c] >> 16;
-        uint32_t cw = 0;
-        if (widx < a.words)
-          for (uint32_t r = 0; r < nr; ++r) {
-            const uint32_t ref = s_prog[first + r];
-            cw |= __ldg((ref < kSmallRefs ? s_refs[ref] : a.refs[ref]) + widx);
-          }
-        s_cw[c][lane] = cw;
-      }
-      __syncthreads();
-    }
-    if (wib == 0) {
-      uint32_t word = 0;
-      if (widx < a.words && !(qp.flags & QF_EMPTY)) {
-        if (qp.flags & QF_MATCH_ALL) {
-          word = tail_mask(widx, a.n_rows);
-        } else {
-          uint32_t acc = kFull;
-          for (uint32_t c = 0; c < s_nc; ++c) acc &= s_cw[c][lane];
-          word = acc & tail_mask(widx, a.n_rows);
-        }
-      }
-      const uint32_t c = __popc(word), incl = warp_incl_scan(c, lane);
-      uint32_t pos = incl - c;
-      for (uint32_t u = word; u; u &= u - 1u) list[pos++] = static_cast<uint16_t>(lane * 32 + __ffs(u) - 1);
-      if (lane == 31) s_cnt = incl;
-    }
-    __syncthreads();
-    const uint32_t cnt = s_cnt, base_n = s_n;
-    const uint32_t row0 = seg * kSegRows;
-    for (uint32_t b = 0; b < cnt; b += nw * G8) {
-      const uint32_t idx = b + wib * G8 + g8;
-      const bool ok = idx < cnt;
-      const uint32_t lr = row0 + (ok ? list[idx] : 0u), rr = lr & 127u;
-      const uint8_t* tile = a.tc_i8 + size_t{lr >> 7} * 16384 + rr * 128;
-      const uint4 v = ok ? ldg_stream(tile + ((static_cast<uint32_t>(l8) ^ (rr & 7u)) << 4)) : make_uint4(0, 0, 0, 0);
-      float acc = I8Chunk::dot(v, q8);  // exact integer partial
-#pragma unroll
-      for (int m = 4; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
-      if (l8 == 0 && ok) {
-        const float ps = a.row_w ? weighted_score(acc * sc8, __ldg(a.row_w + lr)) : clamp_score(acc * sc8);
-        s_keys[base_n + idx] = make_key(ps, a.row_base + lr);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_n = base_n + cnt;
-    __syncthreads();
-  }
-  const uint32_t n = s_n, k = qp.k;
-  if (n == 0) return;
-  // tau: lower edge of the bin of the K-th largest prefilter key
-  float prune = -8.0f;
-  if (n > k) {
-    for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) s_hist[i] = 0;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(s_hist + score_bin(static_cast<uint32_t>(s_keys[i] >> 32)), 1u);
-    __syncthreads();
-    kth_bins(s_hist, k, k, tmp, s_sel);
-    const float tau = -1.0f + static_cast<float>(s_sel[0]) / 2048.0f - 1e-6f;
-    prune = tau - 2.0f * a.qdelta[0];
-  }
-  // exact rescoring of the band (K2's arithmetic: the rescore_list lane layout)
-  {
-    constexpr int G = 32 / LPR, E = Chunk<RowT>::kElems;
-    const int g = lane / LPR, li = lane % LPR;
-    float qv[CPL][E];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c)
-#pragma unroll
-      for (int e = 0; e < E; ++e) qv[c][e] = a.q[(li + c * LPR) * E + e];
-    const RowT* emb = static_cast<const RowT*>(a.emb);
-    for (uint32_t b = 0; b < n; b += nw * G) {
-      const uint32_t idx = b + wib * G + g;
-      const uint64_t key = idx < n ? s_keys[idx] : 0ull;
-      const bool ok = idx < n && key_score(key) >= prune;
-      const uint32_t lr = ok ? key_row(key) - a.row_base : 0u;
-      const RowT* r = emb + static_cast<size_t>(lr) * a.dp;
-      uint4 v[CPL];
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) v[c] = ok ? ldg_stream(r + (li + c * LPR) * E) : make_uint4(0, 0, 0, 0);
-      float acc = 0.0f;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) acc += Chunk<RowT>::dot(v[c], qv[c]);
-#pragma unroll
-      for (int m = LPR / 2; m >= 1; m >>= 1) acc += __shfl_xor_sync(kFull, acc, m);
-      if (li == 0 && idx < n) {
-        const float sc = a.row_w ? weighted_score(acc, __ldg(a.row_w + lr)) : clamp_score(acc);
-        s_keys[idx] = ok ? make_key(sc, a.row_base + lr) : 0ull;
-      }
-    }
-  }
-  __syncthreads();
-  // the CTA's exact top k (exact keys are unique; pruned rows hold 0)
-  if (threadIdx.x == 0) s_cnt = 0;
-  for (uint32_t i = threadIdx.x; i < 4096; i += blockDim.x) s_hist[i] = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-    if (s_keys[i]) atomicAdd(s_hist + score_bin(static_cast<uint32_t>(s_keys[i] >> 32)), 1u);
-  __syncthreads();
-  const uint32_t m_all = kth_bins(s_hist, min(k, n), min(k, n), tmp, s_sel);  // nonzero exact keys
-  const uint32_t take = min(k, m_all);
-  const uint32_t dk = m_all > k ? s_sel[0] : 0u;
-  const bool fits = (m_all > k ? s_sel[1] : m_all) <= kI8Gather;
-  __syncthreads();  // s_hist is reused as the gather buffer below
-  if (fits) {
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t key = s_keys[i];
-      if (key && score_bin(static_cast<uint32_t>(key >> 32)) >= dk) s_gather[atomicAdd(&s_cnt, 1u)] = key;
-    }
-  } else {  // pathological ties in one bin: bitonic over every key (rare)
-    uint32_t p2 = 1;
-    while (p2 < n) p2 <<= 1;
-    for (uint32_t i = n + threadIdx.x; i < p2; i += blockDim.x) s_keys[i] = 0ull;
-    __syncthreads();
-    bitonic_desc(s_keys, p2);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s_base = atomicAdd(a.cand_cnt, take);
-    atomicAdd(a.n_elig, n);
-  }
-  __syncthreads();
-  const uint32_t base = s_base;
-  if (fits) {
-    const uint32_t g_n = s_cnt;
-    for (uint32_t i = threadIdx.x; i < g_n; i += blockDim.x) {  // rank by counting
-      const uint64_t key = s_gather[i];
-      uint32_t rank = 0;
-      for (uint32_t j = 0; j < g_n; ++j) rank += s_gather[j] > key ? 1u : 0u;
-      if (rank < take && base + rank < a.cap) a.cand[base + rank] = key;
-    }
-  } else {
-    for (uint32_t i = threadIdx.x; i < take; i += blockDim.x)
-      if (base + i < a.cap) a.cand[base + i] = s_keys[i];
-  }
-}
-}  // namespace
-
-void launch_small_i8(const SmallArgs& a, bool bf16, cudaStream_t st) {
-  const uint32_t n_seg = (a.n_rows + kSegRows - 1) / kSegRows;
-  const uint32_t ctas = (n_seg + a.segs_per_cta - 1) / a.segs_per_cta;
-  if (ctas == 0) return;
-  using KFn = void (*)(SmallArgs);
-  const uint32_t cpr = a.dp_chunks;
-  KFn k = nullptr;
-  if (bf16) k = cpr == 16 ? small_i8_kernel<__nv_bfloat16, 16, 1> : nullptr;
-  else k = cpr == 32 ? small_i8_kernel<float, 32, 1> : nullptr;
-  if (!k) throw Error(HYRE_INTERNAL, "K7i8: unsupported row stride");
-  const size_t smem = size_t{a.segs_per_cta} * kSegRows * sizeof(uint64_t);
-  static std::atomic<uint64_t> attr[2];
-  set_smem_limit(reinterpret_cast<const void*>(k), static_cast<int>(smem), attr[bf16 ? 1 : 0]);
-  k<<<ctas, 512, smem, st>>>(a);
-}
-
 }  // namespace hyreb

@@ -291,12 +291,6 @@ struct SmallArgs {
   uint32_t* cand_cnt;   // [B] (zeroed)
   uint32_t cap;
   uint32_t* n_elig;     // [B] (zeroed)
-  // K7i8 (one query, int8 prefilter + in-CTA band rescoring)
-  const uint8_t* tc_i8;     // swizzled int8 rows (DevIndex::tc_i8, dp = 128)
-  const int8_t* qi8;        // [dp] int8 query
-  const float* qscale;      // [1] s' = acc x qscale
-  const float* qdelta;      // [1] prefilter bound
-  uint32_t segs_per_cta;    // 1024-row segments per CTA (a power of two)
 };
 constexpr uint32_t kSmallMaxRows = 262144;  // K7 indexes: n_seg x k candidates fit the buffer
 constexpr uint32_t kSmallMaxK = 256;
@@ -305,8 +299,5 @@ constexpr uint32_t kSmallRefs = 512;    // ref pointers staged in shared memory
 constexpr uint32_t kSmallClauses = 32;  // clause slots (hyre_index num_clauses <= 32)
 bool small_supported(uint32_t dp_chunks);
 void launch_small(const SmallArgs& a, bool bf16, cudaStream_t st);
-// K7i8: one query over up to 16 x 1024-row segments per CTA (dp = 128)
-constexpr uint32_t kSmallI8MaxSegs = 16;
-void launch_small_i8(const SmallArgs& a, bool bf16, cudaStream_t st);
 
 }  // namespace hyreb

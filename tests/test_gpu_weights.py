@@ -134,6 +134,22 @@ def test_weighted_match_all_batches(hy, B, dtype):
         dev.set_row_weights(None)
 
 
+@pytest.mark.parametrize("match_all", [False, True])
+def test_weighted_single_query_on_a_larger_index(hy, match_all):
+    # 400K rows, d = 128, B = 1: K1 mask (or none for match-all) + K2 int8 prefilter + K4p
+    prod, ref = _cnf_index(hy, 400_000, 128, 8, 20, 3, 71)
+    dev = prod.device(0, "f32")
+    w = _weights(400_000, 14)
+    dev.set_row_weights(w)
+    try:
+        qs = _queries(hy, 128, 8, 20, 3, [100, 10, 1], 73, match_all_every=1 if match_all else 0, draws=13)
+        one = hy.Executor(dev, 1)
+        got = [run_batch(one, [q])[0][0] for q in qs]
+        _check(ref, qs, got, w)
+    finally:
+        dev.set_row_weights(None)
+
+
 def test_weighted_exact_k2_path_d64(hy):
     # d = 64: no int8 plane, K2 scores exactly and compares w x clamp(dot)
     prod, ref = _cnf_index(hy, 100_000, 64, 4, 12, 3, 31)

@@ -54,6 +54,15 @@ bool fused_enabled() {
   }();
   return v;
 }
+// HYRE_K2_DENSE_SAMPLE=1: the K2 sample fills dense slots + a K-th selection
+// (two extra kernels) instead of score histograms + hist_thr.
+bool k2_hist_sample() {
+  static const bool v = [] {
+    const char* e = std::getenv("HYRE_K2_DENSE_SAMPLE");
+    return !(e && std::string(e) == "1");
+  }();
+  return v;
+}
 // HYRE_TC_SAMPLE_CC=0 keeps the tensor-core sample pass for fused-CNF batches.
 bool cnf_sample_enabled() {
   static const bool v = [] {
@@ -716,6 +725,10 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
                d_thr, cand, cnt, capacity, mode, sample_period, cap, rerun, d_samp, 1, 1};
   sa.row_w = ix->row_w;
   sa.match_all = k2_match_all ? 1u : 0u;
+  if (mode == SCORE_SAMPLE && k2_hist_sample()) {
+    sa.shist = d_shist;
+    sa.hbins = kHistBins;
+  }
   if (pf_i8) {  // int8 prefilter rows (exact rescoring in K4p)
     sa.emb = ix->tc_i8;
     sa.qi8 = d_qi8;
@@ -975,7 +988,9 @@ void Executor::run() {
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;
   mark(0, true);
-  const bool hist_sample = any_emb && use_tc && ix->n_rows > cap;
+  // sampled thresholds through per-query score histograms (K3, and K2 unless
+  // HYRE_K2_DENSE_SAMPLE=1 keeps the dense sample + K-th selection)
+  const bool hist_sample = any_emb && ix->n_rows > cap && (use_tc || k2_hist_sample());
   if (use_fused || all_match) {
     // One init kernel instead of three memsets: counters zeroed; eligible
     // counts unknown (all-ones: eligibility is evaluated inside K3, or every
@@ -987,6 +1002,7 @@ void Executor::run() {
   } else if (k2_match_all) {
     HYRE_CUDA(cudaMemcpyAsync(d_counters, d_blob + o_cinit, sizeof(uint32_t) * max_batch * kNumCounters,
                               cudaMemcpyDeviceToDevice, st));
+    if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
   } else {
     HYRE_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(uint32_t) * max_batch * kNumCounters, st));
     if (hist_sample) HYRE_CUDA(cudaMemsetAsync(d_shist, 0, sizeof(uint32_t) * B * kHistBins, st));
@@ -1071,7 +1087,7 @@ void Executor::run() {
   mark(2, any_quant);
   if (any_emb) {
     if (hist_sample) {
-      // K3 sample pass into per-query score histograms (zeroed above) -> thresholds
+      // K3 / K2 sample pass into per-query score histograms (zeroed above) -> thresholds
       score(SCORE_SAMPLE, nullptr, samp_cnt, samp_cap);
       HistThrArgs ha{d_shist, kHistBins, d_qp, n_elig, cap, sample_period, B, QF_ACTIVE | QF_EMB, d_thr, d_thr_safe,
                      prefilter ? prefilter_delta() : 0.0f, prefilter ? d_qdelta : nullptr};

@@ -655,8 +655,16 @@ __global__ void __launch_bounds__(256) score_kernel(ScoreArgs a) {
         const float ps = a.row_w ? weighted_score(p[0], wr) : clamp_score(p[0]);
         const uint64_t key = make_key(ps, grow);
         if (a.mode == SCORE_SAMPLE) {
-          // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
-          if (my_ok && elig) a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(ps);
+          if (a.shist) {  // one increment in the query's score histogram
+            if (my_ok && elig) {
+              const uint32_t b = min(static_cast<uint32_t>((ps + 1.0f) * (0.5f * static_cast<float>(a.hbins))),
+                                     a.hbins - 1u);
+              atomicAdd(a.shist + static_cast<size_t>(q0 + j) * a.hbins + b, 1u);
+            }
+          } else if (my_ok && elig) {
+            // dense sample slot: segment ordinal x 1024 + row in segment (no atomics)
+            a.samp[static_cast<size_t>(q0 + j) * a.cap + (it / S) * kSegRows + my_off] = f2ord(ps);
+          }
           continue;
         }
         const bool take = my_ok && elig && (kI8 ? (a.row_w ? ps : p[0]) >= ts8[j] : key >= thr[j]);

@@ -92,6 +92,10 @@ struct ScoreArgs {
   // prefilter score is w[r] x clamp(s).  w <= 1 keeps the prefilter bound.
   const float* row_w;
   uint32_t match_all;  // every active query is match-all: tail masks, no K1 mask
+  // SCORE_SAMPLE into per-query score histograms [B][hbins] (linear bins over
+  // [-1, 1]) instead of the dense slots; thresholds then come from hist_thr
+  uint32_t* shist;
+  uint32_t hbins;
 };
 void launch_score(const ScoreArgs& a, bool bf16, cudaStream_t st);
 void launch_score_i8(const ScoreArgs& a, cudaStream_t st);

@@ -63,14 +63,6 @@ bool k2_hist_sample() {
   }();
   return v;
 }
-// HYRE_TC_SAMPLE_CC=0 keeps the tensor-core sample pass for fused-CNF batches.
-bool cnf_sample_enabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("HYRE_TC_SAMPLE_CC");
-    return !(e && std::string(e) == "0");
-  }();
-  return v;
-}
 // HYRE_SMALL=0 disables the K7 single-launch path for small indexes.
 bool small_enabled() {
   static const bool v = [] {
@@ -708,12 +700,8 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
         ta.hc_off = fg.hc - fg.entries;
         ta.live_off = ta.hc_off + ix->num_clauses * tc_fused_chunks(tc_np);
       }
-      if (mode == SCORE_SAMPLE && ta.shist && pf_i8 && !ta.debug && cnf_sample_enabled() && cnf_sample_supported(ta)) {
-        launch_cnf_sample(ta, d_qi8, ix->dp, work, st);  // K3s: CUDA-core dots for the pairs that pass the CNF
-      } else {
-        launch_tc_score(tm_qhi, tm_qlo, ta, grid,
-                        tc_smem_bytes(tc_np, kb, n_ops, stages, fzb, tc_q_planes(), tc_aps), st);
-      }
+      launch_tc_score(tm_qhi, tm_qlo, ta, grid, tc_smem_bytes(tc_np, kb, n_ops, stages, fzb, tc_q_planes(), tc_aps),
+                      st);
       ++kernels;
     }
     return;

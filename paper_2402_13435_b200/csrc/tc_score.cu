@@ -985,102 +985,6 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
 }
 
 // ---------------------------------------------------------------------------
-// Sample pass of a fused-CNF int8 batch on CUDA cores (K3s): one CTA per
-// sampled 128-row tile, one thread per row.  The thread evaluates its row's
-// CNF for every query of the group with K3's CNF code and table, and only for
-// the (row, query) pairs that pass computes the exact int8 dot (dp4a over the
-// swizzled int8 row, the same s' = acc x scale_q as K3) into the query's score
-// histogram.  At ~5 % selectivity that is a few dot products per row: the
-// sample needs no tensor-core pipeline, TMEM or ring set-up.
-// ---------------------------------------------------------------------------
-template <int J, int TB, int NCH, int W>
-__global__ void __launch_bounds__(128) cnf_sample_kernel(TcArgs a, const int8_t* __restrict__ qi8, uint32_t dp) {
-  static_assert(TB == 1, "u8 compact rows only");
-  __shared__ __align__(16) uint32_t s_tbl8[256 * NCH];
-  extern __shared__ __align__(16) uint8_t dyn[];
-  const uint32_t Np = a.Np, q0 = a.q0;
-  uint8_t* s_q = dyn;                                                       // [Np][dp] int8 queries
-  uint32_t* s_fhc = reinterpret_cast<uint32_t*>(dyn + size_t{Np} * dp);    // hc [C][NCH], live [NCH], cslots
-  uint32_t* s_flive = s_fhc + a.C * NCH;
-  uint8_t* s_fslot = reinterpret_cast<uint8_t*>(s_flive + NCH + 1);
-  pdl_trigger();
-  for (uint32_t i = threadIdx.x; i < (a.C + 1) * NCH + 1; i += blockDim.x) s_fhc[i] = a.fz[a.hc_off + i];
-  for (uint32_t i = threadIdx.x; i <= a.T; i += blockDim.x) s_fslot[i] = i < a.T ? a.slot_of[i] : a.C;
-  for (uint32_t i = threadIdx.x; i < Np * dp / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(s_q)[i] = reinterpret_cast<const uint4*>(qi8 + size_t{q0} * dp)[i];
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {  // K3's table: unlisted term -> hc of its slot
-#pragma unroll
-    for (uint32_t c = 0; c < NCH; ++c) {
-      uint32_t x = t < a.T ? s_fhc[s_fslot[t] * NCH + c] : 0xFFFFFFFFu;
-      if (W && t >= a.T && t < a.T + a.C) x = s_fhc[(t - a.T) * NCH + c];
-      if (W && t == 0xFEu) x = 0u;
-      s_tbl8[t * NCH + c] = x;
-    }
-  }
-  __syncthreads();
-  for (uint32_t e = threadIdx.x; e < a.n_entries; e += blockDim.x) {  // listed terms: hc & ~users
-    const uint32_t* en = a.fz + static_cast<size_t>(e) * (1 + NCH);
-#pragma unroll
-    for (uint32_t c = 0; c < NCH; ++c) s_tbl8[en[0] * NCH + c] = en[1 + c];
-  }
-  __syncthreads();
-  pdl_wait();  // the histograms were zeroed by the run's init kernel
-  const uint32_t j = blockIdx.x;
-  const uint32_t t = (j / 8) * a.period * 8 + (j % 8);  // the j-th sampled tile (tile_of, SCORE_SAMPLE)
-  const uint32_t r = threadIdx.x, lr = t * kTileRows + r;
-  if (t >= a.n_tiles || lr >= a.n_rows) return;
-  constexpr int JW = (J * TB + 7) / 8 * 2;
-  uint32_t tw[JW];
-  const uint8_t* idp = a.cnf_ids + static_cast<size_t>(lr) * a.wb;
-#pragma unroll
-  for (int v = 0; v < JW / 2; ++v) {
-    const uint2 x = *reinterpret_cast<const uint2*>(idp + 8 * v);
-    tw[2 * v] = x.x;
-    tw[2 * v + 1] = x.y;
-  }
-  uint32_t el[NCH];
-  if constexpr (W > 0) {
-    cnf_row_grouped<J, W, NCH, NCH, JW>(tw, s_tbl8, smem_u32(s_flive), 0u, el);
-  } else {
-    cnf_row<J, TB, NCH, NCH>(tw, a.cnf_masks[lr], a.T, smem_u32(s_tbl8), smem_u32(s_fhc), smem_u32(s_flive),
-                             s_flive[NCH], 0u, el);
-  }
-  uint32_t any = 0;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) any |= el[c];
-  if (!any) return;
-  // the row's int8 vector (swizzled tiles: 16-byte chunk c of row rr at c ^ (rr % 8))
-  const uint32_t rr = lr & 127u, kb = dp / 128;
-  const float w = a.row_w ? __ldg(a.row_w + lr) : 1.0f;
-  const float scale = 0.5f * static_cast<float>(a.hbins);
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    for (uint32_t bits = el[c]; bits; bits &= bits - 1u) {
-      const uint32_t q = c * 32 + __ffs(bits) - 1;
-      if (q >= Np || q0 + q >= a.B) break;
-      int acc = 0;
-      for (uint32_t k = 0; k < kb; ++k) {
-        const uint8_t* tile = a.tiles + (size_t{lr >> 7} * kb + k) * kAtomBytes + rr * 128;
-#pragma unroll
-        for (uint32_t ch = 0; ch < 8; ++ch) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(tile + ((ch ^ (rr & 7u)) << 4)));
-          const uint4 qv = *reinterpret_cast<const uint4*>(s_q + size_t{q} * dp + k * 128 + ch * 16);
-          acc = __dp4a(static_cast<int>(v.x), static_cast<int>(qv.x), acc);
-          acc = __dp4a(static_cast<int>(v.y), static_cast<int>(qv.y), acc);
-          acc = __dp4a(static_cast<int>(v.z), static_cast<int>(qv.z), acc);
-          acc = __dp4a(static_cast<int>(v.w), static_cast<int>(qv.w), acc);
-        }
-      }
-      const float x = static_cast<float>(acc) * a.qscale[q0 + q];
-      const float sc = a.row_w ? weighted_score(x, w) : clamp_score(x);
-      const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);
-      atomicAdd(a.shist + static_cast<size_t>(q0 + q) * a.hbins + b, 1u);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 namespace {
@@ -1157,35 +1061,6 @@ size_t tc_fused_bytes(uint32_t Np, uint32_t T, uint32_t C, uint32_t row_bytes, u
   const size_t n_tbl = T <= 255 ? 0 : T + 1;  // u8 ids: static 256-entry table (kTcStaticSmem)
   return 128 + size_t{term_slots} * kTileRows * row_bytes + size_t{kEligSlots} * nch * kTileRows * 4 +
          16 * (term_slots + kEligSlots) + 4 * (n_tbl * nch + C * nch + nch + 1) + T + 1 + 16;
-}
-
-bool cnf_sample_supported(const TcArgs& a) {
-  const uint32_t nch = tc_fused_chunks(a.Np);
-  if (!a.fused || !a.i8 || a.tb != 1 || nch > 4) return false;
-  if (a.W) return (a.W == 1 && a.J == 8) || (a.W == 2 && (a.J == 8 || a.J == 16)) || (a.W == 3 && (a.J == 12 || a.J == 24)) ||
-                  (a.W == 4 && (a.J == 16 || a.J == 32));
-  return a.J == 8 || a.J == 16 || a.J == 24 || a.J == 32;
-}
-
-size_t cnf_sample_smem(const TcArgs& a, uint32_t dp) {
-  return size_t{a.Np} * dp + 4 * (size_t{a.C + 1} * tc_fused_chunks(a.Np) + 2) + a.T + 1 + 16;
-}
-
-void launch_cnf_sample(const TcArgs& a, const int8_t* qi8, uint32_t dp, uint32_t n_tiles_sampled, cudaStream_t st) {
-  using KFn = void (*)(TcArgs, const int8_t*, uint32_t);
-#define HYRE_CS_ROW(J, W) {cnf_sample_kernel<J, 1, 1, W>, cnf_sample_kernel<J, 1, 2, W>, cnf_sample_kernel<J, 1, 4, W>}
-  static const KFn ks[11][3] = {HYRE_CS_ROW(8, 0),  HYRE_CS_ROW(16, 0), HYRE_CS_ROW(24, 0), HYRE_CS_ROW(32, 0),
-                                HYRE_CS_ROW(8, 1),  HYRE_CS_ROW(8, 2),  HYRE_CS_ROW(16, 2), HYRE_CS_ROW(12, 3),
-                                HYRE_CS_ROW(24, 3), HYRE_CS_ROW(16, 4), HYRE_CS_ROW(32, 4)};
-#undef HYRE_CS_ROW
-  const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : 2);
-  const uint32_t J = a.J, W = a.W;
-  const int ri = !W ? (J == 8 ? 0 : J == 16 ? 1 : J == 24 ? 2 : 3)
-                    : (W == 1 ? 4 : W == 2 ? (J == 8 ? 5 : 6) : W == 3 ? (J == 12 ? 7 : 8) : (J == 16 ? 9 : 10));
-  const KFn k = ks[ri][ci];
-  const size_t smem = cnf_sample_smem(a, dp);
-  if (smem > 48 * 1024) HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (n_tiles_sampled) launch_pdl(k, dim3(n_tiles_sampled), dim3(128), smem, st, a, qi8, dp);
 }
 
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,

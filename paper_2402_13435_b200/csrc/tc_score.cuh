@@ -97,11 +97,6 @@ uint32_t tc_fused_chunks(uint32_t Np);
 // dynamic shared memory one CTA may use
 uint32_t tc_ctas_per_sm(bool fused, uint32_t Np);
 size_t tc_smem_cap(bool fused, uint32_t Np);
-// K3s: the fused-CNF int8 sample pass on CUDA cores (one CTA per sampled tile,
-// one thread per row; dot products only for the (row, query) pairs that pass
-// the CNF) into the same per-query score histograms as K3's sample mode.
-bool cnf_sample_supported(const TcArgs& a);
-void launch_cnf_sample(const TcArgs& a, const int8_t* qi8, uint32_t dp, uint32_t n_tiles_sampled, cudaStream_t st);
 void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArgs& a, uint32_t grid, size_t smem,
                      cudaStream_t st);
 

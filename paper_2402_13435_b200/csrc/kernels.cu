@@ -1383,7 +1383,19 @@ __global__ void __launch_bounds__(kSelPThreads) select_prefilter_kernel(PrefSele
   // 1. tau: K-th largest prefilter key (no pruning when n <= K)
   const bool resident = n <= kSelResident;
   if (resident) {
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) res[i] = keys[i];
+    for (uint32_t base = 0; base < n; base += 4 * blockDim.x) {  // four independent loads in flight
+      uint64_t kv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        kv[u] = i < n ? keys[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = base + u * blockDim.x + threadIdx.x;
+        if (i < n) res[i] = kv[u];
+      }
+    }
     __syncthreads();
   }
   const uint64_t* src = resident ? res : keys;

@@ -210,14 +210,89 @@ __global__ void __launch_bounds__(128) mask_tm_kernel(MaskArgs a, const __grid_c
   }
 }
 
+// The same for groups of <= 8 queries with four words per thread: one warp
+// per 128-word chunk, every ref read as a 16-byte load, so a thread has a
+// quarter of the load round trips in flight per byte and the grid fits one
+// wave (the single-query mask over 10M rows is load-latency bound).
+template <uint32_t N, int QN>
+__global__ void __launch_bounds__(128) mask_tm4_kernel(MaskArgs a, const __grid_constant__ MaskProg<N> prog) {
+  const uint32_t* c_mask_prog = prog.w;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = blockIdx.y;
+  const uint32_t chunk = blockIdx.x * 4 + wib;
+  if (chunk >= a.n_chunks) return;
+  const uint32_t w0 = chunk * kChunkWords + lane * 4;  // this thread's four words
+  const uint32_t live = c_mask_prog[2 + 2 * g];
+  uint32_t pos = c_mask_prog[1 + 2 * g];
+  const uint32_t q0 = (c_mask_prog[0] + g) * 32;
+  uint32_t tm[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) tm[x] = tail_mask(w0 + x, a.n_rows);
+  uint32_t res[QN][4];
+#pragma unroll
+  for (int q = 0; q < QN; ++q)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) res[q][x] = ((live >> q) & 1u) ? tm[x] : 0u;
+  const uint32_t n_slots = c_mask_prog[pos++];
+  for (uint32_t s = 0; s < n_slots; ++s) {
+    const uint32_t hc = c_mask_prog[pos], n_refs = c_mask_prog[pos + 1];
+    pos += 2;
+    uint32_t acc[QN][4];
+#pragma unroll
+    for (int q = 0; q < QN; ++q)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) acc[q][x] = 0u;
+    for (uint32_t r = 0; r < n_refs; r += 8, pos += 24) {  // up to 8 independent 16-byte loads in flight
+      uint4 w[8];
+      uint32_t u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool on = r + k < n_refs;
+        const uint64_t ptr = on ? (static_cast<uint64_t>(c_mask_prog[pos + 3 * k + 1]) << 32) | c_mask_prog[pos + 3 * k]
+                                : 0ull;
+        w[k] = on ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(ptr) + w0))
+                  : make_uint4(0, 0, 0, 0);
+        u[k] = on ? c_mask_prog[pos + 3 * k + 2] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          if ((u[k] >> q) & 1u) {
+            acc[q][0] |= w[k].x;
+            acc[q][1] |= w[k].y;
+            acc[q][2] |= w[k].z;
+            acc[q][3] |= w[k].w;
+          }
+    }
+    pos -= 24 * ((n_refs + 7) / 8) - 3 * n_refs;  // the loop advanced by whole batches of 8 refs
+#pragma unroll
+    for (int q = 0; q < QN; ++q)
+      if ((hc >> q) & 1u)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) res[q][x] &= acc[q][x];
+  }
+#pragma unroll
+  for (int q = 0; q < QN; ++q) {
+    if (q0 + q < a.B)
+      *reinterpret_cast<uint4*>(a.mask + static_cast<size_t>(q0 + q) * a.words + w0) =
+          make_uint4(res[q][0], res[q][1], res[q][2], res[q][3]);
+    const uint32_t c = __reduce_add_sync(0xffffffffu, __popc(res[q][0]) + __popc(res[q][1]) + __popc(res[q][2]) +
+                                                          __popc(res[q][3]));
+    if (lane == 0 && q0 + q < a.B) {
+      a.chunk_cnt[static_cast<size_t>(q0 + q) * a.n_chunks + chunk] = c;
+      if (c) atomicAdd(a.n_elig + q0 + q, c);
+    }
+  }
+}
+
 template <uint32_t N>
 void launch_mask_tm_n(const MaskArgs& a, const std::vector<uint32_t>& words, uint32_t n_groups, uint32_t live_or,
                       cudaStream_t st) {
   MaskProg<N> p;
   std::memcpy(p.w, words.data(), words.size() * 4);
-  const dim3 grid(a.n_chunks, n_groups);
-  if (live_or <= 1u) mask_tm_kernel<N, 1><<<grid, kChunkWords, 0, st>>>(a, p);
-  else if (live_or <= 0xFFu) mask_tm_kernel<N, 8><<<grid, kChunkWords, 0, st>>>(a, p);
+  const dim3 grid(a.n_chunks, n_groups), grid4((a.n_chunks + 3) / 4, n_groups);
+  if (live_or <= 1u) mask_tm4_kernel<N, 1><<<grid4, kChunkWords, 0, st>>>(a, p);
+  else if (live_or <= 0xFFu) mask_tm4_kernel<N, 8><<<grid4, kChunkWords, 0, st>>>(a, p);
   else mask_tm_kernel<N, 32><<<grid, kChunkWords, 0, st>>>(a, p);
 }
 

@@ -662,7 +662,14 @@ void Executor::score(uint32_t mode, uint64_t* cand, uint32_t* cnt, uint32_t capa
       const uint32_t n_seg = (ix->n_rows + kSegRows - 1) / kSegRows;
       work = (n_seg + sample_period - 1) / sample_period * 8;
     }
-    const uint32_t grid = std::max(1u, std::min(work, 148u * tc_ctas_per_sm(use_fused, tc_np)));
+    uint32_t grid = std::max(1u, std::min(work, 148u * tc_ctas_per_sm(use_fused, tc_np)));
+    if (mode == SCORE_SAMPLE) {  // profiling: HYRE_TC_SAMPLE_GRID caps the sample pass's CTAs
+      static const uint32_t sg = [] {
+        const char* e = std::getenv("HYRE_TC_SAMPLE_GRID");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+      }();
+      if (sg) grid = std::min(grid, sg);
+    }
     for (uint32_t g = 0; g < tc_groups; ++g) {
       TcArgs ta{pf_i8 ? ix->tc_i8 : ix->tc_tiles, ix->n_rows, ix->row_base, ix->words, n_tiles, B, g * tc_np, g * tc_np, tc_np, kb, stages, cols,
                 n_ops == 2 ? 1u : 0u, d_mask, d_qp, n_elig, d_thr, cand, cnt, capacity, mode, sample_period, cap,

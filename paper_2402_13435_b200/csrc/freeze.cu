@@ -16,6 +16,7 @@
 // hands out); rows whose staged slot holds more ids than the device sort
 // buffer are canonicalised on the host with Builder::freeze's code.
 #include <algorithm>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -133,7 +134,7 @@ Frozen* freeze_on_device(Builder& bld, uint32_t num_bits, uint64_t seed, int dev
   const uint32_t C = bld.num_clauses, A = bld.max_num_attr, D = bld.dim;
   const size_t words = codec.num_words();
 
-  auto* f = new Frozen;
+  std::unique_ptr<Frozen> f(new Frozen);  // released to the caller only on success
   f->num_docs = n;
   f->num_clauses = C;
   f->max_num_attr = A;
@@ -162,10 +163,20 @@ Frozen* freeze_on_device(Builder& bld, uint32_t num_bits, uint64_t seed, int dev
     perm.insert(perm.end(), rd.perm.begin(), rd.perm.end());
     sg.insert(sg.end(), rd.signs.begin(), rd.signs.end());
   }
-  uint32_t* d_lo = dalloc<uint32_t>(num_bits);
-  uint32_t* d_hi = dalloc<uint32_t>(num_bits);
-  uint32_t* d_perm = dalloc<uint32_t>(perm.size());
-  float* d_sg = dalloc<float>(sg.size());
+  struct Bufs {  // device buffers freed on every exit
+    std::vector<void*> p;
+    ~Bufs() {
+      for (void* x : p) cudaFree(x);
+    }
+  } bufs;
+  auto keep = [&](auto* x) {
+    bufs.p.push_back(x);
+    return x;
+  };
+  uint32_t* d_lo = keep(dalloc<uint32_t>(num_bits));
+  uint32_t* d_hi = keep(dalloc<uint32_t>(num_bits));
+  uint32_t* d_perm = keep(dalloc<uint32_t>(perm.size()));
+  float* d_sg = keep(dalloc<float>(sg.size()));
   HYRE_CUDA(cudaMemcpy(d_lo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
   HYRE_CUDA(cudaMemcpy(d_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
   HYRE_CUDA(cudaMemcpy(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice));
@@ -178,15 +189,15 @@ Frozen* freeze_on_device(Builder& bld, uint32_t num_bits, uint64_t seed, int dev
     const uint32_t r1 = std::min(n, r0 + chunk);
     max_ids = std::max(max_ids, bld.slot_offsets[size_t{r1} * C] - bld.slot_offsets[size_t{r0} * C]);
   }
-  uint32_t* d_ids = dalloc<uint32_t>(max_ids);
-  uint64_t* d_so = dalloc<uint64_t>(size_t{chunk} * C + 1);
-  float* d_emb = dalloc<float>(size_t{chunk} * D);
-  float* d_out = dalloc<float>(size_t{chunk} * D);
-  uint32_t* d_attr = dalloc<uint32_t>(size_t{chunk} * A);
-  uint32_t* d_offs = dalloc<uint32_t>(size_t{chunk} * (C + 1));
-  uint8_t* d_flags = dalloc<uint8_t>(chunk);
-  uint8_t* d_zero = dalloc<uint8_t>(chunk);
-  uint64_t* d_sig = dalloc<uint64_t>(size_t{chunk} * words);
+  uint32_t* d_ids = keep(dalloc<uint32_t>(max_ids));
+  uint64_t* d_so = keep(dalloc<uint64_t>(size_t{chunk} * C + 1));
+  float* d_emb = keep(dalloc<float>(size_t{chunk} * D));
+  float* d_out = keep(dalloc<float>(size_t{chunk} * D));
+  uint32_t* d_attr = keep(dalloc<uint32_t>(size_t{chunk} * A));
+  uint32_t* d_offs = keep(dalloc<uint32_t>(size_t{chunk} * (C + 1)));
+  uint8_t* d_flags = keep(dalloc<uint8_t>(chunk));
+  uint8_t* d_zero = keep(dalloc<uint8_t>(chunk));
+  uint64_t* d_sig = keep(dalloc<uint64_t>(size_t{chunk} * words));
   const uint32_t warps = 8;
   const size_t smem = size_t{warps} * D * sizeof(float);
   if (smem > 48 * 1024)
@@ -212,9 +223,6 @@ Frozen* freeze_on_device(Builder& bld, uint32_t num_bits, uint64_t seed, int dev
     HYRE_CUDA(cudaMemcpy(f->zero.data() + r0, d_zero, m, cudaMemcpyDeviceToHost));
     HYRE_CUDA(cudaMemcpy(flags.data() + r0, d_flags, m, cudaMemcpyDeviceToHost));
   }
-  for (void* p : {(void*)d_lo, (void*)d_hi, (void*)d_perm, (void*)d_sg, (void*)d_ids, (void*)d_so, (void*)d_emb,
-                  (void*)d_out, (void*)d_attr, (void*)d_offs, (void*)d_flags, (void*)d_zero, (void*)d_sig})
-    cudaFree(p);
 
   // rows with a slot too long for the device sort buffer: the host freeze's
   // canonicalisation (corpus.cpp:61-107)
@@ -243,15 +251,12 @@ Frozen* freeze_on_device(Builder& bld, uint32_t num_bits, uint64_t seed, int dev
     }
     if (flags[r] & 1u) too += " " + bld.doc_ids.at(r);
   }
-  if (!too.empty()) {
-    delete f;
-    validation("documents wider than maxNumAttr=" + std::to_string(A) + ":" + too);
-  }
+  if (!too.empty()) validation("documents wider than maxNumAttr=" + std::to_string(A) + ":" + too);
   f->doc_ids = std::move(bld.doc_ids);
   std::vector<uint32_t>().swap(bld.ids);
   std::vector<float>().swap(bld.embeddings);
   std::vector<uint64_t>().swap(bld.slot_offsets);
-  return f;
+  return f.release();
 }
 
 }  // namespace hyreb

@@ -246,6 +246,7 @@ int64_t parse_row(const std::string& s, size_t from) {
 void DocIds::push(std::string id) {
   if (segs_.empty() || segs_.back().range) segs_.push_back(Seg{n_, 0, false, {}, explicit_.size()});
   explicit_.push_back(std::move(id));
+  explicit_rows_.push_back(n_);
   ++segs_.back().count;
   ++n_;
 }
@@ -281,15 +282,8 @@ int64_t DocIds::find(const std::string& id) const {
     if (r >= s.row0 && r < int64_t{s.row0} + s.count) return r;
   }
   if (explicit_.empty()) return -1;
-  if (mapped_ < explicit_.size()) {  // index the explicit ids added since the last lookup
-    size_t k = 0;
-    for (const Seg& s : segs_) {
-      if (s.range) continue;
-      for (uint32_t i = 0; i < s.count; ++i, ++k)
-        if (k >= mapped_) map_.emplace(explicit_[s.first + i], s.row0 + i);
-    }
-    mapped_ = explicit_.size();
-  }
+  for (; mapped_ < explicit_.size(); ++mapped_)  // index the explicit ids added since the last lookup
+    map_.emplace(explicit_[mapped_], explicit_rows_[mapped_]);
   auto it = map_.find(id);
   return it == map_.end() ? -1 : static_cast<int64_t>(it->second);
 }
@@ -330,6 +324,7 @@ int64_t DocIds::first_collision(const std::string& prefix, uint32_t row0, uint32
 void DocIds::clear() {
   segs_.clear();
   explicit_.clear();
+  explicit_rows_.clear();
   map_.clear();
   mapped_ = 0;
   n_ = 0;

@@ -75,6 +75,7 @@ class DocIds {
   const Seg& seg_of(uint32_t row) const;
   std::vector<Seg> segs_;
   std::vector<std::string> explicit_;
+  std::vector<uint32_t> explicit_rows_;  // row of explicit_[i]
   uint32_t n_ = 0;
   mutable std::unordered_map<std::string, uint32_t> map_;  // explicit ids, built lazily
   mutable size_t mapped_ = 0;                              // explicit ids already in map_

@@ -96,7 +96,7 @@ struct Executor {
   uint32_t* d_samp = nullptr;  // dense sample scores [max_batch][samp_cap] (K2 sample pass)
   uint32_t* d_shist = nullptr;  // K3 sample pass: score histograms [max_batch][kHistBins]
   static constexpr uint32_t kHistBins = 4096;    // linear bins over [-1, 1] (width 4.9e-4)
-  static constexpr uint32_t kTcSampleSegs = 60;  // K3 sample: ~60 x 1024 rows (c3 sweeps 40-640: 60 best)
+  static constexpr uint32_t kTcSampleSegs = 100;  // K3 sample: ~100 x 1024 rows at 10M (r02 sweep 60-240 with the bias K-step: 90-120 best)
   uint32_t* d_qhist = nullptr;
   uint32_t* d_tsel = nullptr;
   uint32_t* d_eqcnt = nullptr;

@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
   // pattern (1, 127, ..., 127); |S| <= 500062.  "No threshold" needs S above
   // every possible -acc (|acc| <= (1 + delta_q) / scale_q).  Main / rerun
   // passes of the unweighted int8 prefilter only; otherwise the IADD compare.
-  bool bias_ok = a.i8 && !a.row_w && a.mode != SCORE_SAMPLE && !(a.debug & 0x3FFu);
+  bool bias_ok = a.i8 && !a.row_w && a.mode != SCORE_SAMPLE && !(a.debug & (1u | 128u | 256u | 0x200u));
   constexpr int32_t kBiasMax = 3937 * 127 + 63;
   for (uint32_t j = threadIdx.x; j < Np && bias_ok; j += blockDim.x) {
     const int32_t T = __float_as_int(s_ts[j]);

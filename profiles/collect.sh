@@ -18,3 +18,9 @@ for w in "c1 --batch 1" "c2 --batch 1" "c2 --batch 256" "c3 --batch 1" "c4 --bat
   set -- $w
   python bench.py --workload $w --no-cpu-baseline > "gpurun_out/${T}_bench_$(echo $w | tr -d ' -').log" 2>&1
 done
+# tensor-heavy configs: one main K3 launch each (c2 B=256: run 1's main = the 4th tc_score launch;
+# c4 B=1024: 4 sample + 4 main launches per run -> run 1's first main is the 13th)
+ncu --set full --clock-control none --import-source on -k regex:tc_score -s 3 -c 1 -o gpurun_out/${T}_tc_c2b256 \
+  python bench.py --workload c2 --batch 256 --steps 1 --warmup 1 --no-cpu-baseline --inflight 1 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tc_score -s 12 -c 1 -o gpurun_out/${T}_tc_c4b1024 \
+  python bench.py --workload c4 --batch 1024 --steps 1 --warmup 1 --no-cpu-baseline --inflight 1 > /dev/null 2>&1

@@ -952,6 +952,22 @@ __device__ __forceinline__ void hist_add(uint32_t* hist, uint32_t digit) {
   if (digit != 0xffffffffu && (threadIdx.x & 31) == static_cast<uint32_t>(__ffs(peers) - 1))
     atomicAdd(hist + digit, static_cast<uint32_t>(__popc(peers)));
 }
+// Number of keys in s[0, m) greater than key: two keys per 16-byte shared
+// load and four independent counters (the serial add chain was the K4p
+// ranking's latency).
+__device__ __forceinline__ uint32_t count_greater(const uint64_t* s, uint32_t m, uint64_t key) {
+  uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, j = 0;
+  for (; j + 4 <= m; j += 4) {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(s + j);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(s + j + 2);
+    r0 += a.x > key ? 1u : 0u;
+    r1 += a.y > key ? 1u : 0u;
+    r2 += b.x > key ? 1u : 0u;
+    r3 += b.y > key ? 1u : 0u;
+  }
+  for (; j < m; ++j) r0 += s[j] > key ? 1u : 0u;
+  return r0 + r1 + r2 + r3;
+}
 // 12-bit histogram bin of an orderable score (f2ord): linear in the score
 // over [-1, 1] (2^-11 wide bins), monotone in the key order.  The top 12 key
 // bits would give one bin per (exponent, 3 mantissa bits): cosines in
@@ -1122,8 +1138,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(SelectArgs a) {
     // gathered keys per key (broadcast shared reads)
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const uint64_t key = sortbuf[i];
-      uint32_t rank = 0;
-      for (uint32_t j = 0; j < m; ++j) rank += sortbuf[j] > key ? 1u : 0u;
+      const uint32_t rank = count_greater(sortbuf, m, key);
       if (rank < take) {
         out[rank].row = key_row(key);
         out[rank].score = key_score(key);
@@ -1544,8 +1559,7 @@ __global__ void __launch_bounds__(kSelPThreads) select_prefilter_kernel(PrefSele
     // survivors per key in shared memory (broadcast reads)
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
       const uint64_t key = sortbuf[i];
-      uint32_t rank = 0;
-      for (uint32_t j = 0; j < m; ++j) rank += sortbuf[j] > key ? 1u : 0u;
+      const uint32_t rank = count_greater(sortbuf, m, key);
       if (rank < take) {
         out[rank].row = key_row(key);
         out[rank].score = key_score(key);

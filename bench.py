@@ -375,6 +375,12 @@ def run_ours(args, w):
     s6 = (C.c_float * 6)()
 
     # ---- timed region: exactly K back-to-back steps, device time ----------
+    # Inner stage events are off here (a stream event between two kernels
+    # ends their programmatic-dependent-launch overlap); each run still
+    # records its start/end events, which give the per-batch latencies.
+    check(lib.hyre_batch_set_stage_events(h, 0))
+    if ex_b is not None:
+        check(lib.hyre_batch_set_stage_events(ex_b._h, 0))
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -396,12 +402,23 @@ def run_ours(args, w):
     # ---- per-call latency + per-kernel times of the timed steps ------------
     # (CUDA events the executor records around each stage on its own stream;
     # it keeps the last 64 runs, read back after the timed region)
+    lat = []
+    for back in range(min(args.steps, 64)):
+        check(lib.hyre_batch_stage_ms_hist(h, back, s6))
+        lat.append(s6[5])
+    # per-stage times (the dominant kernel's launch time for the roofline):
+    # the same K steps again with the stage events on, right after the timed ones
+    check(lib.hyre_batch_set_stage_events(h, 1))
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     stage_rows = []
     for back in range(min(args.steps, 64)):
         check(lib.hyre_batch_stage_ms_hist(h, back, s6))
         stage_rows.append(list(s6))
     inflight2 = None
     if ex_b is not None and not os.environ.get("HYRE_TC_DEBUG"):
+        check(lib.hyre_batch_set_stage_events(h, 0))
         alt[0] = True
         for _ in range(2):
             step()
@@ -422,7 +439,6 @@ def run_ours(args, w):
         inflight2 = {"value": B * args.steps / (ms2 * 1e-3), "unit": "queries/s", "ms_per_step": ms2 / args.steps,
                      "note": "the same K steps with two batches in flight on two executors/streams (device-timed); "
                              "p50 latency then includes queueing behind the other batch"}
-    lat = [r[5] for r in stage_rows]
     main_ms = [r[3] for r in stage_rows]
     p50 = statistics.median(lat)
     lat_sorted = sorted(lat)
@@ -432,6 +448,8 @@ def run_ours(args, w):
     main_avg = statistics.mean(main_ms)
 
     # ---- end-to-end through the C-ABI with host buffers ---------------------
+    # (throughput callers switch the inner stage events off, like the timed steps)
+    check(lib.hyre_batch_set_stage_events(h, 0))
     caps = [min(args.k, re_ - rb)] * B
     offs = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.uint64)
     host_hits = (L.hyre_hit * sum(caps))()
@@ -492,6 +510,8 @@ def run_ours(args, w):
     n_callers = 3
     if world == 1 and not os.environ.get("HYRE_TC_DEBUG"):
         extra = [(hy.Executor(dev, max_batch=args.batch), hy.QueryPack(hq)) for _ in range(n_callers - 1)]
+        for ex_x, _ in extra:
+            check(lib.hyre_batch_set_stage_events(ex_x._h, 0))
 
         def worker(hx, pk, n, out):
             hh = (L.hyre_hit * sum(caps))()
@@ -565,6 +585,8 @@ def run_ours(args, w):
         "p95_ms": pct(95), "p99_ms": pct(99), "latency_samples": len(lat),
         "reruns": reruns,
         "inflight2": inflight2,
+        "stages_ms_note": "per-stage CUDA events from K more steps right after the timed ones (the timed steps record "
+                          "only each run's start/end: an event between kernels ends their PDL overlap)",
         "stages_ms": dict(zip(["mask", "quant", "sample", "main_scorer", "select_firstk", "run"],
                               [statistics.median(r[i] for r in stage_rows) for i in range(6)])),
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm,

@@ -350,6 +350,12 @@ hyre_status hyre_batch_stage_ms(hyre_executor* ex, float* out6);
  * keeps the events of its last 64 runs), so a benchmark can read per-kernel
  * times of every step of a back-to-back timed region afterwards. */
 hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* out6);
+/* Record the inner stage boundaries [1]-[4] (default on).  Off, a run records
+ * only its start and end events: a stream event between two kernels ends the
+ * programmatic-dependent-launch overlap of the second kernel's prologue with
+ * the first one's tail, so throughput runs switch them off and the stage
+ * durations then read 0 (the whole-run time [5] stays). */
+hyre_status hyre_batch_set_stage_events(hyre_executor* ex, int on);
 /* Device pointers of the last run's results (for on-device multi-GPU
  * gathers): hits (hyre_hit[*n_hits]), per-slot hit offsets (u64[b]) and
  * per-slot counts (u32[b]).  Valid until the next prepare. */

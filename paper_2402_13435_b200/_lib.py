@@ -171,6 +171,7 @@ SIGNATURES = {
     "hyre_pool_stats": (C.c_int, [vp, u64p, u64p]),
     "hyre_batch_stage_ms": (C.c_int, [vp, f32p]),
     "hyre_batch_stage_ms_hist": (C.c_int, [vp, C.c_uint32, f32p]),
+    "hyre_batch_set_stage_events": (C.c_int, [vp, C.c_int]),
     "hyre_batch_io_bytes": (C.c_int, [vp, u64p, u64p]),
     "hyre_batch_merge_packed": (C.c_int, [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64]),
     "hyre_batch_merge_gathered": (C.c_int, [vp, vp, vp, vp, C.c_uint32, C.c_uint64]),

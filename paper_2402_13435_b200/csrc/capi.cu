@@ -675,6 +675,13 @@ hyre_status hyre_batch_stage_ms_hist(hyre_executor* ex, uint32_t back, float* ou
   });
 }
 
+hyre_status hyre_batch_set_stage_events(hyre_executor* ex, int on) {
+  return guard([&] {
+    need(ex, "executor");
+    ex->ex->stage_events = on != 0;
+  });
+}
+
 hyre_status hyre_batch_recovery(const hyre_executor* ex, uint32_t* out2) {
   return guard([&] {
     need(ex, "executor");

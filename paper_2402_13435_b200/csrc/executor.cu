@@ -1379,7 +1379,7 @@ void Executor::stage_ms(float* out) const {
 // alias of boundary i - 1 (each event record costs ~1-2 us of stream time).
 void Executor::mark(int i, bool stage_ran) {
   uint8_t* map = ev_map[(n_runs - 1) % kEvRing];
-  if (i == 0 || stage_ran) {
+  if (i == 0 || i == 5 || (stage_ran && stage_events)) {
     HYRE_CUDA(cudaEventRecord(ev[i], st));
     map[i] = static_cast<uint8_t>(i);
   } else {

@@ -84,6 +84,7 @@ struct Executor {
   uint8_t ev_map[kEvRing][6] = {};  // boundary -> recorded event of that slot (see mark())
   cudaEvent_t* ev = ev_ring[0];
   uint64_t n_runs = 0;
+  bool stage_events = true;  // record the inner stage boundaries (hyre_batch_set_stage_events)
 
   // device scratch sized at construction
   uint32_t cap = 0, samp_cap = 0;

@@ -1434,9 +1434,14 @@ __device__ void rescore_list(const PrefSelectArgs& a, uint32_t q, uint64_t* keys
 }
 }  // namespace
 
-constexpr int kSelPThreads = 1024;  // K4p: more warps -> more survivor rows in flight
-template <typename RowT, int LPR, int CPL>
-__global__ void __launch_bounds__(kSelPThreads) select_prefilter_kernel(PrefSelectArgs pa) {
+// K4p block size: 1024 threads (more warps -> more survivor rows in flight)
+// while the batch fits one wave of one CTA per SM; 512 threads and two CTAs
+// per SM for larger batches (one CTA per query: B = 256 is then one wave,
+// not two)
+constexpr int kSelPThreads = 1024;
+constexpr uint32_t kSelPWide = 148;  // batches above this use the 512-thread variant
+template <typename RowT, int LPR, int CPL, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) select_prefilter_kernel(PrefSelectArgs pa) {
   pdl_wait();  // the main pass's candidates
   const SelectArgs& a = pa.s;
   extern __shared__ uint64_t sel_smem[];
@@ -1589,18 +1594,31 @@ void dispatch_select_prefilter(const PrefSelectArgs& a, size_t smem, cudaStream_
   using KFn = void (*)(PrefSelectArgs);
   KFn k = nullptr;
   const uint32_t cpr = a.dp_chunks;
-  if (cpr == 8) k = select_prefilter_kernel<RowT, 8, 1>;
-  else if (cpr == 16) k = select_prefilter_kernel<RowT, 16, 1>;
-  else if (cpr == 32) k = select_prefilter_kernel<RowT, 32, 1>;
-  else if (cpr == 64) k = select_prefilter_kernel<RowT, 32, 2>;
-  else if (cpr == 128) k = select_prefilter_kernel<RowT, 32, 4>;
-  else if (cpr == 256) k = select_prefilter_kernel<RowT, 32, 8>;
+  const bool wide = a.s.B > kSelPWide;
+#define HYRE_K4P(LPR, CPL) (wide ? select_prefilter_kernel<RowT, LPR, CPL, 512> : select_prefilter_kernel<RowT, LPR, CPL, kSelPThreads>)
+  if (cpr == 8) k = HYRE_K4P(8, 1);
+  else if (cpr == 16) k = HYRE_K4P(16, 1);
+  else if (cpr == 32) k = HYRE_K4P(32, 1);
+  else if (cpr == 64) k = HYRE_K4P(32, 2);
+  else if (cpr == 128) k = HYRE_K4P(32, 4);
+  else if (cpr == 256) k = HYRE_K4P(32, 8);
   else throw Error(HYRE_INTERNAL, "unsupported row stride (chunks per row " + std::to_string(cpr) + ")");
-  static std::atomic<uint64_t> attr_set[2][6];  // [bf16][row-width variant]: device bitmask per kernel
+#undef HYRE_K4P
+  static std::atomic<uint64_t> attr_set[2][2][6];  // [bf16][wide][row-width variant]: device bitmask per kernel
   const int vi = cpr == 8 ? 0 : cpr == 16 ? 1 : cpr == 32 ? 2 : cpr == 64 ? 3 : cpr == 128 ? 4 : 5;
   set_smem_limit(reinterpret_cast<const void*>(k), static_cast<int>(smem),
-                 attr_set[std::is_same<RowT, float>::value ? 0 : 1][vi]);
-  launch_pdl(k, dim3(a.s.B), dim3(kSelPThreads), smem, st, a);
+                 attr_set[std::is_same<RowT, float>::value ? 0 : 1][wide ? 1 : 0][vi]);
+  if (wide) {  // two 112 KB CTAs per SM need the largest shared-memory carveout
+    static std::atomic<uint64_t> carve[2][6];
+    std::atomic<uint64_t>& c = carve[std::is_same<RowT, float>::value ? 0 : 1][vi];
+    int dev = 0;
+    HYRE_CUDA(cudaGetDevice(&dev));
+    if (!(c.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
+      HYRE_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      c.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
+    }
+  }
+  launch_pdl(k, dim3(a.s.B), dim3(wide ? 512 : kSelPThreads), smem, st, a);
 }
 }  // namespace
 

@@ -864,6 +864,32 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
             for (uint32_t j = 0; j < 32; ++j) neg = __funnelshift_l(v[j], neg, 1);  // sign of acc / fp32 score
             keep &= __brev(~neg);
           }
+          if constexpr (J < 0) {
+            // match-all: about half of the 32 scores are kept, so one
+            // unrolled pass over all 32 (no per-bit loop with a select tree
+            // per score: measured ~60 instructions per kept score).  (CTA-local
+            // floors -- shared-memory level counts that let scores below the
+            // CTA's own k-th largest skip the global histogram -- measured
+            // slower: the 32 lanes of a query collide on a few counters.)
+            uint32_t* hq = a.shist + static_cast<size_t>(q0 + c * 32) * a.hbins;
+#pragma unroll
+            for (uint32_t j4 = 0; j4 < 8; ++j4) {
+              const float4 s4 = reinterpret_cast<const float4*>(s_sc + c * 32)[j4];
+              const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+              for (uint32_t u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * j4 + u;
+                if ((keep >> j) & 1u) {
+                  const float sc = clamp_score(a.i8 ? static_cast<float>(static_cast<int32_t>(v[j])) * sv[u]
+                                                    : __uint_as_float(v[j]));
+                  const uint32_t b = min(static_cast<uint32_t>((sc + 1.0f) * scale), a.hbins - 1u);
+                  atomicAdd(hq + j * a.hbins + b, 1u);
+                }
+              }
+            }
+            continue;
+          }
+          // (J >= 0: eligible pairs are sparse; a per-bit loop)
           for (uint32_t el = keep; el; el &= el - 1u) {
             const uint32_t j = __ffs(el) - 1;
             const float sc = final_of(pick32(v, j), j);
@@ -1083,12 +1109,16 @@ void launch_tc_score(const CUtensorMap& qhi, const CUtensorMap& qlo, const TcArg
   if (!(attr.load(std::memory_order_acquire) & (1ull << (dev & 63)))) {
     HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<0, 1, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    227 * 1024 - 64));
+    HYRE_CUDA(cudaFuncSetAttribute(tc_score_kernel<-1, 1, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024 - 64));
     for (auto& row : fused)
       for (KFn k : row)
         HYRE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kTcStaticSmem));
     attr.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
   }
-  KFn k = tc_score_kernel<0, 1, 1, 0>;
+  // J = -1: the match-all variant's instance for sample passes (their
+  // unrolled histogram body stays out of the main pass's instruction footprint)
+  KFn k = (a.sample_floor && a.mode == SCORE_SAMPLE) ? tc_score_kernel<-1, 1, 1, 0> : tc_score_kernel<0, 1, 1, 0>;
   if (a.fused) {
     const uint32_t nch = tc_fused_chunks(a.Np), ci = nch == 1 ? 0 : (nch == 2 ? 1 : (nch == 4 ? 2 : 3));
     int ri = -1;

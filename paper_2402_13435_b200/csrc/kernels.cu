@@ -1635,58 +1635,96 @@ void launch_select_prefilter(const PrefSelectArgs& a, bool bf16, cudaStream_t st
 // One CTA per query: scan the per-chunk counts K1 produced, then extract only
 // the chunks that hold output rows.
 // ===========================================================================
-__global__ void __launch_bounds__(128) first_k_kernel(FirstKArgs a) {
+// Grid (G, B): CTA g of query q owns a contiguous range of chunks.  It sums
+// the per-chunk counts before its range (the rows that precede it), exits if
+// those already fill the output, scans its own counts, and its warps extract
+// the non-empty chunks that hold output rows in parallel -- one chunk per
+// warp, four mask words per lane, a warp scan for the output positions.
+// (A single CTA per query walking the chunks one at a time took 1.8 ms for a
+// sparse low-selectivity query over 50M rows: one dependent mask load per
+// non-empty chunk.)
+__global__ void __launch_bounds__(256) first_k_kernel(FirstKArgs a) {
   __shared__ uint32_t tmp[40];
-  const uint32_t q = blockIdx.x;
+  __shared__ uint32_t s_list[256], s_start[256], s_n;
+  const uint32_t q = blockIdx.y;
   const QParam qp = a.qp[q];
   if (!a.all_rows && (qp.flags & (QF_ACTIVE | QF_EMB)) != QF_ACTIVE) return;
   const uint32_t ne = a.n_elig[q];
   const uint64_t want64 = a.all_rows ? a.rows_cap : qp.k;
   const uint32_t want = static_cast<uint32_t>(min(static_cast<uint64_t>(ne), want64));
-  if (threadIdx.x == 0 && a.out_cnt) a.out_cnt[q] = want;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.out_cnt) a.out_cnt[q] = want;
   if (want == 0) return;
+  const uint32_t per = (a.n_chunks + gridDim.x - 1) / gridDim.x;
+  const uint32_t c0 = blockIdx.x * per, c1 = min(c0 + per, a.n_chunks);
+  if (c0 >= c1) return;
   const uint32_t* cc = a.chunk_cnt + static_cast<size_t>(q) * a.n_chunks;
   const uint32_t* mk = a.mask + static_cast<size_t>(q) * a.words;
   hyre_hit* hits = a.hits ? a.hits + a.hit_off[q] : nullptr;
-  __shared__ uint32_t s_cnt[kChunkWords], s_pre[kChunkWords];
-  uint32_t written = 0;
-  for (uint32_t base = 0; base < a.n_chunks && written < want; base += blockDim.x) {
-    const uint32_t ch = base + threadIdx.x;
-    const uint32_t c = ch < a.n_chunks ? cc[ch] : 0u;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // rows in the chunks before this CTA's range, 8 counts per thread per
+  // step; stop as soon as they fill the output (dense queries: one step)
+  uint32_t base = 0;
+  for (uint32_t i0 = 0; i0 < c0 && base < want; i0 += 8 * blockDim.x) {
+    uint32_t part = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < 8; ++u) {
+      const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+      part += i < c0 ? cc[i] : 0u;
+    }
+    uint32_t tot;
+    block_excl_scan(part, tmp, &tot);
+    base += tot;
+  }
+  if (base >= want) return;
+  for (uint32_t t0 = c0; t0 < c1 && base < want; t0 += blockDim.x) {
+    const uint32_t ch = t0 + threadIdx.x;
+    const uint32_t c = ch < c1 ? cc[ch] : 0u;
     uint32_t tot;
     const uint32_t pre = block_excl_scan(c, tmp, &tot);
-    s_cnt[threadIdx.x] = c;
-    s_pre[threadIdx.x] = pre;
+    if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    // prefixes are non-decreasing, so the chunks holding output rows are the
-    // non-empty ones before the first prefix that reaches `want`.
-    for (uint32_t j = 0; j < blockDim.x && written + s_pre[j] < want; ++j) {
-      if (!s_cnt[j]) continue;
-      const uint32_t chunk = base + j;
-      const uint32_t w = mk[chunk * kChunkWords + threadIdx.x];
-      uint32_t wt;
-      const uint32_t wpre = block_excl_scan(__popc(w), tmp, &wt);
-      uint32_t out = written + s_pre[j] + wpre, u = w;
-      while (u && out < want) {
-        const int b = __ffs(u) - 1;
-        u &= u - 1;
-        const uint32_t row = a.row_base + (chunk * kChunkWords + threadIdx.x) * 32 + b;
-        if (hits) {
-          hits[out].row = row;
-          hits[out].score = 0.0f;
+    if (c && base + pre < want) {  // a chunk holding output rows
+      const uint32_t e = atomicAdd(&s_n, 1u);
+      s_list[e] = ch;
+      s_start[e] = base + pre;
+    }
+    __syncthreads();
+    const uint32_t n = s_n;
+    for (uint32_t e = warp; e < n; e += nwarps) {
+      const uint32_t chunk = s_list[e];
+      const uint32_t w0 = chunk * kChunkWords + lane * 4;
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = w0 + u < a.words ? mk[w0 + u] : 0u;
+      const uint32_t p = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+      uint32_t out = s_start[e] + warp_incl_scan(p, lane) - p;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t x = w[u];
+        while (x && out < want) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1;
+          const uint32_t row = a.row_base + (w0 + u) * 32 + b;
+          if (hits) {
+            hits[out].row = row;
+            hits[out].score = 0.0f;
+          }
+          if (a.rows_out) a.rows_out[out] = row;
+          ++out;
         }
-        if (a.rows_out) a.rows_out[out] = row;
-        ++out;
       }
     }
-    written += tot;
-    __syncthreads();
+    base += tot;
+    __syncthreads();  // s_list / s_n reuse
   }
 }
 
 void launch_first_k(const FirstKArgs& a, cudaStream_t st) {
-  if (a.B == 0) return;
-  first_k_kernel<<<a.B, kChunkWords, 0, st>>>(a);
+  if (a.B == 0 || a.n_chunks == 0) return;
+  // ~4 CTAs per SM over the batch, at least 32 chunks (128K rows) per CTA
+  const uint32_t want_g = std::max(1u, 592u / a.B), max_g = (a.n_chunks + 31) / 32;
+  const uint32_t G = std::max(1u, std::min(want_g, max_g));
+  first_k_kernel<<<dim3(G, a.B), 256, 0, st>>>(a);
 }
 
 // ===========================================================================

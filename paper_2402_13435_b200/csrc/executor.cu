@@ -1297,6 +1297,10 @@ void Executor::scan_rows(uint32_t* d_rows, uint64_t n) {
 // query's clauses on the aux executor (K1 mask + K5).
 void Executor::exhaustive(uint32_t i) {
   HYRE_CUDA(cudaSetDevice(ix->device));
+  // the previous exhaustive query's kernels on this stream still read the
+  // shared d_ex_* buffers, which the aux executor's scan (its own stream)
+  // is about to overwrite
+  HYRE_CUDA(cudaStreamSynchronize(st));
   ++exh_count;
   uint32_t* out_cnt = d_counters + 3 * max_batch;
   uint32_t* rerun = d_counters + 4 * max_batch;

@@ -14,8 +14,10 @@ def main(src, dst, per_step=None):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     launches = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", ""))) for r in rows[1:]]
     if per_step is None:  # one step = up to and including the first select kernel
-        per_step = next(i for i, (k, _) in enumerate(launches) if k.startswith("select")) + 1
-    step = launches[:per_step]
+        per_step = next(i for i, (k, _) in enumerate(launches) if k.split("::")[-1].startswith("select")) + 1
+    # the step starts at its run-init kernel (index-upload kernels come first)
+    start = max([i for i, (k, _) in enumerate(launches[:per_step]) if k.endswith("run_init_kernel")] or [0])
+    step = launches[start:per_step]
     total = sum(t for _, t in step)
     out = {"note": "one c3 bench step (10M x d128 fp32, 8-clause CNF, B=64, K=100) from `ncu --metrics "
                    "gpu__time_duration.sum --clock-control none` (cold-cache, serialised: compare shares, not "

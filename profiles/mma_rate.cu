@@ -11,17 +11,23 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-template <int KIND, int N>  // KIND 0: kind::f16 (bf16, K = 16), 1: kind::i8 (K = 32)
+// CH: independent accumulator chains the MMAs rotate over (1 = every MMA
+// accumulates onto the previous one's result, as within one K3 tile)
+// CE: a tcgen05.commit after every CE MMAs (0: none); CB: with CE, a second
+// commit to another barrier right after it (K3's stage-release + accumulator-ready pair)
+template <int KIND, int N, int CH, int CE = 0, int CB = 0>  // KIND 0: kind::f16 (bf16, K = 16), 1: kind::i8 (K = 32)
 __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a = sm;                    // 128 rows x 128 B
   uint8_t* b = sm + 128 * 128;        // N rows x 128 B
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2, bar3;
   __shared__ uint32_t tmem_base;
   for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar3)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -38,7 +44,7 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
   if (threadIdx.x == 0) {
     const unsigned long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      const uint32_t kk = r & 3, d = tmem + (r & 1) * N;
+      const uint32_t kk = r & 3, d = tmem + (r % CH) * N;
       if (KIND)
         asm volatile(
             "{\n .reg .b64 da, db;\n mov.b64 da, {%1, %4};\n mov.b64 db, {%2, %4};\n"
@@ -49,6 +55,13 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
             "{\n .reg .b64 da, db;\n mov.b64 da, {%1, %4};\n mov.b64 db, {%2, %4};\n"
             " tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, 1;\n}" ::"r"(d),
             "r"(a_lo + 2 * kk), "r"(b_lo + 2 * kk), "r"(idesc), "n"(0x40004040));
+      if (CE && (r % CE) == CE - 1) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2))
+                     : "memory");
+        if (CB)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar3))
+                       : "memory");
+      }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar))
                  : "memory");
@@ -66,19 +79,19 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int KIND, int N>
+template <int KIND, int N, int CH, int CE = 0, int CB = 0>
 void run(const char* name, int sms, int clock_khz) {
   const int reps = 20000;
   unsigned long long* d;
   cudaMalloc(&d, sms * sizeof(unsigned long long));
   const int smem = 1024 + (128 + N) * 128;
-  cudaFuncSetAttribute(mma_rate<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mma_rate<KIND, N><<<sms, 128, smem>>>(200, d);  // warm-up
+  cudaFuncSetAttribute(mma_rate<KIND, N, CH, CE, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate<KIND, N, CH, CE, CB><<<sms, 128, smem>>>(200, d);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_rate<KIND, N><<<sms, 128, smem>>>(reps, d);
+  mma_rate<KIND, N, CH, CE, CB><<<sms, 128, smem>>>(reps, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -88,9 +101,9 @@ void run(const char* name, int sms, int clock_khz) {
   double mx = 0;
   for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
   const double kdim = KIND ? 32 : 16, ops = 2.0 * 128 * N * kdim * reps * sms;
-  std::printf("{\"mma\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"cycles_per_mma\": %.1f, \"event_ms\": %.3f, "
+  std::printf("{\"mma\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"chains\": %d, \"commit_every\": %d, \"second_commit\": %d, \"cycles_per_mma\": %.1f, \"event_ms\": %.3f, "
               "\"dense_tops\": %.1f, \"sm_clock_mhz_attr\": %d, \"error\": \"%s\"}\n",
-              name, N, KIND ? 32 : 16, mx / reps, ms, ops / (ms * 1e-3) / 1e12, clock_khz / 1000,
+              name, N, KIND ? 32 : 16, CH, CE, CB, mx / reps, ms, ops / (ms * 1e-3) / 1e12, clock_khz / 1000,
               cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -99,10 +112,17 @@ int main() {
   int sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  run<1, 256>("kind::i8", sms, clk);
-  run<1, 128>("kind::i8", sms, clk);
-  run<1, 64>("kind::i8", sms, clk);
-  run<0, 256>("kind::f16 (bf16)", sms, clk);
-  run<0, 128>("kind::f16 (bf16)", sms, clk);
+  run<1, 256, 1>("kind::i8", sms, clk);
+  run<1, 256, 1, 1>("kind::i8", sms, clk);
+  run<1, 256, 1, 2>("kind::i8", sms, clk);
+  run<1, 256, 1, 3>("kind::i8", sms, clk);
+  run<1, 256, 1, 5>("kind::i8", sms, clk);
+  run<1, 256, 1, 5, 1>("kind::i8", sms, clk);
+  run<1, 256, 1, 10>("kind::i8", sms, clk);
+  run<1, 256, 1, 10, 1>("kind::i8", sms, clk);
+  run<1, 256, 1, 20>("kind::i8", sms, clk);
+  run<1, 128, 1>("kind::i8", sms, clk);
+  run<1, 128, 1, 5>("kind::i8", sms, clk);
+  run<0, 256, 1>("kind::f16 (bf16)", sms, clk);
   return 0;
 }

@@ -415,6 +415,11 @@ void Executor::prepare(const hyre_query* qs, uint32_t b) {
     tc_np = std::min<uint32_t>(kTcMaxGroup, (b + 31) / 32 * 32);
     if (tc_np > 128 && tc_smem_bytes(tc_np, tc_kb(), tc_load_ops(), 3, 0, tc_q_planes(), 1) > 200 * 1024)
       tc_np = 128;
+    static const uint32_t group_cap = [] {  // profiling: HYRE_TC_GROUP caps the query group (32..256)
+      const char* e = std::getenv("HYRE_TC_GROUP");
+      return e ? std::max(32u, std::min(kTcMaxGroup, static_cast<uint32_t>(std::atoi(e)) / 32 * 32)) : kTcMaxGroup;
+    }();
+    tc_np = std::min(tc_np, group_cap);
     tc_groups = (b + tc_np - 1) / tc_np;
   }
   // Fused CNF: an all-hybrid, quant-free tensor-core batch evaluates the

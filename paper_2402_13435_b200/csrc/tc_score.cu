@@ -640,6 +640,9 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
     const uint32_t a_lo0 = (smem_u32(s_stage) >> 4) | 0x10000u;
     const uint32_t qh_lo0 = (smem_u32(s_qhi) >> 4) | 0x10000u, ql_lo0 = (smem_u32(s_qlo) >> 4) | 0x10000u;
     const uint32_t nkk = (a.debug & 16u) ? 1u : 4u;  // debug bit4: one K16 step per atom (timing only)
+    // (non-fused variants only: the fused ones run two CTAs per SM under a
+    // 72-register cap, where the second body spills, and are HBM-bound)
+    const bool i8_only = !kFused && a.i8 && a.prefilter && !a.split && !(a.debug & (1u | 16u | 0x2000u));  // 0x2000: generic body
     mbar_wait(qbar, 0);
     fence_after();
     uint32_t s = 0, ph = 0;
@@ -655,7 +658,21 @@ __global__ void __launch_bounds__(threads_for(J > 0, NCH), (J > 0 && NCH <= 2) ?
         fence_after();
         if (elect_one()) {
           const uint32_t st_lo = a_lo0 + ((s * st_bytes) >> 4);
-          for (uint32_t k = 0; k < aps && !(a.debug & 1u); ++k) {
+          if (i8_only) {
+            // the int8 prefilter: straight-line kind::i8 MMAs only.  (The
+            // generic body below compiles to four predicated tensor
+            // instructions per K step -- i8, f16 hi, f16 lo, split -- and
+            // the predicated-off ones still cost issue time: ~190 instead of
+            // 128 cycles per N = 256 K step.)
+            for (uint32_t k = 0; k < aps; ++k) {
+              const uint32_t ka = st_lo + ((k * a_bytes) >> 4), kq = qh_lo0 + (((k0 + k) * q_box) >> 4);
+              mma_i8w(d, ka, kq, idesc, (k0 + k) != 0);
+              mma_i8w(d, ka + 2, kq + 2, idesc, 1u);
+              mma_i8w(d, ka + 4, kq + 4, idesc, 1u);
+              mma_i8w(d, ka + 6, kq + 6, idesc, 1u);
+            }
+          }
+          for (uint32_t k = 0; k < aps && !i8_only && !(a.debug & 1u); ++k) {
             const uint32_t ka = st_lo + ((k * a_bytes) >> 4), kq = ((k0 + k) * q_box) >> 4;
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; ++kk) {  // 4 x K16 per 128-byte atom (+32 B = +2 per step)

@@ -15,19 +15,31 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uin
 // accumulates onto the previous one's result, as within one K3 tile)
 // CE: a tcgen05.commit after every CE MMAs (0: none); CB: with CE, a second
 // commit to another barrier right after it (K3's stage-release + accumulator-ready pair)
-template <int KIND, int N, int CH, int CE = 0, int CB = 0>  // KIND 0: kind::f16 (bf16, K = 16), 1: kind::i8 (K = 32)
-__global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cycles) {
+template <int KIND, int N, int CH, int CE = 0, int CB = 0, int BC = 0, int RND = 0>  // RND: random operand bytes (else a sparse 0/1/2/3 pattern); BC: warp 1 streams 16 KB bulk copies from HBM into 4 other shared-memory stages meanwhile; KIND 0: kind::f16 (bf16, K = 16), 1: kind::i8 (K = 32)
+__global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cycles, const uint8_t* src, size_t src_bytes) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a = sm;                    // 128 rows x 128 B
   uint8_t* b = sm + 128 * 128;        // N rows x 128 B
-  __shared__ uint64_t bar, bar2, bar3;
+  __shared__ uint64_t bar, bar2, bar3, cbar[4];
+  __shared__ volatile uint32_t stop;
+  uint8_t* cst = sm + (128 + N) * 128;  // 4 x 16 KB copy stages
   __shared__ uint32_t tmem_base;
-  for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += blockDim.x) {
+    uint32_t x = static_cast<uint32_t>(i) * 2654435761u + blockIdx.x * 97u;
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    // RND: random int8 (|v| <= 127) or random bf16 pairs of magnitude ~1
+    const uint32_t r = KIND ? (x & 0x7f7f7f7fu) ^ (x & 0x80808080u) : ((x & 0x007f007fu) | 0x3f003f00u) ^ (x & 0x80008000u);
+    reinterpret_cast<uint32_t*>(sm)[i] = RND ? r : 0x01010101u * (i & 3);
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar3)));
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cbar[i])));
+    stop = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -73,25 +85,61 @@ __global__ void __launch_bounds__(128) mma_rate(int reps, unsigned long long* cy
           : "r"(su32(&bar))
           : "memory");
     cycles[blockIdx.x] = clock64() - t0;
+    stop = 1;
+  }
+  if (BC && threadIdx.x == 32) {  // bulk-copy stream: 16 KB per copy, 4 stages in flight
+    size_t off = static_cast<size_t>(blockIdx.x) * 16384 * 64;
+    uint32_t ph[4] = {0, 0, 0, 0};
+    for (uint32_t i = 0; !stop; ++i) {
+      const uint32_t st = i & 3;
+      if (i >= 4) {  // wait for this stage's previous copy
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+              : "=r"(done)
+              : "r"(su32(&cbar[st])), "r"(ph[st])
+              : "memory");
+        ph[st] ^= 1;
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&cbar[st])), "r"(16384) : "memory");
+      if (off + 16384 > src_bytes) off = 0;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       su32(cst + st * 16384)), "l"(src + off), "r"(16384), "r"(su32(&cbar[st]))
+                   : "memory");
+      off += 16384 * 148;
+    }
+    for (uint32_t st = 0; st < 4; ++st) {  // drain
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(su32(&cbar[st])), "r"(ph[st])
+            : "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int KIND, int N, int CH, int CE = 0, int CB = 0>
+template <int KIND, int N, int CH, int CE = 0, int CB = 0, int BC = 0, int RND = 0>
 void run(const char* name, int sms, int clock_khz) {
   const int reps = 20000;
   unsigned long long* d;
   cudaMalloc(&d, sms * sizeof(unsigned long long));
-  const int smem = 1024 + (128 + N) * 128;
-  cudaFuncSetAttribute(mma_rate<KIND, N, CH, CE, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mma_rate<KIND, N, CH, CE, CB><<<sms, 128, smem>>>(200, d);  // warm-up
+  const int smem = 1024 + (128 + N) * 128 + 4 * 16384;
+  static uint8_t* src = nullptr;
+  const size_t src_bytes = size_t{2} << 30;
+  if (!src) cudaMalloc(&src, src_bytes);
+  cudaFuncSetAttribute(mma_rate<KIND, N, CH, CE, CB, BC, RND>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate<KIND, N, CH, CE, CB, BC, RND><<<sms, 128, smem>>>(200, d, src, src_bytes);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_rate<KIND, N, CH, CE, CB><<<sms, 128, smem>>>(reps, d);
+  mma_rate<KIND, N, CH, CE, CB, BC, RND><<<sms, 128, smem>>>(reps, d, src, src_bytes);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -101,9 +149,9 @@ void run(const char* name, int sms, int clock_khz) {
   double mx = 0;
   for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
   const double kdim = KIND ? 32 : 16, ops = 2.0 * 128 * N * kdim * reps * sms;
-  std::printf("{\"mma\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"chains\": %d, \"commit_every\": %d, \"second_commit\": %d, \"cycles_per_mma\": %.1f, \"event_ms\": %.3f, "
+  std::printf("{\"mma\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"chains\": %d, \"commit_every\": %d, \"second_commit\": %d, \"bulk_copies\": %d, \"random_operands\": %d, \"cycles_per_mma\": %.1f, \"event_ms\": %.3f, "
               "\"dense_tops\": %.1f, \"sm_clock_mhz_attr\": %d, \"error\": \"%s\"}\n",
-              name, N, KIND ? 32 : 16, CH, CE, CB, mx / reps, ms, ops / (ms * 1e-3) / 1e12, clock_khz / 1000,
+              name, N, KIND ? 32 : 16, CH, CE, CB, BC, RND, mx / reps, ms, ops / (ms * 1e-3) / 1e12, clock_khz / 1000,
               cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -113,16 +161,11 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   run<1, 256, 1>("kind::i8", sms, clk);
-  run<1, 256, 1, 1>("kind::i8", sms, clk);
-  run<1, 256, 1, 2>("kind::i8", sms, clk);
-  run<1, 256, 1, 3>("kind::i8", sms, clk);
-  run<1, 256, 1, 5>("kind::i8", sms, clk);
-  run<1, 256, 1, 5, 1>("kind::i8", sms, clk);
-  run<1, 256, 1, 10>("kind::i8", sms, clk);
-  run<1, 256, 1, 10, 1>("kind::i8", sms, clk);
-  run<1, 256, 1, 20>("kind::i8", sms, clk);
-  run<1, 128, 1>("kind::i8", sms, clk);
-  run<1, 128, 1, 5>("kind::i8", sms, clk);
+  run<1, 256, 1, 0, 0, 0, 1>("kind::i8", sms, clk);
+  run<1, 256, 1, 5, 1, 1, 1>("kind::i8", sms, clk);
+  run<1, 128, 1, 0, 0, 0, 1>("kind::i8", sms, clk);
   run<0, 256, 1>("kind::f16 (bf16)", sms, clk);
+  run<0, 256, 1, 0, 0, 0, 1>("kind::f16 (bf16)", sms, clk);
+  run<1, 256, 1, 0, 0, 1>("kind::i8", sms, clk);
   return 0;
 }
